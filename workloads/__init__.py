@@ -1,0 +1,1 @@
+"""Seeded synthetic inputs shared by the oracle and the CUDA path (no method arithmetic)."""
