@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the batched multi-adapter LoRA delta (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1], "c2"): Llama-2-7B q/k/v/o projections (4096->4096,
+bf16), decode batch of 64 tokens over 32 adapters with ranks [8,16,32,64][a mod 4], for
+every one of the model's 32 layers: one STEP = one decode iteration's LoRA delta over all
+32 layers x 4 projections = 128 lora_apply calls, each on its own paged pool (distinct
+adapter weights per layer and projection, as in real serving).  The working set
+(128 pools x 15.7 MB of adapter rows + x/y) is 2.2 GB >> the 126 MB L2, so no L2 flush
+is needed between steps ("inputs larger than L2").
+
+value   tokens/s = (64 tokens x ranks) / step time, device-timed with CUDA events around K
+        replays of a CUDA graph of one step (inputs resident in HBM), max over ranks.
+e2e     the same metric through the public API (LoraPool.apply -> lora_apply) with host
+        buffers: every step copies that step's x (pinned host -> device), runs the 128
+        applies eagerly and reads all y back (device -> pinned host).
+roofline  the decode kernel (the only kernel in the step): algorithmic bytes per launch
+        (adapter rows once + x once + y read and write) / average launch time.
+cpu_baseline  the fp64 oracle (oracle/, C, OpenMP over tokens) on a bounded sample.
+
+Multi-GPU (torchrun): weak scaling, each rank serves its own 64-token batch over its own
+pools (request partitioning, no data-path collective; the process group is only used for
+the barrier and the max-over-ranks timing).
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import gen  # noqa: E402
+
+LAYERS = 32
+PROJS = ("q", "k", "v", "o")
+T_DECODE = 64
+H = 4096
+METRIC = "LoRA-delta tokens/s + % HBM roofline (decode) / % TC peak (prefill), 1/2/4/8 B200"
+UNIT = "tokens/s"
+WORKLOAD = "c2: Llama-2-7B q/k/v/o (4096->4096) bf16 decode, 64 tokens over 32 adapters, ranks 8/16/32/64, x 32 layers"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=2)
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, local):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world > 1
+
+
+def max_over_ranks(v: float, use_dist: bool) -> float:
+    if not use_dist:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(use_dist):
+    import torch
+    if use_dist:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+def layer_batch_meta(rank: int):
+    """seg_indptr / adapter_ids of the c2 decode batch (same for every layer and projection:
+    a decode request keeps its adapter across layers)."""
+    b = gen.config_c2(tag=0)
+    return b.seg_indptr, b.adapter_ids
+
+
+def make_pool_adapters(layer: int, proj: int, world_rank: int):
+    """The 32 adapters of one (layer, projection) pool, generated by workloads.gen with a
+    distinct seed tag per (rank, layer, projection)."""
+    tag = 1 + ((world_rank * LAYERS + layer) * len(PROJS) + proj)
+    return [gen.make_adapter(gen.BASE_SEED + 1, tag, a, gen.C2_RANKS[a % 4], H, H, "bf16") for a in range(32)]
+
+
+def algorithmic_bytes_per_apply(ranks_sum: int, T: int) -> int:
+    """b·[Σ_G r·(H_in+H_out) + T·H_in + 2·T·H_out]."""
+    return 2 * (ranks_sum * (H + H) + T * H + 2 * T * H)
+
+
+def load_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_tokens_per_s(n_layers_sample: int, world_rank: int = 0, n_threads: int = 0, reps: int = 1):
+    """The fp64 oracle on n_layers_sample layers x 4 projections of the same workload,
+    extrapolated to the metric's unit (tokens through all 32 layers x 4 projections)."""
+    from oracle import oracle as O
+    n_threads = n_threads or len(os.sched_getaffinity(0))
+    ip, ids = layer_batch_meta(world_rank)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((T_DECODE, H))
+    y0 = np.zeros((T_DECODE, H))
+    work = []
+    for l in range(n_layers_sample):
+        for p in range(len(PROJS)):
+            ads = make_pool_adapters(l, p, world_rank)
+            work.append([(a.id, a.rank, a.scale, gen.storage_to_f64(a.A, "bf16"), gen.storage_to_f64(a.B, "bf16"))
+                         for a in ads])
+    x = gen.storage_to_f64(gen.f32_to_bf16_bits(x.astype(np.float32)), "bf16")
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for ads in work:
+            O.delta(H, H, ip, ids, ads, x, y0, n_threads=n_threads)
+    dt = time.perf_counter() - t0
+    frac = (n_layers_sample * reps) / LAYERS
+    return T_DECODE * frac / dt, n_threads, dt
+
+
+def run_reference(args):
+    """--impl reference: the oracle (fp64 C, OpenMP) as the reference arm, same metric."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    for _ in range(max(0, args.warmup and 1)):
+        cpu_oracle_tokens_per_s(1, 0)
+    vals, secs = [], 0.0
+    for _ in range(args.steps if args.steps <= 3 else 3):
+        v, cores, dt = cpu_oracle_tokens_per_s(1, 0)
+        vals.append(v)
+        secs += dt
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": len(vals), "warmup": args.warmup, "ms_per_step": 1000.0 * T_DECODE / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (workloads.gen, seeded)",
+            "config": {"workload": WORKLOAD, "layers": LAYERS, "tokens_per_step": T_DECODE, "adapters": 32,
+                       "parallelism": "dp%d" % world},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "1 of 32 layers (4 applies x 64 tokens) per step, extrapolated x32; %.1f s" % secs},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    use_dist = init_dist(world, local)
+    import paper_2401_11240_b200 as L
+
+    layers = args.layers
+    ip, ids = layer_batch_meta(rank)
+    dev = torch.device("cuda", local)
+
+    # ---- pools: generate adapters (threads), load through the cold-start path
+    t_gen = time.perf_counter()
+    pools = []
+    with cf.ThreadPoolExecutor(max_workers=min(16, len(os.sched_getaffinity(0)))) as ex:
+        futs = {(l, p): ex.submit(make_pool_adapters, l, p, rank) for l in range(layers) for p in range(len(PROJS))}
+        ranks_sum = None
+        for l in range(layers):
+            row = []
+            for p in range(len(PROJS)):
+                ads = futs[(l, p)].result()
+                pool = L.LoraPool(H, H, 32, "bf16", max_total_rank=sum(a.rank for a in ads))
+                for a in ads:
+                    A = torch.from_numpy(a.A.view(np.int16)).pin_memory()
+                    B = torch.from_numpy(a.B.view(np.int16)).pin_memory()
+                    pool.load_adapter(a.id, a.rank, A, B, a.scale)
+                ranks_sum = sum(a.rank for a in ads)
+                row.append(pool)
+            pools.append(row)
+    torch.cuda.synchronize()
+    for row in pools:
+        for pool in row:
+            pool.release_host_buffers()
+    t_gen = time.perf_counter() - t_gen
+
+    # ---- activations: x per layer (attention input for q/k/v, o-proj input), y per projection
+    g = torch.Generator(device="cpu").manual_seed(gen.BASE_SEED + 100 + rank)
+    xs = [[torch.randn(T_DECODE, H, generator=g).to(torch.bfloat16).to(dev) for _ in range(2)] for _ in range(layers)]
+    ys = [[torch.zeros(T_DECODE, H, dtype=torch.bfloat16, device=dev) for _ in PROJS] for _ in range(layers)]
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(st):
+        for l in range(layers):
+            for p in range(len(PROJS)):
+                pools[l][p].apply(xs[l][0 if p < 3 else 1], ys[l][p], ip, ids, stream=st)
+
+    with torch.cuda.stream(stream):
+        step(stream)               # sizes the pools' scratch outside capture
+    torch.cuda.synchronize()
+    launches0 = sum(pool.info()["kernel_launches"] for row in pools for pool in row)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step(stream)
+    launches_per_step = sum(pool.info()["kernel_launches"] for row in pools for pool in row) - launches0
+    for _ in range(max(3, args.warmup)):
+        graph.replay()
+    barrier(use_dist)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(use_dist)
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                graph.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(use_dist)
+    ms_total = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_total, use_dist)
+    ms_step = ms_total / args.steps
+    tokens_per_step_all = T_DECODE * world
+    value = tokens_per_step_all / (ms_step / 1000.0)
+
+    # ---- roofline of the decode kernel (the only kernel of the step)
+    hbm_peak, tc_peak, peak_src = measured_peaks()
+    bytes_apply = algorithmic_bytes_per_apply(ranks_sum, T_DECODE)
+    n_kernels = layers * len(PROJS)
+    kernel_us = ms_step * 1000.0 / n_kernels      # includes inter-kernel gaps: conservative
+    achieved = bytes_apply / (kernel_us * 1e-6) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": load_ncu_traffic(),
+                "kernel": "lora_decode_kernel<bf16>", "algorithmic_bytes_per_launch": bytes_apply,
+                "avg_launch_us": round(kernel_us, 3), "peak_source": peak_src,
+                "note": "avg launch time = graph step time / 128 launches (includes launch gaps)"}
+
+    # ---- e2e through the public API with host buffers
+    x_host = [[torch.empty(T_DECODE, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)] for _ in range(layers)]
+    for l in range(layers):
+        for i in range(2):
+            x_host[l][i].copy_(xs[l][i].cpu())
+    y_host = [[torch.empty(T_DECODE, H, dtype=torch.bfloat16).pin_memory() for _ in PROJS] for _ in range(layers)]
+    h2d = sum(t.numel() * 2 for row in x_host for t in row)
+    d2h = sum(t.numel() * 2 for row in y_host for t in row)
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            for l in range(layers):
+                for i in range(2):
+                    xs[l][i].copy_(x_host[l][i], non_blocking=True)
+            step(stream)
+            for l in range(layers):
+                for p in range(len(PROJS)):
+                    y_host[l][p].copy_(ys[l][p], non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    barrier(use_dist)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) * 1000.0
+    e2e_ms = max(e0.elapsed_time(e1), wall) / args.e2e_steps
+    e2e_ms = max_over_ranks(e2e_ms, use_dist)
+    e2e = {"value": tokens_per_step_all / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": round(e2e_ms, 4)}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, dt = cpu_oracle_tokens_per_s(args.cpu_sample_layers, 0)
+        reps = max(1, int(10.0 / max(dt, 1e-3)))
+        if reps > 1:
+            v, cores, dt = cpu_oracle_tokens_per_s(args.cpu_sample_layers, 0, reps=min(reps, 100))
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": "%d of 32 layers x 4 projections (64 tokens), fp64 C oracle, OpenMP over tokens, "
+                         "extrapolated to 32 layers; %.1f s of CPU work" % (args.cpu_sample_layers, dt)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (workloads.gen seeded PCG64 adapters; random-init, no checkpoints)",
+                "config": {"workload": WORKLOAD, "layers": layers, "projections": list(PROJS),
+                           "tokens_per_step_per_gpu": T_DECODE, "adapters_per_pool": 32,
+                           "ranks": list(gen.C2_RANKS), "hidden": H, "parallelism": "dp%d (request partition)" % world,
+                           "l2": "inputs larger than L2 (%.2f GB adapter working set per GPU)" %
+                                 (layers * len(PROJS) * ranks_sum * 2 * H * 2 / 1e9),
+                           "timing": "CUDA graph of one step, K replays, CUDA events, max over ranks"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "gpu_launches": int(launches_per_step * args.steps),
+                "setup_s": round(t_gen, 1)}
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as fh:
+                fh.write(s + "\n")
+    for row in pools:
+        for pool in row:
+            pool.close()
+    if use_dist:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,558 @@
+// decode_kernel.cu -- N1: the SIMT batched multi-adapter LoRA delta for decode tokens
+// (and any token not routed to the tensor-core prefill kernel), sm_100a.
+//
+// Computes, per (adapter group g, token t of g):      (§2.1 Eq. 1)
+//     v_t[j]  = s_g · Σ_k x_t[k] · A_g[k][j]          shrink, fp32 accumulation
+//     y_t[n] += Σ_j v_t[j] · B_g[j][n]                expand, fp32 accumulation, one rounding
+// with no padding to the batch's max rank (MBGMV semantics).
+//
+// Design (DESIGN.md §"N1"):
+//  * Memory-bound on adapter bytes (the prior-art kernels already use > 70% of HBM
+//    bandwidth).  Each CTA owns one work unit and streams its rank rows of A
+//    (shrink) or B (expand) HBM -> SMEM with cp.async.bulk (the TMA bulk-copy engine,
+//    SASS UBLKCP) issued by one warp, so a unit's whole 32 KB is in flight at once without
+//    registers, and ~4 CTAs per SM keep >100 KB per SM in flight.
+//  * Two kernels per apply, chained with programmatic dependent launch (PDL): every CTA
+//    first issues the loads of its adapter rows (immutable pool pages), then signals
+//    launch_dependents and only then executes griddepcontrol.wait before touching data a
+//    preceding kernel may produce (x, y, the v scratch).  So the expand kernel's B rows
+//    stream in while the shrink kernel runs, and the next apply's A rows while this apply
+//    finishes -- the shrink -> expand dependency costs no global flags or atomics.
+//  * v (the rank-r intermediate, fp32) goes through a small L2-resident scratch; partial
+//    sums over k-slices and rank parts are reduced in a fixed order (no float atomics), so
+//    a token's result is a fixed function of (x_t, adapter): bitwise reproducible and
+//    independent of batch order (pin P6).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernel_config.h"
+#include "plan.h"
+
+namespace lora {
+
+struct DecodeArgs {
+    const char* x;
+    char* y;
+    const char* poolA;
+    const char* poolB;
+    float* vbuf;
+    const int32_t* meta_global;  // metadata in device memory (large batches) or null
+    unsigned long long* trace;   // debug: per-unit timestamps, or null
+    int H_in, H_out;
+    int n_shrink, n_expand, n_gc, ksplit;
+};
+
+template <int W>
+struct MetaBlob {
+    int32_t w[W];
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LAB_WAIT;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ void stg128_na(void* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+
+// ------------------------------------------------------------------ element traits
+template <typename T>
+struct Elem;
+
+template <>
+struct Elem<__nv_bfloat16> {
+    static constexpr int kVec = 8;
+    static constexpr int kSize = 2;
+    __device__ __forceinline__ static void unpack(const uint4& v, float (&f)[kVec]) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            f[2 * i] = __uint_as_float(w[i] << 16);
+            f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+    // y (bf16) + d (fp32) -> one round-to-nearest-even to bf16
+    __device__ __forceinline__ static uint4 add_round(const uint4& y, const float (&d)[kVec]) {
+        float f[kVec];
+        unpack(y, f);
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i] + d[2 * i], f[2 * i + 1] + d[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+};
+
+template <>
+struct Elem<float> {
+    static constexpr int kVec = 4;
+    static constexpr int kSize = 4;
+    __device__ __forceinline__ static void unpack(const uint4& v, float (&f)[kVec]) {
+        f[0] = __uint_as_float(v.x);
+        f[1] = __uint_as_float(v.y);
+        f[2] = __uint_as_float(v.z);
+        f[3] = __uint_as_float(v.w);
+    }
+    __device__ __forceinline__ static uint4 add_round(const uint4& y, const float (&d)[kVec]) {
+        return make_uint4(__float_as_uint(__uint_as_float(y.x) + d[0]), __float_as_uint(__uint_as_float(y.y) + d[1]),
+                          __float_as_uint(__uint_as_float(y.z) + d[2]), __float_as_uint(__uint_as_float(y.w) + d[3]));
+    }
+};
+
+// ------------------------------------------------------------------ metadata access
+__device__ __forceinline__ int gc_field(const int32_t* M, int gc, int f) { return M[kHdrWords + gc * kGcFields + f]; }
+
+// Warp-cooperative: the last gc whose base (field f) <= u (bases strictly increase over gc).
+// One metadata round trip per 32 gcs instead of a log2(n_gc)-deep dependent search.
+__device__ __forceinline__ int find_gc_warp(const int32_t* M, int n_gc, int f, int u, int lane) {
+    int res = 0;
+    for (int base = 0; base < n_gc; base += 32) {
+        const int i = base + lane;
+        const int v = i < n_gc ? gc_field(M, i, f) : 0x7fffffff;
+        const unsigned m = __ballot_sync(0xffffffffu, v <= u);
+        if (m == 0u) break;
+        res = base + 31 - __clz(m);
+        if (!(m & 0x80000000u)) break;
+    }
+    return res;
+}
+
+// per-CTA unit description, decoded once by warp 0 and shared through smem
+struct UnitSh {
+    int gc, r, ntok, ks, j0, nj, n0, nc, voff;
+    float scale;
+    int tok[kTokChunk];
+};
+
+// ------------------------------------------------------------------ shrink kernel
+// One CTA = one unit (group-chunk gc, k-slice ks, block of <= 8 rank rows): partial
+// v[t][j0..j0+nj) over k in [k0, k0+nk) for the <= kTokChunk tokens of gc.
+constexpr int kShrinkSmem = 256 + kShrinkRows * kSliceBytes + kTokChunk * kSliceBytes;   // 48.25 KB
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kConsumerThreads)
+    lora_shrink_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    using E = Elem<T>;
+    constexpr int V = E::kVec;
+    constexpr int KS = kSliceBytes / E::kSize;
+    extern __shared__ __align__(128) char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);          // [0] A rows, [1] x rows
+    UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
+    float* red = reinterpret_cast<float*>(smem + 128);            // kShrinkRows * kTokChunk floats
+    char* abuf = smem + 256;
+    char* xbuf = abuf + kShrinkRows * kSliceBytes;
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int u = blockIdx.x;
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
+    if (W == 1) pdl_wait();   // metadata uploaded by the preceding kernel
+
+    int tok = 0;
+    if (warp == 0) {
+        // 1. decode the unit and issue the adapter-row loads (immutable pool pages) before
+        //    waiting on the previous kernel in the stream
+        const int gc = find_gc_warp(M, a.n_gc, GC_SHRINK_BASE, u, lane);
+        const int r = gc_field(M, gc, GC_RANK);
+        const int ntok = gc_field(M, gc, GC_NTOK);
+        const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
+        const int poff = gc_field(M, gc, GC_PAGE_OFF);
+        const int toff = gc_field(M, gc, GC_TOK_OFF);
+        const int njb = shrink_jblocks(r);
+        const int ks = local / njb;
+        const int j0 = (local - ks * njb) * kShrinkRows;
+        const int nj = min(kShrinkRows, r - j0);
+        const int page = lane < nj ? M[poff + j0 + lane] : 0;
+        tok = lane < ntok ? M[toff + lane] : 0;
+        const int k0 = ks * KS;
+        const uint32_t row_bytes = (uint32_t)min(KS, a.H_in - k0) * E::kSize;
+        if (lane == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_arrive_expect_tx(&bars[0], (uint32_t)nj * row_bytes);
+            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
+            sh->voff = gc_field(M, gc, GC_VOFF);
+        }
+        __syncwarp();
+        if (lane < nj)
+            bulk_g2s(abuf + lane * kSliceBytes, a.poolA + ((size_t)page * a.H_in + k0) * E::kSize, row_bytes,
+                     &bars[0], policy_evict_first());
+    }
+    pdl_launch_dependents();
+    __syncthreads();
+    const int r = sh->r, ntok = sh->ntok, ks = sh->ks, j0 = sh->j0, nj = sh->nj;
+    const int k0 = ks * KS;
+    const int nk = min(KS, a.H_in - k0);
+    // 2. x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
+    pdl_wait();
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
+    if (warp == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nk * E::kSize));
+        __syncwarp();
+        if (lane < ntok)
+            bulk_g2s(xbuf + lane * kSliceBytes, a.x + ((size_t)tok * a.H_in + k0) * E::kSize, (uint32_t)nk * E::kSize,
+                     &bars[1], policy_evict_normal());
+    }
+    // 3. partial dot products: warp -> (row, k-part)
+    const int P = kShrinkRows / nj;
+    const int nit = (nk + 32 * V - 1) / (32 * V);
+    const int ipp = (nit + P - 1) / P;
+    mbar_wait(&bars[0], 0);
+    mbar_wait(&bars[1], 0);
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
+    if (warp < nj * P) {
+        const int row = warp % nj, part = warp / nj;
+        float acc[kTokChunk];
+#pragma unroll
+        for (int t = 0; t < kTokChunk; ++t) acc[t] = 0.f;
+        const char* arow = abuf + row * kSliceBytes;
+        const int it1 = min(nit, (part + 1) * ipp);
+#pragma unroll 4
+        for (int it = part * ipp; it < it1; ++it) {
+            const int e = (it * 32 + lane) * V;
+            if (e < nk) {
+                float av[V];
+                E::unpack(lds128(arow + e * E::kSize), av);
+#pragma unroll
+                for (int t = 0; t < kTokChunk; ++t) {
+                    if (t < ntok) {
+                        float xv[V];
+                        E::unpack(lds128(xbuf + t * kSliceBytes + e * E::kSize), xv);
+#pragma unroll
+                        for (int i = 0; i < V; ++i) acc[t] = fmaf(xv[i], av[i], acc[t]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kTokChunk; ++t) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < kTokChunk; ++t)
+                if (t < ntok) red[(row * P + part) * kTokChunk + t] = acc[t];
+        }
+    }
+    __syncthreads();
+    if (tid < nj * ntok) {
+        const int row = tid / ntok, t = tid - row * ntok;
+        float v = 0.f;
+        for (int p = 0; p < P; ++p) v += red[(row * P + p) * kTokChunk + t];
+        a.vbuf[sh->voff + (ks * ntok + t) * r + j0 + row] = v;
+    }
+    if (a.trace && tid == 0) {
+        a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 5] = gtime();
+    }
+}
+
+// ------------------------------------------------------------------ expand kernel
+// One CTA = one unit (group-chunk gc, column slice [n0, n0+nc) of width ncols(r)):
+// y[t][n0..n0+nc) += v[t][:] · B[:, n0..n0+nc) for the <= kTokChunk tokens of gc.
+constexpr int kYBytes = kTokChunk * kConsumerThreads * 16;   // <= 4 tokens x 256 vectors x 16 B
+constexpr int kExpandSmem = 256 + kTokChunk * LORA_MAX_RANK * 4 + kExpandBytes + kYBytes;
+
+template <typename T, int W>
+__global__ void __launch_bounds__(kConsumerThreads)
+    lora_expand_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    using E = Elem<T>;
+    constexpr int V = E::kVec;
+    extern __shared__ __align__(128) char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);          // [0] B rows, [1] y rows
+    UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
+    float* vsm = reinterpret_cast<float*>(smem + 256);            // [kTokChunk][r]
+    char* bbuf = smem + 256 + kTokChunk * LORA_MAX_RANK * 4;      // [r][c] (reused as the reduction buffer)
+    char* ybuf = bbuf + kExpandBytes;                             // [kTokChunk][c]
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ue = blockIdx.x;
+    const int u = ue + a.n_shrink;
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
+    if (W == 1) pdl_wait();   // metadata uploaded by a preceding kernel
+
+    int tok = 0;
+    if (warp == 0) {
+        // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
+        const int gc = find_gc_warp(M, a.n_gc, GC_EXPAND_BASE, ue, lane);
+        const int r = gc_field(M, gc, GC_RANK);
+        const int ntok = gc_field(M, gc, GC_NTOK);
+        const int local = ue - gc_field(M, gc, GC_EXPAND_BASE);
+        const int poff = gc_field(M, gc, GC_PAGE_OFF);
+        const int toff = gc_field(M, gc, GC_TOK_OFF);
+        const int c = expand_ncols(r, E::kSize);
+        const int n0 = local * c;
+        const int nc = min(c, a.H_out - n0);
+        int pages[LORA_MAX_RANK / 32];
+#pragma unroll
+        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? M[poff + q * 32 + lane] : 0;
+        tok = lane < ntok ? M[toff + lane] : 0;
+        const uint32_t row_bytes = (uint32_t)nc * E::kSize;
+        if (lane == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
+            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
+            sh->voff = gc_field(M, gc, GC_VOFF);
+            sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
+        }
+        if (lane < ntok) sh->tok[lane] = tok;
+        __syncwarp();
+        const uint64_t pol = policy_evict_first();
+#pragma unroll
+        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) {
+            const int j = q * 32 + lane;
+            if (j < r)
+                bulk_g2s(bbuf + (size_t)j * c * E::kSize, a.poolB + ((size_t)pages[q] * a.H_out + n0) * E::kSize,
+                         row_bytes, &bars[0], pol);
+        }
+    }
+    pdl_launch_dependents();
+    __syncthreads();
+    const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
+    const int c = expand_ncols(r, E::kSize);
+    const size_t row_stride = (size_t)c * E::kSize;
+    pdl_wait();   // the shrink kernel's v (and y from whoever wrote it) are now visible
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
+    if (warp == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * E::kSize));
+        __syncwarp();
+        if (lane < ntok)
+            bulk_g2s(ybuf + lane * row_stride, a.y + ((size_t)tok * a.H_out + n0) * E::kSize, (uint32_t)nc * E::kSize,
+                     &bars[1], policy_evict_normal());
+    }
+    {
+        const int voff = sh->voff;
+        const float scale = sh->scale;
+        for (int i = tid; i < ntok * r; i += kConsumerThreads) {
+            const int t = i / r, j = i - t * r;
+            float v = 0.f;
+            for (int k = 0; k < a.ksplit; ++k) v += ld_cg_f32(a.vbuf + voff + (k * ntok + t) * r + j);
+            vsm[t * r + j] = v * scale;
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bars[0], 0);
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
+    const int Cf = c / V;                   // vector columns of a full unit (power of two <= 256)
+    const int P = kConsumerThreads / Cf;    // rank parts
+    const int ci = tid % Cf, p = tid / Cf;
+    const bool active = ci * V < nc;
+    float acc[kTokChunk][V];
+#pragma unroll
+    for (int t = 0; t < kTokChunk; ++t)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[t][i] = 0.f;
+    if (active) {
+        const char* col = bbuf + ci * 16;
+#pragma unroll 4
+        for (int j = p; j < r; j += P) {
+            float b[V];
+            E::unpack(lds128(col + j * row_stride), b);
+#pragma unroll
+            for (int t = 0; t < kTokChunk; ++t) {
+                if (t < ntok) {
+                    const float vt = vsm[t * r + j];
+#pragma unroll
+                    for (int i = 0; i < V; ++i) acc[t][i] = fmaf(vt, b[i], acc[t][i]);
+                }
+            }
+        }
+    }
+    if (P == 1) {
+        mbar_wait(&bars[1], 0);
+        if (active) {
+#pragma unroll
+            for (int t = 0; t < kTokChunk; ++t) {
+                if (t < ntok) {
+                    const uint4 yo = lds128(ybuf + t * row_stride + ci * 16);
+                    stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + ci * V) * E::kSize, E::add_round(yo, acc[t]));
+                }
+            }
+        }
+    } else {
+        // fixed-order reduction over the P rank parts, through the (now free) B buffer
+        float* red = reinterpret_cast<float*>(bbuf);
+        __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int t = 0; t < kTokChunk; ++t) {
+                if (t < ntok) {
+                    float* dst = red + ((size_t)(p * kTokChunk + t) * Cf + ci) * V;
+#pragma unroll
+                    for (int i = 0; i < V; i += 4)
+                        *reinterpret_cast<float4*>(dst + i) =
+                            make_float4(acc[t][i], acc[t][i + 1], acc[t][i + 2], acc[t][i + 3]);
+                }
+            }
+        }
+        __syncthreads();
+        mbar_wait(&bars[1], 0);
+        for (int it = tid; it < ntok * Cf; it += kConsumerThreads) {
+            const int t = it / Cf, c2 = it - t * Cf;
+            if (c2 * V >= nc) continue;
+            float d[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) d[i] = 0.f;
+            for (int q = 0; q < P; ++q) {
+                const float* src = red + ((size_t)(q * kTokChunk + t) * Cf + c2) * V;
+#pragma unroll
+                for (int i = 0; i < V; ++i) d[i] += src[i];
+            }
+            const uint4 yo = lds128(ybuf + t * row_stride + c2 * 16);
+            stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + c2 * V) * E::kSize, E::add_round(yo, d));
+        }
+    }
+    if (a.trace && tid == 0) {
+        a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 5] = gtime();
+    }
+}
+
+// copies a metadata blob too large for one kernel's parameters into device memory,
+// kUploadWords per launch (parameters are captured by value in CUDA graphs)
+constexpr int kUploadWords = 7936;
+__global__ void lora_meta_upload_kernel(int32_t* dst, const __grid_constant__ MetaBlob<kUploadWords> b, int n) {
+    pdl_wait();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = b.w[i];
+}
+
+// ------------------------------------------------------------------ host launcher
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kernel, int grid, int block, int smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <typename T, int W>
+static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t st, int* launches) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(lora_shrink_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kShrinkSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(lora_expand_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExpandSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    MetaBlob<W> blob;
+    if (W > 1) {
+        const int n = (int)pl.blob.size();
+        for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
+    }
+    cudaError_t e = launch_pdl(lora_shrink_kernel<T, W>, pl.n_shrink, kConsumerThreads, kShrinkSmem, st, a, blob);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(lora_expand_kernel<T, W>, pl.n_expand, kConsumerThreads, kExpandSmem, st, a, blob);
+    *launches += 2;
+    return e;
+}
+
+template <typename T>
+static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {
+    DecodeArgs a;
+    a.x = static_cast<const char*>(L.x);
+    a.y = static_cast<char*>(L.y);
+    a.poolA = static_cast<const char*>(L.poolA);
+    a.poolB = static_cast<const char*>(L.poolB);
+    a.vbuf = L.vbuf;
+    a.meta_global = L.meta_dev;
+    a.trace = L.trace;
+    a.H_in = L.H_in;
+    a.H_out = L.H_out;
+    a.n_shrink = pl.n_shrink;
+    a.n_expand = pl.n_expand;
+    a.n_gc = pl.n_gc;
+    a.ksplit = ksplit_of(L.H_in, (int)sizeof(T));
+    const int n = (int)pl.blob.size();
+    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches);
+    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches);
+    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches);
+    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches);
+    for (int off = 0; off < n; off += kUploadWords) {
+        const int m = n - off < kUploadWords ? n - off : kUploadWords;
+        MetaBlob<kUploadWords> b;
+        for (int i = 0; i < m; ++i) b.w[i] = pl.blob[off + i];
+        cudaError_t e = launch_pdl(lora_meta_upload_kernel, 1, 256, 0, st, L.meta_dev + off, b, m);
+        *launches += 1;
+        if (e != cudaSuccess) return e;
+    }
+    return launch_pair<T, 1>(a, pl, st, launches);
+}
+
+int launch_decode(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {
+    if (L.esz == 2) return (int)launch_typed<__nv_bfloat16>(pl, L, st, launches);
+    return (int)launch_typed<float>(pl, L, st, launches);
+}
+
+}  // namespace lora

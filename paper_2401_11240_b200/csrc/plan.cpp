@@ -1,0 +1,161 @@
+// plan.cpp -- see plan.h.  Canonical ordering rules (readings R8, R10):
+//   groups = distinct adapter ids >= 0 that own >= 1 token, ascending id;
+//   tokens ascending within a group; pages in rank order;
+//   seg_kind = PREFILL if id >= 0 and len >= L_tc, DECODE if id >= 0 and 1 <= len < L_tc, else NONE.
+#include "plan.h"
+
+#include <algorithm>
+#include <cstring>
+
+#include "kernel_config.h"
+
+namespace lora {
+
+static inline int32_t f32_bits(float f) {
+    int32_t b;
+    std::memcpy(&b, &f, 4);
+    return b;
+}
+
+lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, int H_in, int H_out,
+                       int esz, int L_tc, bool tc_enabled, const AdapterTable& table, std::string& err) {
+    if (S < 0) { err = "num_segments < 0"; return LORA_ERR_ARG; }
+    if (S > 0 && (ip == nullptr || ids == nullptr)) { err = "seg_indptr/adapter_ids is NULL"; return LORA_ERR_ARG; }
+    if (S > 0 && ip[0] != 0) { err = "seg_indptr[0] != 0"; return LORA_ERR_ARG; }
+    for (int i = 0; i < S; ++i) {
+        if (ip[i + 1] < ip[i]) { err = "seg_indptr not non-decreasing at segment " + std::to_string(i); return LORA_ERR_ARG; }
+        if (ids[i] >= 0 && table.find(ids[i]) == table.end()) {
+            err = "adapter_ids[" + std::to_string(i) + "] = " + std::to_string(ids[i]) + " is not loaded";
+            return LORA_ERR_UNKNOWN_ADAPTER;
+        }
+    }
+    const int T = S > 0 ? ip[S] : 0;
+    pl = Plan();
+    pl.T = T; pl.S = S; pl.L_tc = L_tc;
+
+    // M1 token -> segment
+    pl.tok_seg.resize(T);
+    for (int i = 0; i < S; ++i)
+        for (int t = ip[i]; t < ip[i + 1]; ++t) pl.tok_seg[t] = i;
+
+    // M2 groups (ids >= 0 owning >= 1 token), ascending
+    std::vector<int32_t> gids;
+    for (int i = 0; i < S; ++i)
+        if (ids[i] >= 0 && ip[i + 1] > ip[i]) gids.push_back(ids[i]);
+    std::sort(gids.begin(), gids.end());
+    gids.erase(std::unique(gids.begin(), gids.end()), gids.end());
+    const int G = (int)gids.size();
+    pl.G = G;
+    auto gidx = [&](int32_t id) { return (int)(std::lower_bound(gids.begin(), gids.end(), id) - gids.begin()); };
+
+    // M5 seg kinds and M6 features
+    pl.seg_kind.resize(S);
+    std::vector<int32_t> seg_group(S, -1);
+    for (int i = 0; i < S; ++i) {
+        const int len = ip[i + 1] - ip[i];
+        if (ids[i] < 0 || len == 0) { pl.seg_kind[i] = LORA_KIND_NONE; continue; }
+        pl.seg_kind[i] = len >= L_tc ? LORA_KIND_PREFILL : LORA_KIND_DECODE;
+        seg_group[i] = gidx(ids[i]);
+        const int64_t r = table.at(ids[i]).rank;
+        pl.n_seg += 1;
+        pl.max_rank = std::max(pl.max_rank, r);
+        pl.sum_rank_seg += r;
+        pl.sum_rank_tokens += r * len;
+    }
+    pl.nseg_x_maxrank = pl.n_seg * pl.max_rank;
+
+    // M2/M3/M4 per-group tables
+    pl.group_id = gids;
+    pl.group_rank.resize(G); pl.group_scale.resize(G); pl.group_ntok.assign(G, 0);
+    pl.group_page_off.resize(G); pl.group_tok_off.resize(G);
+    for (int g = 0; g < G; ++g) {
+        const AdapterRec& a = table.at(gids[g]);
+        pl.group_rank[g] = a.rank;
+        pl.group_scale[g] = a.scale;
+        pl.group_page_off[g] = (int32_t)pl.pages.size();
+        pl.pages.insert(pl.pages.end(), a.pages.begin(), a.pages.begin() + a.rank);
+        pl.sum_rank_groups += a.rank;
+    }
+    for (int t = 0; t < T; ++t) {
+        const int g = seg_group[pl.tok_seg[t]];
+        if (g >= 0) pl.group_ntok[g] += 1;
+    }
+    int off = 0;
+    for (int g = 0; g < G; ++g) { pl.group_tok_off[g] = off; off += pl.group_ntok[g]; }
+    pl.group_tokens.resize(off);
+    {
+        std::vector<int32_t> fill(pl.group_tok_off);
+        for (int t = 0; t < T; ++t) {
+            const int g = seg_group[pl.tok_seg[t]];
+            if (g >= 0) pl.group_tokens[fill[g]++] = t;
+        }
+    }
+
+    // ---- kernel work ----
+    // tokens of the SIMT path per group (ascending), and tensor-core segments
+    std::vector<std::vector<int32_t>> simt(G);
+    for (int i = 0; i < S; ++i) {
+        if (seg_group[i] < 0) continue;
+        if (tc_enabled && pl.seg_kind[i] == LORA_KIND_PREFILL) {
+            pl.prefill.push_back({ip[i], ip[i + 1] - ip[i], seg_group[i]});
+            pl.n_prefill_tiles += (ip[i + 1] - ip[i] + 127) / 128;
+        }
+    }
+    for (int t = 0; t < T; ++t) {
+        const int i = pl.tok_seg[t];
+        const int g = seg_group[i];
+        if (g < 0) continue;
+        if (tc_enabled && pl.seg_kind[i] == LORA_KIND_PREFILL) continue;
+        simt[g].push_back(t);
+    }
+    const int ksplit = ksplit_of(H_in, esz);
+    // gc = (group, token chunk)
+    struct Gc { int g, tok_off, ntok; };
+    std::vector<Gc> gcs;
+    std::vector<int32_t> blob_pages, blob_toks, group_blob_page(G, -1);
+    for (int g = 0; g < G; ++g) {
+        if (simt[g].empty()) continue;
+        group_blob_page[g] = (int32_t)blob_pages.size();
+        blob_pages.insert(blob_pages.end(), pl.pages.begin() + pl.group_page_off[g],
+                          pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
+        for (size_t c = 0; c < simt[g].size(); c += kTokChunk) {
+            const int n = (int)std::min<size_t>(kTokChunk, simt[g].size() - c);
+            gcs.push_back({g, (int)blob_toks.size(), n});
+            blob_toks.insert(blob_toks.end(), simt[g].begin() + c, simt[g].begin() + c + n);
+        }
+    }
+    const int n_gc = (int)gcs.size();
+    pl.n_gc = n_gc;
+    pl.blob.assign(kHdrWords + kGcFields * n_gc + blob_pages.size() + blob_toks.size(), 0);
+    int32_t* hdr = pl.blob.data();
+    int32_t* gct = hdr + kHdrWords;
+    const int pages_base = kHdrWords + kGcFields * n_gc;
+    const int toks_base = pages_base + (int)blob_pages.size();
+    int shrink = 0, expand = 0;
+    int64_t voff = 0;
+    for (int c = 0; c < n_gc; ++c) {
+        const int g = gcs[c].g, r = pl.group_rank[g];
+        int32_t* e = gct + kGcFields * c;
+        e[GC_RANK] = r;
+        e[GC_PAGE_OFF] = pages_base + group_blob_page[g];
+        e[GC_TOK_OFF] = toks_base + gcs[c].tok_off;
+        e[GC_NTOK] = gcs[c].ntok;
+        e[GC_SHRINK_BASE] = shrink;
+        e[GC_EXPAND_BASE] = expand;
+        e[GC_VOFF] = (int32_t)voff;
+        e[GC_SCALE] = f32_bits(pl.group_scale[g]);
+        shrink += ksplit * shrink_jblocks(r);
+        const int nc = expand_ncols(r, esz);
+        expand += (H_out + nc - 1) / nc;
+        voff += (int64_t)ksplit * gcs[c].ntok * r;
+    }
+    if (voff > INT32_MAX) { err = "batch too large for the SIMT scratch"; return LORA_ERR_ARG; }
+    std::copy(blob_pages.begin(), blob_pages.end(), pl.blob.begin() + pages_base);
+    std::copy(blob_toks.begin(), blob_toks.end(), pl.blob.begin() + toks_base);
+    hdr[0] = n_gc; hdr[1] = shrink; hdr[2] = expand;
+    hdr[3] = (int32_t)blob_pages.size(); hdr[4] = (int32_t)blob_toks.size(); hdr[5] = ksplit;
+    pl.n_shrink = shrink; pl.n_expand = expand; pl.vbuf_floats = voff;
+    return LORA_OK;
+}
+
+}  // namespace lora

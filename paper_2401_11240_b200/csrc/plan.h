@@ -1,0 +1,80 @@
+// plan.h -- host-side batch planner: canonical metadata (M1-M6) and kernel work lists.
+// Step a1 of SURVEY.md §8(a): from seg_indptr / adapter_ids and the pool's id -> pages
+// table, build the batch metadata "that parallelizes the LoRA weight gathering"
+// (§4.1).  Pure C++ (no CUDA), so host-only pools exercise it on CPU.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/lora_delta.h"
+
+namespace lora {
+
+struct AdapterRec {
+    int32_t id = -1;
+    int rank = 0;
+    float scale = 1.f;
+    std::vector<int32_t> pages;   // page indices, rank order
+    void* ready = nullptr;        // cudaEvent_t of the load (owned by the pool)
+    bool ready_known = false;
+};
+
+using AdapterTable = std::unordered_map<int32_t, AdapterRec>;
+
+struct PrefillSeg {          // one tensor-core segment (N2 work)
+    int32_t tok0, len, group;
+};
+
+struct Plan {
+    // ---- canonical metadata (bit-exact contract, checked against oracle/) ----
+    int32_t T = 0, S = 0, G = 0, L_tc = 64;
+    std::vector<int32_t> tok_seg, group_id, group_rank, group_ntok, group_page_off, group_tok_off;
+    std::vector<int32_t> group_tokens, pages, seg_kind;
+    std::vector<float> group_scale;
+    int64_t n_seg = 0, max_rank = 0, nseg_x_maxrank = 0, sum_rank_seg = 0, sum_rank_groups = 0,
+            sum_rank_tokens = 0;
+    // ---- SIMT decode kernel work (N1) ----
+    std::vector<int32_t> blob;           // see kernel_config.h for the layout
+    int32_t n_gc = 0, n_shrink = 0, n_expand = 0;
+    int64_t vbuf_floats = 0;
+    // ---- tcgen05 prefill work (N2) ----
+    std::vector<PrefillSeg> prefill;
+    int32_t n_prefill_tiles = 0;
+};
+
+// Builds `plan`.  tc_enabled=false routes every token through the SIMT kernel.
+// Returns LORA_OK or an error status with `err` naming the offending operand.
+lora_status build_plan(Plan& plan, const int32_t* seg_indptr, const int32_t* adapter_ids, int S,
+                       int H_in, int H_out, int esz, int L_tc, bool tc_enabled,
+                       const AdapterTable& table, std::string& err);
+
+// ---- kernel launch descriptors (pool.cpp -> *_kernel.cu) ----
+struct DecodeLaunch {
+    const void* x;
+    void* y;
+    const void* poolA;
+    const void* poolB;
+    float* vbuf;
+    int32_t* meta_dev;     // device scratch for metadata too large for kernel parameters
+    unsigned long long* trace;   // optional per-unit timestamps (lora_debug_set_trace), or null
+    int H_in, H_out, esz, num_sms;
+};
+struct PrefillLaunch {
+    const void* x;
+    void* y;
+    const void* poolA;
+    const void* poolB;
+    int H_in, H_out, num_sms;
+};
+}  // namespace lora
+
+// implemented in the .cu files (declared here so host code needs no CUDA headers)
+typedef struct CUstream_st* lora_cuda_stream;
+namespace lora {
+int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
+int launch_prefill(const Plan& pl, const PrefillLaunch& L, lora_cuda_stream st, int* launches);
+bool prefill_supported(int H_in, int H_out, int esz);
+
+}  // namespace lora

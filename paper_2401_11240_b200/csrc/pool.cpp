@@ -1,0 +1,460 @@
+// pool.cpp -- the C ABI of include/lora_delta.h: paged HBM adapter pool, cold-start
+// loader on a side stream, host planner, and the launches of the sm_100a kernels.
+//
+// Paper anchors: adapters live in host memory and are fetched to the GPU on demand
+// (§2.3 C1 P:353-392, §3); the GPU LoRA is batched per layer and
+// added to the base output (§4.1); invocation is sync-free, relying on CUDA
+// stream order (§4.2).  The paged store follows "optimized GPU memory
+// management" borrowed from S-LoRA/LightLLM: one page = one rank
+// component (a_j ∈ R^{H_in}, b_j ∈ R^{H_out}) -- DESIGN.md reading R9.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lora_delta.h"
+#include "kernel_config.h"
+#include "plan.h"
+
+
+using namespace lora;
+
+static thread_local std::string g_err;
+
+static lora_status fail(lora_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+struct lora_pool {
+    int H_in = 0, H_out = 0, max_adapters = 0, n_pages = 0, esz = 2, device = 0, num_sms = 148;
+    lora_dtype dtype = LORA_BF16;
+    unsigned flags = 0;
+    bool host_only = false;
+    char* dA = nullptr;                  // [n_pages][H_in]
+    char* dB = nullptr;                  // [n_pages][H_out]
+    std::vector<uint8_t> page_used;
+    int free_pages = 0;
+    AdapterTable table;
+    cudaStream_t side = nullptr;
+    cudaEvent_t unload_fence = nullptr;
+    bool fence_pending = false;
+    std::vector<cudaStream_t> apply_streams;   // streams applied on since the last unload
+    float* vbuf = nullptr;
+    size_t vbuf_cap = 0;                 // floats
+    int32_t* meta_dev = nullptr;
+    size_t meta_cap = 0;                 // words
+    Plan plan;
+    int L_tc = 64;
+    int64_t launches = 0;
+    unsigned long long* trace = nullptr;   // lora_debug_set_trace
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+            cudaSetDevice(dev);
+            changed = true;
+        }
+    }
+    ~DeviceGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
+};
+
+lora_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(LORA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(call, what)                      \
+    do {                                          \
+        cudaError_t _e = (call);                  \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
+// grow a device buffer (rare; synchronises the device so no in-flight kernel uses the old one)
+template <typename T>
+lora_status grow(T*& buf, size_t& cap, size_t need, bool zero, const char* what) {
+    if (need <= cap) return LORA_OK;
+    size_t n = std::max(need, cap * 2);
+    if (buf) {
+        CUDA_TRY(cudaDeviceSynchronize(), what);
+        CUDA_TRY(cudaFree(buf), what);
+        buf = nullptr;
+        cap = 0;
+    }
+    CUDA_TRY(cudaMalloc((void**)&buf, n * sizeof(T)), what);
+    if (zero) {
+        CUDA_TRY(cudaMemset(buf, 0, n * sizeof(T)), what);
+        CUDA_TRY(cudaDeviceSynchronize(), what);
+    }
+    cap = n;
+    return LORA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lora_last_error(void) { return g_err.c_str(); }
+
+int lora_abi_version(void) { return LORA_ABI_VERSION; }
+
+lora_status lora_pool_create_ex(int hidden_in, int hidden_out, int max_adapters, lora_dtype dtype,
+                                int max_total_rank, unsigned flags, lora_pool** out) {
+    if (!out) return fail(LORA_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (dtype != LORA_F32 && dtype != LORA_BF16) return fail(LORA_ERR_ARG, "dtype must be LORA_F32 or LORA_BF16");
+    if (hidden_in <= 0 || hidden_out <= 0) return fail(LORA_ERR_SHAPE, "hidden_in/hidden_out must be > 0");
+    if (max_adapters <= 0) return fail(LORA_ERR_SHAPE, "max_adapters must be > 0");
+    if (max_total_rank < 0) return fail(LORA_ERR_SHAPE, "max_total_rank must be >= 0");
+    const int esz = dtype == LORA_BF16 ? 2 : 4;
+    const int vec = 16 / esz;
+    if (hidden_in % vec || hidden_out % vec)
+        return fail(LORA_ERR_ALIGN, "hidden_in and hidden_out must be multiples of " + std::to_string(vec));
+    lora_pool* p = new lora_pool();
+    p->H_in = hidden_in;
+    p->H_out = hidden_out;
+    p->max_adapters = max_adapters;
+    p->n_pages = max_total_rank > 0 ? max_total_rank : 64 * max_adapters;
+    p->dtype = dtype;
+    p->esz = esz;
+    p->flags = flags;
+    p->host_only = (flags & LORA_POOL_HOST_ONLY) != 0;
+    p->page_used.assign(p->n_pages, 0);
+    p->free_pages = p->n_pages;
+    if (!p->host_only) {
+        cudaError_t e = cudaGetDevice(&p->device);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+        if (e == cudaSuccess) e = cudaMalloc((void**)&p->dA, (size_t)p->n_pages * hidden_in * esz);
+        if (e == cudaSuccess) e = cudaMalloc((void**)&p->dB, (size_t)p->n_pages * hidden_out * esz);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->unload_fence, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            lora_pool_destroy(p);
+            return cuda_fail(e, "lora_pool_create");
+        }
+    }
+    *out = p;
+    return LORA_OK;
+}
+
+lora_status lora_pool_create(int hidden_in, int hidden_out, int max_adapters, lora_dtype dtype,
+                             int max_total_rank, lora_pool** out) {
+    return lora_pool_create_ex(hidden_in, hidden_out, max_adapters, dtype, max_total_rank, 0u, out);
+}
+
+lora_status lora_pool_destroy(lora_pool* p) {
+    if (!p) return LORA_OK;
+    if (!p->host_only) {
+        DeviceGuard g(p->device);
+        if (p->side) cudaStreamSynchronize(p->side);
+        for (cudaStream_t s : p->apply_streams) cudaStreamSynchronize(s);
+        cudaDeviceSynchronize();
+        for (auto& kv : p->table)
+            if (kv.second.ready) cudaEventDestroy((cudaEvent_t)kv.second.ready);
+        if (p->dA) cudaFree(p->dA);
+        if (p->dB) cudaFree(p->dB);
+        if (p->vbuf) cudaFree(p->vbuf);
+        if (p->meta_dev) cudaFree(p->meta_dev);
+        if (p->unload_fence) cudaEventDestroy(p->unload_fence);
+        if (p->side) cudaStreamDestroy(p->side);
+    }
+    delete p;
+    return LORA_OK;
+}
+
+lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_host, const void* B_host,
+                              float scale) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    if (id < 0) return fail(LORA_ERR_ARG, "id must be >= 0");
+    const int rmax = std::min(LORA_MAX_RANK, std::min(p->H_in, p->H_out));
+    if (rank < 1 || rank > rmax)
+        return fail(LORA_ERR_SHAPE, "rank " + std::to_string(rank) + " outside [1, " + std::to_string(rmax) + "]");
+    if (p->table.count(id)) return fail(LORA_ERR_EXISTS, "adapter " + std::to_string(id) + " already loaded");
+    if ((int)p->table.size() >= p->max_adapters) return fail(LORA_ERR_POOL_FULL, "adapter slots exhausted");
+    if (p->free_pages < rank)
+        return fail(LORA_ERR_POOL_FULL, "page budget exhausted: need " + std::to_string(rank) + ", free " +
+                                            std::to_string(p->free_pages));
+    if (!p->host_only) {
+        if (!A_host || !B_host) return fail(LORA_ERR_ARG, "A_host/B_host is NULL");
+        if (!is_pinned(A_host)) return fail(LORA_ERR_NOT_PINNED, "A_host is not pinned host memory");
+        if (!is_pinned(B_host)) return fail(LORA_ERR_NOT_PINNED, "B_host is not pinned host memory");
+    }
+    // lowest free pages, ascending (reading R9)
+    AdapterRec rec;
+    rec.id = id;
+    rec.rank = rank;
+    rec.scale = scale;
+    rec.pages.reserve(rank);
+    for (int pg = 0; pg < p->n_pages && (int)rec.pages.size() < rank; ++pg)
+        if (!p->page_used[pg]) rec.pages.push_back(pg);
+    if (!p->host_only) {
+        DeviceGuard g(p->device);
+        cudaEvent_t ev = nullptr;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "lora_load_adapter: event");
+        if (p->fence_pending) {
+            cudaError_t e = cudaStreamWaitEvent(p->side, p->unload_fence, 0);
+            if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: fence"); }
+            p->fence_pending = false;
+        }
+        const size_t ra = (size_t)p->H_in * p->esz, rb = (size_t)p->H_out * p->esz;
+        // one copy per run of consecutive pages
+        for (int j = 0; j < rank;) {
+            int k = j + 1;
+            while (k < rank && rec.pages[k] == rec.pages[k - 1] + 1) ++k;
+            const size_t n = (size_t)(k - j);
+            cudaError_t e = cudaMemcpyAsync(p->dA + (size_t)rec.pages[j] * ra, (const char*)A_host + j * ra, n * ra,
+                                            cudaMemcpyHostToDevice, p->side);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(p->dB + (size_t)rec.pages[j] * rb, (const char*)B_host + j * rb, n * rb,
+                                    cudaMemcpyHostToDevice, p->side);
+            if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: copy"); }
+            j = k;
+        }
+        cudaError_t e = cudaEventRecord(ev, p->side);
+        if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: record"); }
+        rec.ready = ev;
+    } else {
+        rec.ready_known = true;
+    }
+    for (int pg : rec.pages) p->page_used[pg] = 1;
+    p->free_pages -= rank;
+    p->table.emplace(id, std::move(rec));
+    return LORA_OK;
+}
+
+lora_status lora_unload_adapter(lora_pool* p, int32_t id) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    auto it = p->table.find(id);
+    if (it == p->table.end()) return fail(LORA_ERR_UNKNOWN_ADAPTER, "adapter " + std::to_string(id) + " is not loaded");
+    if (!p->host_only) {
+        DeviceGuard g(p->device);
+        // physical reuse of these pages must follow every apply already enqueued (events)
+        for (cudaStream_t s : p->apply_streams) {
+            CUDA_TRY(cudaEventRecord(p->unload_fence, s), "lora_unload_adapter: fence");
+            CUDA_TRY(cudaStreamWaitEvent(p->side, p->unload_fence, 0), "lora_unload_adapter: fence wait");
+        }
+        p->apply_streams.clear();
+        if (it->second.ready) {
+            // the load itself must also be finished before its pages are rewritten: side-stream order
+            cudaEventDestroy((cudaEvent_t)it->second.ready);
+        }
+    }
+    for (int pg : it->second.pages) p->page_used[pg] = 0;
+    p->free_pages += it->second.rank;
+    p->table.erase(it);
+    return LORA_OK;
+}
+
+lora_status lora_adapter_ready(lora_pool* p, int32_t id, int* ready) {
+    if (!p || !ready) return fail(LORA_ERR_ARG, "pool/ready is NULL");
+    auto it = p->table.find(id);
+    if (it == p->table.end()) return fail(LORA_ERR_UNKNOWN_ADAPTER, "adapter " + std::to_string(id) + " is not loaded");
+    AdapterRec& a = it->second;
+    if (!a.ready_known) {
+        DeviceGuard g(p->device);
+        cudaError_t e = cudaEventQuery((cudaEvent_t)a.ready);
+        if (e == cudaSuccess) a.ready_known = true;
+        else if (e != cudaErrorNotReady) return cuda_fail(e, "lora_adapter_ready");
+        else cudaGetLastError();
+    }
+    *ready = a.ready_known ? 1 : 0;
+    return LORA_OK;
+}
+
+lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* adapter_ids, int num_segments) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    std::string err;
+    const bool tc = !p->host_only ? prefill_supported(p->H_in, p->H_out, p->esz) : p->esz == 2;
+    lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
+                               p->L_tc, tc, p->table, err);
+    if (s != LORA_OK) return fail(s, err);
+    return LORA_OK;
+}
+
+lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr, const int32_t* adapter_ids,
+                       int num_segments, void* stream_ptr) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "lora_apply on a host-only pool");
+    if (num_segments < 0) return fail(LORA_ERR_ARG, "num_segments < 0");
+    if (num_segments == 0) return LORA_OK;
+    if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
+    const int T = seg_indptr[num_segments];
+    if (T == 0) {
+        std::string err;
+        lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
+                                   p->L_tc, false, p->table, err);
+        return s == LORA_OK ? LORA_OK : fail(s, err);
+    }
+    if (!x) return fail(LORA_ERR_ARG, "x is NULL");
+    if (!y) return fail(LORA_ERR_ARG, "y is NULL");
+    if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(LORA_ERR_ALIGN, "x and y must be 16-byte aligned");
+    {
+        const char* xs = (const char*)x;
+        const char* ys = (const char*)y;
+        const size_t xb = (size_t)T * p->H_in * p->esz, yb = (size_t)T * p->H_out * p->esz;
+        if (xs < ys + yb && ys < xs + xb) return fail(LORA_ERR_ARG, "x and y overlap");
+    }
+    DeviceGuard g(p->device);
+    cudaStream_t st = (cudaStream_t)stream_ptr;
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply: pending CUDA error");
+    }
+    std::string err;
+    const bool tc = prefill_supported(p->H_in, p->H_out, p->esz);
+    lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
+                               tc, p->table, err);
+    if (s != LORA_OK) return fail(s, err);
+    const Plan& pl = p->plan;
+    if (pl.G == 0) return LORA_OK;
+
+    // order after in-flight loads of the adapters this batch reads
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply: capture query");
+    for (int gi = 0; gi < pl.G; ++gi) {
+        AdapterRec& a = p->table.at(pl.group_id[gi]);
+        if (a.ready_known) continue;
+        cudaError_t e = cudaEventQuery((cudaEvent_t)a.ready);
+        if (e == cudaSuccess) { a.ready_known = true; continue; }
+        if (e != cudaErrorNotReady) return cuda_fail(e, "lora_apply: load event");
+        cudaGetLastError();
+        CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a.ready,
+                                     cap == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0),
+                 "lora_apply: wait load");
+    }
+    // scratch
+    if (pl.n_gc > 0) {
+        if ((s = grow(p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
+        if ((s = grow(p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
+    }
+    int launches = 0;
+    if (pl.n_gc > 0) {
+        DecodeLaunch L{x, y, p->dA, p->dB, p->vbuf, p->meta_dev, p->trace, p->H_in, p->H_out, p->esz, p->num_sms};
+        cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
+    }
+    if (!pl.prefill.empty()) {
+        PrefillLaunch L{x, y, p->dA, p->dB, p->H_in, p->H_out, p->num_sms};
+        cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
+    }
+    p->launches += launches;
+    if (std::find(p->apply_streams.begin(), p->apply_streams.end(), st) == p->apply_streams.end())
+        p->apply_streams.push_back(st);
+    return LORA_OK;
+}
+
+lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    switch (option) {
+        case LORA_OPT_TC_THRESHOLD:
+            if (value < 1 || value > INT32_MAX) return fail(LORA_ERR_ARG, "L_tc must be >= 1");
+            p->L_tc = (int)value;
+            return LORA_OK;
+        case LORA_OPT_RESERVE_TOKENS: {
+            if (value < 0) return fail(LORA_ERR_ARG, "reserve must be >= 0");
+            if (p->host_only) return LORA_OK;
+            DeviceGuard g(p->device);
+            const int64_t ks = ksplit_of(p->H_in, p->esz);
+            lora_status s = grow(p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(1, value * ks * LORA_MAX_RANK), false, "vbuf");
+            if (s == LORA_OK) s = grow(p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
+            return s;
+        }
+        default:
+            return fail(LORA_ERR_ARG, "unknown option " + std::to_string(option));
+    }
+}
+
+lora_status lora_pool_info(lora_pool* p, lora_pool_info_t* out) {
+    if (!p || !out) return fail(LORA_ERR_ARG, "pool/out is NULL");
+    std::memset(out, 0, sizeof(*out));
+    out->hidden_in = p->H_in;
+    out->hidden_out = p->H_out;
+    out->max_adapters = p->max_adapters;
+    out->max_total_rank = p->n_pages;
+    out->dtype = (int32_t)p->dtype;
+    out->elem_bytes = p->esz;
+    out->resident_adapters = (int32_t)p->table.size();
+    out->free_pages = p->free_pages;
+    out->tc_threshold = p->L_tc;
+    out->device = p->device;
+    out->pool_bytes = (int64_t)p->n_pages * (p->H_in + p->H_out) * p->esz;
+    int64_t rb = 0;
+    for (auto& kv : p->table) rb += (int64_t)kv.second.rank * (p->H_in + p->H_out) * p->esz;
+    out->resident_bytes = rb;
+    out->kernel_launches = p->launches;
+    return LORA_OK;
+}
+
+lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
+    if (!p || !o) return fail(LORA_ERR_ARG, "pool/out is NULL");
+    const Plan& pl = p->plan;
+    std::memset(o, 0, sizeof(*o));
+    o->T = pl.T; o->S = pl.S; o->G = pl.G; o->L_tc = pl.L_tc;
+    o->tok_seg = pl.tok_seg.data();
+    o->group_id = pl.group_id.data();
+    o->group_rank = pl.group_rank.data();
+    o->group_scale = pl.group_scale.data();
+    o->group_ntok = pl.group_ntok.data();
+    o->group_page_off = pl.group_page_off.data();
+    o->group_tok_off = pl.group_tok_off.data();
+    o->group_tokens = pl.group_tokens.data();
+    o->pages = pl.pages.data();
+    o->seg_kind = pl.seg_kind.data();
+    o->n_seg = pl.n_seg; o->max_rank = pl.max_rank; o->nseg_x_maxrank = pl.nseg_x_maxrank;
+    o->sum_rank_seg = pl.sum_rank_seg; o->sum_rank_groups = pl.sum_rank_groups; o->sum_rank_tokens = pl.sum_rank_tokens;
+    o->n_decode_units = pl.n_shrink + pl.n_expand;
+    o->n_prefill_tiles = pl.n_prefill_tiles;
+    return LORA_OK;
+}
+
+lora_status lora_debug_set_trace(lora_pool* p, void* dev_buf) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    p->trace = static_cast<unsigned long long*>(dev_buf);
+    return LORA_OK;
+}
+
+lora_status lora_debug_adapter_pages(lora_pool* p, int32_t id, int32_t* pages, int cap, int* rank) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    auto it = p->table.find(id);
+    if (it == p->table.end()) return fail(LORA_ERR_UNKNOWN_ADAPTER, "adapter " + std::to_string(id) + " is not loaded");
+    if (rank) *rank = it->second.rank;
+    if (pages)
+        for (int j = 0; j < it->second.rank && j < cap; ++j) pages[j] = it->second.pages[j];
+    return LORA_OK;
+}
+
+lora_status lora_debug_read_pages(lora_pool* p, int32_t id, void* A_out, void* B_out) {
+    if (!p || !A_out || !B_out) return fail(LORA_ERR_ARG, "pool/A_out/B_out is NULL");
+    if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "host-only pool has no device pages");
+    auto it = p->table.find(id);
+    if (it == p->table.end()) return fail(LORA_ERR_UNKNOWN_ADAPTER, "adapter " + std::to_string(id) + " is not loaded");
+    DeviceGuard g(p->device);
+    CUDA_TRY(cudaStreamSynchronize(p->side), "lora_debug_read_pages: sync");
+    const size_t ra = (size_t)p->H_in * p->esz, rb = (size_t)p->H_out * p->esz;
+    for (int j = 0; j < it->second.rank; ++j) {
+        CUDA_TRY(cudaMemcpy((char*)A_out + j * ra, p->dA + (size_t)it->second.pages[j] * ra, ra, cudaMemcpyDeviceToHost), "read A");
+        CUDA_TRY(cudaMemcpy((char*)B_out + j * rb, p->dB + (size_t)it->second.pages[j] * rb, rb, cudaMemcpyDeviceToHost), "read B");
+    }
+    return LORA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+"""Per-CTA timeline of decode applies replayed from a CUDA graph (lora_debug_set_trace).
+Builds N pools of one config (distinct adapter weights), captures a graph of N back-to-back
+applies (as in bench.py), replays it after an L2 flush and prints, per apply and kernel,
+when CTAs started, passed griddepcontrol.wait, had their data, and finished.
+usage: python scripts/trace_decode.py [c2|c5q|c5down] [n_pools]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2401_11240_b200 as L  # noqa: E402
+from workloads import gen  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "c2"
+NP = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+mk = {"c2": lambda tag: gen.config_c2(tag=tag), "c5q": lambda tag: gen.config_c5("q"),
+      "c5down": lambda tag: gen.config_c5("down")}[which]
+
+
+def tt(a, pin=False):
+    t = torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a)
+    return t.pin_memory() if pin else t
+
+
+pools, batches = [], []
+for i in range(NP):
+    b = mk(i)
+    pool = L.LoraPool(b.H_in, b.H_out, 64, b.dtype, max_total_rank=sum(a.rank for a in b.adapters))
+    for a in b.adapters:
+        pool.load_adapter(a.id, a.rank, tt(a.A, True), tt(a.B, True), a.scale)
+    pools.append(pool)
+    batches.append(b)
+b = batches[0]
+x = tt(b.x).cuda()
+ys = [tt(bb.y_in).cuda() for bb in batches]
+st = torch.cuda.Stream()
+with torch.cuda.stream(st):
+    for p, y in zip(pools, ys):
+        p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+torch.cuda.synchronize()
+md = pools[0].metadata()
+n_units = md["n_decode_units"]
+ks = -(-b.H_in // (4096 // (2 if b.dtype == "bf16" else 4)))
+n_shrink = int(sum(ks * -(-int(r) // 8) * -(-int(n) // 4) for r, n in zip(md["group_rank"], md["group_ntok"])))
+bufs = [torch.zeros(8 * n_units + 64, dtype=torch.int64, device="cuda") for _ in pools]
+for p, bf in zip(pools, bufs):
+    p.set_trace(bf)
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for p, y in zip(pools, ys):
+        p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+flush = torch.empty(512 * 2 ** 20, dtype=torch.int8, device="cuda")
+times = []
+for rep in range(3):
+    flush.zero_()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    g.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    times.append(e0.elapsed_time(e1) * 1e3)
+print("graph of %d applies: %.2f us per replay (%.2f us / apply), units/apply %d (shrink %d)" %
+      (NP, min(times), min(times) / NP, n_units, n_shrink))
+Us = [bf.cpu().numpy()[:8 * n_units].reshape(n_units, 8) for bf in bufs]
+t0 = min(U[:, 1].min() for U in Us)
+for i, U in enumerate(Us):
+    for name, S in (("S", U[:n_shrink]), ("E", U[n_shrink:])):
+        r = lambda col: (S[:, col] - t0) / 1e3  # noqa
+        print("apply %d %s: start %6.2f..%6.2f  wait-ok %6.2f..%6.2f  data %6.2f..%6.2f  done %6.2f..%6.2f"
+              % (i, name, r(1).min(), r(1).max(), r(2).min(), r(2).max(), r(3).min(), r(3).max(), r(5).min(),
+                 r(5).max()))
+U = np.concatenate([U[:n_shrink] for U in Us])
+for lab, a_, b_ in (("S start->wait", 1, 2), ("S wait->data", 2, 3), ("S data->done", 3, 5)):
+    d = (U[:, b_] - U[:, a_]) / 1e3
+    print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
+U = np.concatenate([U[n_shrink:] for U in Us])
+for lab, a_, b_ in (("E start->wait", 1, 2), ("E wait->data", 2, 3), ("E data->done", 3, 5)):
+    d = (U[:, b_] - U[:, a_]) / 1e3
+    print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))

@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path through the C ABI versus the fp64 oracle on the same seeded
+inputs (SURVEY.md §8(c) "GPU parity test matrix").  Tolerances are BASELINE.json's:
+rel-L2 <= 5e-3 (bf16 inputs, fp32 accumulation), <= 1e-5 (fp32); metadata bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from workloads import gen
+
+from gpu_util import TOL, from_torch, make_pool, rel_l2, run_gpu, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2401_11240_b200 as lib
+    return lib
+
+
+def _md_ref(batch, L_tc=64):
+    table = {}
+    alloc = O.PageAllocatorReplay(sum(a.rank for a in batch.adapters) + 1, len(batch.adapters) + 4)
+    for a in batch.adapters:
+        alloc.load(a.id, a.rank, a.scale)
+    return O.canonical_metadata(batch.seg_indptr, batch.adapter_ids, alloc.table, L_tc)
+
+
+def _check_md(md, ref):
+    for k in ("tok_seg", "group_id", "group_rank", "group_ntok", "group_page_off", "group_tok_off", "group_tokens",
+              "pages", "seg_kind"):
+        assert np.array_equal(md[k], ref[k]), k
+    assert np.array_equal(md["group_scale"].view(np.uint32), ref["group_scale"].view(np.uint32))
+    for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens"):
+        assert md[k] == ref[k], k
+
+
+@pytest.mark.parametrize("y_zero", [True, False], ids=["runA_delta", "runB_accumulate"])
+def test_c1_tiny_fp32(L, y_zero):
+    b = gen.config_c1(y_zero=y_zero)
+    y, md = run_gpu(b, L)
+    ref = O.delta_for_batch(b)
+    assert rel_l2(y, ref, "f32") <= TOL["f32"]
+    _check_md(md, _md_ref(b))
+
+
+@pytest.mark.parametrize("y_zero", [True, False], ids=["runA_delta", "runB_accumulate"])
+def test_c2_decode_bf16(L, y_zero):
+    b = gen.config_c2(y_zero=y_zero)
+    y, md = run_gpu(b, L)
+    ref = O.delta_for_batch(b, n_threads=8)
+    err = rel_l2(y, ref, "bf16")
+    assert err <= TOL["bf16"], err
+    _check_md(md, _md_ref(b))
+
+
+def test_c2_zipf_bf16(L):
+    b = gen.config_c2(zipf=True)
+    y, md = run_gpu(b, L)
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+    _check_md(md, _md_ref(b))
+
+
+def test_prefill_tiles_bf16_and_fp32(L):
+    for dtype in ("bf16", "f32"):
+        for y_zero in (True, False):
+            b = gen.config_c1_prefill_tiles(y_zero=y_zero, dtype=dtype)
+            y, md = run_gpu(b, L)
+            ref = O.delta_for_batch(b, n_threads=8)
+            assert rel_l2(y, ref, dtype) <= TOL[dtype], (dtype, y_zero)
+            _check_md(md, _md_ref(b))
+
+
+def test_c3_prefill_reduced(L):
+    """config 3 shape (4096, ranks 8..128) with 8 x 512-token segments, all tokens checked."""
+    b = gen.config_c3(n_seg=8)
+    y, md = run_gpu(b, L)
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+    _check_md(md, _md_ref(b))
+
+
+def test_c3_full_size_sampled(L):
+    """config 3 at full size (32 x 512 tokens): every token of the GPU result vs the oracle on a
+    sampled subset of tokens (the oracle computes them one by one)."""
+    b = gen.config_c3(y_zero=False)
+    y, md = run_gpu(b, L)
+    rng = np.random.default_rng(3)
+    mask = np.zeros(b.T, np.uint8)
+    mask[rng.choice(b.T, 96, replace=False)] = 1
+    mask[[0, 511, 512, b.T - 1]] = 1
+    ref = O.delta_for_batch(b, token_mask=mask, n_threads=8)
+    sel = mask.astype(bool)
+    assert rel_l2(y.reshape(b.T, -1)[sel], ref[sel], "bf16") <= TOL["bf16"]
+    _check_md(md, _md_ref(b))
+
+
+@pytest.mark.parametrize("proj", ["k", "q", "down"])
+def test_c5_70b_shapes_decode(L, proj):
+    b = gen.config_c5(proj, y_zero=False)
+    y, md = run_gpu(b, L)
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+def test_page_readback_p12(L):
+    for b in (gen.config_c1(), gen.config_c2()):
+        pool = make_pool(b, L)
+        for a in b.adapters:
+            A, B = pool.read_pages(a.id, a.rank)
+            assert np.array_equal(A, a.A) and np.array_equal(B, a.B)
+        pool.close()
+
+
+def test_no_adapter_rows_bitwise_untouched(L):
+    b = gen.config_c2(y_zero=False)
+    ids = b.adapter_ids.copy()
+    ids[::4] = -1
+    y, _ = run_gpu(b, L, adapter_ids=ids)
+    T = b.T
+    y = y.reshape(T, -1)
+    ref = O.delta(b.H_in, b.H_out, b.seg_indptr, ids,
+                  [(a.id, a.rank, a.scale, gen.storage_to_f64(a.A, "bf16"), gen.storage_to_f64(a.B, "bf16"))
+                   for a in b.adapters], gen.storage_to_f64(b.x, "bf16"), gen.storage_to_f64(b.y_in, "bf16"))
+    for i in range(len(ids)):
+        rows = slice(b.seg_indptr[i], b.seg_indptr[i + 1])
+        if ids[i] < 0:
+            assert np.array_equal(y[rows], b.y_in[rows])
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("which", ["A", "B"])
+def test_zero_adapter_p5(L, which):
+    for dtype_batch in (gen.config_c1(y_zero=False), gen.config_c2(y_zero=False)):
+        b = dtype_batch
+        for a in b.adapters:
+            if which == "A":
+                a.A = np.zeros_like(a.A)
+            else:
+                a.B = np.zeros_like(a.B)
+        y, _ = run_gpu(b, L)
+        yv = gen.storage_to_f64(y, b.dtype)
+        assert np.array_equal(yv, gen.storage_to_f64(b.y_in, b.dtype))
+
+
+def test_zero_padded_rank_p4(L):
+    """An adapter zero-padded from r to 2r gives the same delta within tolerance."""
+    b = gen.config_c2()
+    y1, _ = run_gpu(b, L)
+    for a in b.adapters:
+        a.A = np.concatenate([a.A, np.zeros_like(a.A)])
+        a.B = np.concatenate([a.B, np.zeros_like(a.B)])
+        a.rank *= 2
+    y2, _ = run_gpu(b, L)
+    ref = O.delta_for_batch(gen.config_c2(), n_threads=8)
+    assert rel_l2(y2, ref, "bf16") <= TOL["bf16"]
+    assert rel_l2(y2, gen.storage_to_f64(y1, "bf16").reshape(ref.shape), "bf16") <= TOL["bf16"]
+
+
+def test_segment_permutation_bitwise_p6(L):
+    b = gen.config_c2()
+    y, _ = run_gpu(b, L)
+    y = y.reshape(b.T, -1)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(b.S)
+    b2 = gen.config_c2()
+    b2.adapter_ids = b.adapter_ids[perm].copy()
+    b2.x = b.x[perm].copy()           # one-token segments: token index = segment index
+    b2.y_in = b.y_in[perm].copy()
+    y2, _ = run_gpu(b2, L)
+    assert np.array_equal(y2.reshape(b.T, -1), y[perm])
+
+
+def test_segment_split_merge_p7(L):
+    b = gen.config_c1_prefill_tiles()
+    ref = O.delta_for_batch(b, n_threads=8)
+    lens = np.diff(b.seg_indptr)
+    new_lens, new_ids = [], []
+    for ln, aid in zip(lens, b.adapter_ids):
+        if ln > 2:
+            new_lens += [1, ln - 1]
+            new_ids += [aid, aid]
+        else:
+            new_lens.append(ln)
+            new_ids.append(aid)
+    ip = gen.segments_to_indptr(new_lens)
+    y, _ = run_gpu(b, L, seg_indptr=ip, adapter_ids=np.array(new_ids, np.int32))
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+def test_determinism_repeat(L):
+    b = gen.config_c2(y_zero=False)
+    outs = [run_gpu(b, L)[0] for _ in range(3)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_randomized_sweep_p9(L):
+    rng = np.random.default_rng(77)
+    for trial in range(120):
+        dtype = "bf16" if trial % 3 else "f32"
+        vec = 8 if dtype == "bf16" else 4
+        H_in = int(rng.integers(1, 33)) * vec
+        H_out = int(rng.integers(1, 33)) * vec
+        b = gen.random_batch(1000 + trial, dtype, H_in, H_out, max_seg=64, max_rank=min(128, H_in, H_out),
+                             max_len=int(rng.choice([1, 4, 40, 300])), n_adapters=8, y_zero=bool(trial % 2))
+        if b.T == 0:
+            continue
+        y, md = run_gpu(b, L)
+        ref = O.delta_for_batch(b, n_threads=8)
+        assert rel_l2(y, ref, dtype) <= TOL[dtype], (trial, dtype, H_in, H_out)
+        _check_md(md, _md_ref(b))
+
+
+def test_empty_batches_are_noops(L):
+    import torch
+    b = gen.config_c1(y_zero=False)
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    y = to_torch(b.y_in, "cuda")
+    pool.apply(x, y, [0], [])
+    pool.apply(x, y, [0, 0, 0], [0, 1])
+    pool.apply(x, y, [0, 4], [-1])
+    torch.cuda.synchronize()
+    assert np.array_equal(from_torch(y, "f32"), b.y_in)
+    pool.close()
+
+
+def test_cuda_graph_capture_replay(L):
+    import torch
+    b = gen.config_c2()
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    y = torch.zeros((b.T, b.H_out), dtype=torch.int16, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=s)    # warm-up (scratch sizing)
+    torch.cuda.synchronize()
+    y.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=s)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(from_torch(y, "bf16"), ref, "bf16") <= TOL["bf16"]
+    pool.close()
+
+
+def test_async_load_then_apply_orders_on_event(L):
+    """lora_load_adapter returns before the copy lands; an apply issued right after must see
+    the adapter (the stream waits on the load's ready event)."""
+    import torch
+    b = gen.config_c2()
+    pool = L.LoraPool(b.H_in, b.H_out, 64, "bf16", max_total_rank=2048)
+    keep = []
+    for a in b.adapters:
+        A, B = to_torch(a.A, pin=True), to_torch(a.B, pin=True)
+        keep.append((A, B))
+        pool.load_adapter(a.id, a.rank, A, B, a.scale)
+    x = to_torch(b.x, "cuda")
+    y = torch.zeros((b.T, b.H_out), dtype=torch.int16, device="cuda")
+    s = torch.cuda.Stream()
+    pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=s)
+    s.synchronize()
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(from_torch(y, "bf16"), ref, "bf16") <= TOL["bf16"]
+    assert all(pool.adapter_ready(a.id) for a in b.adapters)
+    # unload half, load new adapters into the freed pages, apply again
+    for a in b.adapters[::2]:
+        pool.unload_adapter(a.id)
+    b2 = gen.config_c2(tag=7)
+    for a in b2.adapters[::2]:
+        A, B = to_torch(a.A, pin=True), to_torch(a.B, pin=True)
+        keep.append((A, B))
+        pool.load_adapter(a.id, a.rank, A, B, a.scale)
+    y.zero_()
+    pool.apply(to_torch(b2.x, "cuda"), y, b2.seg_indptr, b2.adapter_ids, stream=s)
+    s.synchronize()
+    mixed = gen.config_c2(tag=7)
+    mixed.adapters = [b2.adapters[i] if i % 2 == 0 else b.adapters[i] for i in range(32)]
+    ref2 = O.delta_for_batch(mixed, n_threads=8)
+    assert rel_l2(from_torch(y, "bf16"), ref2, "bf16") <= TOL["bf16"]
+    pool.close()
+
+
+def test_unknown_adapter_on_apply_has_no_side_effect(L):
+    import torch
+    b = gen.config_c1(y_zero=False)
+    pool = make_pool(b, L, extra_pages=8)
+    x = to_torch(b.x, "cuda")
+    y = to_torch(b.y_in, "cuda")
+    with pytest.raises(L.LoraError) as ei:
+        pool.apply(x, y, [0, 1, 2], [0, 42])
+    assert ei.value.name == "LORA_ERR_UNKNOWN_ADAPTER"
+    torch.cuda.synchronize()
+    assert np.array_equal(from_torch(y, "f32"), b.y_in)
+    with pytest.raises(L.LoraError) as ei:
+        pool.load_adapter(9, 2, np.zeros((2, 64), np.float32), np.zeros((2, 64), np.float32), 1.0)
+    assert ei.value.name == "LORA_ERR_NOT_PINNED"
+    pool.close()
