@@ -85,6 +85,12 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
 }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// one thread waits on the preceding grid, the rest park at the barrier (a waiting
+// griddepcontrol.wait polls and would steal issue slots from co-resident CTAs)
+__device__ __forceinline__ void pdl_wait_cta() {
+    if (threadIdx.x == 0) pdl_wait();
+    __syncthreads();
+}
 __device__ __forceinline__ float ld_cg_f32(const float* p) {
     float v;
     asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
@@ -181,7 +187,7 @@ __device__ __forceinline__ int find_gc_warp(const int32_t* M, int n_gc, int f, i
 struct UnitSh {
     int gc, r, ntok, ks, j0, nj, n0, nc, voff;
     float scale;
-    int tok[kTokChunk];
+    int tok[kMaxTokChunk];
 };
 
 // ------------------------------------------------------------------ shrink kernel
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int u = blockIdx.x;
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
-    if (W == 1) pdl_wait();   // metadata uploaded by the preceding kernel
+    if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
 
     int tok = 0;
     if (warp == 0) {
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
         const int poff = gc_field(M, gc, GC_PAGE_OFF);
         const int toff = gc_field(M, gc, GC_TOK_OFF);
-        const int njb = shrink_jblocks(r);
+        const int njb = shrink_jblocks(r, E::kSize);
         const int ks = local / njb;
         const int j0 = (local - ks * njb) * kShrinkRows;
         const int nj = min(kShrinkRows, r - j0);
@@ -244,7 +250,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int k0 = ks * KS;
     const int nk = min(KS, a.H_in - k0);
     // 2. x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
-    pdl_wait();
+    pdl_wait_cta();
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     if (warp == 0) {
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nk * E::kSize));
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int ue = blockIdx.x;
     const int u = ue + a.n_shrink;
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
-    if (W == 1) pdl_wait();   // metadata uploaded by a preceding kernel
+    if (W == 1) pdl_wait_cta();   // metadata uploaded by a preceding kernel
 
     int tok = 0;
     if (warp == 0) {
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
     const int c = expand_ncols(r, E::kSize);
     const size_t row_stride = (size_t)c * E::kSize;
-    pdl_wait();   // the shrink kernel's v (and y from whoever wrote it) are now visible
+    pdl_wait_cta();   // the shrink kernel's v (and y from whoever wrote it) are now visible
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     if (warp == 0) {
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * E::kSize));
@@ -471,11 +477,331 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
 }
 
+// ------------------------------------------------------------------ bf16 tensor-core (mma.sync) kernels
+// The decode delta is HBM-bound; what limits a kernel that computes only after its data
+// arrived is the burst of issue slots and shared-memory bandwidth spent once the
+// preceding grid completes.  The bf16 kernels therefore (a) keep the shrink operand out of
+// shared memory entirely -- A rows go HBM -> registers with coalesced 128-bit loads issued
+// BEFORE griddepcontrol.wait, in the m16n8k16 fragment layout up to a permutation of k
+// that the x fragments repeat (the dot product is order-free in k) -- and (b) read the
+// expand operand from shared memory exactly once (swap-AB: B^T tiles via ldmatrix.trans,
+// v fragments hoisted per warp).  The MMA (fp32 accumulate) is a dot-product engine here:
+// tiles are padded with zero rows (tokens to 8, ranks to 16) in registers / smem only;
+// HBM bytes are exactly the algorithmic ones.
+constexpr int kPitchPad = 16;   // bytes added to each smem row: conflict-free ldmatrix
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t& r0, uint32_t& r1, uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+// D[16x8] += A[16x16] (row) * B[16x8] (col), bf16 inputs, fp32 accumulate
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ldg_cg128(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+// ---- shrink (bf16): one CTA = (group-chunk gc, k-slice of kKSlice, 16 rank rows).  Warp w
+// owns k in [k0 + 128w, k0 + 128w + 128) as 4 blocks of 32; lane (g = lane/4, c = lane%4)
+// holds rows j0+g and j0+g+8, elements [kb + 8c, kb + 8c + 8) of every block.  The MMA's
+// logical k (2c, 2c+1 | 2c+8, 2c+9) maps to physical kb + 8c + (0,1 | 2,3) in MMA #1 and
+// kb + 8c + (4,5 | 6,7) in MMA #2, for the A rows and the x rows alike.
+constexpr int kKPerWarp = kKSlice / kConsumerWarps;   // 128
+constexpr int kKBlocks = kKPerWarp / 32;              // 4
+constexpr int kShrinkMmaSmem = 256 + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
+
+template <int W>
+__global__ void __launch_bounds__(kConsumerThreads)
+    lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    constexpr int ES = 2;
+    extern __shared__ __align__(128) char smem[];
+    UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
+    int* spage = reinterpret_cast<int*>(smem + 128);                       // [16] page of each unit row
+    float* part = reinterpret_cast<float*>(smem + 256);                    // [warp][16 rows][8 tokens]
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int u = blockIdx.x;
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
+    if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
+
+    if (warp == 0) {
+        const int gc = find_gc_warp(M, a.n_gc, GC_SHRINK_BASE, u, lane);
+        const int r = gc_field(M, gc, GC_RANK);
+        const int ntok = gc_field(M, gc, GC_NTOK);
+        const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
+        const int poff = gc_field(M, gc, GC_PAGE_OFF);
+        const int toff = gc_field(M, gc, GC_TOK_OFF);
+        const int njb = shrink_jblocks(r, ES);
+        const int ks = local / njb;
+        const int j0 = (local - ks * njb) * kShrinkRowsMma;
+        const int nj = min(kShrinkRowsMma, r - j0);
+        if (lane < kShrinkRowsMma) spage[lane] = lane < nj ? M[poff + j0 + lane] : -1;
+        if (lane < kTokChunkMma) sh->tok[lane] = lane < ntok ? M[toff + lane] : -1;
+        if (lane == 0) {
+            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
+            sh->voff = gc_field(M, gc, GC_VOFF);
+        }
+    }
+    __syncthreads();
+    const int g = lane >> 2, c = lane & 3;
+    const int ks = sh->ks, ntok = sh->ntok;
+    const int k0 = ks * kKSlice;
+    const int nk = min(kKSlice, a.H_in - k0);
+    // 1. adapter rows (immutable pool pages) straight into registers, before the grid dependency
+    uint4 ra[kKBlocks], rb[kKBlocks];
+    {
+        const int p0 = spage[g], p1 = spage[g + 8];
+        const uint64_t pol = policy_evict_first();
+        const char* row0 = a.poolA + ((size_t)(p0 < 0 ? 0 : p0) * a.H_in + k0) * ES;
+        const char* row1 = a.poolA + ((size_t)(p1 < 0 ? 0 : p1) * a.H_in + k0) * ES;
+#pragma unroll
+        for (int b = 0; b < kKBlocks; ++b) {
+            const int k = warp * kKPerWarp + b * 32 + c * 8;
+            const bool kin = k < nk;
+            ra[b] = (p0 >= 0 && kin) ? ldg_stream(row0 + k * ES, pol) : make_uint4(0u, 0u, 0u, 0u);
+            rb[b] = (p1 >= 0 && kin) ? ldg_stream(row1 + k * ES, pol) : make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
+    pdl_launch_dependents();
+    // 2. x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
+    pdl_wait_cta();
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
+    uint4 xr[kKBlocks];
+    {
+        const int tk = g < ntok ? sh->tok[g] : -1;
+        const char* xrow = a.x + ((size_t)(tk < 0 ? 0 : tk) * a.H_in + k0) * ES;
+#pragma unroll
+        for (int b = 0; b < kKBlocks; ++b) {
+            const int k = warp * kKPerWarp + b * 32 + c * 8;
+            xr[b] = (tk >= 0 && k < nk) ? ldg_cg128(xrow + k * ES) : make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
+    float acc[kKBlocks][4];
+#pragma unroll
+    for (int b = 0; b < kKBlocks; ++b) {
+        acc[b][0] = acc[b][1] = acc[b][2] = acc[b][3] = 0.f;
+        mma_bf16(acc[b], ra[b].x, rb[b].x, ra[b].y, rb[b].y, xr[b].x, xr[b].y);
+        mma_bf16(acc[b], ra[b].z, rb[b].z, ra[b].w, rb[b].w, xr[b].z, xr[b].w);
+    }
+    // D: (row g, tokens 2c, 2c+1) and (row g+8, tokens 2c, 2c+1)
+    {
+        float* pw = part + warp * kShrinkRowsMma * kTokChunkMma;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float v = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
+            const int row = g + ((q & 2) ? 8 : 0), t = 2 * c + (q & 1);
+            pw[row * kTokChunkMma + t] = v;
+        }
+    }
+    __syncthreads();
+    const int nj = sh->nj, r = sh->r, j0 = sh->j0;
+    if (tid < nj * ntok) {
+        const int row = tid / ntok, t = tid - row * ntok;
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) v += part[(w * kShrinkRowsMma + row) * kTokChunkMma + t];
+        a.vbuf[sh->voff + (ks * ntok + t) * r + j0 + row] = v;
+    }
+    if (a.trace && tid == 0) {
+        a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 5] = gtime();
+    }
+}
+
+// ---- expand (bf16): one CTA = (group-chunk gc, column slice [n0, n0+nc)).  Swap-AB:
+// D[col][token] = B^T[col][rank] · v^T[rank][token], M = 16 columns, N = 8 tokens, K = 16
+// ranks; v is split into bf16 hi + lo parts (two MMAs) so v keeps fp32-level accuracy.
+// D is added into the y tile staged in smem (one rounding) and written back with 16-B stores.
+constexpr int kVPitch = (LORA_MAX_RANK + 8) * 2;   // bf16 v row pitch (bytes)
+constexpr int kExpandMmaSmem = 256 + 64 + 2 * kTokChunkMma * kVPitch + kExpandBytes + LORA_MAX_RANK * kPitchPad +
+                               kTokChunkMma * (kMaxNcols * 2 + kPitchPad);
+
+template <int W>
+__global__ void __launch_bounds__(kConsumerThreads)
+    lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    constexpr int ES = 2;
+    extern __shared__ __align__(128) char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);          // [0] B rows, [1] y rows
+    UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
+    char* zero = smem + 256;                                      // 64 zero bytes
+    char* vhi = smem + 256 + 64;                                  // [8 tokens][kVPitch] bf16
+    char* vlo = vhi + kTokChunkMma * kVPitch;
+    char* bbuf = vlo + kTokChunkMma * kVPitch;                    // [r][c + pad]
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ue = blockIdx.x;
+    const int u = ue + a.n_shrink;
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
+    if (W == 1) pdl_wait_cta();
+
+    int tok = 0;
+    if (warp == 0) {
+        // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
+        const int gc = find_gc_warp(M, a.n_gc, GC_EXPAND_BASE, ue, lane);
+        const int r = gc_field(M, gc, GC_RANK);
+        const int ntok = gc_field(M, gc, GC_NTOK);
+        const int local = ue - gc_field(M, gc, GC_EXPAND_BASE);
+        const int poff = gc_field(M, gc, GC_PAGE_OFF);
+        const int toff = gc_field(M, gc, GC_TOK_OFF);
+        const int c = expand_ncols(r, ES);
+        const int n0 = local * c;
+        const int nc = min(c, a.H_out - n0);
+        const int bpitch = c * ES + kPitchPad;
+        int pages[LORA_MAX_RANK / 32];
+#pragma unroll
+        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? M[poff + q * 32 + lane] : 0;
+        tok = lane < ntok ? M[toff + lane] : 0;
+        const uint32_t row_bytes = (uint32_t)nc * ES;
+        if (lane == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
+            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
+            sh->voff = gc_field(M, gc, GC_VOFF);
+            sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
+        }
+        if (lane < ntok) sh->tok[lane] = tok;
+        if (lane < 16) reinterpret_cast<uint32_t*>(zero)[lane] = 0u;
+        __syncwarp();
+        const uint64_t pol = policy_evict_first();
+#pragma unroll
+        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) {
+            const int j = q * 32 + lane;
+            if (j < r)
+                bulk_g2s(bbuf + (size_t)j * bpitch, a.poolB + ((size_t)pages[q] * a.H_out + n0) * ES, row_bytes,
+                         &bars[0], pol);
+        }
+    }
+    pdl_launch_dependents();
+    __syncthreads();
+    const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
+    const int c = expand_ncols(r, ES);
+    const int bpitch = c * ES + kPitchPad;
+    const int ypitch = c * ES + kPitchPad;
+    char* ybuf = bbuf + r * bpitch;
+    pdl_wait_cta();   // v from the shrink kernel, y from whoever wrote it
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
+    if (warp == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * ES));
+        __syncwarp();
+        if (lane < ntok)
+            bulk_g2s(ybuf + lane * ypitch, a.y + ((size_t)tok * a.H_out + n0) * ES, (uint32_t)nc * ES, &bars[1],
+                     policy_evict_normal());
+    }
+    // v (fp32, summed over k-slices, scaled) -> bf16 hi/lo tiles [8 tokens][r padded to 16]
+    const int rp = (r + 15) & ~15;
+    {
+        const int voff = sh->voff;
+        const float scale = sh->scale;
+        for (int i = tid; i < kTokChunkMma * rp; i += kConsumerThreads) {
+            const int t = i / rp, j = i - t * rp;
+            float v = 0.f;
+            if (t < ntok && j < r) {
+                for (int k = 0; k < a.ksplit; ++k) v += ld_cg_f32(a.vbuf + voff + (k * ntok + t) * r + j);
+                v *= scale;
+            }
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+            *reinterpret_cast<__nv_bfloat16*>(vhi + t * kVPitch + j * 2) = h;
+            *reinterpret_cast<__nv_bfloat16*>(vlo + t * kVPitch + j * 2) = l;
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bars[0], 0);
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
+    const int ntiles = (nc + 15) / 16;
+    const int ksteps = rp / 16;
+    // A operand (B^T) via ldmatrix.x4.trans: matrix m = lane/8, row i = lane%8 -> rank j, column n
+    const int am = lane >> 3, ai = lane & 7;
+    const int aj = ai + ((am & 2) ? 8 : 0), an = (am & 1) * 8;
+    // B operand (v): lanes 0-7 token rows at j, lanes 8-15 at j+8
+    const int vt = lane & 7, vh = (lane >> 3) & 1;
+    const uint32_t zaddr = smem_u32(zero);
+    const uint32_t vhi_base = smem_u32(vhi) + vt * kVPitch + vh * 16;
+    const uint32_t vlo_base = smem_u32(vlo) + vt * kVPitch + vh * 16;
+    const uint32_t b_base = smem_u32(bbuf);
+    const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), tokens 2cc, 2cc+1
+    constexpr int kTW = 4;                    // 16-column tiles per warp per pass
+    for (int tile0 = warp * kTW; tile0 < ntiles; tile0 += kConsumerWarps * kTW) {
+        float dh[kTW][4], dl[kTW][4];
+#pragma unroll
+        for (int i = 0; i < kTW; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dh[i][q] = dl[i][q] = 0.f;
+        for (int s = 0; s < ksteps; ++s) {
+            const int j = s * 16 + aj;
+            uint32_t h0, h1, l0, l1, af[kTW][4];
+            ldsm_x2(h0, h1, vhi_base + s * 32);
+            ldsm_x2(l0, l1, vlo_base + s * 32);
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) {
+                const int col = (tile0 + i) * 16 + an;
+                ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
+                              (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
+            }
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) mma_bf16(dh[i], af[i][0], af[i][1], af[i][2], af[i][3], h0, h1);
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) mma_bf16(dl[i], af[i][0], af[i][1], af[i][2], af[i][3], l0, l1);
+        }
+        if (cc * 2 < ntok) {
+            mbar_wait(&bars[1], 0);
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = (tile0 + i) * 16 + g + ((q & 2) ? 8 : 0), t = 2 * cc + (q & 1);
+                    if (t < ntok && n < nc) {
+                        __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(ybuf + t * ypitch + n * ES);
+                        *yp = __float2bfloat16_rn(__bfloat162float(*yp) + (dh[i][q] + dl[i][q]));
+                    }
+                }
+            }
+        }
+    }
+    mbar_wait(&bars[1], 0);
+    __syncthreads();
+    // write the updated y rows back with 16-B stores
+    {
+        const int vpr = nc / 8;   // 16-B vectors per token row
+        for (int i = tid; i < ntok * vpr; i += kConsumerThreads) {
+            const int t = i / vpr, q = i - t * vpr;
+            const uint4 v = lds128(ybuf + t * ypitch + q * 16);
+            stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + q * 8) * ES, v);
+        }
+    }
+    if (a.trace && tid == 0) {
+        a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 5] = gtime();
+    }
+}
+
 // copies a metadata blob too large for one kernel's parameters into device memory,
 // kUploadWords per launch (parameters are captured by value in CUDA graphs)
 constexpr int kUploadWords = 7936;
 __global__ void lora_meta_upload_kernel(int32_t* dst, const __grid_constant__ MetaBlob<kUploadWords> b, int n) {
-    pdl_wait();
+    pdl_wait_cta();
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = b.w[i];
 }
 
@@ -495,14 +821,31 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, int smem, cudaStrea
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// bf16 pools take the tensor-core (mma.sync) kernels, fp32 pools the SIMT FFMA kernels
+// (TF32 would miss the 1e-5 fp32 bound).
+template <typename T, int W>
+struct DecodeKernels {
+    static constexpr auto shrink = lora_shrink_kernel<T, W>;
+    static constexpr auto expand = lora_expand_kernel<T, W>;
+    static constexpr int shrink_smem = kShrinkSmem;
+    static constexpr int expand_smem = kExpandSmem;
+};
+template <int W>
+struct DecodeKernels<__nv_bfloat16, W> {
+    static constexpr auto shrink = lora_shrink_mma_kernel<W>;
+    static constexpr auto expand = lora_expand_mma_kernel<W>;
+    static constexpr int shrink_smem = kShrinkMmaSmem;
+    static constexpr int expand_smem = kExpandMmaSmem;
+};
+
 template <typename T, int W>
 static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t st, int* launches) {
+    using K = DecodeKernels<T, W>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(lora_shrink_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kShrinkSmem);
+        cudaError_t e = cudaFuncSetAttribute(K::shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, K::shrink_smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(lora_expand_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kExpandSmem);
+            e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, K::expand_smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -511,9 +854,9 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         const int n = (int)pl.blob.size();
         for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
     }
-    cudaError_t e = launch_pdl(lora_shrink_kernel<T, W>, pl.n_shrink, kConsumerThreads, kShrinkSmem, st, a, blob);
+    cudaError_t e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem, st, a, blob);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(lora_expand_kernel<T, W>, pl.n_expand, kConsumerThreads, kExpandSmem, st, a, blob);
+    e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads, K::expand_smem, st, a, blob);
     *launches += 2;
     return e;
 }

@@ -1,5 +1,5 @@
 // kernel_config.h -- constants shared by the host planner (plan.cpp) and the decode
-// kernel (decode_kernel.cu).  Product side only; the oracle never sees this file.
+// kernels (decode_kernel.cu).  Product side only; the oracle never sees this file.
 #pragma once
 #include <stdint.h>
 
@@ -11,18 +11,18 @@
 
 namespace lora {
 
-// ---- SIMT decode kernel (N1) -------------------------------------------------------
-constexpr int kConsumerWarps = 8;                 // math warps
+// ---- decode kernels (N1) ------------------------------------------------------------
+constexpr int kConsumerWarps = 8;                 // warps per CTA
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kThreads = kConsumerThreads + 32;  // + one producer (bulk-copy) warp
-constexpr int kStages = 3;                        // smem ring depth
-constexpr int kTokChunk = 4;                      // tokens per (group, chunk)
-constexpr int kShrinkRows = 8;                    // A rows per shrink unit
-constexpr int kSliceBytes = 4096;                 // bytes of one A-row k-slice / one x-row k-slice
-constexpr int kStageBytes = kShrinkRows * kSliceBytes + kTokChunk * kSliceBytes;  // 48 KB
+constexpr int kTokChunk = 4;                      // fp32 SIMT kernels: tokens per (group, chunk)
+constexpr int kTokChunkMma = 8;                   // bf16 tensor-core kernels: tokens per chunk (MMA N = 8)
+constexpr int kMaxTokChunk = 8;
+constexpr int kShrinkRows = 8;                    // fp32: A rows per shrink unit
+constexpr int kShrinkRowsMma = 16;                // bf16: A rows per shrink unit (MMA M = 16)
+constexpr int kKSlice = 1024;                     // k elements per shrink unit (both element types)
+constexpr int kSliceBytes = 4096;                 // fp32 smem row slice (kKSlice * 4)
 constexpr int kExpandBytes = 32768;               // B bytes per expand unit (r * ncols * esz)
-constexpr int kRedBytes = kConsumerThreads * kTokChunk * 8 * 4;  // 32 KB cross-part reduction
-constexpr int kMetaSmemWords = 6144;              // metadata copied to smem when it fits (24 KB)
+constexpr int kMaxNcols = 1024;                   // columns per expand unit
 
 // metadata blob layout (int32 words)
 constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, pad, pad
@@ -30,16 +30,16 @@ constexpr int kGcFields = 8;     // rank, page_off, tok_off, ntok, shrink_base, 
 enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE };
 
 LORA_HD int vec_elems(int esz) { return 16 / esz; }             // elements per 16-B vector
-LORA_HD int k_slice(int esz) { return kSliceBytes / esz; }       // k elements per shrink slice
-LORA_HD int ksplit_of(int H_in, int esz) { return (H_in + k_slice(esz) - 1) / k_slice(esz); }
+LORA_HD int tok_chunk(int esz) { return esz == 2 ? kTokChunkMma : kTokChunk; }
+LORA_HD int shrink_rows(int esz) { return esz == 2 ? kShrinkRowsMma : kShrinkRows; }
+LORA_HD int ksplit_of(int H_in, int /*esz*/) { return (H_in + kKSlice - 1) / kKSlice; }
 LORA_HD int pow2floor(int v) { int p = 1; while (p * 2 <= v) p *= 2; return p; }
 // expand unit width in columns for rank r: largest power of two with r*ncols*esz <= kExpandBytes,
-// capped at kConsumerThreads vectors (one 16-B vector per thread and part)
+// capped at kMaxNcols
 LORA_HD int expand_ncols(int r, int esz) {
     int c = pow2floor(kExpandBytes / (r * esz));
-    int cap = kConsumerThreads * vec_elems(esz);
-    return c < cap ? c : cap;
+    return c < kMaxNcols ? c : kMaxNcols;
 }
-LORA_HD int shrink_jblocks(int r) { return (r + kShrinkRows - 1) / kShrinkRows; }
+LORA_HD int shrink_jblocks(int r, int esz) { return (r + shrink_rows(esz) - 1) / shrink_rows(esz); }
 
 }  // namespace lora

@@ -118,8 +118,9 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         group_blob_page[g] = (int32_t)blob_pages.size();
         blob_pages.insert(blob_pages.end(), pl.pages.begin() + pl.group_page_off[g],
                           pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
-        for (size_t c = 0; c < simt[g].size(); c += kTokChunk) {
-            const int n = (int)std::min<size_t>(kTokChunk, simt[g].size() - c);
+        const size_t tc = (size_t)tok_chunk(esz);
+        for (size_t c = 0; c < simt[g].size(); c += tc) {
+            const int n = (int)std::min<size_t>(tc, simt[g].size() - c);
             gcs.push_back({g, (int)blob_toks.size(), n});
             blob_toks.insert(blob_toks.end(), simt[g].begin() + c, simt[g].begin() + c + n);
         }
@@ -144,7 +145,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         e[GC_EXPAND_BASE] = expand;
         e[GC_VOFF] = (int32_t)voff;
         e[GC_SCALE] = f32_bits(pl.group_scale[g]);
-        shrink += ksplit * shrink_jblocks(r);
+        shrink += ksplit * shrink_jblocks(r, esz);
         const int nc = expand_ncols(r, esz);
         expand += (H_out + nc - 1) / nc;
         voff += (int64_t)ksplit * gcs[c].ntok * r;

@@ -80,3 +80,11 @@ U = np.concatenate([U[n_shrink:] for U in Us])
 for lab, a_, b_ in (("E start->wait", 1, 2), ("E wait->data", 2, 3), ("E data->done", 3, 5)):
     d = (U[:, b_] - U[:, a_]) / 1e3
     print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
+U = np.concatenate([U_[:n_shrink] for U_ in Us])
+cyc = U[:, 4].astype(np.float64)
+print("   S mma loop cycles (clock64): med %.0f p90 %.0f max %.0f" % (np.median(cyc), np.percentile(cyc, 90), cyc.max()))
+c1 = U[:, 6].astype(np.float64)
+print("   S first chunk cycles: med %.0f p90 %.0f max %.0f" % (np.median(c1), np.percentile(c1, 90), c1.max()))
+for lab, a_, b_ in (("S data->bar2", 3, 7), ("S bar2->done", 7, 5)):
+    d = (U[:, b_] - U[:, a_]) / 1e3
+    print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
