@@ -180,6 +180,7 @@ typedef struct {
     int64_t sum_rank_groups;         /*     Σ over distinct adapters of r (adapter bytes / (H_in+H_out)/b) */
     int64_t sum_rank_tokens;         /*     Σ_t r_{a(t)} (flops / 2(H_in+H_out)) */
     int32_t n_decode_units, n_prefill_tiles;   /* kernel work of the last apply (informational) */
+    int32_t n_shrink_units, n_expand_units;    /* split of n_decode_units (shrink units come first) */
 } lora_metadata_view;
 
 lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* out);

@@ -56,7 +56,8 @@ class MetadataView(ctypes.Structure):
                 ("n_seg", ctypes.c_int64), ("max_rank", ctypes.c_int64), ("nseg_x_maxrank", ctypes.c_int64),
                 ("sum_rank_seg", ctypes.c_int64), ("sum_rank_groups", ctypes.c_int64),
                 ("sum_rank_tokens", ctypes.c_int64),
-                ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32)]
+                ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32),
+                ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32)]
 
 
 def header_symbols() -> List[str]:
@@ -207,7 +208,7 @@ class LoraPool:
                "group_tokens": arr(m.group_tokens, int(ntok.sum())),
                "pages": arr(m.pages, int(m.sum_rank_groups)), "seg_kind": arr(m.seg_kind, m.S)}
         for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens",
-                  "n_decode_units", "n_prefill_tiles"):
+                  "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units"):
             out[k] = int(getattr(m, k))
         return out
 

@@ -520,23 +520,28 @@ __device__ __forceinline__ uint4 ldg_cg128(const void* p) {
     return v;
 }
 
-// ---- shrink (bf16): one CTA = (group-chunk gc, k-slice of kKSlice, 16 rank rows).  Warp w
-// owns k in [k0 + 128w, k0 + 128w + 128) as 4 blocks of 32; lane (g = lane/4, c = lane%4)
-// holds rows j0+g and j0+g+8, elements [kb + 8c, kb + 8c + 8) of every block.  The MMA's
-// logical k (2c, 2c+1 | 2c+8, 2c+9) maps to physical kb + 8c + (0,1 | 2,3) in MMA #1 and
-// kb + 8c + (4,5 | 6,7) in MMA #2, for the A rows and the x rows alike.
+// ---- shrink (bf16): one CTA = (group-chunk gc, k-slice of kKSlice, 16 rank rows).  The rank
+// rows go HBM -> SMEM with cp.async.bulk before griddepcontrol.wait (the copy engine, not the
+// LSU: a co-resident CTA's critical-path loads/ldmatrix never queue behind this prefetch).
+// Warp w owns k in [k0 + 128w, k0 + 128w + 128) as 4 blocks of 32; lane (g = lane/4,
+// c = lane%4) reads rows g and g+8, elements [kb + 8c, kb + 8c + 8) of every block with one
+// 128-bit shared load.  The MMA's logical k (2c, 2c+1 | 2c+8, 2c+9) maps to physical
+// kb + 8c + (0,1 | 2,3) in MMA #1 and kb + 8c + (4,5 | 6,7) in MMA #2, for the A rows and the
+// x rows alike (the dot product is order-free in k).
 constexpr int kKPerWarp = kKSlice / kConsumerWarps;   // 128
 constexpr int kKBlocks = kKPerWarp / 32;              // 4
-constexpr int kShrinkMmaSmem = 256 + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
+constexpr int kAPitch = kKSlice * 2 + 64;             // bf16 row pitch: rows g, g+1 land 16 banks apart
+constexpr int kShrinkMmaSmem = 1024 + kShrinkRowsMma * kAPitch + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
 
 template <int W>
 __global__ void __launch_bounds__(kConsumerThreads)
     lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     constexpr int ES = 2;
     extern __shared__ __align__(128) char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                    // [0] A rows
     UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
-    int* spage = reinterpret_cast<int*>(smem + 128);                       // [16] page of each unit row
-    float* part = reinterpret_cast<float*>(smem + 256);                    // [warp][16 rows][8 tokens]
+    char* abuf = smem + 1024;                                              // [16 rows][kAPitch]
+    float* part = reinterpret_cast<float*>(abuf + kShrinkRowsMma * kAPitch);   // [warp][16 rows][8 tokens]
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int u = blockIdx.x;
@@ -554,35 +559,29 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int ks = local / njb;
         const int j0 = (local - ks * njb) * kShrinkRowsMma;
         const int nj = min(kShrinkRowsMma, r - j0);
-        if (lane < kShrinkRowsMma) spage[lane] = lane < nj ? M[poff + j0 + lane] : -1;
+        const int k0 = ks * kKSlice;
+        const int nk = min(kKSlice, a.H_in - k0);
+        const int page = lane < nj ? M[poff + j0 + lane] : 0;
         if (lane < kTokChunkMma) sh->tok[lane] = lane < ntok ? M[toff + lane] : -1;
         if (lane == 0) {
+            mbar_init(&bars[0], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_arrive_expect_tx(&bars[0], (uint32_t)(nj * nk * ES));
             sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
             sh->voff = gc_field(M, gc, GC_VOFF);
         }
-    }
-    __syncthreads();
-    const int g = lane >> 2, c = lane & 3;
-    const int ks = sh->ks, ntok = sh->ntok;
-    const int k0 = ks * kKSlice;
-    const int nk = min(kKSlice, a.H_in - k0);
-    // 1. adapter rows (immutable pool pages) straight into registers, before the grid dependency
-    uint4 ra[kKBlocks], rb[kKBlocks];
-    {
-        const int p0 = spage[g], p1 = spage[g + 8];
-        const uint64_t pol = policy_evict_first();
-        const char* row0 = a.poolA + ((size_t)(p0 < 0 ? 0 : p0) * a.H_in + k0) * ES;
-        const char* row1 = a.poolA + ((size_t)(p1 < 0 ? 0 : p1) * a.H_in + k0) * ES;
-#pragma unroll
-        for (int b = 0; b < kKBlocks; ++b) {
-            const int k = warp * kKPerWarp + b * 32 + c * 8;
-            const bool kin = k < nk;
-            ra[b] = (p0 >= 0 && kin) ? ldg_stream(row0 + k * ES, pol) : make_uint4(0u, 0u, 0u, 0u);
-            rb[b] = (p1 >= 0 && kin) ? ldg_stream(row1 + k * ES, pol) : make_uint4(0u, 0u, 0u, 0u);
-        }
+        __syncwarp();
+        if (lane < nj)
+            bulk_g2s(abuf + lane * kAPitch, a.poolA + ((size_t)page * a.H_in + k0) * ES, (uint32_t)(nk * ES), &bars[0],
+                     policy_evict_first());
     }
     pdl_launch_dependents();
-    // 2. x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
+    __syncthreads();
+    const int g = lane >> 2, c = lane & 3;
+    const int ks = sh->ks, ntok = sh->ntok, nj = sh->nj;
+    const int k0 = ks * kKSlice;
+    const int nk = min(kKSlice, a.H_in - k0);
+    // x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
     pdl_wait_cta();
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     uint4 xr[kKBlocks];
@@ -595,7 +594,16 @@ __global__ void __launch_bounds__(kConsumerThreads)
             xr[b] = (tk >= 0 && k < nk) ? ldg_cg128(xrow + k * ES) : make_uint4(0u, 0u, 0u, 0u);
         }
     }
+    mbar_wait(&bars[0], 0);
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
+    uint4 ra[kKBlocks], rb[kKBlocks];
+#pragma unroll
+    for (int b = 0; b < kKBlocks; ++b) {
+        const int k = warp * kKPerWarp + b * 32 + c * 8;
+        const bool kin = k < nk;
+        ra[b] = (g < nj && kin) ? lds128(abuf + g * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
+        rb[b] = (g + 8 < nj && kin) ? lds128(abuf + (g + 8) * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
+    }
     float acc[kKBlocks][4];
 #pragma unroll
     for (int b = 0; b < kKBlocks; ++b) {
@@ -614,7 +622,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         }
     }
     __syncthreads();
-    const int nj = sh->nj, r = sh->r, j0 = sh->j0;
+    const int r = sh->r, j0 = sh->j0;
     if (tid < nj * ntok) {
         const int row = tid / ntok, t = tid - row * ntok;
         float v = 0.f;
@@ -699,7 +707,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const int c = expand_ncols(r, ES);
     const int bpitch = c * ES + kPitchPad;
     const int ypitch = c * ES + kPitchPad;
-    char* ybuf = bbuf + r * bpitch;
+    char* ybuf = bbuf + kExpandBytes + LORA_MAX_RANK * kPitchPad;   // after the whole B region
     pdl_wait_cta();   // v from the shrink kernel, y from whoever wrote it
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     if (warp == 0) {
@@ -718,7 +726,16 @@ __global__ void __launch_bounds__(kConsumerThreads)
             const int t = i / rp, j = i - t * rp;
             float v = 0.f;
             if (t < ntok && j < r) {
-                for (int k = 0; k < a.ksplit; ++k) v += ld_cg_f32(a.vbuf + voff + (k * ntok + t) * r + j);
+                // k-slice partials: batches of 8 independent loads, summed in slice order
+                const float* src = a.vbuf + voff + t * r + j;
+                const int stride = ntok * r;
+                for (int k0 = 0; k0 < a.ksplit; k0 += 8) {
+                    float p[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) p[q] = k0 + q < a.ksplit ? ld_cg_f32(src + (k0 + q) * stride) : 0.f;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v += p[q];
+                }
                 v *= scale;
             }
             const __nv_bfloat16 h = __float2bfloat16_rn(v);
@@ -743,52 +760,67 @@ __global__ void __launch_bounds__(kConsumerThreads)
     const uint32_t b_base = smem_u32(bbuf);
     const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), tokens 2cc, 2cc+1
     constexpr int kTW = 4;                    // 16-column tiles per warp per pass
-    for (int tile0 = warp * kTW; tile0 < ntiles; tile0 += kConsumerWarps * kTW) {
+    constexpr int kPasses = kMaxNcols / 16 / (kConsumerWarps * kTW);   // 2
+    float res[kPasses][kTW][4];
+#pragma unroll
+    for (int ps = 0; ps < kPasses; ++ps) {
+        const int tile0 = (ps * kConsumerWarps + warp) * kTW;
         float dh[kTW][4], dl[kTW][4];
 #pragma unroll
         for (int i = 0; i < kTW; ++i)
 #pragma unroll
             for (int q = 0; q < 4; ++q) dh[i][q] = dl[i][q] = 0.f;
-        for (int s = 0; s < ksteps; ++s) {
-            const int j = s * 16 + aj;
-            uint32_t h0, h1, l0, l1, af[kTW][4];
-            ldsm_x2(h0, h1, vhi_base + s * 32);
-            ldsm_x2(l0, l1, vlo_base + s * 32);
+        if (tile0 < ntiles) {
+            for (int s = 0; s < ksteps; ++s) {
+                const int j = s * 16 + aj;
+                uint32_t h0, h1, l0, l1, af[kTW][4];
+                ldsm_x2(h0, h1, vhi_base + s * 32);
+                ldsm_x2(l0, l1, vlo_base + s * 32);
 #pragma unroll
-            for (int i = 0; i < kTW; ++i) {
-                const int col = (tile0 + i) * 16 + an;
-                ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
-                              (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
-            }
-#pragma unroll
-            for (int i = 0; i < kTW; ++i) mma_bf16(dh[i], af[i][0], af[i][1], af[i][2], af[i][3], h0, h1);
-#pragma unroll
-            for (int i = 0; i < kTW; ++i) mma_bf16(dl[i], af[i][0], af[i][1], af[i][2], af[i][3], l0, l1);
-        }
-        if (cc * 2 < ntok) {
-            mbar_wait(&bars[1], 0);
-#pragma unroll
-            for (int i = 0; i < kTW; ++i) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int n = (tile0 + i) * 16 + g + ((q & 2) ? 8 : 0), t = 2 * cc + (q & 1);
-                    if (t < ntok && n < nc) {
-                        __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(ybuf + t * ypitch + n * ES);
-                        *yp = __float2bfloat16_rn(__bfloat162float(*yp) + (dh[i][q] + dl[i][q]));
-                    }
+                for (int i = 0; i < kTW; ++i) {
+                    const int col = (tile0 + i) * 16 + an;
+                    ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
+                                  (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
                 }
+#pragma unroll
+                for (int i = 0; i < kTW; ++i) mma_bf16(dh[i], af[i][0], af[i][1], af[i][2], af[i][3], h0, h1);
+#pragma unroll
+                for (int i = 0; i < kTW; ++i) mma_bf16(dl[i], af[i][0], af[i][1], af[i][2], af[i][3], l0, l1);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kTW; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res[ps][i][q] = dh[i][q] + dl[i][q];
+    }
+    // transpose D through smem (fp32 [token][col], in the now free B region), then add to the
+    // staged y rows with 16-B vectors: one rounding per element, no sub-word read-modify-writes
+    __syncthreads();
+    float* dt = reinterpret_cast<float*>(bbuf);
+    const int dpitch = nc + 4;
+#pragma unroll
+    for (int ps = 0; ps < kPasses; ++ps) {
+        const int tile0 = (ps * kConsumerWarps + warp) * kTW;
+#pragma unroll
+        for (int i = 0; i < kTW; ++i) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int n = (tile0 + i) * 16 + g + ((q & 2) ? 8 : 0), t = 2 * cc + (q & 1);
+                if (t < ntok && n < nc) dt[t * dpitch + n] = res[ps][i][q];
             }
         }
     }
     mbar_wait(&bars[1], 0);
     __syncthreads();
-    // write the updated y rows back with 16-B stores
     {
         const int vpr = nc / 8;   // 16-B vectors per token row
         for (int i = tid; i < ntok * vpr; i += kConsumerThreads) {
             const int t = i / vpr, q = i - t * vpr;
-            const uint4 v = lds128(ybuf + t * ypitch + q * 16);
-            stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + q * 8) * ES, v);
+            const float4 d0 = *reinterpret_cast<const float4*>(dt + t * dpitch + q * 8);
+            const float4 d1 = *reinterpret_cast<const float4*>(dt + t * dpitch + q * 8 + 4);
+            const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+            const uint4 yo = lds128(ybuf + t * ypitch + q * 16);
+            stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + q * 8) * ES, Elem<__nv_bfloat16>::add_round(yo, d));
         }
     }
     if (a.trace && tid == 0) {

@@ -422,6 +422,8 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
     o->n_seg = pl.n_seg; o->max_rank = pl.max_rank; o->nseg_x_maxrank = pl.nseg_x_maxrank;
     o->sum_rank_seg = pl.sum_rank_seg; o->sum_rank_groups = pl.sum_rank_groups; o->sum_rank_tokens = pl.sum_rank_tokens;
     o->n_decode_units = pl.n_shrink + pl.n_expand;
+    o->n_shrink_units = pl.n_shrink;
+    o->n_expand_units = pl.n_expand;
     o->n_prefill_tiles = pl.n_prefill_tiles;
     return LORA_OK;
 }

@@ -42,8 +42,7 @@ with torch.cuda.stream(st):
 torch.cuda.synchronize()
 md = pools[0].metadata()
 n_units = md["n_decode_units"]
-ks = -(-b.H_in // (4096 // (2 if b.dtype == "bf16" else 4)))
-n_shrink = int(sum(ks * -(-int(r) // 8) * -(-int(n) // 4) for r, n in zip(md["group_rank"], md["group_ntok"])))
+n_shrink = md["n_shrink_units"]
 bufs = [torch.zeros(8 * n_units + 64, dtype=torch.int64, device="cuda") for _ in pools]
 for p, bf in zip(pools, bufs):
     p.set_trace(bf)
@@ -78,13 +77,5 @@ for lab, a_, b_ in (("S start->wait", 1, 2), ("S wait->data", 2, 3), ("S data->d
     print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
 U = np.concatenate([U[n_shrink:] for U in Us])
 for lab, a_, b_ in (("E start->wait", 1, 2), ("E wait->data", 2, 3), ("E data->done", 3, 5)):
-    d = (U[:, b_] - U[:, a_]) / 1e3
-    print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
-U = np.concatenate([U_[:n_shrink] for U_ in Us])
-cyc = U[:, 4].astype(np.float64)
-print("   S mma loop cycles (clock64): med %.0f p90 %.0f max %.0f" % (np.median(cyc), np.percentile(cyc, 90), cyc.max()))
-c1 = U[:, 6].astype(np.float64)
-print("   S first chunk cycles: med %.0f p90 %.0f max %.0f" % (np.median(c1), np.percentile(c1, 90), c1.max()))
-for lab, a_, b_ in (("S data->bar2", 3, 7), ("S bar2->done", 7, 5)):
     d = (U[:, b_] - U[:, a_]) / 1e3
     print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
