@@ -94,18 +94,50 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     // ---- kernel work ----
     // tokens of the SIMT path per group (ascending), and tensor-core segments
     std::vector<std::vector<int32_t>> simt(G);
-    for (int i = 0; i < S; ++i) {
-        if (seg_group[i] < 0) continue;
-        if (tc_enabled && pl.seg_kind[i] == LORA_KIND_PREFILL) {
-            pl.prefill.push_back({ip[i], ip[i + 1] - ip[i], seg_group[i]});
-            pl.n_prefill_tiles += (ip[i + 1] - ip[i] + 127) / 128;
+    // tensor-core routing: PREFILL segments of rank <= kPfMaxRank while the tile records and
+    // page lists fit the kernel-parameter blob; everything else takes the decode kernels
+    std::vector<uint8_t> on_tc(S, 0);
+    if (tc_enabled) {
+        std::vector<int32_t> group_pf_off(G, -1);
+        std::vector<int32_t> pages_words;
+        int tiles = 0;
+        for (int i = 0; i < S; ++i) {
+            const int g = seg_group[i];
+            if (g < 0 || pl.seg_kind[i] != LORA_KIND_PREFILL || pl.group_rank[g] > kPfMaxRank) continue;
+            const int len = ip[i + 1] - ip[i];
+            const int nt = (len + 127) / 128;
+            const int extra_pages = group_pf_off[g] < 0 ? pl.group_rank[g] : 0;
+            if ((tiles + nt) * 8 + (int)pages_words.size() + extra_pages > kPfMaxBlobWords) continue;
+            if (group_pf_off[g] < 0) {
+                group_pf_off[g] = (int32_t)pages_words.size();
+                pages_words.insert(pages_words.end(), pl.pages.begin() + pl.group_page_off[g],
+                                   pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
+            }
+            on_tc[i] = 1;
+            tiles += nt;
+            pl.prefill.push_back({ip[i], len, g});
         }
+        pl.n_pf_tiles = tiles;
+        pl.n_prefill_tiles = tiles;
+        pl.pf_blob.assign((size_t)tiles * 8 + pages_words.size(), 0);
+        int tix = 0;
+        for (const PrefillSeg& sg : pl.prefill) {
+            for (int t0 = 0; t0 < sg.len; t0 += 128) {
+                int32_t* rec = pl.pf_blob.data() + (size_t)tix * 8;
+                rec[0] = sg.tok0 + t0;
+                rec[1] = std::min(128, sg.len - t0);
+                rec[2] = pl.group_rank[sg.group];
+                rec[3] = tiles * 8 + group_pf_off[sg.group];
+                rec[4] = f32_bits(pl.group_scale[sg.group]);
+                ++tix;
+            }
+        }
+        std::copy(pages_words.begin(), pages_words.end(), pl.pf_blob.begin() + (size_t)tiles * 8);
     }
     for (int t = 0; t < T; ++t) {
         const int i = pl.tok_seg[t];
         const int g = seg_group[i];
-        if (g < 0) continue;
-        if (tc_enabled && pl.seg_kind[i] == LORA_KIND_PREFILL) continue;
+        if (g < 0 || on_tc[i]) continue;
         simt[g].push_back(t);
     }
     const int ksplit = ksplit_of(H_in, esz);

@@ -41,7 +41,9 @@ struct Plan {
     int64_t vbuf_floats = 0;
     // ---- tcgen05 prefill work (N2) ----
     std::vector<PrefillSeg> prefill;
-    int32_t n_prefill_tiles = 0;
+    int32_t n_prefill_tiles = 0;     // == n_pf_tiles (128-token tiles on the tensor-core path)
+    std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] tile records {tok0, nvalid, rank, page_off, scale_bits}, then pages
+    int32_t n_pf_tiles = 0;
 };
 
 // Builds `plan`.  tc_enabled=false routes every token through the SIMT kernel.
@@ -64,9 +66,11 @@ struct DecodeLaunch {
 struct PrefillLaunch {
     const void* x;
     void* y;
-    const void* poolA;
-    const void* poolB;
-    int H_in, H_out, num_sms;
+    const void* tm_a;      // 128-B CUtensorMap of the A pages (gather4 box {64, 1})
+    const void* tm_b;      // 128-B CUtensorMap of the B pages
+    const int32_t* meta_dev;
+    unsigned long long* trace;
+    int T, H_in, H_out, zero_page, num_sms;
 };
 }  // namespace lora
 
@@ -76,5 +80,8 @@ namespace lora {
 int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
 int launch_prefill(const Plan& pl, const PrefillLaunch& L, lora_cuda_stream st, int* launches);
 bool prefill_supported(int H_in, int H_out, int esz);
+int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);
+constexpr int kPfMaxRank = 128;        // tensor-core prefill path handles ranks up to this
+constexpr int kPfMaxBlobWords = 7680;
 
 }  // namespace lora

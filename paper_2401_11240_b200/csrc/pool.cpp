@@ -34,8 +34,11 @@ struct lora_pool {
     lora_dtype dtype = LORA_BF16;
     unsigned flags = 0;
     bool host_only = false;
-    char* dA = nullptr;                  // [n_pages][H_in]
-    char* dB = nullptr;                  // [n_pages][H_out]
+    char* dA = nullptr;                  // [n_pages + 1][H_in]  (row n_pages: all-zero page)
+    char* dB = nullptr;                  // [n_pages + 1][H_out]
+    bool tc_prefill = false;             // tensor-core prefill path available for this pool
+    alignas(64) unsigned char tm_a[128]; // TMA maps of the page arrays (gather4 boxes {64, 1})
+    alignas(64) unsigned char tm_b[128];
     std::vector<uint8_t> page_used;
     int free_pages = 0;
     AdapterTable table;
@@ -142,8 +145,14 @@ lora_status lora_pool_create_ex(int hidden_in, int hidden_out, int max_adapters,
     if (!p->host_only) {
         cudaError_t e = cudaGetDevice(&p->device);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device);
-        if (e == cudaSuccess) e = cudaMalloc((void**)&p->dA, (size_t)p->n_pages * hidden_in * esz);
-        if (e == cudaSuccess) e = cudaMalloc((void**)&p->dB, (size_t)p->n_pages * hidden_out * esz);
+        if (e == cudaSuccess) e = cudaMalloc((void**)&p->dA, (size_t)(p->n_pages + 1) * hidden_in * esz);
+        if (e == cudaSuccess) e = cudaMalloc((void**)&p->dB, (size_t)(p->n_pages + 1) * hidden_out * esz);
+        if (e == cudaSuccess) e = cudaMemset(p->dA + (size_t)p->n_pages * hidden_in * esz, 0, (size_t)hidden_in * esz);
+        if (e == cudaSuccess) e = cudaMemset(p->dB + (size_t)p->n_pages * hidden_out * esz, 0, (size_t)hidden_out * esz);
+        if (e == cudaSuccess && prefill_supported(hidden_in, hidden_out, esz)) {
+            p->tc_prefill = make_tmap_bf16(p->tm_a, p->dA, p->n_pages + 1, hidden_in, 1) == 0 &&
+                            make_tmap_bf16(p->tm_b, p->dB, p->n_pages + 1, hidden_out, 1) == 0;
+        }
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->unload_fence, cudaEventDisableTiming);
         if (e != cudaSuccess) {
@@ -282,7 +291,7 @@ lora_status lora_adapter_ready(lora_pool* p, int32_t id, int* ready) {
 lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* adapter_ids, int num_segments) {
     if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
     std::string err;
-    const bool tc = !p->host_only ? prefill_supported(p->H_in, p->H_out, p->esz) : p->esz == 2;
+    const bool tc = !p->host_only ? p->tc_prefill : prefill_supported(p->H_in, p->H_out, p->esz);
     lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
                                p->L_tc, tc, p->table, err);
     if (s != LORA_OK) return fail(s, err);
@@ -319,12 +328,13 @@ lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: pending CUDA error");
     }
     std::string err;
-    const bool tc = prefill_supported(p->H_in, p->H_out, p->esz);
+    const bool tc = p->tc_prefill;
     lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
                                tc, p->table, err);
     if (s != LORA_OK) return fail(s, err);
     const Plan& pl = p->plan;
     if (pl.G == 0) return LORA_OK;
+    if (pl.n_gc == 0 && pl.n_pf_tiles == 0) return LORA_OK;
 
     // order after in-flight loads of the adapters this batch reads
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -351,8 +361,8 @@ lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
-    if (!pl.prefill.empty()) {
-        PrefillLaunch L{x, y, p->dA, p->dB, p->H_in, p->H_out, p->num_sms};
+    if (pl.n_pf_tiles > 0) {
+        PrefillLaunch L{x, y, p->tm_a, p->tm_b, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
         cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
     }

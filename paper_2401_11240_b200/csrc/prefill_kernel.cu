@@ -1,14 +1,437 @@
-// prefill_kernel.cu -- N2: tensor-core (tcgen05) path for long prefill segments.
-// Placeholder until the tcgen05 kernel lands: prefill_supported() returns false, so the
-// planner routes every token through the SIMT kernel (N1), which is exact for any length.
+// prefill_kernel.cu -- N2: the LoRA delta of long prefill segments on the 5th-gen tensor
+// cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// For a segment of tokens [t0, t0+len) on adapter g (rank r <= 128), per 128-token tile:
+//     V[t][j]  = s_g · Σ_k X[t][k] · A_g[k][j]      shrink  D1[128 x r16] in TMEM  (Eq. 1)
+//     Y[t][n] += Σ_j V[t][j] · B_g[j][n]            expand  D2[128 x 128] in TMEM, per 128-column tile
+//
+// * X tiles arrive by TMA (2D tiled, SWIZZLE_128B); the adapter's rank rows are gathered from
+//   the paged pool by TMA tile::gather4 (4 page rows per instruction) straight into the
+//   canonical UMMA smem layouts: A rows K-major for the shrink, B rows MN-major for the
+//   expand (no transposition anywhere).  Rank padding to a multiple of 16 uses the pool's
+//   all-zero page, in SMEM only.
+// * One elected thread issues tcgen05.mma (M=128, kind::f16, bf16 inputs, fp32 accumulate);
+//   tcgen05.commit releases ring slots and signals the epilogue.
+// * The epilogue (4 warps = the 128 TMEM lanes) reads D1, applies s_g, splits v into bf16
+//   hi + lo parts written as the expand's A operand (K-major SW128) -- so the expand keeps
+//   v's fp32 accuracy with two MMAs per k-step -- then, per expand tile, reads D2 and adds it
+//   to y with one rounding.  D2 is double-buffered in TMEM so the epilogue of tile n overlaps
+//   the MMAs of tile n+1.
+// The path is HBM-bound (x read once, y read+written once per tile; adapter rows mostly
+// from L2), so tensor-pipe utilisation is reported next to the HBM roofline.
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
+#include <cstring>
+
+#include "kernel_config.h"
 #include "plan.h"
 
 namespace lora {
 
-bool prefill_supported(int, int, int) { return false; }
+constexpr int kPfThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
+constexpr int kPfStages = 4;
+constexpr int kPfStageBytes = 32768;   // X chunk 16 KB + A chunk <= 16 KB, or one B tile (<= 32 KB)
+constexpr int kPfVBytes = 128 * 128 * 2;   // one V part (hi or lo): 128 tokens x r16 <= 128, bf16
+constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 256;
+constexpr int kPfNTile = 128;          // expand columns per tile
+constexpr int kPfTileWords = 8;        // per-tile record in the metadata blob
 
-int launch_prefill(const Plan&, const PrefillLaunch&, cudaStream_t, int*) { return (int)cudaErrorNotSupported; }
+struct PrefillArgs {
+    CUtensorMap tm_x;   // x [T][H_in], box {64, 128}, SW128
+    CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1}, SW128 (gather4)
+    CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1}, SW128 (gather4)
+    char* y;
+    const int32_t* meta_global;
+    unsigned long long* trace;
+    int H_in, H_out, n_tiles, zero_page;
+};
+
+template <int W>
+struct PfBlob {
+    int32_t w[W];
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t pf_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void pf_bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void pf_arrive_tx(uint32_t bar, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void pf_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void pf_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_PFW:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LAB_PFW;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tm), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm, int col, int r0, int r1, int r2, int r3,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5, %6}], [%7];" ::"r"(dst),
+        "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1 (sm_100)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor: D fp32, A/B bf16, M=128, N=n, B K-major (0) or MN-major (1)
+__device__ __forceinline__ uint32_t umma_idesc(int n, int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 32 lanes x 32 consecutive fp32 columns: thread i of the warp gets lane (base_lane + i), cols [col, col+32)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ unsigned long long pf_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ------------------------------------------------------------------ kernel
+template <int W>
+__global__ void __launch_bounds__(kPfThreads, 1)
+    lora_prefill_tc_kernel(const __grid_constant__ PrefillArgs a, const __grid_constant__ PfBlob<W> blob) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = pf_smem(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;      // SW128 atoms need 1 KB alignment
+    uint8_t* gbase = smem_raw + (base - raw);
+    const uint32_t ring = base;                         // kPfStages x 32 KB
+    const uint32_t vhi = base + kPfStages * kPfStageBytes;
+    const uint32_t vlo = vhi + kPfVBytes;
+    uint8_t* gv = gbase + kPfStages * kPfStageBytes;   // generic pointer to vhi
+    const uint32_t bars = vlo + kPfVBytes;              // 14 mbarriers + tmem slot
+    auto full = [&](int s) { return bars + 8u * s; };
+    auto empty = [&](int s) { return bars + 8u * (kPfStages + s); };
+    const uint32_t d1_full = bars + 8u * (2 * kPfStages);
+    const uint32_t v_ready = d1_full + 8u;
+    auto tm_full = [&](int b) { return v_ready + 8u + 8u * b; };
+    auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfStages + 6) - base));
+
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile = blockIdx.x;
+    const int32_t* rec = M + tile * kPfTileWords;
+    const int tok0 = rec[0], nvalid = rec[1], r = rec[2], poff = rec[3];
+    const float scale = __int_as_float(rec[4]);
+    const int rp = (r + 15) & ~15;                      // rank padded to the MMA N/K granularity
+    const int nkc = a.H_in / 64;                        // shrink K chunks
+    const int nnt = a.H_out / kPfNTile;                 // expand column tiles
+    if (a.trace && tid == 0) a.trace[(size_t)tile * 4 + 0] = pf_gtime();
+
+    if (tid == 0) {
+        for (int s = 0; s < kPfStages; ++s) {
+            pf_bar_init(full(s), 1);
+            pf_bar_init(empty(s), 1);
+        }
+        pf_bar_init(d1_full, 1);
+        pf_bar_init(v_ready, 128);
+        for (int b = 0; b < 2; ++b) {
+            pf_bar_init(tm_full(b), 1);
+            pf_bar_init(tm_empty(b), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {   // TMEM: D1 at columns [0,128), D2 buffers at [128,256) and [256,384)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(pf_smem(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    // x and y may be produced by the preceding kernel in the stream
+    if (tid == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        int stage = 0;
+        uint32_t phase = 0;
+        const int ngr = rp / 4;   // gather4 groups (rank rows, padded with the zero page)
+        // each lane owns <= 1 gather4 group per chunk (rp <= 128 -> ngr <= 32)
+        int pg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = lane * 4 + q;
+            pg[q] = j < r ? M[poff + j] : a.zero_page;
+        }
+        for (int kc = 0; kc < nkc; ++kc) {
+            pf_wait(empty(stage), phase ^ 1u);
+            const uint32_t sb = ring + stage * kPfStageBytes;
+            if (lane == 0) {
+                pf_arrive_tx(full(stage), (uint32_t)(128 * 128 + rp * 128));
+                tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
+            }
+            __syncwarp();
+            if (lane < ngr)
+                tma_gather4(sb + 16384 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
+            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
+        }
+        // expand: B rows of each 128-column tile, MN-major SW128 atoms (8 rank rows x 64 cols);
+        // atom (kg, ng) at (ng * rp/8 + kg) * 1 KB; a gather4 fills 4 rows of one atom
+        for (int nt = 0; nt < nnt; ++nt) {
+            pf_wait(empty(stage), phase ^ 1u);
+            const uint32_t sb = ring + stage * kPfStageBytes;
+            if (lane == 0) pf_arrive_tx(full(stage), (uint32_t)(rp * kPfNTile * 2));
+            __syncwarp();
+            if (lane < ngr) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t dst = sb + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
+                    tma_gather4(dst, &a.tm_b, nt * kPfNTile + h * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
+                }
+            }
+            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (one elected lane) =====================
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t id1 = umma_idesc(rp, 0);
+        const uint32_t id2 = umma_idesc(kPfNTile, 1);
+        for (int kc = 0; kc < nkc; ++kc) {
+            pf_wait(full(stage), phase);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t sb = ring + stage * kPfStageBytes;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_f16(tmem, umma_desc(sb + kk * 32, 16, 1024), umma_desc(sb + 16384 + kk * 32, 16, 1024), id1,
+                             (kc | kk) != 0);
+                umma_commit(empty(stage));
+                if (kc == nkc - 1) umma_commit(d1_full);
+            }
+            __syncwarp();
+            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
+        }
+        pf_wait(v_ready, 0);
+        tc_fence_after();
+        const int ksteps = rp / 16;
+        for (int nt = 0; nt < nnt; ++nt) {
+            const int b = nt & 1;
+            pf_wait(tm_empty(b), ((nt >> 1) & 1) ^ 1u);
+            pf_wait(full(stage), phase);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t sb = ring + stage * kPfStageBytes;
+                const uint32_t dcol = tmem + 128u + 128u * b;
+                const uint32_t lbo = (uint32_t)(rp / 8) * 1024u;   // MN-direction atom stride
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    const uint32_t voff = (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u;
+                    const uint64_t bd = umma_desc(sb + (uint32_t)ks * 2048u, lbo, 1024);
+                    umma_f16(dcol, umma_desc(vhi + voff, 16, 1024), bd, id2, ks != 0);
+                    umma_f16(dcol, umma_desc(vlo + voff, 16, 1024), bd, id2, 1);
+                }
+                umma_commit(empty(stage));
+                umma_commit(tm_full(b));
+            }
+            __syncwarp();
+            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
+        }
+    } else {
+        // ===================== epilogue: warps 2..5 -> TMEM lanes 32*(warp%4) .. +32 =====================
+        const int sub = warp & 3;
+        const int row = sub * 32 + lane;   // token row within the tile
+        const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
+        // ---- v = s * D1 -> bf16 hi/lo, K-major SW128: atom kk = cols [64kk, 64kk+64), row at
+        //      (row/8)*1024 + (row%8)*128 inside the 16 KB atom, 16-B chunk c stored at c ^ (row%8)
+        pf_wait(d1_full, 0);
+        tc_fence_after();
+        for (int c0 = 0; c0 < rp; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {   // four 16-B chunks of 8 columns
+                uint32_t hw[4], lw[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float f0 = v[q * 8 + 2 * e] * scale, f1 = v[q * 8 + 2 * e + 1] * scale;
+                    __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+                    const float2 hf = __bfloat1622float2(h);
+                    __nv_bfloat162 l = __floats2bfloat162_rn(f0 - hf.x, f1 - hf.y);
+                    hw[e] = *reinterpret_cast<uint32_t*>(&h);
+                    lw[e] = *reinterpret_cast<uint32_t*>(&l);
+                }
+                const int col = c0 + q * 8;
+                const int kk = col >> 6, chunk = (col & 63) >> 3;
+                const uint32_t off = (uint32_t)kk * 16384u + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
+                                     (uint32_t)((chunk ^ (row & 7)) * 16);
+                *reinterpret_cast<uint4*>(gv + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                *reinterpret_cast<uint4*>(gv + kPfVBytes + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
+        tc_fence_before();
+        pf_arrive(v_ready);
+        // ---- per expand tile: y[row][n0 .. n0+128) += D2 (one rounding), straight to global
+        const bool valid = row < nvalid;
+        char* yrow = a.y + ((size_t)(tok0 + row) * a.H_out) * 2;
+        for (int nt = 0; nt < nnt; ++nt) {
+            const int b = nt & 1;
+            pf_wait(tm_full(b), (nt >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < kPfNTile; c0 += 32) {
+                float d[32];
+                tmem_ld32(tmem + lane_addr + 128u + 128u * b + (uint32_t)c0, d);
+                if (valid) {
+                    uint4* yp = reinterpret_cast<uint4*>(yrow + (size_t)(nt * kPfNTile + c0) * 2);
+                    uint4 yv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) yv[q] = yp[q];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t w[4] = {yv[q].x, yv[q].y, yv[q].z, yv[q].w};
+                        uint32_t o[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float lo = __uint_as_float(w[e] << 16) + d[q * 8 + 2 * e];
+                            const float hi = __uint_as_float(w[e] & 0xffff0000u) + d[q * 8 + 2 * e + 1];
+                            __nv_bfloat162 hb = __floats2bfloat162_rn(lo, hi);
+                            o[e] = *reinterpret_cast<uint32_t*>(&hb);
+                        }
+                        yp[q] = make_uint4(o[0], o[1], o[2], o[3]);
+                    }
+                }
+            }
+            tc_fence_before();
+            pf_arrive(tm_empty(b));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+    if (a.trace && tid == 0) a.trace[(size_t)tile * 4 + 1] = pf_gtime();
+}
+
+// ------------------------------------------------------------------ host side
+bool prefill_supported(int H_in, int H_out, int esz) {
+    return esz == 2 && H_in % 64 == 0 && H_out % kPfNTile == 0 && H_in >= 64;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2D bf16 tensor map [rows][cols] with a {64, box_rows} SWIZZLE_128B box
+int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return (int)cudaErrorNotSupported;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap*>(tm_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+template <int W>
+static cudaError_t launch_pf(const PrefillArgs& a, const Plan& pl, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(lora_prefill_tc_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kPfSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    PfBlob<W> blob;
+    if (W > 1)
+        for (size_t i = 0; i < pl.pf_blob.size(); ++i) blob.w[i] = pl.pf_blob[i];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.n_pf_tiles);
+    cfg.blockDim = dim3(kPfThreads);
+    cfg.dynamicSmemBytes = kPfSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, lora_prefill_tc_kernel<W>, a, blob);
+}
+
+int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int* launches) {
+    PrefillArgs a;
+    std::memset(&a, 0, sizeof(a));
+    int e = make_tmap_bf16(&a.tm_x, L.x, L.T, L.H_in, 128);
+    if (e) return e;
+    std::memcpy(&a.tm_a, L.tm_a, sizeof(CUtensorMap));
+    std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
+    a.y = static_cast<char*>(L.y);
+    a.meta_global = L.meta_dev;
+    a.trace = L.trace;
+    a.H_in = L.H_in;
+    a.H_out = L.H_out;
+    a.n_tiles = pl.n_pf_tiles;
+    a.zero_page = L.zero_page;
+    const size_t n = pl.pf_blob.size();
+    cudaError_t r;
+    if (n <= 2048) r = launch_pf<2048>(a, pl, st);
+    else if (n <= 7680) r = launch_pf<7680>(a, pl, st);
+    else return (int)cudaErrorNotSupported;   // planner caps prefill work to the parameter blob
+    *launches += 1;
+    return (int)r;
+}
 
 }  // namespace lora
