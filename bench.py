@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=2)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--prefill-layers", type=int, default=2,
+                    help="layers of the c3 prefill measurement reported in the 'prefill' object (0 = skip)")
+    ap.add_argument("--prefill-steps", type=int, default=20)
     return ap.parse_args()
 
 
@@ -244,6 +247,77 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------- prefill (config 3) measurement
+def bench_prefill(L, layers: int, steps: int, dev, hbm_peak: float, tc_peak: float, world_rank: int = 0):
+    """c3: 32 requests x 512-token prompts over 32 adapters (ranks 8..128), 4096->4096 bf16, per
+    layer q/k/v/o on distinct pools; x/y (256 MB per layer) >> L2.  Returns the 'prefill' object."""
+    import torch
+    T, n_seg, seg_len = 32 * 512, 32, 512
+    ranks = {i: gen.C3_RANKS[i % 5] for i in range(n_seg)}
+    ip = gen.segments_to_indptr([seg_len] * n_seg)
+    ids = np.arange(n_seg, dtype=np.int32)
+    pools = []
+    with cf.ThreadPoolExecutor(max_workers=min(16, len(os.sched_getaffinity(0)))) as ex:
+        futs = [ex.submit(lambda lp: [gen.make_adapter(gen.BASE_SEED + 2, 1000 + lp + 10000 * world_rank, a, ranks[a],
+                                                       H, H, "bf16") for a in range(n_seg)], lp)
+                for lp in range(layers * len(PROJS))]
+        for f in futs:
+            ads = f.result()
+            pool = L.LoraPool(H, H, n_seg, "bf16", max_total_rank=sum(a.rank for a in ads))
+            for a in ads:
+                pool.load_adapter(a.id, a.rank, torch.from_numpy(a.A.view(np.int16)).pin_memory(),
+                                  torch.from_numpy(a.B.view(np.int16)).pin_memory(), a.scale)
+            pools.append(pool)
+    torch.cuda.synchronize()
+    for pool in pools:
+        pool.release_host_buffers()
+    g = torch.Generator(device="cpu").manual_seed(gen.BASE_SEED + 200 + world_rank)
+    xs = [torch.randn(T, H, generator=g).to(torch.bfloat16).to(dev) for _ in range(2)]
+    ys = [torch.zeros(T, H, dtype=torch.bfloat16, device=dev) for _ in pools]
+    st = torch.cuda.Stream(device=dev)
+
+    def step():
+        for i, (pool, y) in enumerate(zip(pools, ys)):
+            pool.apply(xs[0 if i % 4 < 3 else 1], y, ip, ids, stream=st)
+
+    with torch.cuda.stream(st):
+        step()
+    torch.cuda.synchronize()
+    md = pools[0].metadata()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    with torch.cuda.stream(st):
+        for _ in range(steps):
+            graph.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_apply = e0.elapsed_time(e1) / steps / len(pools)
+    sum_r = sum(ranks.values())
+    bytes_apply = 2 * (sum_r * 2 * H + T * H + 2 * T * H)
+    flops_apply = sum(2 * ranks[i] * seg_len * 2 * H for i in range(n_seg))
+    gbs = bytes_apply / (ms_apply * 1e-3) / 1e9
+    tfs = flops_apply / (ms_apply * 1e-3) / 1e12
+    out = {"workload": "c3: Llama-2-7B prefill 32 x 512 tokens, 32 adapters ranks 8..128, 4096->4096 bf16, "
+                       "%d layers x q/k/v/o" % layers,
+           "value": round(T / (ms_apply * 1e-3), 1), "unit": "tokens/s per projection apply",
+           "ms_per_apply": round(ms_apply, 5), "tensor_core_tiles_per_apply": md["n_prefill_tiles"],
+           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                        "frac": round(gbs / hbm_peak, 4), "algorithmic_bytes_per_launch": bytes_apply,
+                        "kernel": "lora_prefill_tc_kernel (tcgen05)"},
+           "tensor": {"achieved_tflops": round(tfs, 2), "peak_tflops": tc_peak, "frac": round(tfs / tc_peak, 5),
+                      "ceiling_frac": round((flops_apply / tc_peak / 1e12) / (bytes_apply / hbm_peak / 1e9), 4),
+                      "note": "algorithmic flops; HBM-bound at AI %.1f flop/B" % (flops_apply / bytes_apply)}}
+    for pool in pools:
+        pool.close()
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -369,6 +443,11 @@ def main():
     e2e = {"value": tokens_per_step_all / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": round(e2e_ms, 4)}
 
+    # ---- config 3 prefill on the tensor-core kernel (reported beside the decode headline)
+    prefill = None
+    if args.prefill_layers > 0:
+        prefill = bench_prefill(L, args.prefill_layers, args.prefill_steps, dev, hbm_peak, tc_peak, rank)
+
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -393,6 +472,7 @@ def main():
                            "timing": "CUDA graph of one step, K replays, CUDA events, max over ranks"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": int(launches_per_step * args.steps),
+                "prefill": prefill,
                 "setup_s": round(t_gen, 1)}
         s = json.dumps(line)
         print(s, flush=True)

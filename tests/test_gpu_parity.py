@@ -73,6 +73,29 @@ def test_prefill_tiles_bf16_and_fp32(L):
             ref = O.delta_for_batch(b, n_threads=8)
             assert rel_l2(y, ref, dtype) <= TOL[dtype], (dtype, y_zero)
             _check_md(md, _md_ref(b))
+            if dtype == "bf16":
+                # segments >= L_tc with rank <= 128 ran on the tcgen05 kernel: 63->0 (decode), 64, 127,
+                # 128, 129, 300 tokens -> 1+1+1+2+3 tiles, minus the rank-128 segment routing rule (all <= 128)
+                assert md["n_prefill_tiles"] == 1 + 1 + 1 + 2 + 3, md["n_prefill_tiles"]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tcgen05_prefill_vs_simt_path_and_oracle(L, seed):
+    """The same prefill batch through the tcgen05 kernel (L_tc = 16) and through the decode
+    kernels only (L_tc huge): both within tolerance of the oracle, ragged tiles, all ranks 1..128."""
+    rng = np.random.default_rng(seed)
+    lens = [int(v) for v in rng.integers(16, 400, size=6)]
+    ranks = {i: int(r) for i, r in enumerate(rng.choice([1, 3, 8, 16, 24, 40, 64, 100, 128], size=6))}
+    ids = list(range(6))
+    H_in, H_out = [(256, 384), (512, 128), (1024, 1024)][seed]
+    b = gen.build_batch("tcp%d" % seed, 777 + seed, "bf16", H_in, H_out, lens, ids, ranks, y_zero=bool(seed % 2))
+    ref = O.delta_for_batch(b, n_threads=8)
+    y_tc, md_tc = run_gpu(b, L, L_tc=16)
+    y_simt, md_simt = run_gpu(b, L, L_tc=1 << 30)
+    assert md_tc["n_prefill_tiles"] == sum((n + 127) // 128 for n in lens)
+    assert md_simt["n_prefill_tiles"] == 0
+    assert rel_l2(y_tc, ref, "bf16") <= TOL["bf16"]
+    assert rel_l2(y_simt, ref, "bf16") <= TOL["bf16"]
 
 
 def test_c3_prefill_reduced(L):
