@@ -32,10 +32,11 @@
 namespace lora {
 
 constexpr int kPfThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
-constexpr int kPfStages = 4;
+constexpr int kPfStages = 3;
 constexpr int kPfStageBytes = 32768;   // X chunk 16 KB + A chunk <= 16 KB, or one B tile (<= 32 KB)
 constexpr int kPfVBytes = 128 * 128 * 2;   // one V part (hi or lo): 128 tokens x r16 <= 128, bf16
-constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 256;
+constexpr int kPfYBytes = 128 * 128 * 2;   // one staged y tile (128 tokens x 128 columns, bf16)
+constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 2 * kPfYBytes + 256;
 constexpr int kPfNTile = 128;          // expand columns per tile
 constexpr int kPfTileWords = 8;        // per-tile record in the metadata blob
 
@@ -43,6 +44,7 @@ struct PrefillArgs {
     CUtensorMap tm_x;   // x [T][H_in], box {64, 128}, SW128
     CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1}, SW128 (gather4)
+    CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads; writes go per row)
     char* y;
     const int32_t* meta_global;
     unsigned long long* trace;
@@ -145,14 +147,17 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const uint32_t vhi = base + kPfStages * kPfStageBytes;
     const uint32_t vlo = vhi + kPfVBytes;
     uint8_t* gv = gbase + kPfStages * kPfStageBytes;   // generic pointer to vhi
-    const uint32_t bars = vlo + kPfVBytes;              // 14 mbarriers + tmem slot
+    const uint32_t yring = vlo + kPfVBytes;             // 2 x 32 KB staged y tiles
+    uint8_t* gy = gbase + (yring - base);
+    const uint32_t bars = yring + 2 * kPfYBytes;        // 14 mbarriers + tmem slot
     auto full = [&](int s) { return bars + 8u * s; };
     auto empty = [&](int s) { return bars + 8u * (kPfStages + s); };
     const uint32_t d1_full = bars + 8u * (2 * kPfStages);
     const uint32_t v_ready = d1_full + 8u;
     auto tm_full = [&](int b) { return v_ready + 8u + 8u * b; };
     auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfStages + 6) - base));
+    auto y_full = [&](int b) { return v_ready + 40u + 8u * b; };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfStages + 8) - base));
 
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -175,6 +180,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         for (int b = 0; b < 2; ++b) {
             pf_bar_init(tm_full(b), 1);
             pf_bar_init(tm_empty(b), 128);
+            pf_bar_init(y_full(b), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -311,25 +317,42 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
         tc_fence_before();
         pf_arrive(v_ready);
-        // ---- per expand tile: y[row][n0 .. n0+128) += D2 (one rounding), straight to global
+        // ---- per expand tile: y[row][n0 .. n0+128) += D2 (one rounding).  y tiles are staged
+        //      by TMA one tile ahead (2 slots, SW128: row at (row/8)*1024 + (row%8)*128 per 64-col
+        //      half, 16-B chunk c at c ^ (row%8)); results go straight to global, valid rows only
+        //      (rows past the segment belong to other segments' tiles).
         const bool valid = row < nvalid;
         char* yrow = a.y + ((size_t)(tok0 + row) * a.H_out) * 2;
+        const bool leader = (tid == 64);
+        auto issue_y = [&](int nt) {
+            const int b = nt & 1;
+            const uint32_t dst = yring + (uint32_t)b * kPfYBytes;
+            pf_arrive_tx(y_full(b), (uint32_t)kPfYBytes);
+            tma_2d(dst, &a.tm_y, nt * kPfNTile, tok0, y_full(b));
+            tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(b));
+        };
+        if (leader) {
+            issue_y(0);
+            if (nnt > 1) issue_y(1);
+        }
         for (int nt = 0; nt < nnt; ++nt) {
             const int b = nt & 1;
             pf_wait(tm_full(b), (nt >> 1) & 1);
+            pf_wait(y_full(b), (nt >> 1) & 1);
             tc_fence_after();
+            const uint8_t* ys = gy + b * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll 1
             for (int c0 = 0; c0 < kPfNTile; c0 += 32) {
                 float d[32];
                 tmem_ld32(tmem + lane_addr + 128u + 128u * b + (uint32_t)c0, d);
                 if (valid) {
-                    uint4* yp = reinterpret_cast<uint4*>(yrow + (size_t)(nt * kPfNTile + c0) * 2);
-                    uint4 yv[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) yv[q] = yp[q];
+                    uint4 o4[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint32_t w[4] = {yv[q].x, yv[q].y, yv[q].z, yv[q].w};
+                        const int col = c0 + q * 8;
+                        const int h = col >> 6, chunk = (col & 63) >> 3;
+                        const uint4 yv = *reinterpret_cast<const uint4*>(ys + h * (kPfYBytes / 2) + ((chunk ^ (row & 7)) << 4));
+                        const uint32_t w[4] = {yv.x, yv.y, yv.z, yv.w};
                         uint32_t o[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
@@ -338,12 +361,18 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                             __nv_bfloat162 hb = __floats2bfloat162_rn(lo, hi);
                             o[e] = *reinterpret_cast<uint32_t*>(&hb);
                         }
-                        yp[q] = make_uint4(o[0], o[1], o[2], o[3]);
+                        o4[q] = make_uint4(o[0], o[1], o[2], o[3]);
                     }
+                    uint4* yp = reinterpret_cast<uint4*>(yrow + (size_t)(nt * kPfNTile + c0) * 2);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) yp[q] = o4[q];
                 }
             }
             tc_fence_before();
             pf_arrive(tm_empty(b));
+            // every epilogue thread is done with y slot b -> refill it with tile nt + 2
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (leader && nt + 2 < nnt) issue_y(nt + 2);
         }
     }
     tc_fence_before();
@@ -418,6 +447,8 @@ int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int*
     if (e) return e;
     std::memcpy(&a.tm_a, L.tm_a, sizeof(CUtensorMap));
     std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
+    e = make_tmap_bf16(&a.tm_y, L.y, L.T, L.H_out, 128);
+    if (e) return e;
     a.y = static_cast<char*>(L.y);
     a.meta_global = L.meta_dev;
     a.trace = L.trace;
