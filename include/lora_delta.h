@@ -141,6 +141,28 @@ lora_status lora_apply(lora_pool* p, const void* x, void* y,
                        const int32_t* seg_indptr, const int32_t* adapter_ids,
                        int num_segments, void* stream);
 
+/*
+ * Tensor-parallel split of lora_apply (BASELINE.json north_star: "splits B's output dimension
+ * (and A's input dimension, with an NCCL all-reduce of the tiny rank-r intermediate)").
+ * A TP rank's pool holds the shards A[:, its H_in slice] and B[:, its H_out slice], so the pool's
+ * hidden_in / hidden_out are the shard widths.
+ *
+ * lora_apply_shrink -- partial v over this rank's H_in slice:
+ *   x           device [T][hidden_in] (the rank's x columns), pool dtype.
+ *   v_out       device fp32 buffer of v_capacity floats; receives the partial intermediate in the
+ *               library's internal layout (per group-chunk [k_slice][token][rank], unscaled); its
+ *               size is lora_metadata_view.v_floats of the same batch (lora_plan).  Identical
+ *               batches on every TP rank give identical layouts, so an elementwise SUM all-reduce
+ *               of v_out across ranks (NCCL, done by the caller) yields the full-H_in partials.
+ *   Every token takes the decode kernels (the tcgen05 prefill path fuses shrink and expand).
+ * lora_apply_expand -- y[:, this rank's H_out slice] += s · (Σ v) · B_shard for the batch of the
+ *   immediately preceding lora_apply_shrink on this pool, reading the (all-reduced) v_in.
+ * Errors: as lora_apply; ARG if v_capacity is too small or expand has no pending shrink.
+ */
+lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_indptr, const int32_t* adapter_ids,
+                              int num_segments, float* v_out, int64_t v_capacity, void* stream);
+lora_status lora_apply_expand(lora_pool* p, void* y, const float* v_in, void* stream);
+
 /* lora_plan -- build (and keep for lora_debug_metadata) the canonical metadata of a batch
  * without launching anything.  Pure host code; works on host-only pools. */
 lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* adapter_ids,
@@ -181,6 +203,7 @@ typedef struct {
     int64_t sum_rank_tokens;         /*     Σ_t r_{a(t)} (flops / 2(H_in+H_out)) */
     int32_t n_decode_units, n_prefill_tiles;   /* kernel work of the last apply (informational) */
     int32_t n_shrink_units, n_expand_units;    /* split of n_decode_units (shrink units come first) */
+    int64_t v_floats;                          /* size of the partial-v buffer (lora_apply_shrink) */
 } lora_metadata_view;
 
 lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* out);

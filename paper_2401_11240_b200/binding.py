@@ -57,7 +57,8 @@ class MetadataView(ctypes.Structure):
                 ("sum_rank_seg", ctypes.c_int64), ("sum_rank_groups", ctypes.c_int64),
                 ("sum_rank_tokens", ctypes.c_int64),
                 ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32),
-                ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32)]
+                ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32),
+                ("v_floats", ctypes.c_int64)]
 
 
 def header_symbols() -> List[str]:
@@ -87,6 +88,8 @@ def _load() -> ctypes.CDLL:
         "lora_debug_adapter_pages": [vp, c_i32, _P32, c_int, P(c_int)],
         "lora_debug_read_pages": [vp, c_i32, vp, vp],
         "lora_debug_set_trace": [vp, vp],
+        "lora_apply_shrink": [vp, vp, _P32, _P32, c_int, vp, c_i64, vp],
+        "lora_apply_expand": [vp, vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -177,6 +180,25 @@ class LoraPool:
         _check(LIB.lora_apply(self.handle, _ptr_of(x), _ptr_of(y), ip.ctypes.data_as(_P32),
                               ids.ctypes.data_as(_P32), int(ids.shape[0]), sp))
 
+    def apply_shrink(self, x, seg_indptr, adapter_ids, v_out, stream=None) -> None:
+        """Tensor-parallel first half: partial v (fp32, caller-owned device buffer v_out) over
+        this pool's H_in shard.  The caller sums v_out across TP ranks, then calls apply_expand."""
+        ip, ids = _i32(seg_indptr), _i32(adapter_ids)
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
+        cap = int(v_out.numel()) if hasattr(v_out, "numel") else 0
+        _check(LIB.lora_apply_shrink(self.handle, _ptr_of(x), ip.ctypes.data_as(_P32), ids.ctypes.data_as(_P32),
+                                     int(ids.shape[0]), _ptr_of(v_out), cap, sp))
+
+    def apply_expand(self, y, v_in, stream=None) -> None:
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
+        _check(LIB.lora_apply_expand(self.handle, _ptr_of(y), _ptr_of(v_in), sp))
+
     def plan(self, seg_indptr, adapter_ids) -> None:
         ip, ids = _i32(seg_indptr), _i32(adapter_ids)
         _check(LIB.lora_plan(self.handle, ip.ctypes.data_as(_P32), ids.ctypes.data_as(_P32), int(ids.shape[0])))
@@ -208,7 +230,7 @@ class LoraPool:
                "group_tokens": arr(m.group_tokens, int(ntok.sum())),
                "pages": arr(m.pages, int(m.sum_rank_groups)), "seg_kind": arr(m.seg_kind, m.S)}
         for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens",
-                  "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units"):
+                  "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units", "v_floats"):
             out[k] = int(getattr(m, k))
         return out
 

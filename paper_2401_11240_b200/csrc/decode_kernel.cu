@@ -871,7 +871,7 @@ struct DecodeKernels<__nv_bfloat16, W> {
 };
 
 template <typename T, int W>
-static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t st, int* launches) {
+static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t st, int* launches, int phases) {
     using K = DecodeKernels<T, W>;
     static bool configured = false;
     if (!configured) {
@@ -886,10 +886,16 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         const int n = (int)pl.blob.size();
         for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
     }
-    cudaError_t e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem, st, a, blob);
-    if (e != cudaSuccess) return e;
-    e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads, K::expand_smem, st, a, blob);
-    *launches += 2;
+    cudaError_t e = cudaSuccess;
+    if (phases & 1) {
+        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem, st, a, blob);
+        if (e != cudaSuccess) return e;
+        *launches += 1;
+    }
+    if (phases & 2) {
+        e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads, K::expand_smem, st, a, blob);
+        *launches += 1;
+    }
     return e;
 }
 
@@ -910,11 +916,11 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
     a.n_gc = pl.n_gc;
     a.ksplit = ksplit_of(L.H_in, (int)sizeof(T));
     const int n = (int)pl.blob.size();
-    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches);
-    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches);
-    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches);
-    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches);
-    for (int off = 0; off < n; off += kUploadWords) {
+    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases);
+    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases);
+    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches, L.phases);
+    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches, L.phases);
+    for (int off = 0; off < n && (L.phases & 1); off += kUploadWords) {   // expand-only reuses the shrink's upload
         const int m = n - off < kUploadWords ? n - off : kUploadWords;
         MetaBlob<kUploadWords> b;
         for (int i = 0; i < m; ++i) b.w[i] = pl.blob[off + i];
@@ -922,7 +928,7 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         *launches += 1;
         if (e != cudaSuccess) return e;
     }
-    return launch_pair<T, 1>(a, pl, st, launches);
+    return launch_pair<T, 1>(a, pl, st, launches, L.phases);
 }
 
 int launch_decode(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {

@@ -62,6 +62,7 @@ struct DecodeLaunch {
     int32_t* meta_dev;     // device scratch for metadata too large for kernel parameters
     unsigned long long* trace;   // optional per-unit timestamps (lora_debug_set_trace), or null
     int H_in, H_out, esz, num_sms;
+    int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel
 };
 struct PrefillLaunch {
     const void* x;

@@ -53,6 +53,7 @@ struct lora_pool {
     Plan plan;
     int L_tc = 64;
     int64_t launches = 0;
+    bool split_ready = false;             // a lora_apply_shrink awaits its lora_apply_expand
     unsigned long long* trace = nullptr;   // lora_debug_set_trace
 };
 
@@ -298,43 +299,73 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     return LORA_OK;
 }
 
-lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr, const int32_t* adapter_ids,
-                       int num_segments, void* stream_ptr) {
+// mode 0: full apply; 1: shrink only (partial v -> v_ext); 2: expand only (v_ext -> y, plan of the
+// last shrink).  Modes 1/2 serve tensor parallelism: the caller all-reduces v in between.
+static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr,
+                              const int32_t* adapter_ids, int num_segments, void* stream_ptr, int mode, float* v_ext,
+                              int64_t v_cap) {
     if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
-    if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "lora_apply on a host-only pool");
-    if (num_segments < 0) return fail(LORA_ERR_ARG, "num_segments < 0");
-    if (num_segments == 0) return LORA_OK;
-    if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
-    const int T = seg_indptr[num_segments];
-    if (T == 0) {
-        std::string err;
-        lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
-                                   p->L_tc, false, p->table, err);
-        return s == LORA_OK ? LORA_OK : fail(s, err);
+    if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "apply on a host-only pool");
+    lora_status s = LORA_OK;
+    int T = 0;
+    if (mode != 2) {
+        if (num_segments < 0) return fail(LORA_ERR_ARG, "num_segments < 0");
+        if (num_segments == 0) {
+            p->split_ready = mode == 1;
+            p->plan = Plan();
+            return LORA_OK;
+        }
+        if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
+        T = seg_indptr[num_segments];
+        if (T == 0) {
+            std::string err;
+            s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, false,
+                           p->table, err);
+            p->split_ready = (s == LORA_OK && mode == 1);
+            return s == LORA_OK ? LORA_OK : fail(s, err);
+        }
+        if (!x) return fail(LORA_ERR_ARG, "x is NULL");
+        if (((uintptr_t)x & 15)) return fail(LORA_ERR_ALIGN, "x must be 16-byte aligned");
+    } else {
+        if (!p->split_ready) return fail(LORA_ERR_ARG, "lora_apply_expand without a preceding lora_apply_shrink");
+        T = p->plan.T;
+        if (T == 0 || p->plan.n_gc == 0) {
+            p->split_ready = false;
+            return LORA_OK;
+        }
     }
-    if (!x) return fail(LORA_ERR_ARG, "x is NULL");
-    if (!y) return fail(LORA_ERR_ARG, "y is NULL");
-    if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(LORA_ERR_ALIGN, "x and y must be 16-byte aligned");
-    {
+    if (mode != 1) {
+        if (!y) return fail(LORA_ERR_ARG, "y is NULL");
+        if (((uintptr_t)y & 15)) return fail(LORA_ERR_ALIGN, "y must be 16-byte aligned");
+    }
+    if (mode == 0) {
         const char* xs = (const char*)x;
         const char* ys = (const char*)y;
         const size_t xb = (size_t)T * p->H_in * p->esz, yb = (size_t)T * p->H_out * p->esz;
         if (xs < ys + yb && ys < xs + xb) return fail(LORA_ERR_ARG, "x and y overlap");
     }
+    if (mode != 0 && !v_ext) return fail(LORA_ERR_ARG, "v buffer is NULL");
     DeviceGuard g(p->device);
     cudaStream_t st = (cudaStream_t)stream_ptr;
     {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: pending CUDA error");
     }
-    std::string err;
-    const bool tc = p->tc_prefill;
-    lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
-                               tc, p->table, err);
-    if (s != LORA_OK) return fail(s, err);
+    if (mode != 2) {
+        std::string err;
+        const bool tc = p->tc_prefill && mode == 0;   // the split path keeps every token on the decode kernels
+        s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, tc, p->table,
+                       err);
+        if (s != LORA_OK) return fail(s, err);
+        if (mode == 1 && p->plan.vbuf_floats > v_cap)
+            return fail(LORA_ERR_ARG, "v buffer too small: need " + std::to_string(p->plan.vbuf_floats) + " floats");
+        p->split_ready = false;
+    }
     const Plan& pl = p->plan;
+    if (mode == 1) p->split_ready = true;
     if (pl.G == 0) return LORA_OK;
     if (pl.n_gc == 0 && pl.n_pf_tiles == 0) return LORA_OK;
+    if (mode == 2) p->split_ready = false;
 
     // order after in-flight loads of the adapters this batch reads
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -351,17 +382,21 @@ lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_
                  "lora_apply: wait load");
     }
     // scratch
-    if (pl.n_gc > 0) {
+    if (pl.n_gc > 0 && mode == 0) {
         if ((s = grow(p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
+    }
+    if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
     }
     int launches = 0;
     if (pl.n_gc > 0) {
-        DecodeLaunch L{x, y, p->dA, p->dB, p->vbuf, p->meta_dev, p->trace, p->H_in, p->H_out, p->esz, p->num_sms};
+        DecodeLaunch L{x, y, p->dA, p->dB, mode == 0 ? p->vbuf : v_ext, p->meta_dev, p->trace, p->H_in, p->H_out,
+                       p->esz, p->num_sms};
+        L.phases = mode == 0 ? 3 : mode;
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
-    if (pl.n_pf_tiles > 0) {
+    if (pl.n_pf_tiles > 0 && mode == 0) {
         PrefillLaunch L{x, y, p->tm_a, p->tm_b, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
         cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
@@ -370,6 +405,20 @@ lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_
     if (std::find(p->apply_streams.begin(), p->apply_streams.end(), st) == p->apply_streams.end())
         p->apply_streams.push_back(st);
     return LORA_OK;
+}
+
+lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr, const int32_t* adapter_ids,
+                       int num_segments, void* stream) {
+    return apply_impl(p, x, y, seg_indptr, adapter_ids, num_segments, stream, 0, nullptr, 0);
+}
+
+lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_indptr, const int32_t* adapter_ids,
+                              int num_segments, float* v_out, int64_t v_capacity, void* stream) {
+    return apply_impl(p, x, nullptr, seg_indptr, adapter_ids, num_segments, stream, 1, v_out, v_capacity);
+}
+
+lora_status lora_apply_expand(lora_pool* p, void* y, const float* v_in, void* stream) {
+    return apply_impl(p, nullptr, y, nullptr, nullptr, 0, stream, 2, const_cast<float*>(v_in), 0);
 }
 
 lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
@@ -434,6 +483,7 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
     o->n_decode_units = pl.n_shrink + pl.n_expand;
     o->n_shrink_units = pl.n_shrink;
     o->n_expand_units = pl.n_expand;
+    o->v_floats = pl.vbuf_floats;
     o->n_prefill_tiles = pl.n_prefill_tiles;
     return LORA_OK;
 }

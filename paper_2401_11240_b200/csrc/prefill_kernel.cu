@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         //      (row/8)*1024 + (row%8)*128 inside the 16 KB atom, 16-B chunk c stored at c ^ (row%8)
         pf_wait(d1_full, 0);
         tc_fence_after();
+        if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 2] = pf_gtime();
         for (int c0 = 0; c0 < rp; c0 += 32) {
             float v[32];
             tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
         tc_fence_before();
         pf_arrive(v_ready);
+        if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 3] = pf_gtime();
         // ---- per expand tile: y[row][n0 .. n0+128) += D2 (one rounding).  y tiles are staged
         //      by TMA one tile ahead (2 slots, SW128: row at (row/8)*1024 + (row%8)*128 per 64-col
         //      half, 16-B chunk c at c ^ (row%8)); results go straight to global, valid rows only
