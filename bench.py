@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--prefill-layers", type=int, default=2,
                     help="layers of the c3 prefill measurement reported in the 'prefill' object (0 = skip)")
     ap.add_argument("--prefill-steps", type=int, default=20)
+    ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
     return ap.parse_args()
 
 
@@ -318,6 +319,107 @@ def bench_prefill(L, layers: int, steps: int, dev, hbm_peak: float, tc_peak: flo
     return out
 
 
+# ---------------------------------------------------------------- config 4: Zipf paged pool + cold starts
+def h2d_peak_gbs(dev) -> float:
+    """Pinned host -> device copy bandwidth (256 MiB cudaMemcpyAsync, best of 5)."""
+    import torch
+    src = torch.empty(256 * 2 ** 20, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return src.numel() / (best * 1e-3) / 1e9
+
+
+def bench_c4(L, dev, steps: int, world: int, rank: int):
+    """Llama-2-13B (5120) projection, 1000 adapters (ranks 8..128) in pinned host memory, a pool of
+    20% of their ranks per GPU, Zipf(1.0) requests: per step 64 decode tokens + one 512-token
+    prefill; misses load on the side stream (LRU eviction) and overlap the applies.  Requests are
+    partitioned by adapter home (id mod N, top-16 replicated).  Reports tokens/s with the loads
+    included, hit rate, and the cold-start latency next to the measured pinned H2D bandwidth."""
+    import torch
+    import time as _t
+    from paper_2401_11240_b200.serving import AdapterCache, HostRepository, serves
+    H, n_ad, hot = 5120, 1000, list(range(16))
+    mine = [a for a in range(n_ad) if serves(a, rank, world, [int(gen.zipf_perm(gen.BASE_SEED + 3, n_ad)[i]) for i in hot])]
+    hot_ids = [int(gen.zipf_perm(gen.BASE_SEED + 3, n_ad)[i]) for i in hot]
+    repo = HostRepository()
+    t0 = _t.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=min(16, len(os.sched_getaffinity(0)))) as ex:
+        for a, ad in zip(mine, ex.map(lambda a: gen.c4_adapter(a, H), mine)):
+            repo.add(a, ad.rank, ad.scale, torch.from_numpy(ad.A.view(np.int16)).pin_memory(),
+                     torch.from_numpy(ad.B.view(np.int16)).pin_memory())
+    gen_s = _t.perf_counter() - t0
+    budget = sum(gen.c4_rank(a) for a in range(n_ad)) // 5
+    pool = L.LoraPool(H, H, n_ad, "bf16", max_total_rank=budget)
+    cache = AdapterCache(pool, repo, budget, n_ad)
+    st = torch.cuda.Stream(device=dev)
+    T = 64 + 512
+    g = torch.Generator(device="cpu").manual_seed(gen.BASE_SEED + 300 + rank)
+    x = torch.randn(T, H, generator=g).to(torch.bfloat16).to(dev)
+    y = torch.zeros(T, H, dtype=torch.bfloat16, device=dev)
+
+    def draw(step):
+        ids = []
+        s2 = step
+        while len(ids) < 65:   # redraw until 64 decode + 1 prefill requests served by this rank
+            d = gen.config_c4_draw(s2, n_decode=64, prefill_len=512, n_adapters=n_ad, world=world, rank=rank)
+            ids += [int(a) for a in list(d["decode_ids"]) + [int(d["prefill_id"][0])] if serves(int(a), rank, world, hot_ids)]
+            s2 += 100000
+        dec, pre = ids[:64], ids[64]
+        return np.array(dec + [pre], np.int32)
+
+    ip = gen.segments_to_indptr([1] * 64 + [512])
+
+    def step(sidx):
+        ids = draw(sidx)
+        cache.ensure(ids.tolist())
+        pool.apply(x, y, ip, ids, stream=st)
+
+    for s_ in range(5):                      # warm the cache
+        step(1000000 + s_)
+    torch.cuda.synchronize()
+    h0, m0, b0 = cache.hits, cache.misses, cache.loaded_bytes
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = _t.perf_counter()
+    e0.record(st)
+    for s_ in range(steps):
+        step(s_)
+    e1.record(st)
+    torch.cuda.synchronize()
+    wall = _t.perf_counter() - w0
+    ms = max(e0.elapsed_time(e1), wall * 1e3) / steps
+    hits, misses = cache.hits - h0, cache.misses - m0
+    loaded = cache.loaded_bytes - b0
+    # cold-start latency: load 8 non-resident adapters one at a time, call -> ready
+    lat = []
+    cold = [a for a in mine if a not in cache.lru][:8]
+    for a in cold:
+        cache.ensure([a])
+        t1 = _t.perf_counter()
+        while not pool.adapter_ready(a):
+            pass
+        lat.append((_t.perf_counter() - t1) * 1e3)
+    lat_bytes = np.mean([repo.bytes_of(a, 2) for a in cold]) if cold else 0
+    peak = h2d_peak_gbs(dev)
+    out = {"workload": "c4: Llama-2-13B 5120->5120 bf16, 1000 adapters ranks 8..128 in pinned host memory, pool = 20%% "
+                       "of their ranks, Zipf(1.0), 64 decode + 1x512 prefill tokens/step, LRU, rank %d/%d" % (rank, world),
+           "value": round(T / (ms * 1e-3), 1), "unit": "tokens/s per GPU (loads included)", "ms_per_step": round(ms, 4),
+           "steps": steps, "hit_rate": round(hits / max(1, hits + misses), 4), "loads_per_step": round(misses / steps, 2),
+           "load_GBps_effective": round(loaded / (ms * steps * 1e-3) / 1e9, 2),
+           "cold_start_ms_per_adapter": round(float(np.median(lat)), 3) if lat else None,
+           "cold_start_bytes_per_adapter": int(lat_bytes),
+           "cold_start_GBps": round(lat_bytes / (np.median(lat) * 1e-3) / 1e9, 2) if lat else None,
+           "h2d_pinned_peak_GBps": round(peak, 1), "host_repo_setup_s": round(gen_s, 1)}
+    pool.close()
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -448,6 +550,10 @@ def main():
     if args.prefill_layers > 0:
         prefill = bench_prefill(L, args.prefill_layers, args.prefill_steps, dev, hbm_peak, tc_peak, rank)
 
+    c4 = None
+    if args.c4_steps > 0:
+        c4 = bench_c4(L, dev, args.c4_steps, world, rank)
+
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -473,6 +579,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": int(launches_per_step * args.steps),
                 "prefill": prefill,
+                "c4": c4,
                 "setup_s": round(t_gen, 1)}
         s = json.dumps(line)
         print(s, flush=True)
