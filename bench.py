@@ -176,13 +176,13 @@ def algorithmic_bytes_per_apply(ranks_sum: int, T: int) -> int:
     return 2 * (ranks_sum * (H + H) + T * H + 2 * T * H)
 
 
-def load_ncu_traffic():
+def load_ncu_traffic(key="dram_bytes_per_launch"):
+    """DRAM bytes per launch from the committed ncu --set full summary (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     if not os.path.exists(p):
         return None
     try:
-        d = json.load(open(p))
-        return d.get("dram_bytes_per_launch")
+        return json.load(open(p)).get(key)
     except Exception:
         return None
 
@@ -310,7 +310,8 @@ def bench_prefill(L, layers: int, steps: int, dev, hbm_peak: float, tc_peak: flo
            "ms_per_apply": round(ms_apply, 5), "tensor_core_tiles_per_apply": md["n_prefill_tiles"],
            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(gbs / hbm_peak, 4), "algorithmic_bytes_per_launch": bytes_apply,
-                        "kernel": "lora_prefill_tc_kernel (tcgen05)"},
+                        "kernel": "lora_prefill_tc_kernel (tcgen05)",
+                        "traffic": load_ncu_traffic("prefill_dram_bytes_per_launch")},
            "tensor": {"achieved_tflops": round(tfs, 2), "peak_tflops": tc_peak, "frac": round(tfs / tc_peak, 5),
                       "ceiling_frac": round((flops_apply / tc_peak / 1e12) / (bytes_apply / hbm_peak / 1e9), 4),
                       "note": "algorithmic flops; HBM-bound at AI %.1f flop/B" % (flops_apply / bytes_apply)}}
@@ -506,9 +507,11 @@ def main():
     achieved = bytes_apply / (kernel_us * 1e-6) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": load_ncu_traffic(),
-                "kernel": "lora_decode_kernel<bf16>", "algorithmic_bytes_per_launch": bytes_apply,
+                "kernel": "decode apply = lora_shrink_mma_kernel + lora_expand_mma_kernel (PDL-chained pair)",
+                "algorithmic_bytes_per_launch": bytes_apply,
                 "avg_launch_us": round(kernel_us, 3), "peak_source": peak_src,
-                "note": "avg launch time = graph step time / 128 launches (includes launch gaps)"}
+                "note": "per apply (one launch pair): graph step time / 128 applies, gaps included; "
+                        "traffic = ncu dram read+write of the pair (profiles/ncu_decode_summary.json)"}
 
     # ---- e2e through the public API with host buffers
     x_host = [[torch.empty(T_DECODE, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)] for _ in range(layers)]

@@ -34,7 +34,7 @@ def main():
     ix = {n: i for i, n in enumerate(h)}
     kern = {}
     for r in rows[1:]:
-        if len(r) != len(h):
+        if len(r) <= ix["Metric Value"]:
             continue
         k = kern.setdefault(r[ix["ID"]], {"name": r[ix["Kernel Name"]]})
         if r[ix["Metric Name"]] in WANT:
