@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--prefill-layers", type=int, default=2,
                     help="layers of the c3 prefill measurement reported in the 'prefill' object (0 = skip)")
     ap.add_argument("--prefill-steps", type=int, default=20)
+    ap.add_argument("--qkv-mode", choices=["serial", "fused", "streams"], default="serial",
+                    help="q/k/v: one lora_apply each in stream order, one lora_apply_multi, or forked onto 3 streams")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
     return ap.parse_args()
 
@@ -466,10 +468,30 @@ def main():
     ys = [[torch.zeros(T_DECODE, H, dtype=torch.bfloat16, device=dev) for _ in PROJS] for _ in range(layers)]
     stream = torch.cuda.Stream(device=dev)
 
+    mode = args.qkv_mode
+    fuse = mode == "fused"
+    side = [torch.cuda.Stream(device=dev) for _ in range(2)]
+
     def step(st):
         for l in range(layers):
-            for p in range(len(PROJS)):
-                pools[l][p].apply(xs[l][0 if p < 3 else 1], ys[l][p], ip, ids, stream=st)
+            if mode == "fused":   # q, k, v share x and the batch: one fused launch pair (lora_apply_multi), then o
+                L.apply_multi(pools[l][:3], [xs[l][0]] * 3, ys[l][:3], ip, ids, stream=st)
+                pools[l][3].apply(xs[l][1], ys[l][3], ip, ids, stream=st)
+            elif mode == "streams":   # q, k, v are independent: fork onto 3 streams, join before o
+                ev = torch.cuda.Event()
+                ev.record(st)
+                for k, s2 in enumerate(side):
+                    s2.wait_event(ev)
+                    pools[l][k + 1].apply(xs[l][0], ys[l][k + 1], ip, ids, stream=s2)
+                pools[l][0].apply(xs[l][0], ys[l][0], ip, ids, stream=st)
+                for s2 in side:
+                    e2 = torch.cuda.Event()
+                    e2.record(s2)
+                    st.wait_event(e2)
+                pools[l][3].apply(xs[l][1], ys[l][3], ip, ids, stream=st)
+            else:
+                for p in range(len(PROJS)):
+                    pools[l][p].apply(xs[l][0 if p < 3 else 1], ys[l][p], ip, ids, stream=st)
 
     with torch.cuda.stream(stream):
         step(stream)               # sizes the pools' scratch outside capture
@@ -502,16 +524,17 @@ def main():
     # ---- roofline of the decode kernel (the only kernel of the step)
     hbm_peak, tc_peak, peak_src = measured_peaks()
     bytes_apply = algorithmic_bytes_per_apply(ranks_sum, T_DECODE)
-    n_kernels = layers * len(PROJS)
-    kernel_us = ms_step * 1000.0 / n_kernels      # includes inter-kernel gaps: conservative
+    n_applies = layers * len(PROJS)
+    kernel_us = ms_step * 1000.0 / n_applies      # per projection apply; includes inter-kernel gaps
     achieved = bytes_apply / (kernel_us * 1e-6) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": load_ncu_traffic(),
-                "kernel": "decode apply = lora_shrink_mma_kernel + lora_expand_mma_kernel (PDL-chained pair)",
+                "kernel": "decode: lora_shrink_mma_kernel + lora_expand_mma_kernel (PDL-chained pair per apply; "
+                          "q/k/v mode %s)" % mode,
                 "algorithmic_bytes_per_launch": bytes_apply,
                 "avg_launch_us": round(kernel_us, 3), "peak_source": peak_src,
-                "note": "per apply (one launch pair): graph step time / 128 applies, gaps included; "
-                        "traffic = ncu dram read+write of the pair (profiles/ncu_decode_summary.json)"}
+                "note": "per projection apply: graph step time / 128 applies (gaps included); traffic = ncu dram "
+                        "read+write per projection apply (profiles/ncu_decode_summary.json)"}
 
     # ---- e2e through the public API with host buffers
     x_host = [[torch.empty(T_DECODE, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)] for _ in range(layers)]
@@ -578,7 +601,8 @@ def main():
                            "ranks": list(gen.C2_RANKS), "hidden": H, "parallelism": "dp%d (request partition)" % world,
                            "l2": "inputs larger than L2 (%.2f GB adapter working set per GPU)" %
                                  (layers * len(PROJS) * ranks_sum * 2 * H * 2 / 1e9),
-                           "timing": "CUDA graph of one step, K replays, CUDA events, max over ranks"},
+                           "timing": "CUDA graph of one step, K replays, CUDA events, max over ranks",
+                           "qkv_mode": mode},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": int(launches_per_step * args.steps),
                 "prefill": prefill,

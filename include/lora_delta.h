@@ -142,6 +142,19 @@ lora_status lora_apply(lora_pool* p, const void* x, void* y,
                        int num_segments, void* stream);
 
 /*
+ * lora_apply_multi -- lora_apply on up to 4 pools that share one batch layout (e.g. the W_Q, W_K,
+ * W_V projections of a layer, which the paper adapts together), fused into ONE launch
+ * pair of the decode kernels (prefill tiles still launch per pool).  Same semantics as calling
+ * lora_apply(pools[i], xs[i], ys[i], seg_indptr, adapter_ids, num_segments, stream) for each i;
+ * the work of all pools shares the kernels' prologue/epilogue latency instead of paying it per
+ * pool.  The pools must be distinct, on one device and of one dtype; the first pool's scratch is
+ * used.  All plans are validated before anything is launched.
+ * Errors: as lora_apply (the message names the offending pool index).
+ */
+lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, void* const* ys, int n_pools,
+                             const int32_t* seg_indptr, const int32_t* adapter_ids, int num_segments, void* stream);
+
+/*
  * Tensor-parallel split of lora_apply (BASELINE.json north_star: "splits B's output dimension
  * (and A's input dimension, with an NCCL all-reduce of the tiny rank-r intermediate)").
  * A TP rank's pool holds the shards A[:, its H_in slice] and B[:, its H_out slice], so the pool's

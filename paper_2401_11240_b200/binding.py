@@ -89,6 +89,7 @@ def _load() -> ctypes.CDLL:
         "lora_debug_read_pages": [vp, c_i32, vp, vp],
         "lora_debug_set_trace": [vp, vp],
         "lora_apply_shrink": [vp, vp, _P32, _P32, c_int, vp, c_i64, vp],
+        "lora_apply_multi": [P(vp), P(vp), P(vp), c_int, _P32, _P32, c_int, vp],
         "lora_apply_expand": [vp, vp, vp, vp],
     }
     for name, args in sig.items():
@@ -125,6 +126,21 @@ def _ptr_of(t) -> int:
     if isinstance(t, np.ndarray):
         return int(t.ctypes.data)
     raise TypeError(type(t))
+
+
+def apply_multi(pools, xs, ys, seg_indptr, adapter_ids, stream=None) -> None:
+    """lora_apply_multi: pools[i] applies to (xs[i], ys[i]) in one fused launch pair."""
+    n = len(pools)
+    ip, ids = _i32(seg_indptr), _i32(adapter_ids)
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
+    VP = ctypes.c_void_p * n
+    hp = VP(*[p.handle.value for p in pools])
+    xp = VP(*[_ptr_of(x) for x in xs])
+    yp = VP(*[_ptr_of(y) for y in ys])
+    _check(LIB.lora_apply_multi(hp, xp, yp, n, ip.ctypes.data_as(_P32), ids.ctypes.data_as(_P32), int(ids.shape[0]), sp))
 
 
 class LoraPool:

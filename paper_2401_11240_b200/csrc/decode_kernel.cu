@@ -25,22 +25,39 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "kernel_config.h"
 #include "plan.h"
 
 namespace lora {
 
-struct DecodeArgs {
+struct DecodeJob {                // one pool's operands (lora_apply_multi fuses up to kMaxJobs)
     const char* x;
     char* y;
-    const char* poolA;
-    const char* poolB;
+    const char* A;                // pool page arrays
+    const char* B;
+    int H_in, H_out, ksplit, pad;
+};
+
+struct DecodeArgs {
+    DecodeJob jobs[kMaxJobs];
     float* vbuf;
     const int32_t* meta_global;  // metadata in device memory (large batches) or null
     unsigned long long* trace;   // debug: per-unit timestamps, or null
-    int H_in, H_out;
-    int n_shrink, n_expand, n_gc, ksplit;
+    int n_shrink, n_expand, n_gc, n_jobs;
+    int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
+    int job_expand_base[kMaxJobs];
 };
+
+// job of unit u from the per-job unit bases (kernel parameters: no dependent memory load)
+__device__ __forceinline__ int job_of(int u, int n_jobs, const int (&base)[kMaxJobs]) {
+    int j = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxJobs; ++i)
+        if (i < n_jobs && u >= base[i]) j = i;
+    return j;
+}
 
 template <int W>
 struct MetaBlob {
@@ -185,6 +202,7 @@ __device__ __forceinline__ int find_gc_warp(const int32_t* M, int n_gc, int f, i
 
 // per-CTA unit description, decoded once by warp 0 and shared through smem
 struct UnitSh {
+    int job;
     int gc, r, ntok, ks, j0, nj, n0, nc, voff;
     float scale;
     int tok[kMaxTokChunk];
@@ -217,7 +235,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
     if (warp == 0) {
         // 1. decode the unit and issue the adapter-row loads (immutable pool pages) before
         //    waiting on the previous kernel in the stream
+        const int job = job_of(u, a.n_jobs, a.job_shrink_base);
         const int gc = find_gc_warp(M, a.n_gc, GC_SHRINK_BASE, u, lane);
+        const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
         const int ntok = gc_field(M, gc, GC_NTOK);
         const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
@@ -230,25 +250,26 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int page = lane < nj ? M[poff + j0 + lane] : 0;
         tok = lane < ntok ? M[toff + lane] : 0;
         const int k0 = ks * KS;
-        const uint32_t row_bytes = (uint32_t)min(KS, a.H_in - k0) * E::kSize;
+        const uint32_t row_bytes = (uint32_t)min(KS, J.H_in - k0) * E::kSize;
         if (lane == 0) {
             mbar_init(&bars[0], 1);
             mbar_init(&bars[1], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_arrive_expect_tx(&bars[0], (uint32_t)nj * row_bytes);
-            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
+            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
             sh->voff = gc_field(M, gc, GC_VOFF);
         }
         __syncwarp();
         if (lane < nj)
-            bulk_g2s(abuf + lane * kSliceBytes, a.poolA + ((size_t)page * a.H_in + k0) * E::kSize, row_bytes,
+            bulk_g2s(abuf + lane * kSliceBytes, J.A + ((size_t)page * J.H_in + k0) * E::kSize, row_bytes,
                      &bars[0], policy_evict_first());
     }
     pdl_launch_dependents();
     __syncthreads();
+    const DecodeJob J = a.jobs[sh->job];
     const int r = sh->r, ntok = sh->ntok, ks = sh->ks, j0 = sh->j0, nj = sh->nj;
     const int k0 = ks * KS;
-    const int nk = min(KS, a.H_in - k0);
+    const int nk = min(KS, J.H_in - k0);
     // 2. x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
     pdl_wait_cta();
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
@@ -256,7 +277,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nk * E::kSize));
         __syncwarp();
         if (lane < ntok)
-            bulk_g2s(xbuf + lane * kSliceBytes, a.x + ((size_t)tok * a.H_in + k0) * E::kSize, (uint32_t)nk * E::kSize,
+            bulk_g2s(xbuf + lane * kSliceBytes, J.x + ((size_t)tok * J.H_in + k0) * E::kSize, (uint32_t)nk * E::kSize,
                      &bars[1], policy_evict_normal());
     }
     // 3. partial dot products: warp -> (row, k-part)
@@ -341,7 +362,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
     int tok = 0;
     if (warp == 0) {
         // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
+        const int job = job_of(ue, a.n_jobs, a.job_expand_base);
         const int gc = find_gc_warp(M, a.n_gc, GC_EXPAND_BASE, ue, lane);
+        const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
         const int ntok = gc_field(M, gc, GC_NTOK);
         const int local = ue - gc_field(M, gc, GC_EXPAND_BASE);
@@ -349,7 +372,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int toff = gc_field(M, gc, GC_TOK_OFF);
         const int c = expand_ncols(r, E::kSize);
         const int n0 = local * c;
-        const int nc = min(c, a.H_out - n0);
+        const int nc = min(c, J.H_out - n0);
         int pages[LORA_MAX_RANK / 32];
 #pragma unroll
         for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? M[poff + q * 32 + lane] : 0;
@@ -360,7 +383,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             mbar_init(&bars[1], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
-            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
+            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
             sh->voff = gc_field(M, gc, GC_VOFF);
             sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
         }
@@ -371,12 +394,13 @@ __global__ void __launch_bounds__(kConsumerThreads)
         for (int q = 0; q < LORA_MAX_RANK / 32; ++q) {
             const int j = q * 32 + lane;
             if (j < r)
-                bulk_g2s(bbuf + (size_t)j * c * E::kSize, a.poolB + ((size_t)pages[q] * a.H_out + n0) * E::kSize,
+                bulk_g2s(bbuf + (size_t)j * c * E::kSize, J.B + ((size_t)pages[q] * J.H_out + n0) * E::kSize,
                          row_bytes, &bars[0], pol);
         }
     }
     pdl_launch_dependents();
     __syncthreads();
+    const DecodeJob J = a.jobs[sh->job];
     const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
     const int c = expand_ncols(r, E::kSize);
     const size_t row_stride = (size_t)c * E::kSize;
@@ -386,7 +410,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * E::kSize));
         __syncwarp();
         if (lane < ntok)
-            bulk_g2s(ybuf + lane * row_stride, a.y + ((size_t)tok * a.H_out + n0) * E::kSize, (uint32_t)nc * E::kSize,
+            bulk_g2s(ybuf + lane * row_stride, J.y + ((size_t)tok * J.H_out + n0) * E::kSize, (uint32_t)nc * E::kSize,
                      &bars[1], policy_evict_normal());
     }
     {
@@ -395,7 +419,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         for (int i = tid; i < ntok * r; i += kConsumerThreads) {
             const int t = i / r, j = i - t * r;
             float v = 0.f;
-            for (int k = 0; k < a.ksplit; ++k) v += ld_cg_f32(a.vbuf + voff + (k * ntok + t) * r + j);
+            for (int k = 0; k < J.ksplit; ++k) v += ld_cg_f32(a.vbuf + voff + (k * ntok + t) * r + j);
             vsm[t * r + j] = v * scale;
         }
     }
@@ -434,7 +458,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             for (int t = 0; t < kTokChunk; ++t) {
                 if (t < ntok) {
                     const uint4 yo = lds128(ybuf + t * row_stride + ci * 16);
-                    stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + ci * V) * E::kSize, E::add_round(yo, acc[t]));
+                    stg128_na(J.y + ((size_t)sh->tok[t] * J.H_out + n0 + ci * V) * E::kSize, E::add_round(yo, acc[t]));
                 }
             }
         }
@@ -468,7 +492,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
                 for (int i = 0; i < V; ++i) d[i] += src[i];
             }
             const uint4 yo = lds128(ybuf + t * row_stride + c2 * 16);
-            stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + c2 * V) * E::kSize, E::add_round(yo, d));
+            stg128_na(J.y + ((size_t)sh->tok[t] * J.H_out + n0 + c2 * V) * E::kSize, E::add_round(yo, d));
         }
     }
     if (a.trace && tid == 0) {
@@ -549,7 +573,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
     if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
 
     if (warp == 0) {
+        const int job = job_of(u, a.n_jobs, a.job_shrink_base);
         const int gc = find_gc_warp(M, a.n_gc, GC_SHRINK_BASE, u, lane);
+        const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
         const int ntok = gc_field(M, gc, GC_NTOK);
         const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
@@ -560,34 +586,35 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int j0 = (local - ks * njb) * kShrinkRowsMma;
         const int nj = min(kShrinkRowsMma, r - j0);
         const int k0 = ks * kKSlice;
-        const int nk = min(kKSlice, a.H_in - k0);
+        const int nk = min(kKSlice, J.H_in - k0);
         const int page = lane < nj ? M[poff + j0 + lane] : 0;
         if (lane < kTokChunkMma) sh->tok[lane] = lane < ntok ? M[toff + lane] : -1;
         if (lane == 0) {
             mbar_init(&bars[0], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_arrive_expect_tx(&bars[0], (uint32_t)(nj * nk * ES));
-            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
+            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
             sh->voff = gc_field(M, gc, GC_VOFF);
         }
         __syncwarp();
         if (lane < nj)
-            bulk_g2s(abuf + lane * kAPitch, a.poolA + ((size_t)page * a.H_in + k0) * ES, (uint32_t)(nk * ES), &bars[0],
+            bulk_g2s(abuf + lane * kAPitch, J.A + ((size_t)page * J.H_in + k0) * ES, (uint32_t)(nk * ES), &bars[0],
                      policy_evict_first());
     }
     pdl_launch_dependents();
     __syncthreads();
+    const DecodeJob J = a.jobs[sh->job];
     const int g = lane >> 2, c = lane & 3;
     const int ks = sh->ks, ntok = sh->ntok, nj = sh->nj;
     const int k0 = ks * kKSlice;
-    const int nk = min(kKSlice, a.H_in - k0);
+    const int nk = min(kKSlice, J.H_in - k0);
     // x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
     pdl_wait_cta();
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     uint4 xr[kKBlocks];
     {
         const int tk = g < ntok ? sh->tok[g] : -1;
-        const char* xrow = a.x + ((size_t)(tk < 0 ? 0 : tk) * a.H_in + k0) * ES;
+        const char* xrow = J.x + ((size_t)(tk < 0 ? 0 : tk) * J.H_in + k0) * ES;
 #pragma unroll
         for (int b = 0; b < kKBlocks; ++b) {
             const int k = warp * kKPerWarp + b * 32 + c * 8;
@@ -645,7 +672,7 @@ constexpr int kExpandMmaSmem = 256 + 64 + 2 * kTokChunkMma * kVPitch + kExpandBy
                                kTokChunkMma * (kMaxNcols * 2 + kPitchPad);
 
 template <int W>
-__global__ void __launch_bounds__(kConsumerThreads)
+__global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 CTAs per SM */
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     constexpr int ES = 2;
     extern __shared__ __align__(128) char smem[];
@@ -665,7 +692,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
     int tok = 0;
     if (warp == 0) {
         // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
+        const int job = job_of(ue, a.n_jobs, a.job_expand_base);
         const int gc = find_gc_warp(M, a.n_gc, GC_EXPAND_BASE, ue, lane);
+        const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
         const int ntok = gc_field(M, gc, GC_NTOK);
         const int local = ue - gc_field(M, gc, GC_EXPAND_BASE);
@@ -673,7 +702,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int toff = gc_field(M, gc, GC_TOK_OFF);
         const int c = expand_ncols(r, ES);
         const int n0 = local * c;
-        const int nc = min(c, a.H_out - n0);
+        const int nc = min(c, J.H_out - n0);
         const int bpitch = c * ES + kPitchPad;
         int pages[LORA_MAX_RANK / 32];
 #pragma unroll
@@ -685,7 +714,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             mbar_init(&bars[1], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
-            sh->gc = gc; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
+            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
             sh->voff = gc_field(M, gc, GC_VOFF);
             sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
         }
@@ -697,12 +726,13 @@ __global__ void __launch_bounds__(kConsumerThreads)
         for (int q = 0; q < LORA_MAX_RANK / 32; ++q) {
             const int j = q * 32 + lane;
             if (j < r)
-                bulk_g2s(bbuf + (size_t)j * bpitch, a.poolB + ((size_t)pages[q] * a.H_out + n0) * ES, row_bytes,
+                bulk_g2s(bbuf + (size_t)j * bpitch, J.B + ((size_t)pages[q] * J.H_out + n0) * ES, row_bytes,
                          &bars[0], pol);
         }
     }
     pdl_launch_dependents();
     __syncthreads();
+    const DecodeJob J = a.jobs[sh->job];
     const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
     const int c = expand_ncols(r, ES);
     const int bpitch = c * ES + kPitchPad;
@@ -714,7 +744,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * ES));
         __syncwarp();
         if (lane < ntok)
-            bulk_g2s(ybuf + lane * ypitch, a.y + ((size_t)tok * a.H_out + n0) * ES, (uint32_t)nc * ES, &bars[1],
+            bulk_g2s(ybuf + lane * ypitch, J.y + ((size_t)tok * J.H_out + n0) * ES, (uint32_t)nc * ES, &bars[1],
                      policy_evict_normal());
     }
     // v (fp32, summed over k-slices, scaled) -> bf16 hi/lo tiles [8 tokens][r padded to 16]
@@ -729,10 +759,10 @@ __global__ void __launch_bounds__(kConsumerThreads)
                 // k-slice partials: batches of 8 independent loads, summed in slice order
                 const float* src = a.vbuf + voff + t * r + j;
                 const int stride = ntok * r;
-                for (int k0 = 0; k0 < a.ksplit; k0 += 8) {
+                for (int k0 = 0; k0 < J.ksplit; k0 += 8) {
                     float p[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) p[q] = k0 + q < a.ksplit ? ld_cg_f32(src + (k0 + q) * stride) : 0.f;
+                    for (int q = 0; q < 8; ++q) p[q] = k0 + q < J.ksplit ? ld_cg_f32(src + (k0 + q) * stride) : 0.f;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) v += p[q];
                 }
@@ -820,7 +850,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             const float4 d1 = *reinterpret_cast<const float4*>(dt + t * dpitch + q * 8 + 4);
             const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
             const uint4 yo = lds128(ybuf + t * ypitch + q * 16);
-            stg128_na(a.y + ((size_t)sh->tok[t] * a.H_out + n0 + q * 8) * ES, Elem<__nv_bfloat16>::add_round(yo, d));
+            stg128_na(J.y + ((size_t)sh->tok[t] * J.H_out + n0 + q * 8) * ES, Elem<__nv_bfloat16>::add_round(yo, d));
         }
     }
     if (a.trace && tid == 0) {
@@ -902,19 +932,27 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
 template <typename T>
 static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {
     DecodeArgs a;
-    a.x = static_cast<const char*>(L.x);
-    a.y = static_cast<char*>(L.y);
-    a.poolA = static_cast<const char*>(L.poolA);
-    a.poolB = static_cast<const char*>(L.poolB);
+    memset(&a, 0, sizeof(a));
+    for (int j = 0; j < L.n_jobs && j < kMaxJobs; ++j) {
+        const void* x = j == 0 ? L.x : L.more[j - 1].x;
+        void* y = j == 0 ? L.y : L.more[j - 1].y;
+        const void* A = j == 0 ? L.poolA : L.more[j - 1].poolA;
+        const void* B = j == 0 ? L.poolB : L.more[j - 1].poolB;
+        const int hin = j == 0 ? L.H_in : L.more[j - 1].H_in, hout = j == 0 ? L.H_out : L.more[j - 1].H_out;
+        a.jobs[j] = DecodeJob{static_cast<const char*>(x), static_cast<char*>(y), static_cast<const char*>(A),
+                              static_cast<const char*>(B), hin, hout, ksplit_of(hin, (int)sizeof(T)), 0};
+    }
     a.vbuf = L.vbuf;
     a.meta_global = L.meta_dev;
     a.trace = L.trace;
-    a.H_in = L.H_in;
-    a.H_out = L.H_out;
     a.n_shrink = pl.n_shrink;
     a.n_expand = pl.n_expand;
     a.n_gc = pl.n_gc;
-    a.ksplit = ksplit_of(L.H_in, (int)sizeof(T));
+    a.n_jobs = pl.n_jobs;
+    for (int j = 0; j < kMaxJobs; ++j) {
+        a.job_shrink_base[j] = pl.job_shrink_base[j];
+        a.job_expand_base[j] = pl.job_expand_base[j];
+    }
     const int n = (int)pl.blob.size();
     if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases);
     if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases);

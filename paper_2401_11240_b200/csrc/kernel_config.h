@@ -26,8 +26,9 @@ constexpr int kMaxNcols = 1024;                   // columns per expand unit
 
 // metadata blob layout (int32 words)
 constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, pad, pad
-constexpr int kGcFields = 8;     // rank, page_off, tok_off, ntok, shrink_base, expand_base, voff, scale_bits
-enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE };
+constexpr int kGcFields = 9;     // rank, page_off, tok_off, ntok, shrink_base, expand_base, voff, scale_bits, job
+enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB };
+constexpr int kMaxJobs = 4;      // pools fused into one launch pair by lora_apply_multi (e.g. q, k, v)
 
 LORA_HD int vec_elems(int esz) { return 16 / esz; }             // elements per 16-B vector
 LORA_HD int tok_chunk(int esz) { return esz == 2 ? kTokChunkMma : kTokChunk; }

@@ -177,6 +177,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         e[GC_EXPAND_BASE] = expand;
         e[GC_VOFF] = (int32_t)voff;
         e[GC_SCALE] = f32_bits(pl.group_scale[g]);
+        e[GC_JOB] = 0;
         shrink += ksplit * shrink_jblocks(r, esz);
         const int nc = expand_ncols(r, esz);
         expand += (H_out + nc - 1) / nc;
@@ -188,6 +189,64 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     hdr[0] = n_gc; hdr[1] = shrink; hdr[2] = expand;
     hdr[3] = (int32_t)blob_pages.size(); hdr[4] = (int32_t)blob_toks.size(); hdr[5] = ksplit;
     pl.n_shrink = shrink; pl.n_expand = expand; pl.vbuf_floats = voff;
+    return LORA_OK;
+}
+
+lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& err) {
+    m = Plan();
+    if (n < 1 || n > kMaxJobs) { err = "between 1 and 4 pools per fused apply"; return LORA_ERR_ARG; }
+    int n_gc = 0, n_pages = 0, n_toks = 0;
+    for (int p = 0; p < n; ++p) {
+        const int32_t* h = plans[p]->blob.data();
+        if (plans[p]->blob.empty()) continue;
+        n_gc += h[0];
+        n_pages += h[3];
+        n_toks += h[4];
+    }
+    m.blob.assign(kHdrWords + (size_t)kGcFields * n_gc + n_pages + n_toks, 0);
+    const int pages_base = kHdrWords + kGcFields * n_gc, toks_base = pages_base + n_pages;
+    int gc = 0, pg = 0, tk = 0, shrink = 0, expand = 0;
+    int64_t voff = 0;
+    for (int p = 0; p < n; ++p) {
+        const Plan& q = *plans[p];
+        if (q.blob.empty() || q.n_gc == 0) continue;
+        const int32_t* h = q.blob.data();
+        m.job_shrink_base[p] = shrink;
+        m.job_expand_base[p] = expand;
+        const int qpb = kHdrWords + kGcFields * h[0], qtb = qpb + h[3];
+        for (int c = 0; c < h[0]; ++c) {
+            const int32_t* e = h + kHdrWords + kGcFields * c;
+            int32_t* o = m.blob.data() + kHdrWords + kGcFields * gc;
+            for (int f = 0; f < kGcFields; ++f) o[f] = e[f];
+            o[GC_PAGE_OFF] = pages_base + pg + (e[GC_PAGE_OFF] - qpb);
+            o[GC_TOK_OFF] = toks_base + tk + (e[GC_TOK_OFF] - qtb);
+            o[GC_SHRINK_BASE] = e[GC_SHRINK_BASE] + shrink;
+            o[GC_EXPAND_BASE] = e[GC_EXPAND_BASE] + expand;
+            o[GC_VOFF] = (int32_t)(e[GC_VOFF] + voff);
+            o[GC_JOB] = p;
+            ++gc;
+        }
+        std::copy(h + qpb, h + qpb + h[3], m.blob.begin() + pages_base + pg);
+        std::copy(h + qtb, h + qtb + h[4], m.blob.begin() + toks_base + tk);
+        pg += h[3];
+        tk += h[4];
+        shrink += q.n_shrink;
+        expand += q.n_expand;
+        voff += q.vbuf_floats;
+    }
+    if (voff > INT32_MAX) { err = "fused batch too large for the SIMT scratch"; return LORA_ERR_ARG; }
+    int32_t* h = m.blob.data();
+    h[0] = n_gc; h[1] = shrink; h[2] = expand; h[3] = n_pages; h[4] = n_toks; h[5] = 0;
+    for (int p = 0; p < n; ++p)
+        if (plans[p]->blob.empty() || plans[p]->n_gc == 0) {   // empty jobs own no units
+            m.job_shrink_base[p] = p + 1 < n ? 0x7fffffff : 0x7fffffff;
+            m.job_expand_base[p] = 0x7fffffff;
+        }
+    m.n_jobs = n;
+    m.n_gc = n_gc;
+    m.n_shrink = shrink;
+    m.n_expand = expand;
+    m.vbuf_floats = voff;
     return LORA_OK;
 }
 

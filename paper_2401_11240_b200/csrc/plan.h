@@ -39,6 +39,9 @@ struct Plan {
     std::vector<int32_t> blob;           // see kernel_config.h for the layout
     int32_t n_gc = 0, n_shrink = 0, n_expand = 0;
     int64_t vbuf_floats = 0;
+    int32_t n_jobs = 1;                          // pools fused by lora_apply_multi
+    int32_t job_shrink_base[4] = {0, 0, 0, 0};   // first shrink / expand unit of each job
+    int32_t job_expand_base[4] = {0, 0, 0, 0};
     // ---- tcgen05 prefill work (N2) ----
     std::vector<PrefillSeg> prefill;
     int32_t n_prefill_tiles = 0;     // == n_pf_tiles (128-token tiles on the tensor-core path)
@@ -63,6 +66,14 @@ struct DecodeLaunch {
     unsigned long long* trace;   // optional per-unit timestamps (lora_debug_set_trace), or null
     int H_in, H_out, esz, num_sms;
     int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel
+    struct More {                // jobs 1.. of a fused multi-pool apply (job 0 = the fields above)
+        const void* x;
+        void* y;
+        const void* poolA;
+        const void* poolB;
+        int H_in, H_out;
+    } more[3];
+    int n_jobs = 1;
 };
 struct PrefillLaunch {
     const void* x;
@@ -73,6 +84,10 @@ struct PrefillLaunch {
     unsigned long long* trace;
     int T, H_in, H_out, zero_page, num_sms;
 };
+
+// Concatenates the SIMT work lists of plans[0..n) (one per fused pool = job index) into merged
+// (only the kernel-work fields of merged are meaningful).
+lora_status merge_plans(const Plan* const* plans, int n, Plan& merged, std::string& err);
 }  // namespace lora
 
 // implemented in the .cu files (declared here so host code needs no CUDA headers)

@@ -51,6 +51,7 @@ struct lora_pool {
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
     Plan plan;
+    Plan fused;                          // merged kernel work of the last lora_apply_multi led by this pool
     int L_tc = 64;
     int64_t launches = 0;
     bool split_ready = false;             // a lora_apply_shrink awaits its lora_apply_expand
@@ -410,6 +411,90 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
 lora_status lora_apply(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr, const int32_t* adapter_ids,
                        int num_segments, void* stream) {
     return apply_impl(p, x, y, seg_indptr, adapter_ids, num_segments, stream, 0, nullptr, 0);
+}
+
+lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, void* const* ys, int n_pools,
+                             const int32_t* seg_indptr, const int32_t* adapter_ids, int num_segments, void* stream) {
+    if (!pools || !xs || !ys) return fail(LORA_ERR_ARG, "pools/xs/ys is NULL");
+    if (n_pools < 1 || n_pools > kMaxJobs) return fail(LORA_ERR_ARG, "n_pools must be in [1, 4]");
+    if (n_pools == 1) return lora_apply(pools[0], xs[0], ys[0], seg_indptr, adapter_ids, num_segments, stream);
+    lora_pool* p0 = pools[0];
+    for (int i = 0; i < n_pools; ++i) {
+        lora_pool* p = pools[i];
+        if (!p) return fail(LORA_ERR_ARG, "pools[" + std::to_string(i) + "] is NULL");
+        if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "apply on a host-only pool");
+        if (p->device != p0->device || p->esz != p0->esz)
+            return fail(LORA_ERR_ARG, "fused pools must share device and dtype");
+        for (int j = 0; j < i; ++j)
+            if (pools[j] == p) return fail(LORA_ERR_ARG, "a pool appears twice in one fused apply");
+        if (!xs[i] || !ys[i]) return fail(LORA_ERR_ARG, "x/y of pool " + std::to_string(i) + " is NULL");
+        if (((uintptr_t)xs[i] & 15) || ((uintptr_t)ys[i] & 15)) return fail(LORA_ERR_ALIGN, "x and y must be 16-byte aligned");
+    }
+    if (num_segments < 0) return fail(LORA_ERR_ARG, "num_segments < 0");
+    if (num_segments == 0) return LORA_OK;
+    if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
+    const int T = seg_indptr[num_segments];
+    DeviceGuard g(p0->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: pending CUDA error");
+    }
+    // plans first (all validation before any launch: a failed call has no side effects)
+    std::string err;
+    for (int i = 0; i < n_pools; ++i) {
+        lora_pool* p = pools[i];
+        lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
+                                   p->tc_prefill, p->table, err);
+        if (s != LORA_OK) return fail(s, "pool " + std::to_string(i) + ": " + err);
+        p->split_ready = false;
+    }
+    if (T == 0) return LORA_OK;
+    const Plan* parts[kMaxJobs];
+    for (int i = 0; i < n_pools; ++i) parts[i] = &pools[i]->plan;
+    lora_status s = merge_plans(parts, n_pools, p0->fused, err);
+    if (s != LORA_OK) return fail(s, err);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply_multi: capture query");
+    for (int i = 0; i < n_pools; ++i) {
+        lora_pool* p = pools[i];
+        for (int gi = 0; gi < p->plan.G; ++gi) {
+            AdapterRec& a = p->table.at(p->plan.group_id[gi]);
+            if (a.ready_known) continue;
+            cudaError_t e = cudaEventQuery((cudaEvent_t)a.ready);
+            if (e == cudaSuccess) { a.ready_known = true; continue; }
+            if (e != cudaErrorNotReady) return cuda_fail(e, "lora_apply_multi: load event");
+            cudaGetLastError();
+            CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a.ready,
+                                         cap == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0),
+                     "lora_apply_multi: wait load");
+        }
+    }
+    const Plan& fz = p0->fused;
+    int launches = 0;
+    if (fz.n_gc > 0) {
+        if ((s = grow(p0->vbuf, p0->vbuf_cap, (size_t)std::max<int64_t>(fz.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
+        if ((s = grow(p0->meta_dev, p0->meta_cap, fz.blob.size(), false, "meta")) != LORA_OK) return s;
+        DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
+                       p0->num_sms};
+        L.n_jobs = n_pools;
+        for (int i = 1; i < n_pools; ++i)
+            L.more[i - 1] = DecodeLaunch::More{xs[i], ys[i], pools[i]->dA, pools[i]->dB, pools[i]->H_in, pools[i]->H_out};
+        cudaError_t e = (cudaError_t)launch_decode(fz, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: decode kernel launch");
+    }
+    for (int i = 0; i < n_pools; ++i) {
+        lora_pool* p = pools[i];
+        if (p->plan.n_pf_tiles == 0) continue;
+        PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
+        cudaError_t e = (cudaError_t)launch_prefill(p->plan, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: prefill kernel launch");
+    }
+    p0->launches += launches;
+    for (int i = 0; i < n_pools; ++i)
+        if (std::find(pools[i]->apply_streams.begin(), pools[i]->apply_streams.end(), st) == pools[i]->apply_streams.end())
+            pools[i]->apply_streams.push_back(st);
+    return LORA_OK;
 }
 
 lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_indptr, const int32_t* adapter_ids,

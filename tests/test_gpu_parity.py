@@ -326,3 +326,31 @@ def test_unknown_adapter_on_apply_has_no_side_effect(L):
         pool.load_adapter(9, 2, np.zeros((2, 64), np.float32), np.zeros((2, 64), np.float32), 1.0)
     assert ei.value.name == "LORA_ERR_NOT_PINNED"
     pool.close()
+
+
+def test_apply_multi_qkv_fused_equals_separate(L):
+    """lora_apply_multi over 3 pools (q, k, v of one layer; k/v with GQA-like narrower output) in
+    one launch pair == three separate lora_apply calls, bit for bit, and within tolerance of the oracle."""
+    import torch
+    shapes = [(512, 512), (512, 128), (512, 128)]
+    batches = []
+    for i, (hin, hout) in enumerate(shapes):
+        b = gen.build_batch("m%d" % i, 900 + i, "bf16", hin, hout, [1] * 24 + [3, 70], list(range(24)) + [2, 5],
+                            {a: [8, 16, 32, 64][a % 4] for a in range(24)}, y_zero=False)
+        batches.append(b)
+    batches[1].x = batches[0].x.copy()
+    batches[2].x = batches[0].x.copy()
+    pools = [make_pool(b, L) for b in batches]
+    xs = [to_torch(b.x, "cuda") for b in batches]
+    y_sep = [to_torch(b.y_in, "cuda") for b in batches]
+    y_fus = [to_torch(b.y_in, "cuda") for b in batches]
+    for p, x, y, b in zip(pools, xs, y_sep, batches):
+        p.apply(x, y, b.seg_indptr, b.adapter_ids)
+    L.apply_multi(pools, xs, y_fus, batches[0].seg_indptr, batches[0].adapter_ids)
+    torch.cuda.synchronize()
+    for b, ys_, yf in zip(batches, y_sep, y_fus):
+        assert torch.equal(ys_, yf)
+        ref = O.delta_for_batch(b, n_threads=8)
+        assert rel_l2(from_torch(yf, "bf16"), ref, "bf16") <= TOL["bf16"]
+    for p in pools:
+        p.close()
