@@ -74,6 +74,8 @@ typedef enum {
 #define LORA_OPT_TC_THRESHOLD 1    /* L_tc (default 64); segments with len >= L_tc take the tcgen05 path.
                                       A value larger than any segment forces the SIMT path everywhere. */
 #define LORA_OPT_RESERVE_TOKENS 2  /* pre-size scratch for this many tokens (avoids a cudaMalloc in apply) */
+#define LORA_OPT_DECODE_FUSED 3    /* bf16 decode as ONE grid per apply (1) or a PDL-chained (0, default)
+                                      shrink/expand kernel pair (0).  Same arithmetic, bitwise equal. */
 
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.

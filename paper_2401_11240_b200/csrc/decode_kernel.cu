@@ -46,6 +46,10 @@ struct DecodeArgs {
     const int32_t* meta_global;  // metadata in device memory (large batches) or null
     unsigned long long* trace;   // debug: per-unit timestamps, or null
     int n_shrink, n_expand, n_gc, n_jobs;
+    int unit_tab;                // blob word offset of the per-unit table (plan.cpp append_unit_table)
+    // bf16 expand smem layout, sized per launch from the batch (max rank / tokens / columns)
+    int e_vpitch, e_boff, e_yoff, e_dtoff, e_pgoff, e_smem;
+    int* gc_sync;                // fused mode: [n_gc] shrink-done, [n_gc] expand-done counters; gc_sync[-1] = timeout flag
     int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
     int job_expand_base[kMaxJobs];
 };
@@ -90,6 +94,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// per-thread 16-B async copy HBM -> SMEM (LDGSTS): no per-request copy-engine overhead, so it
+// keeps up with HBM for sub-2-KB row slices where cp.async.bulk does not (scripts/microbench_stream.cu)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(policy)
+                 : "memory");
+}
+// L2 prefetch (no data returned to the SM).  Safe before griddepcontrol.wait even for lines a
+// preceding kernel still writes: L2 is the point of coherence, the later real read sees them.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -100,6 +118,11 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ unsigned long long gtime_raw() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // one thread waits on the preceding grid, the rest park at the barrier (a waiting
@@ -107,6 +130,27 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_wait_cta() {
     if (threadIdx.x == 0) pdl_wait();
     __syncthreads();
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// waits until *p >= target; gives up after ~0.5 s (a scheduling assumption broke: the result is
+// wrong, but the device stays alive and the host sees *err != 0 on the pool's next apply)
+__device__ __forceinline__ void spin_acquire_geq(const int* p, int target, int* err) {
+    if (ld_acquire(p) >= target) return;
+    const unsigned long long t0 = gtime_raw();
+    while (ld_acquire(p) < target) {
+        __nanosleep(64);
+        if (gtime_raw() - t0 > 500000000ull) {
+            atomicExch(err, 1);
+            break;
+        }
+    }
 }
 __device__ __forceinline__ float ld_cg_f32(const float* p) {
     float v;
@@ -185,21 +229,6 @@ struct Elem<float> {
 // ------------------------------------------------------------------ metadata access
 __device__ __forceinline__ int gc_field(const int32_t* M, int gc, int f) { return M[kHdrWords + gc * kGcFields + f]; }
 
-// Warp-cooperative: the last gc whose base (field f) <= u (bases strictly increase over gc).
-// One metadata round trip per 32 gcs instead of a log2(n_gc)-deep dependent search.
-__device__ __forceinline__ int find_gc_warp(const int32_t* M, int n_gc, int f, int u, int lane) {
-    int res = 0;
-    for (int base = 0; base < n_gc; base += 32) {
-        const int i = base + lane;
-        const int v = i < n_gc ? gc_field(M, i, f) : 0x7fffffff;
-        const unsigned m = __ballot_sync(0xffffffffu, v <= u);
-        if (m == 0u) break;
-        res = base + 31 - __clz(m);
-        if (!(m & 0x80000000u)) break;
-    }
-    return res;
-}
-
 // per-CTA unit description, decoded once by warp 0 and shared through smem
 struct UnitSh {
     int job;
@@ -236,11 +265,12 @@ __global__ void __launch_bounds__(kConsumerThreads)
         // 1. decode the unit and issue the adapter-row loads (immutable pool pages) before
         //    waiting on the previous kernel in the stream
         const int job = job_of(u, a.n_jobs, a.job_shrink_base);
-        const int gc = find_gc_warp(M, a.n_gc, GC_SHRINK_BASE, u, lane);
+        const uint32_t uw = (uint32_t)M[a.unit_tab + kUnitWords * u];   // (gc, index in gc)
+        const int gc = (int)(uw >> 16);
         const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
         const int ntok = gc_field(M, gc, GC_NTOK);
-        const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
+        const int local = (int)(uw & 0xffffu);
         const int poff = gc_field(M, gc, GC_PAGE_OFF);
         const int toff = gc_field(M, gc, GC_TOK_OFF);
         const int njb = shrink_jblocks(r, E::kSize);
@@ -331,6 +361,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     if (a.trace && tid == 0) {
         a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 4] = sh->r;
         a.trace[(size_t)u * 8 + 5] = gtime();
     }
 }
@@ -363,11 +394,12 @@ __global__ void __launch_bounds__(kConsumerThreads)
     if (warp == 0) {
         // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
         const int job = job_of(ue, a.n_jobs, a.job_expand_base);
-        const int gc = find_gc_warp(M, a.n_gc, GC_EXPAND_BASE, ue, lane);
+        const uint32_t uw = (uint32_t)M[a.unit_tab + kUnitWords * (a.n_shrink + ue)];
+        const int gc = (int)(uw >> 16);
         const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
         const int ntok = gc_field(M, gc, GC_NTOK);
-        const int local = ue - gc_field(M, gc, GC_EXPAND_BASE);
+        const int local = (int)(uw & 0xffffu);
         const int poff = gc_field(M, gc, GC_PAGE_OFF);
         const int toff = gc_field(M, gc, GC_TOK_OFF);
         const int c = expand_ncols(r, E::kSize);
@@ -497,6 +529,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     }
     if (a.trace && tid == 0) {
         a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 4] = sh->r;
         a.trace[(size_t)u * 8 + 5] = gtime();
     }
 }
@@ -557,44 +590,47 @@ constexpr int kKBlocks = kKPerWarp / 32;              // 4
 constexpr int kAPitch = kKSlice * 2 + 64;             // bf16 row pitch: rows g, g+1 land 16 banks apart
 constexpr int kShrinkMmaSmem = 1024 + kShrinkRowsMma * kAPitch + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
 
-template <int W>
-__global__ void __launch_bounds__(kConsumerThreads)
-    lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+// FUSED: the unit runs inside lora_decode_fused_kernel and publishes its v partials to the
+// gc's expand units with a release-increment of the gc's counter (see that kernel).
+template <bool FUSED>
+__device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32_t* M, const int u, char* smem) {
     constexpr int ES = 2;
-    extern __shared__ __align__(128) char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                    // [0] A rows
     UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
     char* abuf = smem + 1024;                                              // [16 rows][kAPitch]
     float* part = reinterpret_cast<float*>(abuf + kShrinkRowsMma * kAPitch);   // [warp][16 rows][8 tokens]
-    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u = blockIdx.x;
-    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
-    if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
 
     if (warp == 0) {
+        if (lane == 0) {   // barrier init first: its fence overlaps the metadata round trip
+            mbar_init(&bars[0], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         const int job = job_of(u, a.n_jobs, a.job_shrink_base);
-        const int gc = find_gc_warp(M, a.n_gc, GC_SHRINK_BASE, u, lane);
+        // round 1: the unit record (independent uniform loads)
+        const int32_t* rec = M + a.unit_tab + kUnitWords * u;
+        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[3];
+        const int pg0 = rec[1], toff = rec[2];
+        const int gc = (int)(uw >> 16), local = (int)(uw & 0xffffu);
+        const int r = (int)(rn >> 16), ntok = (int)(rn & 0xffffu);
         const DecodeJob J = a.jobs[job];
-        const int r = gc_field(M, gc, GC_RANK);
-        const int ntok = gc_field(M, gc, GC_NTOK);
-        const int local = u - gc_field(M, gc, GC_SHRINK_BASE);
-        const int poff = gc_field(M, gc, GC_PAGE_OFF);
-        const int toff = gc_field(M, gc, GC_TOK_OFF);
         const int njb = shrink_jblocks(r, ES);
         const int ks = local / njb;
         const int j0 = (local - ks * njb) * kShrinkRowsMma;
         const int nj = min(kShrinkRowsMma, r - j0);
         const int k0 = ks * kKSlice;
         const int nk = min(kKSlice, J.H_in - k0);
-        const int page = lane < nj ? M[poff + j0 + lane] : 0;
-        if (lane < kTokChunkMma) sh->tok[lane] = lane < ntok ? M[toff + lane] : -1;
+        // round 2: pages, tokens, v offset
+        const int page = lane < nj ? M[pg0 + lane] : 0;
+        const int tokv = lane < ntok ? M[toff + lane] : -1;
+        const int voff = gc_field(M, gc, GC_VOFF);
+        if (a.trace) { asm volatile("" ::"r"(page), "r"(tokv)); if (lane == 0) a.trace[(size_t)u * 8 + 7] = gtime(); }
+        if (lane < kTokChunkMma) sh->tok[lane] = tokv;
+        if (tokv >= 0) prefetch_l2(J.x + ((size_t)tokv * J.H_in + k0) * ES, (uint32_t)(nk * ES));
         if (lane == 0) {
-            mbar_init(&bars[0], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             mbar_arrive_expect_tx(&bars[0], (uint32_t)(nj * nk * ES));
             sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
-            sh->voff = gc_field(M, gc, GC_VOFF);
+            sh->voff = voff;
         }
         __syncwarp();
         if (lane < nj)
@@ -602,6 +638,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
                      policy_evict_first());
     }
     pdl_launch_dependents();
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 6] = gtime();
     __syncthreads();
     const DecodeJob J = a.jobs[sh->job];
     const int g = lane >> 2, c = lane & 3;
@@ -657,49 +694,73 @@ __global__ void __launch_bounds__(kConsumerThreads)
         for (int w = 0; w < kConsumerWarps; ++w) v += part[(w * kShrinkRowsMma + row) * kTokChunkMma + t];
         a.vbuf[sh->voff + (ks * ntok + t) * r + j0 + row] = v;
     }
+    if (FUSED) {
+        __syncthreads();   // every v store of the CTA precedes thread 0's release
+        if (tid == 0) red_release_add(a.gc_sync + sh->gc, 1);
+    }
     if (a.trace && tid == 0) {
         a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 4] = sh->r;
         a.trace[(size_t)u * 8 + 5] = gtime();
     }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kConsumerThreads)
+    lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    extern __shared__ __align__(128) char smem[];
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)blockIdx.x * 8 + 1] = gtime();
+    if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
+    shrink_mma_body<false>(a, M, blockIdx.x, smem);
 }
 
 // ---- expand (bf16): one CTA = (group-chunk gc, column slice [n0, n0+nc)).  Swap-AB:
 // D[col][token] = B^T[col][rank] · v^T[rank][token], M = 16 columns, N = 8 tokens, K = 16
 // ranks; v is split into bf16 hi + lo parts (two MMAs) so v keeps fp32-level accuracy.
 // D is added into the y tile staged in smem (one rounding) and written back with 16-B stores.
-constexpr int kVPitch = (LORA_MAX_RANK + 8) * 2;   // bf16 v row pitch (bytes)
-constexpr int kExpandMmaSmem = 256 + 64 + 2 * kTokChunkMma * kVPitch + kExpandBytes + LORA_MAX_RANK * kPitchPad +
-                               kTokChunkMma * (kMaxNcols * 2 + kPitchPad);
+// smem: [0,256) barriers + UnitSh | 64 zero bytes | v hi, v lo [8 tokens][e_vpitch] bf16 |
+// B rows [r][c + pad] | y rows [ntok][c + pad] | D^T fp32 [ntok][c + 4] | pages [r]; the region
+// sizes follow the launch's largest rank / token chunk / column slice (expand_smem_layout).
+constexpr int kExpandMmaSmemMax = 320 + 2 * kTokChunkMma * ((LORA_MAX_RANK + 8) * 2) + kExpandBytes +
+                                  LORA_MAX_RANK * kPitchPad + kTokChunkMma * (kMaxNcols * 2 + kPitchPad) +
+                                  kTokChunkMma * (kMaxNcols + 4) * 4 + LORA_MAX_RANK * 4;
+constexpr int kBulkMinBytes = 2048;   // B row slices at least this long go through cp.async.bulk
 
-template <int W>
-__global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 CTAs per SM */
-    lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+// FUSED: v comes from shrink units of the same grid; thread 0 acquires the gc's counter
+// (all n_s shrink units released) instead of a grid dependency, and the gc's last expand unit
+// to finish reading v re-arms the counters for the pool's next apply.
+template <bool FUSED>
+__device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32_t* M, const int ue, char* smem) {
     constexpr int ES = 2;
-    extern __shared__ __align__(128) char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);          // [0] B rows, [1] y rows
     UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
     char* zero = smem + 256;                                      // 64 zero bytes
-    char* vhi = smem + 256 + 64;                                  // [8 tokens][kVPitch] bf16
-    char* vlo = vhi + kTokChunkMma * kVPitch;
-    char* bbuf = vlo + kTokChunkMma * kVPitch;                    // [r][c + pad]
-    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int vpitch = a.e_vpitch;
+    char* vhi = smem + 320;                                       // [8 tokens][vpitch] bf16
+    char* vlo = vhi + kTokChunkMma * vpitch;
+    char* bbuf = smem + a.e_boff;                                 // [r][c + pad]
+    char* ybuf = smem + a.e_yoff;                                 // [ntok][c + pad]
+    float* dt = reinterpret_cast<float*>(smem + a.e_dtoff);      // [ntok][nc + 4]
+    int* spages = reinterpret_cast<int*>(smem + a.e_pgoff);       // [r]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ue = blockIdx.x;
     const int u = ue + a.n_shrink;
-    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
-    if (W == 1) pdl_wait_cta();
 
     int tok = 0;
     if (warp == 0) {
         // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
+        if (lane == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         const int job = job_of(ue, a.n_jobs, a.job_expand_base);
-        const int gc = find_gc_warp(M, a.n_gc, GC_EXPAND_BASE, ue, lane);
+        const int32_t* rec = M + a.unit_tab + kUnitWords * (a.n_shrink + ue);
+        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[3];
+        const int poff = rec[1], toff = rec[2];
+        const int gc = (int)(uw >> 16), local = (int)(uw & 0xffffu);
+        const int r = (int)(rn >> 16), ntok = (int)(rn & 0xffffu);
         const DecodeJob J = a.jobs[job];
-        const int r = gc_field(M, gc, GC_RANK);
-        const int ntok = gc_field(M, gc, GC_NTOK);
-        const int local = ue - gc_field(M, gc, GC_EXPAND_BASE);
-        const int poff = gc_field(M, gc, GC_PAGE_OFF);
-        const int toff = gc_field(M, gc, GC_TOK_OFF);
         const int c = expand_ncols(r, ES);
         const int n0 = local * c;
         const int nc = min(c, J.H_out - n0);
@@ -709,36 +770,67 @@ __global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 C
         for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? M[poff + q * 32 + lane] : 0;
         tok = lane < ntok ? M[toff + lane] : 0;
         const uint32_t row_bytes = (uint32_t)nc * ES;
+        const bool bulk = row_bytes >= kBulkMinBytes;
         if (lane == 0) {
-            mbar_init(&bars[0], 1);
-            mbar_init(&bars[1], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
+            if (bulk) mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
             sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
             sh->voff = gc_field(M, gc, GC_VOFF);
             sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
+            if (FUSED) {   // unit counts of this gc (bases are global over the fused jobs)
+                const bool last = gc + 1 >= a.n_gc;
+                sh->ks = (last ? a.n_shrink : gc_field(M, gc + 1, GC_SHRINK_BASE)) - gc_field(M, gc, GC_SHRINK_BASE);
+                sh->nj = (last ? a.n_expand : gc_field(M, gc + 1, GC_EXPAND_BASE)) - gc_field(M, gc, GC_EXPAND_BASE);
+            }
         }
-        if (lane < ntok) sh->tok[lane] = tok;
+        if (lane < ntok) {
+            sh->tok[lane] = tok;
+            prefetch_l2(J.y + ((size_t)tok * J.H_out + n0) * ES, row_bytes);
+        }
         if (lane < 16) reinterpret_cast<uint32_t*>(zero)[lane] = 0u;
         __syncwarp();
         const uint64_t pol = policy_evict_first();
+        if (bulk) {
 #pragma unroll
-        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) {
-            const int j = q * 32 + lane;
-            if (j < r)
-                bulk_g2s(bbuf + (size_t)j * bpitch, J.B + ((size_t)pages[q] * J.H_out + n0) * ES, row_bytes,
-                         &bars[0], pol);
+            for (int q = 0; q < LORA_MAX_RANK / 32; ++q) {
+                const int j = q * 32 + lane;
+                if (j < r)
+                    bulk_g2s(bbuf + (size_t)j * bpitch, J.B + ((size_t)pages[q] * J.H_out + n0) * ES, row_bytes,
+                             &bars[0], pol);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < LORA_MAX_RANK / 32; ++q)
+                if (q * 32 + lane < r) spages[q * 32 + lane] = pages[q];
         }
     }
-    pdl_launch_dependents();
     __syncthreads();
     const DecodeJob J = a.jobs[sh->job];
     const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
     const int c = expand_ncols(r, ES);
     const int bpitch = c * ES + kPitchPad;
     const int ypitch = c * ES + kPitchPad;
-    char* ybuf = bbuf + kExpandBytes + LORA_MAX_RANK * kPitchPad;   // after the whole B region
-    pdl_wait_cta();   // v from the shrink kernel, y from whoever wrote it
+    const bool bulk = nc * ES >= kBulkMinBytes;
+    if (!bulk) {
+        // sub-2-KB row slices: every thread streams 16-B pieces (a warp covers 512 contiguous bytes)
+        const uint64_t pol = policy_evict_first();
+        const int vpr = nc / 8;
+        for (int i = tid; i < r * vpr; i += kConsumerThreads) {
+            const int j = i / vpr, q = i - j * vpr;
+            cp_async16(bbuf + (size_t)j * bpitch + q * 16, J.B + ((size_t)spages[j] * J.H_out + n0 + q * 8) * ES, pol);
+        }
+        cp_async_commit();
+    }
+    pdl_launch_dependents();
+    if (FUSED) {
+        // y (and the counters) from the preceding grid; v from this grid's shrink units of the gc
+        if (tid == 0) {
+            pdl_wait();
+            spin_acquire_geq(a.gc_sync + sh->gc, sh->ks, a.gc_sync - 1);
+        }
+        __syncthreads();
+    } else {
+        pdl_wait_cta();   // v from the shrink kernel, y from whoever wrote it
+    }
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     if (warp == 0) {
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * ES));
@@ -770,12 +862,20 @@ __global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 C
             }
             const __nv_bfloat16 h = __float2bfloat16_rn(v);
             const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
-            *reinterpret_cast<__nv_bfloat16*>(vhi + t * kVPitch + j * 2) = h;
-            *reinterpret_cast<__nv_bfloat16*>(vlo + t * kVPitch + j * 2) = l;
+            *reinterpret_cast<__nv_bfloat16*>(vhi + t * vpitch + j * 2) = h;
+            *reinterpret_cast<__nv_bfloat16*>(vlo + t * vpitch + j * 2) = l;
         }
     }
+    if (!bulk) cp_async_wait_all();
     __syncthreads();
-    mbar_wait(&bars[0], 0);
+    if (FUSED && tid == 0) {
+        // every v read of this CTA is done: the gc's last expand unit re-arms its counters
+        if (atomicAdd(a.gc_sync + a.n_gc + sh->gc, 1) == sh->nj - 1) {
+            a.gc_sync[sh->gc] = 0;
+            a.gc_sync[a.n_gc + sh->gc] = 0;
+        }
+    }
+    if (bulk) mbar_wait(&bars[0], 0);
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
     const int ntiles = (nc + 15) / 16;
     const int ksteps = rp / 16;
@@ -785,62 +885,52 @@ __global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 C
     // B operand (v): lanes 0-7 token rows at j, lanes 8-15 at j+8
     const int vt = lane & 7, vh = (lane >> 3) & 1;
     const uint32_t zaddr = smem_u32(zero);
-    const uint32_t vhi_base = smem_u32(vhi) + vt * kVPitch + vh * 16;
-    const uint32_t vlo_base = smem_u32(vlo) + vt * kVPitch + vh * 16;
+    const uint32_t vhi_base = smem_u32(vhi) + vt * vpitch + vh * 16;
+    const uint32_t vlo_base = smem_u32(vlo) + vt * vpitch + vh * 16;
     const uint32_t b_base = smem_u32(bbuf);
     const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), tokens 2cc, 2cc+1
     constexpr int kTW = 4;                    // 16-column tiles per warp per pass
     constexpr int kPasses = kMaxNcols / 16 / (kConsumerWarps * kTW);   // 2
-    float res[kPasses][kTW][4];
-#pragma unroll
-    for (int ps = 0; ps < kPasses; ++ps) {
-        const int tile0 = (ps * kConsumerWarps + warp) * kTW;
-        float dh[kTW][4], dl[kTW][4];
-#pragma unroll
-        for (int i = 0; i < kTW; ++i)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) dh[i][q] = dl[i][q] = 0.f;
-        if (tile0 < ntiles) {
-            for (int s = 0; s < ksteps; ++s) {
-                const int j = s * 16 + aj;
-                uint32_t h0, h1, l0, l1, af[kTW][4];
-                ldsm_x2(h0, h1, vhi_base + s * 32);
-                ldsm_x2(l0, l1, vlo_base + s * 32);
-#pragma unroll
-                for (int i = 0; i < kTW; ++i) {
-                    const int col = (tile0 + i) * 16 + an;
-                    ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
-                                  (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
-                }
-#pragma unroll
-                for (int i = 0; i < kTW; ++i) mma_bf16(dh[i], af[i][0], af[i][1], af[i][2], af[i][3], h0, h1);
-#pragma unroll
-                for (int i = 0; i < kTW; ++i) mma_bf16(dl[i], af[i][0], af[i][1], af[i][2], af[i][3], l0, l1);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kTW; ++i)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) res[ps][i][q] = dh[i][q] + dl[i][q];
-    }
-    // transpose D through smem (fp32 [token][col], in the now free B region), then add to the
-    // staged y rows with 16-B vectors: one rounding per element, no sub-word read-modify-writes
-    __syncthreads();
-    float* dt = reinterpret_cast<float*>(bbuf);
     const int dpitch = nc + 4;
-#pragma unroll
+#pragma unroll 1
     for (int ps = 0; ps < kPasses; ++ps) {
         const int tile0 = (ps * kConsumerWarps + warp) * kTW;
+        if (tile0 >= ntiles) break;
+        // v = v_hi + v_lo: both MMAs accumulate into one fp32 tile (fixed order)
+        float d[kTW][4];
+#pragma unroll
+        for (int i = 0; i < kTW; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[i][q] = 0.f;
+        for (int s = 0; s < ksteps; ++s) {
+            const int j = s * 16 + aj;
+            uint32_t h0, h1, l0, l1, af[kTW][4];
+            ldsm_x2(h0, h1, vhi_base + s * 32);
+            ldsm_x2(l0, l1, vlo_base + s * 32);
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) {
+                const int col = (tile0 + i) * 16 + an;
+                ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
+                              (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
+            }
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) mma_bf16(d[i], af[i][0], af[i][1], af[i][2], af[i][3], h0, h1);
+#pragma unroll
+            for (int i = 0; i < kTW; ++i) mma_bf16(d[i], af[i][0], af[i][1], af[i][2], af[i][3], l0, l1);
+        }
+        // D^T -> fp32 [token][col] staging (its own region: no barrier against B readers)
 #pragma unroll
         for (int i = 0; i < kTW; ++i) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int n = (tile0 + i) * 16 + g + ((q & 2) ? 8 : 0), t = 2 * cc + (q & 1);
-                if (t < ntok && n < nc) dt[t * dpitch + n] = res[ps][i][q];
+                if (t < ntok && n < nc) dt[t * dpitch + n] = d[i][q];
             }
         }
     }
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 7] = gtime();
     mbar_wait(&bars[1], 0);
+    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 6] = gtime();
     __syncthreads();
     {
         const int vpr = nc / 8;   // 16-B vectors per token row
@@ -855,8 +945,40 @@ __global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 C
     }
     if (a.trace && tid == 0) {
         a.trace[(size_t)u * 8 + 0] = smid();
+        a.trace[(size_t)u * 8 + 4] = sh->r;
         a.trace[(size_t)u * 8 + 5] = gtime();
     }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kConsumerThreads, 4)   /* <= 64 registers: 4 CTAs per SM */
+    lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    extern __shared__ __align__(128) char smem[];
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)(blockIdx.x + a.n_shrink) * 8 + 1] = gtime();
+    if (W == 1) pdl_wait_cta();
+    expand_mma_body<false>(a, M, blockIdx.x, smem);
+}
+
+// ---- fused decode (bf16): ONE grid per apply, CTAs [0, n_shrink) run shrink units and CTAs
+// [n_shrink, n_shrink + n_expand) expand units.  An expand unit waits only for the n_s shrink
+// units of its own gc (a per-gc counter in the pool's sync buffer, release/acquire at gpu
+// scope), so the shrink -> expand hand-off costs one L2 round trip instead of a grid
+// completion + programmatic launch, and early gcs expand while later gcs still shrink.
+// Forward progress: expand CTAs only wait on lower-indexed CTAs, which the block scheduler has
+// already dispatched (the same assumption as a decoupled look-back); the wait is bounded
+// (spin_acquire_geq) so a violated assumption cannot hang the device.
+template <int W>
+__global__ void __launch_bounds__(kConsumerThreads, 4)
+    lora_decode_fused_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    extern __shared__ __align__(128) char smem[];
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)blockIdx.x * 8 + 1] = gtime();
+    if (W == 1) pdl_wait_cta();
+    if ((int)blockIdx.x < a.n_shrink)
+        shrink_mma_body<true>(a, M, blockIdx.x, smem);
+    else
+        expand_mma_body<true>(a, M, blockIdx.x - a.n_shrink, smem);
 }
 
 // copies a metadata blob too large for one kernel's parameters into device memory,
@@ -891,13 +1013,19 @@ struct DecodeKernels {
     static constexpr auto expand = lora_expand_kernel<T, W>;
     static constexpr int shrink_smem = kShrinkSmem;
     static constexpr int expand_smem = kExpandSmem;
+    static int expand_launch_smem(const DecodeArgs&) { return kExpandSmem; }
+    static constexpr bool has_fused = false;
+    static constexpr auto fused = lora_shrink_kernel<T, W>;   // unused
 };
 template <int W>
 struct DecodeKernels<__nv_bfloat16, W> {
     static constexpr auto shrink = lora_shrink_mma_kernel<W>;
     static constexpr auto expand = lora_expand_mma_kernel<W>;
     static constexpr int shrink_smem = kShrinkMmaSmem;
-    static constexpr int expand_smem = kExpandMmaSmem;
+    static constexpr int expand_smem = kExpandMmaSmemMax;
+    static int expand_launch_smem(const DecodeArgs& a) { return a.e_smem; }
+    static constexpr bool has_fused = true;
+    static constexpr auto fused = lora_decode_fused_kernel<W>;
 };
 
 template <typename T, int W>
@@ -908,6 +1036,9 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         cudaError_t e = cudaFuncSetAttribute(K::shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, K::shrink_smem);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, K::expand_smem);
+        if (e == cudaSuccess && K::has_fused)
+            e = cudaFuncSetAttribute(K::fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     K::shrink_smem > K::expand_smem ? K::shrink_smem : K::expand_smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -917,13 +1048,20 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
     }
     cudaError_t e = cudaSuccess;
+    if ((phases & 4) && K::has_fused && a.gc_sync) {   // one grid: shrink units, then expand units
+        const int es = K::expand_launch_smem(a);
+        e = launch_pdl(K::fused, pl.n_shrink + pl.n_expand, kConsumerThreads, K::shrink_smem > es ? K::shrink_smem : es, st,
+                       a, blob);
+        *launches += 1;
+        return e;
+    }
     if (phases & 1) {
         e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem, st, a, blob);
         if (e != cudaSuccess) return e;
         *launches += 1;
     }
     if (phases & 2) {
-        e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads, K::expand_smem, st, a, blob);
+        e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads, K::expand_launch_smem(a), st, a, blob);
         *launches += 1;
     }
     return e;
@@ -948,10 +1086,31 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
     a.n_shrink = pl.n_shrink;
     a.n_expand = pl.n_expand;
     a.n_gc = pl.n_gc;
+    a.unit_tab = pl.unit_tab;
+    a.gc_sync = L.gc_sync;
     a.n_jobs = pl.n_jobs;
     for (int j = 0; j < kMaxJobs; ++j) {
         a.job_shrink_base[j] = pl.job_shrink_base[j];
         a.job_expand_base[j] = pl.job_expand_base[j];
+    }
+    if (sizeof(T) == 2) {
+        // bf16 expand smem regions sized for this launch's largest unit
+        int maxr = 1, maxtok = 1, maxc = 8, bsize = 0;
+        for (int gc = 0; gc < pl.n_gc; ++gc) {
+            const int32_t* e = pl.blob.data() + kHdrWords + kGcFields * gc;
+            const int r = e[GC_RANK], c = expand_ncols(r, 2);
+            maxr = r > maxr ? r : maxr;
+            maxtok = e[GC_NTOK] > maxtok ? e[GC_NTOK] : maxtok;
+            maxc = c > maxc ? c : maxc;
+            bsize = r * (c * 2 + kPitchPad) > bsize ? r * (c * 2 + kPitchPad) : bsize;
+        }
+        const int rp = (maxr + 15) & ~15;
+        a.e_vpitch = (rp + 8) * 2;
+        a.e_boff = (320 + 2 * kTokChunkMma * a.e_vpitch + 127) & ~127;
+        a.e_yoff = a.e_boff + bsize;
+        a.e_dtoff = a.e_yoff + maxtok * (maxc * 2 + kPitchPad);
+        a.e_pgoff = a.e_dtoff + maxtok * (maxc + 4) * 4;
+        a.e_smem = a.e_pgoff + maxr * 4;
     }
     const int n = (int)pl.blob.size();
     if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases);

@@ -25,7 +25,10 @@ constexpr int kExpandBytes = 32768;               // B bytes per expand unit (r 
 constexpr int kMaxNcols = 1024;                   // columns per expand unit
 
 // metadata blob layout (int32 words)
-constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, pad, pad
+constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, unit_tab, pad
+// blob = header | gc records [n_gc][kGcFields] | pages | tokens | unit table [n_shrink + n_expand]
+// (unit record = kUnitWords words, see plan.cpp append_unit_table)
+constexpr int kUnitWords = 4;
 constexpr int kGcFields = 9;     // rank, page_off, tok_off, ntok, shrink_base, expand_base, voff, scale_bits, job
 enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB };
 constexpr int kMaxJobs = 4;      // pools fused into one launch pair by lora_apply_multi (e.g. q, k, v)

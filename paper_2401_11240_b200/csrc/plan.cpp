@@ -17,6 +17,8 @@ static inline int32_t f32_bits(float f) {
     return b;
 }
 
+static lora_status append_unit_table(Plan& pl, std::string& err);
+
 lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, int H_in, int H_out,
                        int esz, int L_tc, bool tc_enabled, const AdapterTable& table, std::string& err) {
     if (S < 0) { err = "num_segments < 0"; return LORA_ERR_ARG; }
@@ -189,6 +191,49 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     hdr[0] = n_gc; hdr[1] = shrink; hdr[2] = expand;
     hdr[3] = (int32_t)blob_pages.size(); hdr[4] = (int32_t)blob_toks.size(); hdr[5] = ksplit;
     pl.n_shrink = shrink; pl.n_expand = expand; pl.vbuf_floats = voff;
+    pl.blob_esz = esz;
+    return append_unit_table(pl, err);
+}
+
+// Appends the per-unit table (kernel_config.h): kUnitWords words per unit, shrink units first,
+// {(gc << 16) | index of the unit in its gc, first page word of the unit, first token word of
+// the gc, (rank << 16) | ntok}, so a CTA reads its whole work description with independent
+// uniform parameter loads: one round trip, no search over the gc records, no dependent chain.
+static lora_status append_unit_table(Plan& pl, std::string& err) {
+    int32_t* h = pl.blob.data();
+    const int n_gc = h[0], n_shrink = h[1], n_expand = h[2];
+    if (n_gc >= (1 << 15)) { err = "too many (group, token-chunk) units"; return LORA_ERR_ARG; }
+    const size_t base = pl.blob.size();
+    pl.blob.resize(base + (size_t)kUnitWords * (n_shrink + n_expand));
+    h = pl.blob.data();
+    const int esz = pl.blob_esz;
+    for (int c = 0; c < n_gc; ++c) {
+        const int32_t* e = h + kHdrWords + kGcFields * c;
+        const int s1 = c + 1 < n_gc ? e[kGcFields + GC_SHRINK_BASE] : n_shrink;
+        const int e1 = c + 1 < n_gc ? e[kGcFields + GC_EXPAND_BASE] : n_expand;
+        if (s1 - e[GC_SHRINK_BASE] > 0xffff || e1 - e[GC_EXPAND_BASE] > 0xffff) {
+            err = "too many units per (group, token-chunk)";
+            return LORA_ERR_ARG;
+        }
+        const int r = e[GC_RANK], njb = shrink_jblocks(r, esz);
+        for (int u = e[GC_SHRINK_BASE]; u < s1; ++u) {
+            const int local = u - e[GC_SHRINK_BASE];
+            int32_t* w = h + base + (size_t)kUnitWords * u;
+            w[0] = (c << 16) | local;
+            w[1] = e[GC_PAGE_OFF] + (local % njb) * shrink_rows(esz);
+            w[2] = e[GC_TOK_OFF];
+            w[3] = (r << 16) | e[GC_NTOK];
+        }
+        for (int u = e[GC_EXPAND_BASE]; u < e1; ++u) {
+            int32_t* w = h + base + (size_t)kUnitWords * (n_shrink + u);
+            w[0] = (c << 16) | (u - e[GC_EXPAND_BASE]);
+            w[1] = e[GC_PAGE_OFF];
+            w[2] = e[GC_TOK_OFF];
+            w[3] = (r << 16) | e[GC_NTOK];
+        }
+    }
+    h[6] = (int32_t)base;
+    pl.unit_tab = (int32_t)base;
     return LORA_OK;
 }
 
@@ -247,7 +292,8 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
     m.n_shrink = shrink;
     m.n_expand = expand;
     m.vbuf_floats = voff;
-    return LORA_OK;
+    m.blob_esz = plans[0]->blob_esz;
+    return append_unit_table(m, err);
 }
 
 }  // namespace lora

@@ -38,6 +38,8 @@ struct Plan {
     // ---- SIMT decode kernel work (N1) ----
     std::vector<int32_t> blob;           // see kernel_config.h for the layout
     int32_t n_gc = 0, n_shrink = 0, n_expand = 0;
+    int32_t unit_tab = 0;                // blob word offset of the per-unit table
+    int32_t blob_esz = 2;                // element size the unit table was built for
     int64_t vbuf_floats = 0;
     int32_t n_jobs = 1;                          // pools fused by lora_apply_multi
     int32_t job_shrink_base[4] = {0, 0, 0, 0};   // first shrink / expand unit of each job
@@ -65,7 +67,8 @@ struct DecodeLaunch {
     int32_t* meta_dev;     // device scratch for metadata too large for kernel parameters
     unsigned long long* trace;   // optional per-unit timestamps (lora_debug_set_trace), or null
     int H_in, H_out, esz, num_sms;
-    int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel
+    int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel, bit 2: one fused grid (bf16)
+    int* gc_sync = nullptr;      // fused mode: pool's zeroed counter buffer + 1 (2 * n_gc words)
     struct More {                // jobs 1.. of a fused multi-pool apply (job 0 = the fields above)
         const void* x;
         void* y;

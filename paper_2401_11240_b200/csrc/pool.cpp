@@ -50,6 +50,9 @@ struct lora_pool {
     size_t vbuf_cap = 0;                 // floats
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
+    int32_t* gc_sync = nullptr;          // fused decode: [0] timeout flag, then 2 counters per gc (zeroed)
+    size_t gc_sync_cap = 0;
+    bool fused_decode = false;           // LORA_OPT_DECODE_FUSED
     Plan plan;
     Plan fused;                          // merged kernel work of the last lora_apply_multi led by this pool
     int L_tc = 64;
@@ -183,6 +186,7 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->dA) cudaFree(p->dA);
         if (p->dB) cudaFree(p->dB);
         if (p->vbuf) cudaFree(p->vbuf);
+        if (p->gc_sync) cudaFree(p->gc_sync);
         if (p->meta_dev) cudaFree(p->meta_dev);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
         if (p->side) cudaStreamDestroy(p->side);
@@ -389,11 +393,17 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
     }
+    const bool fused = mode == 0 && p->fused_decode && p->esz == 2 && pl.n_gc > 0;
+    if (fused && (s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync")) != LORA_OK) return s;
     int launches = 0;
     if (pl.n_gc > 0) {
         DecodeLaunch L{x, y, p->dA, p->dB, mode == 0 ? p->vbuf : v_ext, p->meta_dev, p->trace, p->H_in, p->H_out,
                        p->esz, p->num_sms};
         L.phases = mode == 0 ? 3 : mode;
+        if (fused) {
+            L.phases |= 4;
+            L.gc_sync = p->gc_sync + 1;
+        }
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
@@ -478,6 +488,11 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
                        p0->num_sms};
         L.n_jobs = n_pools;
+        if (p0->fused_decode && p0->esz == 2) {
+            if ((s = grow(p0->gc_sync, p0->gc_sync_cap, (size_t)(1 + 2 * fz.n_gc), true, "gc_sync")) != LORA_OK) return s;
+            L.phases |= 4;
+            L.gc_sync = p0->gc_sync + 1;
+        }
         for (int i = 1; i < n_pools; ++i)
             L.more[i - 1] = DecodeLaunch::More{xs[i], ys[i], pools[i]->dA, pools[i]->dB, pools[i]->H_in, pools[i]->H_out};
         cudaError_t e = (cudaError_t)launch_decode(fz, L, st, &launches);
@@ -519,9 +534,15 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             DeviceGuard g(p->device);
             const int64_t ks = ksplit_of(p->H_in, p->esz);
             lora_status s = grow(p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(1, value * ks * LORA_MAX_RANK), false, "vbuf");
-            if (s == LORA_OK) s = grow(p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
+            if (s == LORA_OK)
+                s = grow(p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
+            if (s == LORA_OK) s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
             return s;
         }
+        case LORA_OPT_DECODE_FUSED:
+            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_FUSED takes 0 or 1");
+            p->fused_decode = value == 1;
+            return LORA_OK;
         default:
             return fail(LORA_ERR_ARG, "unknown option " + std::to_string(option));
     }

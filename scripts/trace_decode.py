@@ -57,7 +57,8 @@ for rep in range(3):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    g.replay()
+    with torch.cuda.stream(st):
+        g.replay()
     e1.record(st)
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1) * 1e3)
@@ -79,3 +80,50 @@ U = np.concatenate([U[n_shrink:] for U in Us])
 for lab, a_, b_ in (("E start->wait", 1, 2), ("E wait->data", 2, 3), ("E data->done", 3, 5)):
     d = (U[:, b_] - U[:, a_]) / 1e3
     print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
+# per-rank breakdown (slot 4 = unit rank) and per-apply critical path
+for name, sl in (("S", slice(0, n_shrink)), ("E", slice(n_shrink, n_units))):
+    U = np.concatenate([u[sl] for u in Us])
+    for r in sorted(set(U[:, 4].tolist())):
+        V = U[U[:, 4] == r]
+        print("   %s r=%3d n=%4d  start->wait %.2f  wait->data %.2f  data->done %.2f  start->done %.2f (med us)" % (
+            name, r, len(V), np.median((V[:, 2] - V[:, 1]) / 1e3), np.median((V[:, 3] - V[:, 2]) / 1e3),
+            np.median((V[:, 5] - V[:, 3]) / 1e3), np.median((V[:, 5] - V[:, 1]) / 1e3)))
+prev_done = None
+for i, U in enumerate(Us):
+    S, E = U[:n_shrink], U[n_shrink:]
+    s_wait, s_done = S[:, 2].min(), S[:, 5].max()
+    e_wait, e_done = E[:, 2].min(), E[:, 5].max()
+    print("apply %d: prevE.done->S.wait %6.2f  S wait->done %5.2f  S.done->E.wait %5.2f  E wait->done %5.2f" % (
+        i, (s_wait - prev_done) / 1e3 if prev_done is not None else float("nan"), (s_done - s_wait) / 1e3,
+        (e_wait - s_done) / 1e3, (e_done - e_wait) / 1e3))
+    prev_done = e_done
+# finer phases (slots 6/7): S 6 = loads issued; E 7 = MMAs done, E 6 = y tile arrived
+U = np.concatenate([u[:n_shrink] for u in Us])
+print("   S start->issued med %.2f p90 %.2f" % (np.median((U[:, 6] - U[:, 1]) / 1e3), np.percentile((U[:, 6] - U[:, 1]) / 1e3, 90)))
+U = np.concatenate([u[n_shrink:] for u in Us])
+for lab, a_, b_ in (("E data->mma", 3, 7), ("E mma->y", 7, 6), ("E y->done", 6, 5), ("E wait->y", 2, 6)):
+    d = (U[:, b_] - U[:, a_]) / 1e3
+    print("   %-14s med %.2f p90 %.2f max %.2f" % (lab, np.median(d), np.percentile(d, 90), d.max()))
+# co-residency: per SM, max number of simultaneously resident CTAs of each kind
+ev = []
+for i, u in enumerate(Us):
+    for k, sl in (("S", slice(0, n_shrink)), ("E", slice(n_shrink, n_units))):
+        for row in u[sl]:
+            ev.append((int(row[0]), row[1], row[5], k, i))
+from collections import defaultdict
+per_sm = defaultdict(list)
+for e in ev:
+    per_sm[e[0]].append(e)
+mx = defaultdict(int)
+hist = defaultdict(int)
+for sm, L_ in per_sm.items():
+    for e in L_:
+        t = e[1]
+        live = [f for f in L_ if f[1] <= t < f[2]]
+        key = "S%dE%d" % (sum(f[3] == "S" for f in live), sum(f[3] == "E" for f in live))
+        hist[key] += 1
+print("   residency at CTA start (S count, E count incl. itself):", dict(sorted(hist.items())))
+print("   SMs used:", len(per_sm))
+U = np.concatenate([u[:n_shrink] for u in Us])
+print("   S start->meta-decoded med %.2f p90 %.2f; meta->issued med %.2f" % (
+    np.median((U[:, 7] - U[:, 1]) / 1e3), np.percentile((U[:, 7] - U[:, 1]) / 1e3, 90), np.median((U[:, 6] - U[:, 7]) / 1e3)))

@@ -354,3 +354,43 @@ def test_apply_multi_qkv_fused_equals_separate(L):
         assert rel_l2(from_torch(yf, "bf16"), ref, "bf16") <= TOL["bf16"]
     for p in pools:
         p.close()
+
+
+def test_fused_decode_grid_equals_kernel_pair(L):
+    """LORA_OPT_DECODE_FUSED: one grid per apply (expand units wait on per-gc counters) is bit
+    for bit the PDL kernel pair, over many back-to-back applies on one pool with changing batches
+    (the counters must re-arm after every apply), eagerly and inside a CUDA graph."""
+    import torch
+    from paper_2401_11240_b200 import binding as B
+    batches = [gen.config_c2(y_zero=False), gen.config_c2(zipf=True, y_zero=False, tag=3),
+               gen.random_batch(4242, "bf16", 4096, 4096, max_seg=40, max_rank=128, max_len=5, n_adapters=32,
+                                y_zero=False)]
+    for b in batches:
+        pool = make_pool(b, L, L_tc=1 << 30)
+        x = to_torch(b.x, "cuda")
+        outs = {}
+        for fused in (0, 1):
+            pool.set_option(B.LORA_OPT_DECODE_FUSED, fused)
+            y = to_torch(b.y_in, "cuda")
+            for _ in range(7):   # y accumulates 7 deltas
+                pool.apply(x, y, b.seg_indptr, b.adapter_ids)
+            torch.cuda.synchronize()
+            outs[fused] = y.clone()
+        assert torch.equal(outs[0], outs[1])
+        # graph replays of the fused apply
+        pool.set_option(B.LORA_OPT_DECODE_FUSED, 1)
+        y = to_torch(b.y_in, "cuda")
+        st = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+        y.copy_(to_torch(b.y_in, "cuda"))
+        with torch.cuda.stream(st):
+            for _ in range(7):
+                g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y, outs[1])
+        ref = O.delta_for_batch(b, n_threads=8)
+        y1, _ = run_gpu(b, L, pool=pool)
+        assert rel_l2(y1, ref, "bf16") <= TOL["bf16"]
+        pool.close()
