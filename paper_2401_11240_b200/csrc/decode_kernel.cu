@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "kernel_config.h"
@@ -589,6 +590,11 @@ constexpr int kKPerWarp = kKSlice / kConsumerWarps;   // 128
 constexpr int kKBlocks = kKPerWarp / 32;              // 4
 constexpr int kAPitch = kKSlice * 2 + 64;             // bf16 row pitch: rows g, g+1 land 16 banks apart
 constexpr int kShrinkMmaSmem = 1024 + kShrinkRowsMma * kAPitch + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
+// Launch size of the bf16 shrink CTA: 52 KB instead of the ~39 KB it touches caps co-residency
+// at 4 shrink CTAs per SM, so a shrink grid spreads over more SMs (more HBM request streams)
+// and leaves room for the expand CTAs it overlaps with (c2 sweep, scripts/occ_sweep.sh:
+// 39 KB -> 88.3K tok/s, 50-57 KB -> 91.8K, >= 66 KB -> 70K).
+constexpr int kShrinkMmaLaunchSmem = 52 * 1024;
 
 // FUSED: the unit runs inside lora_decode_fused_kernel and publishes its v partials to the
 // gc's expand units with a release-increment of the gc's counter (see that kernel).
@@ -951,7 +957,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
 }
 
 template <int W>
-__global__ void __launch_bounds__(kConsumerThreads, 4)   /* <= 64 registers: 4 CTAs per SM */
+__global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 CTAs per SM */
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
@@ -1021,7 +1027,7 @@ template <int W>
 struct DecodeKernels<__nv_bfloat16, W> {
     static constexpr auto shrink = lora_shrink_mma_kernel<W>;
     static constexpr auto expand = lora_expand_mma_kernel<W>;
-    static constexpr int shrink_smem = kShrinkMmaSmem;
+    static constexpr int shrink_smem = kShrinkMmaLaunchSmem;
     static constexpr int expand_smem = kExpandMmaSmemMax;
     static int expand_launch_smem(const DecodeArgs& a) { return a.e_smem; }
     static constexpr bool has_fused = true;
@@ -1033,12 +1039,12 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
     using K = DecodeKernels<T, W>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(K::shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, K::shrink_smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, K::expand_smem);
+        // the opt-in maximum (the launch passes the real size; it decides occupancy)
+        constexpr int kMaxOptin = 227 * 1024;
+        cudaError_t e = cudaFuncSetAttribute(K::shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
         if (e == cudaSuccess && K::has_fused)
-            e = cudaFuncSetAttribute(K::fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     K::shrink_smem > K::expand_smem ? K::shrink_smem : K::expand_smem);
+            e = cudaFuncSetAttribute(K::fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -1048,6 +1054,9 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
     }
     cudaError_t e = cudaSuccess;
+    // experiment knobs (occupancy sweeps): pad the dynamic smem of the shrink / expand CTAs
+    static const int pad_s = getenv("LORA_EXP_SSMEM") ? atoi(getenv("LORA_EXP_SSMEM")) : 0;
+    static const int pad_e = getenv("LORA_EXP_ESMEM") ? atoi(getenv("LORA_EXP_ESMEM")) : 0;
     if ((phases & 4) && K::has_fused && a.gc_sync) {   // one grid: shrink units, then expand units
         const int es = K::expand_launch_smem(a);
         e = launch_pdl(K::fused, pl.n_shrink + pl.n_expand, kConsumerThreads, K::shrink_smem > es ? K::shrink_smem : es, st,
@@ -1056,12 +1065,13 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         return e;
     }
     if (phases & 1) {
-        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem, st, a, blob);
+        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem > pad_s ? K::shrink_smem : pad_s, st, a, blob);
         if (e != cudaSuccess) return e;
         *launches += 1;
     }
     if (phases & 2) {
-        e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads, K::expand_launch_smem(a), st, a, blob);
+        e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads,
+                       K::expand_launch_smem(a) > pad_e ? K::expand_launch_smem(a) : pad_e, st, a, blob);
         *launches += 1;
     }
     return e;
