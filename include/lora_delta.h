@@ -76,6 +76,13 @@ typedef enum {
 #define LORA_OPT_RESERVE_TOKENS 2  /* pre-size scratch for this many tokens (avoids a cudaMalloc in apply) */
 #define LORA_OPT_DECODE_FUSED 3    /* bf16 decode as ONE grid per apply (1) or a PDL-chained (0, default)
                                       shrink/expand kernel pair (0).  Same arithmetic, bitwise equal. */
+#define LORA_OPT_DECODE_PATH 4     /* bf16 decode tokens: 0 (default) = the PDL-chained shrink/expand
+                                      kernel pair; 1 = EXPERIMENTAL one-grid cluster-span kernel
+                                      (csrc/span_kernel.cu: shrink partials reduced over distributed
+                                      shared memory, adapter rows by 2D TMA boxes; DESIGN.md §6 N1c
+                                      records why it is slower on B200 today).  Batches it cannot
+                                      take (fragmented pages, > 8 tokens per chunk, slices > 2048)
+                                      fall back to the pair.  The two sum in different orders. */
 
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.
@@ -219,6 +226,8 @@ typedef struct {
     int32_t n_decode_units, n_prefill_tiles;   /* kernel work of the last apply (informational) */
     int32_t n_shrink_units, n_expand_units;    /* split of n_decode_units (shrink units come first) */
     int64_t v_floats;                          /* size of the partial-v buffer (lora_apply_shrink) */
+    int32_t n_span_ctas, span_cluster;         /* cluster-span decode grid of the last apply (0 if the
+                                                  kernel pair ran): CTAs and cluster size */
 } lora_metadata_view;
 
 lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* out);

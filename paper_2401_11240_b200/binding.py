@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "lora_delta.h")
 LORA_F32, LORA_BF16 = 0, 1
 LORA_POOL_HOST_ONLY = 1
 LORA_KIND_NONE, LORA_KIND_DECODE, LORA_KIND_PREFILL = -1, 0, 1
-LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS, LORA_OPT_DECODE_FUSED = 1, 2, 3
+LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS, LORA_OPT_DECODE_FUSED, LORA_OPT_DECODE_PATH = 1, 2, 3, 4
 LORA_MAX_RANK = 256
 
 STATUS = {0: "LORA_OK", 1: "LORA_ERR_ARG", 2: "LORA_ERR_SHAPE", 3: "LORA_ERR_ALIGN",
@@ -58,7 +58,7 @@ class MetadataView(ctypes.Structure):
                 ("sum_rank_tokens", ctypes.c_int64),
                 ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32),
                 ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32),
-                ("v_floats", ctypes.c_int64)]
+                ("v_floats", ctypes.c_int64), ("n_span_ctas", ctypes.c_int32), ("span_cluster", ctypes.c_int32)]
 
 
 def header_symbols() -> List[str]:
@@ -246,7 +246,8 @@ class LoraPool:
                "group_tokens": arr(m.group_tokens, int(ntok.sum())),
                "pages": arr(m.pages, int(m.sum_rank_groups)), "seg_kind": arr(m.seg_kind, m.S)}
         for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens",
-                  "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units", "v_floats"):
+                  "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units", "v_floats",
+                  "n_span_ctas", "span_cluster"):
             out[k] = int(getattr(m, k))
         return out
 

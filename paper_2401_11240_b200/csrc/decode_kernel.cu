@@ -895,7 +895,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     const uint32_t vlo_base = smem_u32(vlo) + vt * vpitch + vh * 16;
     const uint32_t b_base = smem_u32(bbuf);
     const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), tokens 2cc, 2cc+1
-    constexpr int kTW = 4;                    // 16-column tiles per warp per pass
+    constexpr int kTW = 4;                    // 16-column tiles per warp per pass (2 measured no better on c2)
     constexpr int kPasses = kMaxNcols / 16 / (kConsumerWarps * kTW);   // 2
     const int dpitch = nc + 4;
 #pragma unroll 1

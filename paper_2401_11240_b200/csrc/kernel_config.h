@@ -33,6 +33,17 @@ constexpr int kGcFields = 9;     // rank, page_off, tok_off, ntok, shrink_base, 
 enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB };
 constexpr int kMaxJobs = 4;      // pools fused into one launch pair by lora_apply_multi (e.g. q, k, v)
 
+// cluster-span decode kernel (span_kernel.cu): CTA record of kSpanRecWords int32 words
+//   [0] job | span << 4 | index in span << 12 | span leader's rank in the cluster << 20
+//   [1] rank | ntok << 16      (rank 0: idle CTA padding the last cluster)
+//   [2] first page of the gc's (contiguous) rank rows   [3] blob word of the gc's first token
+//   [4] scale (fp32 bits)      [5] kc | nc << 16 (ring chunk widths, powers of two)
+//   [6] k0 | nk << 16          [7] n0 | nn << 16 (this CTA's slices of H_in and H_out)
+constexpr int kSpanRecWords = 8;
+constexpr int kSpanTok = 8;                       // tokens per group-chunk (MMA N)
+constexpr int kSpanMaxStages = 12;
+constexpr int kSpanBoxKinds = 5;                  // TMA boxes {64 columns, 8 << k rows}, k < 5 (<= 128 rows)
+
 LORA_HD int vec_elems(int esz) { return 16 / esz; }             // elements per 16-B vector
 LORA_HD int tok_chunk(int esz) { return esz == 2 ? kTokChunkMma : kTokChunk; }
 LORA_HD int shrink_rows(int esz) { return esz == 2 ? kShrinkRowsMma : kShrinkRows; }

@@ -49,7 +49,27 @@ struct Plan {
     int32_t n_prefill_tiles = 0;     // == n_pf_tiles (128-token tiles on the tensor-core path)
     std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] tile records {tok0, nvalid, rank, page_off, scale_bits}, then pages
     int32_t n_pf_tiles = 0;
+    // ---- cluster-span decode work (N1c, span_kernel.cu): one grid per apply ----
+    std::vector<int32_t> span_blob;  // [n_span_cta][kSpanRecWords] CTA records, then pages, then tokens
+    int32_t n_span_cta = 0;          // multiple of the cluster size (idle CTAs pad the last cluster)
+    int32_t span_cluster = 0;        // cluster size the records were packed for (0 = not built)
+    int32_t span_max_rank = 0, span_max_sk = 0, span_max_sn = 0;
 };
+
+// Span-path parameters (per pool; fixed for a device so the result of a token is a fixed
+// function of (x_t, adapter): the span of a rank depends only on r, H_in, H_out and these).
+struct SpanParams {
+    int cluster = 16;          // thread-block cluster size (CTAs); spans are powers of two <= cluster
+    int target_bytes = 65536;  // adapter bytes per CTA the span size aims at
+    int stage_bytes = 16384;   // bytes of one ring stage (A or B chunk: r rows x kc|nc columns)
+    int n_stages = 4;          // ring stages (all issued before griddepcontrol.wait)
+    int max_slice = 2048;      // largest per-CTA k or n slice (x / y staging is [8][slice])
+};
+// span (CTAs per group-chunk) for rank r, or 0 if the shape needs more than `cluster` CTAs
+int span_of(int r, int H_in, int H_out, const SpanParams& sp);
+// Builds pl.span_blob from the gc records of pl.blob (a build_plan or merge_plans result);
+// H_in/H_out per job.  Returns false (pl.span_cluster = 0) if some gc does not fit the span path.
+bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanParams& sp);
 
 // Builds `plan`.  tc_enabled=false routes every token through the SIMT kernel.
 // Returns LORA_OK or an error status with `err` naming the offending operand.
@@ -78,6 +98,14 @@ struct DecodeLaunch {
     } more[3];
     int n_jobs = 1;
 };
+struct SpanLaunchDesc {     // the cluster-span decode kernel's operands, per fused job
+    const void* x[4];
+    void* y[4];
+    const void* tmaps[4];    // device copy of the pool's span tensor maps (span_make_tmaps)
+    int H_in[4], H_out[4];
+    int n_jobs;
+    unsigned long long* trace;
+};
 struct PrefillLaunch {
     const void* x;
     void* y;
@@ -97,6 +125,12 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& merged, std::stri
 typedef struct CUstream_st* lora_cuda_stream;
 namespace lora {
 int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
+int launch_span(const Plan& pl, const SpanLaunchDesc& L, lora_cuda_stream st, int* launches);
+bool span_fits(const Plan& pl);           // the launch's smem layout fits one CTA
+const SpanParams& span_params();          // process-wide (env knobs LORA_SPAN_* for sweeps)
+int span_max_blob_words();
+// writes the 2 * kSpanBoxKinds CUtensorMaps (128 B each) of a bf16 pool to host_out; 0 on success
+int span_make_tmaps(void* host_out, const void* dA, const void* dB, int n_rows, int H_in, int H_out);
 int launch_prefill(const Plan& pl, const PrefillLaunch& L, lora_cuda_stream st, int* launches);
 bool prefill_supported(int H_in, int H_out, int esz);
 int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);

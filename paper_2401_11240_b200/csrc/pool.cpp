@@ -39,6 +39,7 @@ struct lora_pool {
     bool tc_prefill = false;             // tensor-core prefill path available for this pool
     alignas(64) unsigned char tm_a[128]; // TMA maps of the page arrays (gather4 boxes {64, 1})
     alignas(64) unsigned char tm_b[128];
+    void* span_tmaps = nullptr;          // device: 2 x kSpanBoxKinds tensor maps of the page arrays (span kernel)
     std::vector<uint8_t> page_used;
     int free_pages = 0;
     AdapterTable table;
@@ -53,6 +54,7 @@ struct lora_pool {
     int32_t* gc_sync = nullptr;          // fused decode: [0] timeout flag, then 2 counters per gc (zeroed)
     size_t gc_sync_cap = 0;
     bool fused_decode = false;           // LORA_OPT_DECODE_FUSED
+    int decode_path = 0;                 // LORA_OPT_DECODE_PATH: 0 kernel pair, 1 cluster-span kernel (bf16)
     Plan plan;
     Plan fused;                          // merged kernel work of the last lora_apply_multi led by this pool
     int L_tc = 64;
@@ -158,6 +160,16 @@ lora_status lora_pool_create_ex(int hidden_in, int hidden_out, int max_adapters,
             p->tc_prefill = make_tmap_bf16(p->tm_a, p->dA, p->n_pages + 1, hidden_in, 1) == 0 &&
                             make_tmap_bf16(p->tm_b, p->dB, p->n_pages + 1, hidden_out, 1) == 0;
         }
+        // page contents start zeroed (rows a TMA box loads past an adapter are then finite)
+        if (e == cudaSuccess) e = cudaMemset(p->dA, 0, (size_t)(p->n_pages + 1) * hidden_in * esz);
+        if (e == cudaSuccess) e = cudaMemset(p->dB, 0, (size_t)(p->n_pages + 1) * hidden_out * esz);
+        if (e == cudaSuccess && esz == 2) {
+            alignas(64) unsigned char maps[2 * kSpanBoxKinds * 128];
+            if (span_make_tmaps(maps, p->dA, p->dB, p->n_pages + 1, hidden_in, hidden_out) == 0) {
+                e = cudaMalloc(&p->span_tmaps, sizeof(maps));
+                if (e == cudaSuccess) e = cudaMemcpy(p->span_tmaps, maps, sizeof(maps), cudaMemcpyHostToDevice);
+            }
+        }
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->unload_fence, cudaEventDisableTiming);
         if (e != cudaSuccess) {
@@ -184,6 +196,7 @@ lora_status lora_pool_destroy(lora_pool* p) {
         for (auto& kv : p->table)
             if (kv.second.ready) cudaEventDestroy((cudaEvent_t)kv.second.ready);
         if (p->dA) cudaFree(p->dA);
+        if (p->span_tmaps) cudaFree(p->span_tmaps);
         if (p->dB) cudaFree(p->dB);
         if (p->vbuf) cudaFree(p->vbuf);
         if (p->gc_sync) cudaFree(p->gc_sync);
@@ -393,10 +406,25 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
     }
-    const bool fused = mode == 0 && p->fused_decode && p->esz == 2 && pl.n_gc > 0;
-    if (fused && (s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync")) != LORA_OK) return s;
     int launches = 0;
-    if (pl.n_gc > 0) {
+    bool span = false;
+    if (mode == 0 && p->esz == 2 && p->decode_path == 1 && p->span_tmaps && pl.n_gc > 0) {
+        const int hi[1] = {p->H_in}, ho[1] = {p->H_out};
+        span = build_span_work(p->plan, hi, ho, span_params()) && span_fits(pl) &&
+               (int)pl.span_blob.size() <= span_max_blob_words();
+        if (!span) p->plan.n_span_cta = p->plan.span_cluster = 0;
+    }
+    if (span) {
+        SpanLaunchDesc L{};
+        L.x[0] = x; L.y[0] = y; L.tmaps[0] = p->span_tmaps; L.H_in[0] = p->H_in; L.H_out[0] = p->H_out;
+        L.n_jobs = 1;
+        L.trace = p->trace;
+        cudaError_t e = (cudaError_t)launch_span(pl, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply: span decode kernel launch");
+    }
+    const bool fused = !span && mode == 0 && p->fused_decode && p->esz == 2 && pl.n_gc > 0;
+    if (fused && (s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync")) != LORA_OK) return s;
+    if (pl.n_gc > 0 && !span) {
         DecodeLaunch L{x, y, p->dA, p->dB, mode == 0 ? p->vbuf : v_ext, p->meta_dev, p->trace, p->H_in, p->H_out,
                        p->esz, p->num_sms};
         L.phases = mode == 0 ? 3 : mode;
@@ -480,9 +508,30 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
                      "lora_apply_multi: wait load");
         }
     }
-    const Plan& fz = p0->fused;
+    Plan& fz = p0->fused;
     int launches = 0;
-    if (fz.n_gc > 0) {
+    bool span = false;
+    bool maps_ok = true;
+    for (int i = 0; i < n_pools; ++i) maps_ok = maps_ok && pools[i]->span_tmaps;
+    if (p0->esz == 2 && p0->decode_path == 1 && maps_ok && fz.n_gc > 0) {
+        int hi[kMaxJobs], ho[kMaxJobs];
+        for (int i = 0; i < n_pools; ++i) { hi[i] = pools[i]->H_in; ho[i] = pools[i]->H_out; }
+        span = build_span_work(fz, hi, ho, span_params()) && span_fits(fz) &&
+               (int)fz.span_blob.size() <= span_max_blob_words();
+        if (!span) fz.n_span_cta = fz.span_cluster = 0;
+    }
+    if (span) {
+        SpanLaunchDesc L{};
+        for (int i = 0; i < n_pools; ++i) {
+            L.x[i] = xs[i]; L.y[i] = ys[i]; L.tmaps[i] = pools[i]->span_tmaps;
+            L.H_in[i] = pools[i]->H_in; L.H_out[i] = pools[i]->H_out;
+        }
+        L.n_jobs = n_pools;
+        L.trace = p0->trace;
+        cudaError_t e = (cudaError_t)launch_span(fz, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: span decode kernel launch");
+    }
+    if (fz.n_gc > 0 && !span) {
         if ((s = grow(p0->vbuf, p0->vbuf_cap, (size_t)std::max<int64_t>(fz.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
         if ((s = grow(p0->meta_dev, p0->meta_cap, fz.blob.size(), false, "meta")) != LORA_OK) return s;
         DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
@@ -539,6 +588,10 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             if (s == LORA_OK) s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
             return s;
         }
+        case LORA_OPT_DECODE_PATH:
+            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_PATH takes 0 or 1");
+            p->decode_path = (int)value;
+            return LORA_OK;
         case LORA_OPT_DECODE_FUSED:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_FUSED takes 0 or 1");
             p->fused_decode = value == 1;
@@ -590,6 +643,8 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
     o->n_shrink_units = pl.n_shrink;
     o->n_expand_units = pl.n_expand;
     o->v_floats = pl.vbuf_floats;
+    o->n_span_ctas = pl.n_span_cta;
+    o->span_cluster = pl.span_cluster;
     o->n_prefill_tiles = pl.n_prefill_tiles;
     return LORA_OK;
 }

@@ -67,3 +67,29 @@ split = run(lambda: [(p.apply_shrink(x, b.seg_indptr, b.adapter_ids, v, stream=s
 md = pools[0].metadata()
 print("c2 x %d pools: us/apply  full %.2f | shrink-only %.2f | expand-only %.2f | split pair %.2f  (units S %d E %d)"
       % (NP, full, shr, exp, split, md["n_shrink_units"], md["n_decode_units"] - md["n_shrink_units"]))
+
+# the shrink/expand kernel pair, and its one-grid variant (per-gc counters)
+for p in pools:
+    p.set_option(L.binding.LORA_OPT_DECODE_PATH, 1)
+span = run(lambda: [p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st) for p, y in zip(pools, ys)])
+for p in pools:
+    p.set_option(L.binding.LORA_OPT_DECODE_PATH, 0)
+print("c2 x %d pools: us/apply  kernel pair (default) %.2f | cluster span %.2f" % (NP, full, span))
+for p in pools:
+    p.set_option(L.binding.LORA_OPT_DECODE_FUSED, 1)
+with torch.cuda.stream(st):
+    for p, y in zip(pools, ys):
+        p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+torch.cuda.synchronize()
+fused = run(lambda: [p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st) for p, y in zip(pools, ys)])
+for p in pools:
+    p.set_option(L.binding.LORA_OPT_DECODE_FUSED, 0)
+# q/k/v style: 3 pools per lora_apply_multi launch pair
+trip = [(pools[i:i + 3], ys[i:i + 3]) for i in range(0, NP - 2, 3)]
+with torch.cuda.stream(st):
+    for ps, yy in trip:
+        L.apply_multi(ps, [x] * 3, yy, b.seg_indptr, b.adapter_ids, stream=st)
+torch.cuda.synchronize()
+multi = run(lambda: [L.apply_multi(ps, [x] * 3, yy, b.seg_indptr, b.adapter_ids, stream=st) for ps, yy in trip]) \
+    * NP / (3 * len(trip))
+print("c2 x %d pools: us/apply  fused-grid %.2f | multi(3) %.2f" % (NP, fused, multi))
