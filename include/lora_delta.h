@@ -84,6 +84,12 @@ typedef enum {
                                       take (fragmented pages, > 8 tokens per chunk, slices > 2048)
                                       fall back to the pair.  The two sum in different orders. */
 
+#define LORA_OPT_PAD_MAX_RANK 5    /* comparison mode: 1 pads every adapter's
+                                      decode work to the batch's max rank with the pool's all-zero
+                                      page, i.e. the padded BGMV of Punica that the paper contrasts
+                                      with MBGMV (§3.1).  Same result (zero rows
+                                      add 0); more bytes and time.  Not for production. */
+
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.
  *   hidden_in, hidden_out  H_in, H_out of the adapted projection (Eq. 1's H1, H2).

@@ -20,7 +20,8 @@ static inline int32_t f32_bits(float f) {
 static lora_status append_unit_table(Plan& pl, std::string& err);
 
 lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, int H_in, int H_out,
-                       int esz, int L_tc, bool tc_enabled, const AdapterTable& table, std::string& err) {
+                       int esz, int L_tc, bool tc_enabled, const AdapterTable& table, std::string& err,
+                       int pad_zero_page) {
     if (S < 0) { err = "num_segments < 0"; return LORA_ERR_ARG; }
     if (S > 0 && (ip == nullptr || ids == nullptr)) { err = "seg_indptr/adapter_ids is NULL"; return LORA_ERR_ARG; }
     if (S > 0 && ip[0] != 0) { err = "seg_indptr[0] != 0"; return LORA_ERR_ARG; }
@@ -152,6 +153,10 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         group_blob_page[g] = (int32_t)blob_pages.size();
         blob_pages.insert(blob_pages.end(), pl.pages.begin() + pl.group_page_off[g],
                           pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
+        // padded-BGMV comparison mode (NEXT f4): every group's rank rows are padded to
+        // the batch's max rank with the pool's all-zero page -- the work Punica's BGMV does
+        if (pad_zero_page >= 0)
+            blob_pages.insert(blob_pages.end(), (size_t)(pl.max_rank - pl.group_rank[g]), pad_zero_page);
         const size_t tc = (size_t)tok_chunk(esz);
         for (size_t c = 0; c < simt[g].size(); c += tc) {
             const int n = (int)std::min<size_t>(tc, simt[g].size() - c);
@@ -169,7 +174,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     int shrink = 0, expand = 0;
     int64_t voff = 0;
     for (int c = 0; c < n_gc; ++c) {
-        const int g = gcs[c].g, r = pl.group_rank[g];
+        const int g = gcs[c].g, r = pad_zero_page >= 0 ? (int)pl.max_rank : pl.group_rank[g];
         int32_t* e = gct + kGcFields * c;
         e[GC_RANK] = r;
         e[GC_PAGE_OFF] = pages_base + group_blob_page[g];

@@ -71,11 +71,13 @@ int span_of(int r, int H_in, int H_out, const SpanParams& sp);
 // H_in/H_out per job.  Returns false (pl.span_cluster = 0) if some gc does not fit the span path.
 bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanParams& sp);
 
-// Builds `plan`.  tc_enabled=false routes every token through the SIMT kernel.
+// Builds `plan`.  tc_enabled=false routes every token through the SIMT kernel.  pad_zero_page >= 0
+// pads every group's decode work to the batch's max rank with that (all-zero) page (BGMV mode;
+// the canonical metadata M1-M6 is unchanged).
 // Returns LORA_OK or an error status with `err` naming the offending operand.
 lora_status build_plan(Plan& plan, const int32_t* seg_indptr, const int32_t* adapter_ids, int S,
                        int H_in, int H_out, int esz, int L_tc, bool tc_enabled,
-                       const AdapterTable& table, std::string& err);
+                       const AdapterTable& table, std::string& err, int pad_zero_page = -1);
 
 // ---- kernel launch descriptors (pool.cpp -> *_kernel.cu) ----
 struct DecodeLaunch {

@@ -55,6 +55,7 @@ struct lora_pool {
     size_t gc_sync_cap = 0;
     bool fused_decode = false;           // LORA_OPT_DECODE_FUSED
     int decode_path = 0;                 // LORA_OPT_DECODE_PATH: 0 kernel pair, 1 cluster-span kernel (bf16)
+    bool pad_max_rank = false;           // LORA_OPT_PAD_MAX_RANK: BGMV-style padded decode work (comparison)
     Plan plan;
     Plan fused;                          // merged kernel work of the last lora_apply_multi led by this pool
     int L_tc = 64;
@@ -312,7 +313,7 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     std::string err;
     const bool tc = !p->host_only ? p->tc_prefill : prefill_supported(p->H_in, p->H_out, p->esz);
     lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
-                               p->L_tc, tc, p->table, err);
+                               p->L_tc, tc, p->table, err, p->pad_max_rank ? p->n_pages : -1);
     if (s != LORA_OK) return fail(s, err);
     return LORA_OK;
 }
@@ -373,7 +374,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         std::string err;
         const bool tc = p->tc_prefill && mode == 0;   // the split path keeps every token on the decode kernels
         s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, tc, p->table,
-                       err);
+                       err, p->pad_max_rank ? p->n_pages : -1);
         if (s != LORA_OK) return fail(s, err);
         if (mode == 1 && p->plan.vbuf_floats > v_cap)
             return fail(LORA_ERR_ARG, "v buffer too small: need " + std::to_string(p->plan.vbuf_floats) + " floats");
@@ -588,6 +589,10 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             if (s == LORA_OK) s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
             return s;
         }
+        case LORA_OPT_PAD_MAX_RANK:
+            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_PAD_MAX_RANK takes 0 or 1");
+            p->pad_max_rank = value == 1;
+            return LORA_OK;
         case LORA_OPT_DECODE_PATH:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_PATH takes 0 or 1");
             p->decode_path = (int)value;

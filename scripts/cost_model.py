@@ -1,0 +1,112 @@
+"""Paper-law check (§4.3): time decode applies over many
+batch compositions in MBGMV mode (default: each adapter's own rank) and padded-BGMV mode
+(LORA_OPT_PAD_MAX_RANK), fit t = alpha * feature + beta for the MBGMV feature sum_G r and the BGMV
+feature |S| * max r, and report R^2 (the paper fits its kernel-cost model with R^2 = 0.96).
+Also checks that at fixed sum_G r the MBGMV time stays flat as max r grows (no padding).
+
+Every batch: 64 one-token decode segments over G adapters (ranks drawn from {8,16,32,64,128}),
+4096 -> 4096 bf16; t = device time per apply from a CUDA graph of NP applies on NP distinct pools
+(inputs > L2).  usage: python scripts/cost_model.py [out.json]"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2401_11240_b200 as L  # noqa: E402
+from paper_2401_11240_b200 import binding as B  # noqa: E402
+from workloads import gen  # noqa: E402
+
+H, T, NP, N_AD = 4096, 64, 16, 80
+RANKS = (8, 16, 32, 64, 128)
+rank_of = {a: RANKS[a % 5] for a in range(N_AD)}
+pools = []
+for p in range(NP):
+    pool = L.LoraPool(H, H, N_AD, "bf16", max_total_rank=sum(rank_of.values()) + 1)
+    for a in range(N_AD):
+        ad = gen.make_adapter(gen.BASE_SEED + 9, 100 + p, a, rank_of[a], H, H, "bf16")
+        pool.load_adapter(a, ad.rank, torch.from_numpy(ad.A.view(np.int16)).pin_memory(),
+                          torch.from_numpy(ad.B.view(np.int16)).pin_memory(), ad.scale)
+    pools.append(pool)
+torch.cuda.synchronize()
+x = torch.randn(T, H).to(torch.bfloat16).cuda()
+ys = [torch.zeros(T, H, dtype=torch.bfloat16, device="cuda") for _ in pools]
+st = torch.cuda.Stream()
+flush = torch.empty(512 * 2 ** 20, dtype=torch.int8, device="cuda")
+
+
+def t_apply(ip, ids, pad):
+    for p in pools:
+        p.set_option(B.LORA_OPT_PAD_MAX_RANK, pad)
+    with torch.cuda.stream(st):
+        for p, y in zip(pools, ys):
+            p.apply(x, y, ip, ids, stream=st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for p, y in zip(pools, ys):
+            p.apply(x, y, ip, ids, stream=st)
+    ts = []
+    for _ in range(5):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        with torch.cuda.stream(st):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / NP)
+    return float(np.median(ts))
+
+
+def fit(xs, ys):
+    xs, ys = np.asarray(xs, float), np.asarray(ys, float)
+    A = np.stack([xs, np.ones_like(xs)], 1)
+    coef, *_ = np.linalg.lstsq(A, ys, rcond=None)
+    pred = A @ coef
+    r2 = 1.0 - float(((ys - pred) ** 2).sum() / ((ys - ys.mean()) ** 2).sum())
+    return {"alpha_us_per_unit": float(coef[0]), "beta_us": float(coef[1]), "r2": r2}
+
+
+rng = np.random.default_rng(11)
+rows = []
+ip = gen.segments_to_indptr([1] * T)
+for trial in range(36):
+    G = int(rng.choice([2, 4, 8, 16, 32, 64]))
+    ads = rng.choice(N_AD, size=G, replace=False)
+    ids = np.array([ads[t % G] for t in range(T)], dtype=np.int32)
+    rng.shuffle(ids)
+    sum_r = int(sum(rank_of[int(a)] for a in ads))
+    max_r = int(max(rank_of[int(a)] for a in ads))
+    row = {"G": G, "sum_rank_groups": sum_r, "max_rank": max_r, "nseg_x_maxrank": T * max_r,
+           "sum_rank_tokens": int(sum(rank_of[int(a)] for a in ids)), "G_x_maxrank": G * max_r,
+           "t_mbgmv_us": t_apply(ip, ids, 0), "t_bgmv_us": t_apply(ip, ids, 1)}
+    rows.append(row)
+    print(row, flush=True)
+# flatness at fixed sum_G r = 256: 32 x r8 vs 16 x r16 vs 8 x r32 vs 4 x r64 vs 2 x r128
+flat = []
+for r in RANKS:
+    cand = [a for a in range(N_AD) if rank_of[a] == r][:256 // r]
+    if len(cand) < 256 // r:
+        continue
+    ids = np.array([cand[t % len(cand)] for t in range(T)], dtype=np.int32)
+    mix = list(cand)
+    # one max-rank adapter + small ones with the same sum_G r
+    flat.append({"ranks": "%d x r%d" % (len(cand), r), "sum_rank_groups": 256, "t_mbgmv_us": t_apply(ip, ids, 0)})
+out = {
+    "workload": "64 one-token decode segments, 4096->4096 bf16, adapters ranks {8..128}, %d random compositions" % len(rows),
+    "mbgmv_time_vs_sum_rank_groups": fit([r["sum_rank_groups"] for r in rows], [r["t_mbgmv_us"] for r in rows]),
+    "mbgmv_time_vs_nseg_x_maxrank": fit([r["nseg_x_maxrank"] for r in rows], [r["t_mbgmv_us"] for r in rows]),
+    "bgmv_time_vs_G_x_maxrank": fit([r["G_x_maxrank"] for r in rows], [r["t_bgmv_us"] for r in rows]),
+    "bgmv_time_vs_sum_rank_groups": fit([r["sum_rank_groups"] for r in rows], [r["t_bgmv_us"] for r in rows]),
+    "paper_r2": 0.96,
+    "fixed_sum_rank_256": flat,
+    "rows": rows,
+}
+s = json.dumps(out, indent=1)
+print(s)
+if len(sys.argv) > 1:
+    open(sys.argv[1], "w").write(s)

@@ -147,3 +147,26 @@ def test_device_pool_without_gpu_fails_cleanly():
     with pytest.raises(L.LoraError) as ei:
         L.LoraPool(64, 64, 2, "bf16")
     assert ei.value.name == "LORA_ERR_CUDA"
+
+
+def test_pad_max_rank_keeps_metadata_and_pads_work():
+    """LORA_OPT_PAD_MAX_RANK (BGMV comparison mode): canonical metadata is unchanged,
+    the decode work lists grow to the batch's max rank for every group (units per group of the
+    max rank)."""
+    b = gen.config_c2()
+    pools = []
+    for pad in (0, 1):
+        pool = L.LoraPool(b.H_in, b.H_out, 40, "bf16", max_total_rank=sum(a.rank for a in b.adapters), host_only=True)
+        pool.set_option(B.LORA_OPT_PAD_MAX_RANK, pad)
+        for a in b.adapters:
+            pool.load_adapter(a.id, a.rank, None, None, a.scale)
+        pool.plan(b.seg_indptr, b.adapter_ids)
+        pools.append(pool.metadata())
+        pool.close()
+    plain, padded = pools
+    _compare_md(padded, plain)
+    # c2: ranks 8/16/32/64 -> every group padded to 64: shrink units = ksplit 4 x 64/16 per gc
+    n_gc = len(set(b.adapter_ids.tolist()))
+    assert padded["n_shrink_units"] == n_gc * 4 * (64 // 16)
+    assert padded["n_shrink_units"] > plain["n_shrink_units"]
+    assert padded["n_expand_units"] > plain["n_expand_units"]

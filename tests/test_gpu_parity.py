@@ -394,3 +394,23 @@ def test_fused_decode_grid_equals_kernel_pair(L):
         y1, _ = run_gpu(b, L, pool=pool)
         assert rel_l2(y1, ref, "bf16") <= TOL["bf16"]
         pool.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c2_zipf", "c1"])
+def test_pad_max_rank_bgmv_mode(L, name):
+    """LORA_OPT_PAD_MAX_RANK (padded BGMV) computes the same delta: zero rank rows add
+    exact zeros, so the bf16 tensor-core path is bitwise equal to MBGMV; fp32 within tolerance."""
+    from paper_2401_11240_b200 import binding as B
+    b = {"c2": lambda: gen.config_c2(y_zero=False), "c2_zipf": lambda: gen.config_c2(zipf=True, y_zero=False, tag=4),
+         "c1": lambda: gen.config_c1(y_zero=False)}[name]()
+    outs = []
+    for pad in (0, 1):
+        pool = make_pool(b, L, L_tc=1 << 30)
+        pool.set_option(B.LORA_OPT_PAD_MAX_RANK, pad)
+        y, _ = run_gpu(b, L, pool=pool)
+        outs.append(y)
+        pool.close()
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(outs[1], ref, b.dtype) <= TOL[b.dtype]
+    if b.dtype == "bf16":
+        assert np.array_equal(outs[0], outs[1])
