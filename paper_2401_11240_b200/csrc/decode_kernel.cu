@@ -229,6 +229,8 @@ struct Elem<float> {
 
 // ------------------------------------------------------------------ metadata access
 __device__ __forceinline__ int gc_field(const int32_t* M, int gc, int f) { return M[kHdrWords + gc * kGcFields + f]; }
+// page of rank row j of a page reference (kernel_config.h page_ref_add)
+__device__ __forceinline__ int page_at(const int32_t* M, int ref, int j) { return ref >= 0 ? M[ref + j] : (~ref) + j; }
 
 // per-CTA unit description, decoded once by warp 0 and shared through smem
 struct UnitSh {
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int ks = local / njb;
         const int j0 = (local - ks * njb) * kShrinkRows;
         const int nj = min(kShrinkRows, r - j0);
-        const int page = lane < nj ? M[poff + j0 + lane] : 0;
+        const int page = lane < nj ? page_at(M, poff, j0 + lane) : 0;
         tok = lane < ntok ? M[toff + lane] : 0;
         const int k0 = ks * KS;
         const uint32_t row_bytes = (uint32_t)min(KS, J.H_in - k0) * E::kSize;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         const int nc = min(c, J.H_out - n0);
         int pages[LORA_MAX_RANK / 32];
 #pragma unroll
-        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? M[poff + q * 32 + lane] : 0;
+        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? page_at(M, poff, q * 32 + lane) : 0;
         tok = lane < ntok ? M[toff + lane] : 0;
         const uint32_t row_bytes = (uint32_t)nc * E::kSize;
         if (lane == 0) {
@@ -615,10 +617,10 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         const int job = job_of(u, a.n_jobs, a.job_shrink_base);
         // round 1: the unit record (independent uniform loads)
         const int32_t* rec = M + a.unit_tab + kUnitWords * u;
-        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[3];
-        const int pg0 = rec[1], toff = rec[2];
+        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[2];
+        const int pg0 = rec[1], toff = unit_tok_off(rn);
         const int gc = (int)(uw >> 16), local = (int)(uw & 0xffffu);
-        const int r = (int)(rn >> 16), ntok = (int)(rn & 0xffffu);
+        const int r = unit_rank(rn), ntok = unit_ntok(rn);
         const DecodeJob J = a.jobs[job];
         const int njb = shrink_jblocks(r, ES);
         const int ks = local / njb;
@@ -627,7 +629,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         const int k0 = ks * kKSlice;
         const int nk = min(kKSlice, J.H_in - k0);
         // round 2: pages, tokens, v offset
-        const int page = lane < nj ? M[pg0 + lane] : 0;
+        const int page = lane < nj ? page_at(M, pg0, lane) : 0;
         const int tokv = lane < ntok ? M[toff + lane] : -1;
         const int voff = gc_field(M, gc, GC_VOFF);
         if (a.trace) { asm volatile("" ::"r"(page), "r"(tokv)); if (lane == 0) a.trace[(size_t)u * 8 + 7] = gtime(); }
@@ -762,10 +764,10 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         }
         const int job = job_of(ue, a.n_jobs, a.job_expand_base);
         const int32_t* rec = M + a.unit_tab + kUnitWords * (a.n_shrink + ue);
-        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[3];
-        const int poff = rec[1], toff = rec[2];
+        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[2];
+        const int poff = rec[1], toff = unit_tok_off(rn);
         const int gc = (int)(uw >> 16), local = (int)(uw & 0xffffu);
-        const int r = (int)(rn >> 16), ntok = (int)(rn & 0xffffu);
+        const int r = unit_rank(rn), ntok = unit_ntok(rn);
         const DecodeJob J = a.jobs[job];
         const int c = expand_ncols(r, ES);
         const int n0 = local * c;
@@ -773,7 +775,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         const int bpitch = c * ES + kPitchPad;
         int pages[LORA_MAX_RANK / 32];
 #pragma unroll
-        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? M[poff + q * 32 + lane] : 0;
+        for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? page_at(M, poff, q * 32 + lane) : 0;
         tok = lane < ntok ? M[toff + lane] : 0;
         const uint32_t row_bytes = (uint32_t)nc * ES;
         const bool bulk = row_bytes >= kBulkMinBytes;

@@ -28,7 +28,15 @@ constexpr int kMaxNcols = 1024;                   // columns per expand unit
 constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, unit_tab, pad
 // blob = header | gc records [n_gc][kGcFields] | pages | tokens | unit table [n_shrink + n_expand]
 // (unit record = kUnitWords words, see plan.cpp append_unit_table)
-constexpr int kUnitWords = 4;
+constexpr int kUnitWords = 3;
+// A page reference is either a blob word offset of an explicit page list (>= 0) or, for a run of
+// consecutive pages, ~first_page (< 0): page j = first_page + j.  Contiguous adapters (the
+// allocator's lowest-free-first order makes them the common case) then cost no blob words.
+LORA_HD int page_ref_add(int ref, int k) { return ref >= 0 ? ref + k : ~((~ref) + k); }
+// unit word 2: rank | ntok << 9 | token offset << 13
+LORA_HD int unit_rank(uint32_t w) { return (int)(w & 0x1ffu); }
+LORA_HD int unit_ntok(uint32_t w) { return (int)((w >> 9) & 0xfu); }
+LORA_HD int unit_tok_off(uint32_t w) { return (int)(w >> 13); }
 constexpr int kGcFields = 9;     // rank, page_off, tok_off, ntok, shrink_base, expand_base, voff, scale_bits, job
 enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB };
 constexpr int kMaxJobs = 4;      // pools fused into one launch pair by lora_apply_multi (e.g. q, k, v)

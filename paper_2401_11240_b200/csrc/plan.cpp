@@ -150,13 +150,19 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     std::vector<int32_t> blob_pages, blob_toks, group_blob_page(G, -1);
     for (int g = 0; g < G; ++g) {
         if (simt[g].empty()) continue;
-        group_blob_page[g] = (int32_t)blob_pages.size();
-        blob_pages.insert(blob_pages.end(), pl.pages.begin() + pl.group_page_off[g],
-                          pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
+        std::vector<int32_t> gp(pl.pages.begin() + pl.group_page_off[g],
+                                pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
         // padded-BGMV comparison mode (NEXT f4): every group's rank rows are padded to
         // the batch's max rank with the pool's all-zero page -- the work Punica's BGMV does
-        if (pad_zero_page >= 0)
-            blob_pages.insert(blob_pages.end(), (size_t)(pl.max_rank - pl.group_rank[g]), pad_zero_page);
+        if (pad_zero_page >= 0) gp.insert(gp.end(), (size_t)(pl.max_rank - pl.group_rank[g]), pad_zero_page);
+        bool contiguous = true;
+        for (size_t j = 1; j < gp.size() && contiguous; ++j) contiguous = gp[j] == gp[0] + (int32_t)j;
+        if (contiguous) {
+            group_blob_page[g] = ~gp[0];   // page reference ~first_page: no page words in the blob
+        } else {
+            group_blob_page[g] = (int32_t)blob_pages.size();
+            blob_pages.insert(blob_pages.end(), gp.begin(), gp.end());
+        }
         const size_t tc = (size_t)tok_chunk(esz);
         for (size_t c = 0; c < simt[g].size(); c += tc) {
             const int n = (int)std::min<size_t>(tc, simt[g].size() - c);
@@ -177,7 +183,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         const int g = gcs[c].g, r = pad_zero_page >= 0 ? (int)pl.max_rank : pl.group_rank[g];
         int32_t* e = gct + kGcFields * c;
         e[GC_RANK] = r;
-        e[GC_PAGE_OFF] = pages_base + group_blob_page[g];
+        e[GC_PAGE_OFF] = group_blob_page[g] < 0 ? group_blob_page[g] : pages_base + group_blob_page[g];
         e[GC_TOK_OFF] = toks_base + gcs[c].tok_off;
         e[GC_NTOK] = gcs[c].ntok;
         e[GC_SHRINK_BASE] = shrink;
@@ -208,6 +214,7 @@ static lora_status append_unit_table(Plan& pl, std::string& err) {
     int32_t* h = pl.blob.data();
     const int n_gc = h[0], n_shrink = h[1], n_expand = h[2];
     if (n_gc >= (1 << 15)) { err = "too many (group, token-chunk) units"; return LORA_ERR_ARG; }
+    if (pl.blob.size() >= ((size_t)1 << 19)) { err = "batch metadata too large"; return LORA_ERR_ARG; }
     const size_t base = pl.blob.size();
     pl.blob.resize(base + (size_t)kUnitWords * (n_shrink + n_expand));
     h = pl.blob.data();
@@ -225,16 +232,14 @@ static lora_status append_unit_table(Plan& pl, std::string& err) {
             const int local = u - e[GC_SHRINK_BASE];
             int32_t* w = h + base + (size_t)kUnitWords * u;
             w[0] = (c << 16) | local;
-            w[1] = e[GC_PAGE_OFF] + (local % njb) * shrink_rows(esz);
-            w[2] = e[GC_TOK_OFF];
-            w[3] = (r << 16) | e[GC_NTOK];
+            w[1] = page_ref_add(e[GC_PAGE_OFF], (local % njb) * shrink_rows(esz));
+            w[2] = r | (e[GC_NTOK] << 9) | (e[GC_TOK_OFF] << 13);
         }
         for (int u = e[GC_EXPAND_BASE]; u < e1; ++u) {
             int32_t* w = h + base + (size_t)kUnitWords * (n_shrink + u);
             w[0] = (c << 16) | (u - e[GC_EXPAND_BASE]);
             w[1] = e[GC_PAGE_OFF];
-            w[2] = e[GC_TOK_OFF];
-            w[3] = (r << 16) | e[GC_NTOK];
+            w[2] = r | (e[GC_NTOK] << 9) | (e[GC_TOK_OFF] << 13);
         }
     }
     h[6] = (int32_t)base;
@@ -268,7 +273,7 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
             const int32_t* e = h + kHdrWords + kGcFields * c;
             int32_t* o = m.blob.data() + kHdrWords + kGcFields * gc;
             for (int f = 0; f < kGcFields; ++f) o[f] = e[f];
-            o[GC_PAGE_OFF] = pages_base + pg + (e[GC_PAGE_OFF] - qpb);
+            o[GC_PAGE_OFF] = e[GC_PAGE_OFF] < 0 ? e[GC_PAGE_OFF] : pages_base + pg + (e[GC_PAGE_OFF] - qpb);
             o[GC_TOK_OFF] = toks_base + tk + (e[GC_TOK_OFF] - qtb);
             o[GC_SHRINK_BASE] = e[GC_SHRINK_BASE] + shrink;
             o[GC_EXPAND_BASE] = e[GC_EXPAND_BASE] + expand;
@@ -338,10 +343,8 @@ bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanPara
         const int job = e[GC_JOB];
         const int s = span_of(e[GC_RANK], H_in[job], H_out[job], sp);
         if (s == 0 || e[GC_NTOK] > kSpanTok) return false;
-        // TMA boxes need the rank rows as one run of consecutive pages
-        const int32_t* pg = h + e[GC_PAGE_OFF];
-        for (int j = 1; j < e[GC_RANK]; ++j)
-            if (pg[j] != pg[0] + j) return false;
+        // TMA boxes need the rank rows as one run of consecutive pages (page reference < 0)
+        if (e[GC_PAGE_OFF] >= 0) return false;
         order.push_back({c, s});
     }
     // spans are powers of two: placed in descending size, each starts at a multiple of its size,
@@ -374,7 +377,7 @@ bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanPara
             const int nk = std::max(0, std::min(sk, hi - k0)), nn = std::max(0, std::min(sn, ho - n0));
             w[0] = job | (s << 4) | (i << 12) | (leader << 20);
             w[1] = r | (e[GC_NTOK] << 16);
-            w[2] = h[e[GC_PAGE_OFF]];   // first page (contiguous run checked above)
+            w[2] = ~e[GC_PAGE_OFF];   // first page of the contiguous run
             w[3] = rec_words + n_pages + (e[GC_TOK_OFF] - toks_base);
             w[4] = e[GC_SCALE];
             w[5] = kc | (nc << 16);
