@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--qkv-mode", choices=["serial", "fused", "streams"], default="serial",
                     help="q/k/v: one lora_apply each in stream order, one lora_apply_multi, or forked onto 3 streams")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
+    ap.add_argument("--c5-reps", type=int, default=5, help="config 5 (70B shapes, tp 1/2/4/8 shards) timing reps; 0 = skip")
     return ap.parse_args()
 
 
@@ -410,6 +411,21 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
         lat.append((_t.perf_counter() - t1) * 1e3)
     lat_bytes = np.mean([repo.bytes_of(a, 2) for a in cold]) if cold else 0
     peak = h2d_peak_gbs(dev)
+    # NEXT f1 analysis: the paper computes a cold adapter's prefill delta on host cores
+    # while the adapter uploads.  Paper-style CPU LoRA (torch CPU bf16 x@A@B, all host threads) for
+    # the 512-token prefill at rank 64 vs the measured load latency of that adapter.
+    ad64 = next(a for a in mine if gen.c4_rank(a) == 64)
+    _, _, A64, B64 = repo.items[ad64]
+    xc = torch.randn(512, H).to(torch.bfloat16)
+    A64c = A64.view(torch.bfloat16).reshape(64, H).t().contiguous()   # stored rank-major [r][H_in]
+    B64c = B64.view(torch.bfloat16).reshape(64, H)
+    torch.set_num_threads(len(os.sched_getaffinity(0)))
+    (xc @ A64c) @ B64c
+    t1 = _t.perf_counter()
+    for _ in range(3):
+        (xc @ A64c) @ B64c
+    cpu_ms = (_t.perf_counter() - t1) / 3 * 1e3
+    load_ms = (64 * 2 * H * 2) / (lat_bytes / np.median(lat)) if lat else None   # bytes / measured bytes per ms
     out = {"workload": "c4: Llama-2-13B 5120->5120 bf16, 1000 adapters ranks 8..128 in pinned host memory, pool = 20%% "
                        "of their ranks, Zipf(1.0), 64 decode + 1x512 prefill tokens/step, LRU, rank %d/%d" % (rank, world),
            "value": round(T / (ms * 1e-3), 1), "unit": "tokens/s per GPU (loads included)", "ms_per_step": round(ms, 4),
@@ -418,9 +434,95 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
            "cold_start_ms_per_adapter": round(float(np.median(lat)), 3) if lat else None,
            "cold_start_bytes_per_adapter": int(lat_bytes),
            "cold_start_GBps": round(lat_bytes / (np.median(lat) * 1e-3) / 1e9, 2) if lat else None,
-           "h2d_pinned_peak_GBps": round(peak, 1), "host_repo_setup_s": round(gen_s, 1)}
+           "h2d_pinned_peak_GBps": round(peak, 1), "host_repo_setup_s": round(gen_s, 1),
+           "cpu_assist": {"cpu_prefill_delta_ms": round(cpu_ms, 3), "threads": torch.get_num_threads(),
+                          "adapter_load_ms": round(float(load_ms), 4) if load_ms else None,
+                          "cpu_wins": bool(load_ms is not None and cpu_ms < load_ms),
+                          "what": "torch CPU bf16 (x@A)@B, 512 tokens, r=64, 5120->5120, vs measured load of a "
+                                  "rank-64 adapter (scaled from the cold-start latency)"}}
     pool.close()
     return out
+
+
+# ---------------------------------------------------------------- config 5: Llama-2-70B shapes, TP shards
+def bench_c5(L, dev, reps: int, hbm_peak: float):
+    """c5: Llama-2-70B per-layer projection shapes (q/o 8192^2, k/v 8192->1024, gate/up 8192->28672,
+    down 28672->8192), decode 64 tokens over 32 adapters of ranks [16,32,64,128][a mod 4].  tp = 1:
+    lora_apply on the full shape.  tp = 2/4/8 (BJ scheme): ONE rank's work, i.e.
+    lora_apply_shrink on its H_in slice + lora_apply_expand on its H_out slice, with the v
+    all-reduce between them excluded (one GPU here; correctness of the split is tested on gloo and
+    NCCL world-1).  Device time per apply from a CUDA graph over enough distinct pools that the
+    adapter rows exceed L2."""
+    import torch
+    shapes = {"q": (8192, 8192), "kv": (8192, 1024), "gate_up": (8192, 28672), "down": (28672, 8192)}
+    ranks = [gen.C5_RANKS[a % 4] for a in range(32)]
+    b = gen.config_c5("q")
+    ip, ids = b.seg_indptr, b.adapter_ids
+    T = 64
+    st = torch.cuda.Stream(device=dev)
+    out = {}
+    for name, (H_in, H_out) in shapes.items():
+        full = [gen.make_adapter(gen.BASE_SEED + 4, 50 + list(shapes).index(name), a, ranks[a], H_in, H_out, "bf16")
+                for a in range(32)]
+        row = {}
+        for tp in (1, 2, 4, 8):
+            hi, ho = H_in // tp, H_out // tp
+            adapter_bytes = sum(ranks) * (hi + ho) * 2
+            n_pools = max(2, -(-400_000_000 // adapter_bytes))
+            pools = []
+            for _ in range(n_pools):
+                pool = L.LoraPool(hi, ho, 32, "bf16", max_total_rank=sum(ranks))
+                for a in full:   # rank 0's shard: A[:, :hi] (stored [r][H_in]) and B[:, :ho]
+                    A = torch.from_numpy(np.ascontiguousarray(a.A[:, :hi]).view(np.int16)).pin_memory()
+                    B = torch.from_numpy(np.ascontiguousarray(a.B[:, :ho]).view(np.int16)).pin_memory()
+                    pool.load_adapter(a.id, a.rank, A, B, a.scale)
+                pools.append(pool)
+            torch.cuda.synchronize()
+            x = torch.randn(T, hi).to(torch.bfloat16).to(dev)
+            ys = [torch.zeros(T, ho, dtype=torch.bfloat16, device=dev) for _ in pools]
+            vs = None
+            if tp > 1:
+                pools[0].plan(ip, ids)
+                nv = pools[0].metadata()["v_floats"]
+                vs = [torch.zeros(max(1, nv), dtype=torch.float32, device=dev) for _ in pools]
+
+            def body():
+                for i, (pool, y) in enumerate(zip(pools, ys)):
+                    if tp == 1:
+                        pool.apply(x, y, ip, ids, stream=st)
+                    else:
+                        pool.apply_shrink(x, ip, ids, vs[i], stream=st)
+                        pool.apply_expand(y, vs[i], stream=st)
+
+            with torch.cuda.stream(st):
+                body()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                body()
+            ts = []
+            for _ in range(max(1, reps)):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                with torch.cuda.stream(st):
+                    g.replay()
+                e1.record(st)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3 / n_pools)
+            us = float(np.median(ts))
+            byts = adapter_bytes + T * hi * 2 + 2 * T * ho * 2
+            row["tp%d" % tp] = {"us_per_apply": round(us, 3), "adapter_MB_per_gpu": round(adapter_bytes / 1e6, 2),
+                                "GBps": round(byts / (us * 1e-6) / 1e9, 1),
+                                "roofline_frac": round(byts / (us * 1e-6) / 1e9 / hbm_peak, 4)}
+            for pool in pools:
+                pool.close()
+            del pools, ys, vs
+        for tp in (2, 4, 8):
+            row["tp%d" % tp]["speedup_vs_tp1"] = round(row["tp1"]["us_per_apply"] / row["tp%d" % tp]["us_per_apply"], 2)
+        out[name] = row
+    return {"workload": "c5: Llama-2-70B projection shapes, decode 64 tokens over 32 adapters ranks 16..128, bf16; "
+                        "tp>1 = one rank's shard kernels (shrink + expand), v all-reduce excluded",
+            "shapes": {k: list(v) for k, v in shapes.items()}, "per_shape": out}
 
 
 # ---------------------------------------------------------------- our arm
@@ -580,6 +682,10 @@ def main():
     if args.c4_steps > 0:
         c4 = bench_c4(L, dev, args.c4_steps, world, rank)
 
+    c5 = None
+    if args.c5_reps > 0:
+        c5 = bench_c5(L, dev, args.c5_reps, hbm_peak)
+
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -607,6 +713,7 @@ def main():
                 "gpu_launches": int(launches_per_step * args.steps),
                 "prefill": prefill,
                 "c4": c4,
+                "c5": c5,
                 "setup_s": round(t_gen, 1)}
         s = json.dumps(line)
         print(s, flush=True)

@@ -48,6 +48,7 @@ struct DecodeArgs {
     unsigned long long* trace;   // debug: per-unit timestamps, or null
     int n_shrink, n_expand, n_gc, n_jobs;
     int unit_tab;                // blob word offset of the per-unit table (plan.cpp append_unit_table)
+    int unit_words;              // 3 (full unit records) or 1 (gc | local only: large batches)
     // bf16 expand smem layout, sized per launch from the batch (max rank / tokens / columns)
     int e_vpitch, e_boff, e_yoff, e_dtoff, e_pgoff, e_smem;
     int* gc_sync;                // fused mode: [n_gc] shrink-done, [n_gc] expand-done counters; gc_sync[-1] = timeout flag
@@ -231,6 +232,32 @@ struct Elem<float> {
 __device__ __forceinline__ int gc_field(const int32_t* M, int gc, int f) { return M[kHdrWords + gc * kGcFields + f]; }
 // page of rank row j of a page reference (kernel_config.h page_ref_add)
 __device__ __forceinline__ int page_at(const int32_t* M, int ref, int j) { return ref >= 0 ? M[ref + j] : (~ref) + j; }
+// unit u's work record.  3-word mode: one round of independent uniform loads; 1-word mode (batches
+// whose 3-word table would overflow the kernel parameters): the rest comes from the gc record.
+struct UnitRec {
+    int gc, local, pref, toff, r, ntok;
+};
+__device__ __forceinline__ UnitRec load_unit(const int32_t* M, int unit_tab, int unit_words, int u, bool shrink) {
+    UnitRec d;
+    const int32_t* rec = M + unit_tab + unit_words * u;
+    const uint32_t uw = (uint32_t)rec[0];
+    d.gc = (int)(uw >> 16);
+    d.local = (int)(uw & 0xffffu);
+    if (unit_words == 3) {
+        const uint32_t rn = (uint32_t)rec[2];
+        d.pref = rec[1];
+        d.toff = unit_tok_off(rn);
+        d.r = unit_rank(rn);
+        d.ntok = unit_ntok(rn);
+    } else {
+        d.r = gc_field(M, d.gc, GC_RANK);
+        d.ntok = gc_field(M, d.gc, GC_NTOK);
+        d.toff = gc_field(M, d.gc, GC_TOK_OFF);
+        d.pref = gc_field(M, d.gc, GC_PAGE_OFF);
+        if (shrink) d.pref = page_ref_add(d.pref, (d.local % shrink_jblocks(d.r, 2)) * kShrinkRowsMma);
+    }
+    return d;
+}
 
 // per-CTA unit description, decoded once by warp 0 and shared through smem
 struct UnitSh {
@@ -268,7 +295,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         // 1. decode the unit and issue the adapter-row loads (immutable pool pages) before
         //    waiting on the previous kernel in the stream
         const int job = job_of(u, a.n_jobs, a.job_shrink_base);
-        const uint32_t uw = (uint32_t)M[a.unit_tab + kUnitWords * u];   // (gc, index in gc)
+        const uint32_t uw = (uint32_t)M[a.unit_tab + a.unit_words * u];   // (gc, index in gc)
         const int gc = (int)(uw >> 16);
         const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
@@ -397,7 +424,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     if (warp == 0) {
         // 1. decode the unit; B rows (immutable pool pages) before waiting on the shrink kernel
         const int job = job_of(ue, a.n_jobs, a.job_expand_base);
-        const uint32_t uw = (uint32_t)M[a.unit_tab + kUnitWords * (a.n_shrink + ue)];
+        const uint32_t uw = (uint32_t)M[a.unit_tab + a.unit_words * (a.n_shrink + ue)];
         const int gc = (int)(uw >> 16);
         const DecodeJob J = a.jobs[job];
         const int r = gc_field(M, gc, GC_RANK);
@@ -616,11 +643,10 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         }
         const int job = job_of(u, a.n_jobs, a.job_shrink_base);
         // round 1: the unit record (independent uniform loads)
-        const int32_t* rec = M + a.unit_tab + kUnitWords * u;
-        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[2];
-        const int pg0 = rec[1], toff = unit_tok_off(rn);
-        const int gc = (int)(uw >> 16), local = (int)(uw & 0xffffu);
-        const int r = unit_rank(rn), ntok = unit_ntok(rn);
+        const UnitRec ur = load_unit(M, a.unit_tab, a.unit_words, u, true);
+        const int pg0 = ur.pref, toff = ur.toff;
+        const int gc = ur.gc, local = ur.local;
+        const int r = ur.r, ntok = ur.ntok;
         const DecodeJob J = a.jobs[job];
         const int njb = shrink_jblocks(r, ES);
         const int ks = local / njb;
@@ -763,11 +789,10 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         const int job = job_of(ue, a.n_jobs, a.job_expand_base);
-        const int32_t* rec = M + a.unit_tab + kUnitWords * (a.n_shrink + ue);
-        const uint32_t uw = (uint32_t)rec[0], rn = (uint32_t)rec[2];
-        const int poff = rec[1], toff = unit_tok_off(rn);
-        const int gc = (int)(uw >> 16), local = (int)(uw & 0xffffu);
-        const int r = unit_rank(rn), ntok = unit_ntok(rn);
+        const UnitRec ur = load_unit(M, a.unit_tab, a.unit_words, a.n_shrink + ue, false);
+        const int poff = ur.pref, toff = ur.toff;
+        const int gc = ur.gc, local = ur.local;
+        const int r = ur.r, ntok = ur.ntok;
         const DecodeJob J = a.jobs[job];
         const int c = expand_ncols(r, ES);
         const int n0 = local * c;
@@ -1099,6 +1124,7 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
     a.n_expand = pl.n_expand;
     a.n_gc = pl.n_gc;
     a.unit_tab = pl.unit_tab;
+    a.unit_words = pl.unit_words;
     a.gc_sync = L.gc_sync;
     a.n_jobs = pl.n_jobs;
     for (int j = 0; j < kMaxJobs; ++j) {

@@ -29,6 +29,7 @@ constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, k
 // blob = header | gc records [n_gc][kGcFields] | pages | tokens | unit table [n_shrink + n_expand]
 // (unit record = kUnitWords words, see plan.cpp append_unit_table)
 constexpr int kUnitWords = 3;
+constexpr int kMaxParamBlobWords = 7936;   // largest metadata blob passed as kernel parameters
 // A page reference is either a blob word offset of an explicit page list (>= 0) or, for a run of
 // consecutive pages, ~first_page (< 0): page j = first_page + j.  Contiguous adapters (the
 // allocator's lowest-free-first order makes them the common case) then cost no blob words.

@@ -216,7 +216,12 @@ static lora_status append_unit_table(Plan& pl, std::string& err) {
     if (n_gc >= (1 << 15)) { err = "too many (group, token-chunk) units"; return LORA_ERR_ARG; }
     if (pl.blob.size() >= ((size_t)1 << 19)) { err = "batch metadata too large"; return LORA_ERR_ARG; }
     const size_t base = pl.blob.size();
-    pl.blob.resize(base + (size_t)kUnitWords * (n_shrink + n_expand));
+    // full 3-word records while the blob fits the kernel parameters, else 1 word per unit (the
+    // kernels then read rank / tokens / pages from the gc record: one more dependent load)
+    const size_t units = (size_t)n_shrink + n_expand;
+    const int uw = base + (size_t)kUnitWords * units <= (size_t)kMaxParamBlobWords ? kUnitWords : 1;
+    pl.unit_words = uw;
+    pl.blob.resize(base + (size_t)uw * units);
     h = pl.blob.data();
     const int esz = pl.blob_esz;
     for (int c = 0; c < n_gc; ++c) {
@@ -230,14 +235,16 @@ static lora_status append_unit_table(Plan& pl, std::string& err) {
         const int r = e[GC_RANK], njb = shrink_jblocks(r, esz);
         for (int u = e[GC_SHRINK_BASE]; u < s1; ++u) {
             const int local = u - e[GC_SHRINK_BASE];
-            int32_t* w = h + base + (size_t)kUnitWords * u;
+            int32_t* w = h + base + (size_t)uw * u;
             w[0] = (c << 16) | local;
+            if (uw == 1) continue;
             w[1] = page_ref_add(e[GC_PAGE_OFF], (local % njb) * shrink_rows(esz));
             w[2] = r | (e[GC_NTOK] << 9) | (e[GC_TOK_OFF] << 13);
         }
         for (int u = e[GC_EXPAND_BASE]; u < e1; ++u) {
-            int32_t* w = h + base + (size_t)kUnitWords * (n_shrink + u);
+            int32_t* w = h + base + (size_t)uw * (n_shrink + u);
             w[0] = (c << 16) | (u - e[GC_EXPAND_BASE]);
+            if (uw == 1) continue;
             w[1] = e[GC_PAGE_OFF];
             w[2] = r | (e[GC_NTOK] << 9) | (e[GC_TOK_OFF] << 13);
         }

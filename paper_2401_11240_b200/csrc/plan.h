@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/lora_delta.h"
+#include "kernel_config.h"
 
 namespace lora {
 
@@ -39,6 +40,7 @@ struct Plan {
     std::vector<int32_t> blob;           // see kernel_config.h for the layout
     int32_t n_gc = 0, n_shrink = 0, n_expand = 0;
     int32_t unit_tab = 0;                // blob word offset of the per-unit table
+    int32_t unit_words = kUnitWords;     // words per unit record: kUnitWords, or 1 for large batches
     int32_t blob_esz = 2;                // element size the unit table was built for
     int64_t vbuf_floats = 0;
     int32_t n_jobs = 1;                          // pools fused by lora_apply_multi
