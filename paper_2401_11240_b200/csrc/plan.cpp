@@ -132,6 +132,13 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
                 rec[2] = pl.group_rank[sg.group];
                 rec[3] = tiles * 8 + group_pf_off[sg.group];
                 rec[4] = f32_bits(pl.group_scale[sg.group]);
+                // rec[5]: first page when the adapter's pages are one run (2D TMA boxes), else -1
+                {
+                    const int32_t* gp = pl.pages.data() + pl.group_page_off[sg.group];
+                    bool run = true;
+                    for (int j = 1; j < pl.group_rank[sg.group] && run; ++j) run = gp[j] == gp[0] + j;
+                    rec[5] = run ? gp[0] : -1;
+                }
                 ++tix;
             }
         }

@@ -49,7 +49,7 @@ struct Plan {
     // ---- tcgen05 prefill work (N2) ----
     std::vector<PrefillSeg> prefill;
     int32_t n_prefill_tiles = 0;     // == n_pf_tiles (128-token tiles on the tensor-core path)
-    std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] tile records {tok0, nvalid, rank, page_off, scale_bits}, then pages
+    std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] tile records {tok0, nvalid, rank, page_off, scale_bits, first_page|-1}, then pages
     int32_t n_pf_tiles = 0;
     // ---- cluster-span decode work (N1c, span_kernel.cu): one grid per apply ----
     std::vector<int32_t> span_blob;  // [n_span_cta][kSpanRecWords] CTA records, then pages, then tokens
@@ -115,6 +115,7 @@ struct PrefillLaunch {
     void* y;
     const void* tm_a;      // 128-B CUtensorMap of the A pages (gather4 box {64, 1})
     const void* tm_b;      // 128-B CUtensorMap of the B pages
+    const void* box_maps;  // device: the pool's 2D box maps (span_make_tmaps: A boxes {64, 8<<k}, then B)
     const int32_t* meta_dev;
     unsigned long long* trace;
     int T, H_in, H_out, zero_page, num_sms;

@@ -437,7 +437,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
     if (pl.n_pf_tiles > 0 && mode == 0) {
-        PrefillLaunch L{x, y, p->tm_a, p->tm_b, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
+        PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
         cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
     }
@@ -551,7 +551,8 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
         if (p->plan.n_pf_tiles == 0) continue;
-        PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
+        PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
+                        p->num_sms};
         cudaError_t e = (cudaError_t)launch_prefill(p->plan, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: prefill kernel launch");
     }

@@ -45,6 +45,7 @@ struct PrefillArgs {
     CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads; writes go per row)
+    const char* box_maps;   // pool page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), SW128
     char* y;
     const int32_t* meta_global;
     unsigned long long* trace;
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const int32_t* rec = M + tile * kPfTileWords;
     const int tok0 = rec[0], nvalid = rec[1], r = rec[2], poff = rec[3];
     const float scale = __int_as_float(rec[4]);
+    const int first_page = rec[5];   // >= 0: rank rows are pages [first_page, first_page + r)
     const int rp = (r + 15) & ~15;                      // rank padded to the MMA N/K granularity
     const int nkc = a.H_in / 64;                        // shrink K chunks
     const int nnt = a.H_out / kPfNTile;                 // expand column tiles
@@ -209,15 +211,32 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             const int j = lane * 4 + q;
             pg[q] = j < r ? M[poff + j] : a.zero_page;
         }
+        // contiguous adapters: rp rank rows as 2D boxes of 128/64/32/16 rows (one TMA request
+        // instead of rp/4 gather4s; the request rate bounded the rank-128 tiles); rows r..rp-1
+        // then hold neighbouring pages, which the epilogue neutralises by zeroing V there
+        auto boxes = [&](uint32_t dst, int map_base, int col) {
+            int row = 0;
+            for (int k = 4; k >= 1; --k) {
+                const int R = 8 << k;
+                while (rp - row >= R) {
+                    tma_2d(dst + (uint32_t)row * 128u,
+                           reinterpret_cast<const CUtensorMap*>(a.box_maps + (map_base + k) * 128), col,
+                           first_page + row, full(stage));
+                    row += R;
+                }
+            }
+        };
+        const bool use_box = first_page >= 0 && a.box_maps != nullptr;
         for (int kc = 0; kc < nkc; ++kc) {
             pf_wait(empty(stage), phase ^ 1u);
             const uint32_t sb = ring + stage * kPfStageBytes;
             if (lane == 0) {
                 pf_arrive_tx(full(stage), (uint32_t)(128 * 128 + rp * 128));
                 tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
+                if (use_box) boxes(sb + 16384, 0, kc * 64);
             }
             __syncwarp();
-            if (lane < ngr)
+            if (!use_box && lane < ngr)
                 tma_gather4(sb + 16384 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
             if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
         }
@@ -226,9 +245,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         for (int nt = 0; nt < nnt; ++nt) {
             pf_wait(empty(stage), phase ^ 1u);
             const uint32_t sb = ring + stage * kPfStageBytes;
-            if (lane == 0) pf_arrive_tx(full(stage), (uint32_t)(rp * kPfNTile * 2));
+            if (lane == 0) {
+                pf_arrive_tx(full(stage), (uint32_t)(rp * kPfNTile * 2));
+                if (use_box)
+                    for (int h = 0; h < 2; ++h)
+                        boxes(sb + (uint32_t)(h * (rp / 8)) * 1024u, kSpanBoxKinds, nt * kPfNTile + h * 64);
+            }
             __syncwarp();
-            if (lane < ngr) {
+            if (!use_box && lane < ngr) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t dst = sb + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
@@ -300,7 +324,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 uint32_t hw[4], lw[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const float f0 = v[q * 8 + 2 * e] * scale, f1 = v[q * 8 + 2 * e + 1] * scale;
+                    // columns >= r are exact zeros (they may come from neighbouring pages on the box path)
+                    const int j0 = c0 + q * 8 + 2 * e;
+                    const float f0 = j0 < r ? v[q * 8 + 2 * e] * scale : 0.f;
+                    const float f1 = j0 + 1 < r ? v[q * 8 + 2 * e + 1] * scale : 0.f;
                     __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
                     const float2 hf = __bfloat1622float2(h);
                     __nv_bfloat162 l = __floats2bfloat162_rn(f0 - hf.x, f1 - hf.y);
@@ -449,6 +476,7 @@ int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int*
     if (e) return e;
     std::memcpy(&a.tm_a, L.tm_a, sizeof(CUtensorMap));
     std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
+    a.box_maps = static_cast<const char*>(L.box_maps);
     e = make_tmap_bf16(&a.tm_y, L.y, L.T, L.H_out, 128);
     if (e) return e;
     a.y = static_cast<char*>(L.y);
