@@ -32,7 +32,8 @@
 namespace lora {
 
 constexpr int kPfThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
-constexpr int kPfStages = 3;
+constexpr int kPfStages = 3;           // expand-phase ring (B tiles)
+constexpr int kPfShrinkStages = 7;     // shrink-phase ring: the 3 ring stages + the V and y buffers, idle until D1 is done
 constexpr int kPfStageBytes = 32768;   // X chunk 16 KB + A chunk <= 16 KB, or one B tile (<= 32 KB)
 constexpr int kPfVBytes = 128 * 128 * 2;   // one V part (hi or lo): 128 tokens x r16 <= 128, bf16
 constexpr int kPfYBytes = 128 * 128 * 2;   // one staged y tile (128 tokens x 128 columns, bf16)
@@ -151,14 +152,18 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const uint32_t yring = vlo + kPfVBytes;             // 2 x 32 KB staged y tiles
     uint8_t* gy = gbase + (yring - base);
     const uint32_t bars = yring + 2 * kPfYBytes;        // 14 mbarriers + tmem slot
+    // barriers: shrink ring full/empty [7] x 2, expand ring full/empty [3] x 2, then the rest
     auto full = [&](int s) { return bars + 8u * s; };
-    auto empty = [&](int s) { return bars + 8u * (kPfStages + s); };
-    const uint32_t d1_full = bars + 8u * (2 * kPfStages);
+    auto empty = [&](int s) { return bars + 8u * (kPfShrinkStages + s); };
+    auto full2 = [&](int s) { return bars + 8u * (2 * kPfShrinkStages + s); };
+    auto empty2 = [&](int s) { return bars + 8u * (2 * kPfShrinkStages + kPfStages + s); };
+    const uint32_t d1_full = bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages);
     const uint32_t v_ready = d1_full + 8u;
     auto tm_full = [&](int b) { return v_ready + 8u + 8u * b; };
     auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
     auto y_full = [&](int b) { return v_ready + 40u + 8u * b; };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfStages + 8) - base));
+    uint32_t* tmem_slot =
+        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 8) - base));
 
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -173,9 +178,13 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     if (a.trace && tid == 0) a.trace[(size_t)tile * 4 + 0] = pf_gtime();
 
     if (tid == 0) {
-        for (int s = 0; s < kPfStages; ++s) {
+        for (int s = 0; s < kPfShrinkStages; ++s) {
             pf_bar_init(full(s), 1);
             pf_bar_init(empty(s), 1);
+        }
+        for (int s = 0; s < kPfStages; ++s) {
+            pf_bar_init(full2(s), 1);
+            pf_bar_init(empty2(s), 1);
         }
         pf_bar_init(d1_full, 1);
         pf_bar_init(v_ready, 128);
@@ -214,14 +223,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         // contiguous adapters: rp rank rows as 2D boxes of 128/64/32/16 rows (one TMA request
         // instead of rp/4 gather4s; the request rate bounded the rank-128 tiles); rows r..rp-1
         // then hold neighbouring pages, which the epilogue neutralises by zeroing V there
-        auto boxes = [&](uint32_t dst, int map_base, int col) {
+        auto boxes = [&](uint32_t dst, int map_base, int col, uint32_t bar) {
             int row = 0;
             for (int k = 4; k >= 1; --k) {
                 const int R = 8 << k;
                 while (rp - row >= R) {
                     tma_2d(dst + (uint32_t)row * 128u,
                            reinterpret_cast<const CUtensorMap*>(a.box_maps + (map_base + k) * 128), col,
-                           first_page + row, full(stage));
+                           first_page + row, bar);
                     row += R;
                 }
             }
@@ -233,30 +242,34 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             if (lane == 0) {
                 pf_arrive_tx(full(stage), (uint32_t)(128 * 128 + rp * 128));
                 tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
-                if (use_box) boxes(sb + 16384, 0, kc * 64);
+                if (use_box) boxes(sb + 16384, 0, kc * 64, full(stage));
             }
             __syncwarp();
             if (!use_box && lane < ngr)
                 tma_gather4(sb + 16384 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
-            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
+            if (++stage == kPfShrinkStages) { stage = 0; phase ^= 1u; }
         }
+        // the expand ring reuses shrink stages 0-2: wait until every shrink MMA has read them
+        pf_wait(d1_full, 0);
+        stage = 0;
+        phase = 0;
         // expand: B rows of each 128-column tile, MN-major SW128 atoms (8 rank rows x 64 cols);
         // atom (kg, ng) at (ng * rp/8 + kg) * 1 KB; a gather4 fills 4 rows of one atom
         for (int nt = 0; nt < nnt; ++nt) {
-            pf_wait(empty(stage), phase ^ 1u);
+            pf_wait(empty2(stage), phase ^ 1u);
             const uint32_t sb = ring + stage * kPfStageBytes;
             if (lane == 0) {
-                pf_arrive_tx(full(stage), (uint32_t)(rp * kPfNTile * 2));
+                pf_arrive_tx(full2(stage), (uint32_t)(rp * kPfNTile * 2));
                 if (use_box)
                     for (int h = 0; h < 2; ++h)
-                        boxes(sb + (uint32_t)(h * (rp / 8)) * 1024u, kSpanBoxKinds, nt * kPfNTile + h * 64);
+                        boxes(sb + (uint32_t)(h * (rp / 8)) * 1024u, kSpanBoxKinds, nt * kPfNTile + h * 64, full2(stage));
             }
             __syncwarp();
             if (!use_box && lane < ngr) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t dst = sb + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
-                    tma_gather4(dst, &a.tm_b, nt * kPfNTile + h * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
+                    tma_gather4(dst, &a.tm_b, nt * kPfNTile + h * 64, pg[0], pg[1], pg[2], pg[3], full2(stage));
                 }
             }
             if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
@@ -280,15 +293,17 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 if (kc == nkc - 1) umma_commit(d1_full);
             }
             __syncwarp();
-            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
+            if (++stage == kPfShrinkStages) { stage = 0; phase ^= 1u; }
         }
+        stage = 0;
+        phase = 0;
         pf_wait(v_ready, 0);
         tc_fence_after();
         const int ksteps = rp / 16;
         for (int nt = 0; nt < nnt; ++nt) {
             const int b = nt & 1;
             pf_wait(tm_empty(b), ((nt >> 1) & 1) ^ 1u);
-            pf_wait(full(stage), phase);
+            pf_wait(full2(stage), phase);
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t sb = ring + stage * kPfStageBytes;
@@ -300,7 +315,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                     umma_f16(dcol, umma_desc(vhi + voff, 16, 1024), bd, id2, ks != 0);
                     umma_f16(dcol, umma_desc(vlo + voff, 16, 1024), bd, id2, 1);
                 }
-                umma_commit(empty(stage));
+                umma_commit(empty2(stage));
                 umma_commit(tm_full(b));
             }
             __syncwarp();
