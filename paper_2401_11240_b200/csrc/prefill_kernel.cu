@@ -366,7 +366,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         //      half, 16-B chunk c at c ^ (row%8)); results go straight to global, valid rows only
         //      (rows past the segment belong to other segments' tiles).
         const bool valid = row < nvalid;
-        char* yrow = a.y + ((size_t)(tok0 + row) * a.H_out) * 2;
         const bool leader = (tid == 64);
         auto issue_y = [&](int nt) {
             const int b = nt & 1;
@@ -384,7 +383,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             pf_wait(tm_full(b), (nt >> 1) & 1);
             pf_wait(y_full(b), (nt >> 1) & 1);
             tc_fence_after();
-            const uint8_t* ys = gy + b * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
+            uint8_t* ys = gy + b * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll 1
             for (int c0 = 0; c0 < kPfNTile; c0 += 32) {
                 float d[32];
@@ -407,13 +406,33 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                         }
                         o4[q] = make_uint4(o[0], o[1], o[2], o[3]);
                     }
-                    uint4* yp = reinterpret_cast<uint4*>(yrow + (size_t)(nt * kPfNTile + c0) * 2);
+                    // back into the row's own (swizzled) slots of the staged tile
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) yp[q] = o4[q];
+                    for (int q = 0; q < 4; ++q) {
+                        const int col = c0 + q * 8;
+                        const int h = col >> 6, chunk = (col & 63) >> 3;
+                        *reinterpret_cast<uint4*>(ys + h * (kPfYBytes / 2) + ((chunk ^ (row & 7)) << 4)) = o4[q];
+                    }
                 }
             }
             tc_fence_before();
             pf_arrive(tm_empty(b));
+            // coalesced write-back: the warp's 32 rows leave as 256-B row segments, two rows per
+            // STG.128 instruction (a thread-per-row store touches 32 rows per instruction)
+            __syncwarp();
+            {
+                const uint8_t* yslot = gy + b * kPfYBytes;
+#pragma unroll 4
+                for (int i = 0; i < 16; ++i) {
+                    const int rr = sub * 32 + i * 2 + (lane >> 4), c16 = lane & 15;
+                    if (rr < nvalid) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(
+                            yslot + (c16 >> 3) * (kPfYBytes / 2) + (rr >> 3) * 1024 + (rr & 7) * 128 +
+                            (((c16 & 7) ^ (rr & 7)) << 4));
+                        *reinterpret_cast<uint4*>(a.y + ((size_t)(tok0 + rr) * a.H_out + nt * kPfNTile + c16 * 8) * 2) = v;
+                    }
+                }
+            }
             // every epilogue thread is done with y slot b -> refill it with tile nt + 2
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (leader && nt + 2 < nnt) issue_y(nt + 2);
