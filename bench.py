@@ -9,6 +9,9 @@ adapter weights per layer and projection, as in real serving).  The working set
 (128 pools x 15.7 MB of adapter rows + x/y) is 2.2 GB >> the 126 MB L2, so no L2 flush
 is needed between steps ("inputs larger than L2").
 
+Per layer the step issues one lora_apply_multi for q/k/v (they share x and are independent) and
+one lora_apply for o (its input is the attention output); --qkv-mode serial issues 4 applies.
+
 value   tokens/s = (64 tokens x ranks) / step time, device-timed with CUDA events around K
         replays of a CUDA graph of one step (inputs resident in HBM), max over ranks.
 e2e     the same metric through the public API (LoraPool.apply -> lora_apply) with host
@@ -63,8 +66,10 @@ def parse():
     ap.add_argument("--prefill-layers", type=int, default=2,
                     help="layers of the c3 prefill measurement reported in the 'prefill' object (0 = skip)")
     ap.add_argument("--prefill-steps", type=int, default=20)
-    ap.add_argument("--qkv-mode", choices=["serial", "fused", "streams"], default="serial",
-                    help="q/k/v: one lora_apply each in stream order, one lora_apply_multi, or forked onto 3 streams")
+    ap.add_argument("--qkv-mode", choices=["serial", "fused", "streams"], default="fused",
+                    help="q/k/v (same x, independent deltas; the paper adapts W_Q/W_K/W_V together, P:875): one "
+                         "lora_apply_multi (default), one lora_apply each in stream order, or forked onto 3 streams; "
+                         "o (input = attention output) is always its own lora_apply")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
     ap.add_argument("--c5-reps", type=int, default=5, help="config 5 (70B shapes, tp 1/2/4/8 shards) timing reps; 0 = skip")
     return ap.parse_args()

@@ -74,8 +74,11 @@ typedef enum {
 #define LORA_OPT_TC_THRESHOLD 1    /* L_tc (default 64); segments with len >= L_tc take the tcgen05 path.
                                       A value larger than any segment forces the SIMT path everywhere. */
 #define LORA_OPT_RESERVE_TOKENS 2  /* pre-size scratch for this many tokens (avoids a cudaMalloc in apply) */
-#define LORA_OPT_DECODE_FUSED 3    /* bf16 decode as ONE grid per apply (1) or a PDL-chained (0, default)
-                                      shrink/expand kernel pair (0).  Same arithmetic, bitwise equal. */
+#define LORA_OPT_DECODE_FUSED 3    /* bf16 decode hand-off: 0 (default) = PDL-chained shrink/expand kernel
+                                      pair; 1 = ONE grid per apply (expand units wait on per-gc counters);
+                                      2 = flag-chained pair (two grids, the expand grid acquires the per-gc
+                                      counters instead of waiting for the whole shrink grid).  Same
+                                      arithmetic, bitwise equal. */
 #define LORA_OPT_DECODE_PATH 4     /* bf16 decode tokens: 0 (default) = the PDL-chained shrink/expand
                                       kernel pair; 1 = EXPERIMENTAL one-grid cluster-span kernel
                                       (csrc/span_kernel.cu: shrink partials reduced over distributed

@@ -52,6 +52,7 @@ struct DecodeArgs {
     // bf16 expand smem layout, sized per launch from the batch (max rank / tokens / columns)
     int e_vpitch, e_boff, e_yoff, e_dtoff, e_pgoff, e_smem;
     int* gc_sync;                // fused mode: [n_gc] shrink-done, [n_gc] expand-done counters; gc_sync[-1] = timeout flag
+    int flag_chain;              // flag-chained pair: the expand grid skips griddepcontrol.wait (see launch_pair)
     int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
     int job_expand_base[kMaxJobs];
 };
@@ -671,7 +672,9 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
             bulk_g2s(abuf + lane * kAPitch, J.A + ((size_t)page * J.H_in + k0) * ES, (uint32_t)(nk * ES), &bars[0],
                      policy_evict_first());
     }
-    pdl_launch_dependents();
+    // flag-chained pair: trigger the expand grid only after this CTA passed its grid wait (below),
+    // so no expand CTA can read counters the preceding apply of this pool has not re-armed yet
+    if (!(FUSED && a.flag_chain)) pdl_launch_dependents();
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 6] = gtime();
     __syncthreads();
     const DecodeJob J = a.jobs[sh->job];
@@ -681,6 +684,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
     const int nk = min(kKSlice, J.H_in - k0);
     // x (and the v scratch we overwrite) may belong to the preceding kernel in the stream
     pdl_wait_cta();
+    if (FUSED && a.flag_chain) pdl_launch_dependents();
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
     uint4 xr[kKBlocks];
     {
@@ -739,14 +743,14 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
     }
 }
 
-template <int W>
+template <int W, bool FLAG>
 __global__ void __launch_bounds__(kConsumerThreads)
     lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     if (a.trace && threadIdx.x == 0) a.trace[(size_t)blockIdx.x * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
-    shrink_mma_body<false>(a, M, blockIdx.x, smem);
+    shrink_mma_body<FLAG>(a, M, blockIdx.x, smem);
 }
 
 // ---- expand (bf16): one CTA = (group-chunk gc, column slice [n0, n0+nc)).  Swap-AB:
@@ -857,7 +861,12 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     if (FUSED) {
         // y (and the counters) from the preceding grid; v from this grid's shrink units of the gc
         if (tid == 0) {
-            pdl_wait();
+            // one grid: wait for the preceding grid (y).  Flag-chained pair: no grid wait at all --
+            // the gc's shrink CTAs released the counter after passing THEIR griddepcontrol.wait on
+            // the preceding grid, so acquiring it orders this CTA after that grid's writes too; and
+            // PDL launched this grid only once every shrink CTA had triggered, i.e. was resident or
+            // done, so the spin cannot wait on an unscheduled CTA.
+            if (!a.flag_chain) pdl_wait();
             spin_acquire_geq(a.gc_sync + sh->gc, sh->ks, a.gc_sync - 1);
         }
         __syncthreads();
@@ -983,14 +992,14 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     }
 }
 
-template <int W>
+template <int W, bool FLAG>
 __global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 CTAs per SM */
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     if (a.trace && threadIdx.x == 0) a.trace[(size_t)(blockIdx.x + a.n_shrink) * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();
-    expand_mma_body<false>(a, M, blockIdx.x, smem);
+    expand_mma_body<FLAG>(a, M, blockIdx.x, smem);
 }
 
 // ---- fused decode (bf16): ONE grid per apply, CTAs [0, n_shrink) run shrink units and CTAs
@@ -1049,11 +1058,15 @@ struct DecodeKernels {
     static int expand_launch_smem(const DecodeArgs&) { return kExpandSmem; }
     static constexpr bool has_fused = false;
     static constexpr auto fused = lora_shrink_kernel<T, W>;   // unused
+    static constexpr auto shrink_flag = lora_shrink_kernel<T, W>;   // unused
+    static constexpr auto expand_flag = lora_expand_kernel<T, W>;   // unused
 };
 template <int W>
 struct DecodeKernels<__nv_bfloat16, W> {
-    static constexpr auto shrink = lora_shrink_mma_kernel<W>;
-    static constexpr auto expand = lora_expand_mma_kernel<W>;
+    static constexpr auto shrink = lora_shrink_mma_kernel<W, false>;
+    static constexpr auto expand = lora_expand_mma_kernel<W, false>;
+    static constexpr auto shrink_flag = lora_shrink_mma_kernel<W, true>;
+    static constexpr auto expand_flag = lora_expand_mma_kernel<W, true>;
     static constexpr int shrink_smem = kShrinkMmaLaunchSmem;
     static constexpr int expand_smem = kExpandMmaSmemMax;
     static int expand_launch_smem(const DecodeArgs& a) { return a.e_smem; }
@@ -1070,8 +1083,11 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         constexpr int kMaxOptin = 227 * 1024;
         cudaError_t e = cudaFuncSetAttribute(K::shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
-        if (e == cudaSuccess && K::has_fused)
+        if (e == cudaSuccess && K::has_fused) {
             e = cudaFuncSetAttribute(K::fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(K::shrink_flag, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand_flag, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+        }
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -1084,6 +1100,17 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
     // experiment knobs (occupancy sweeps): pad the dynamic smem of the shrink / expand CTAs
     static const int pad_s = getenv("LORA_EXP_SSMEM") ? atoi(getenv("LORA_EXP_SSMEM")) : 0;
     static const int pad_e = getenv("LORA_EXP_ESMEM") ? atoi(getenv("LORA_EXP_ESMEM")) : 0;
+    if ((phases & 8) && K::has_fused && a.gc_sync && W > 1 && (phases & 3) == 3) {
+        // flag-chained pair: shrink units publish per-gc counters, the expand grid acquires them
+        // instead of waiting for the whole shrink grid (DecodeArgs::flag_chain)
+        DecodeArgs af = a;
+        af.flag_chain = 1;
+        e = launch_pdl(K::shrink_flag, pl.n_shrink, kConsumerThreads, K::shrink_smem, st, af, blob);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(K::expand_flag, pl.n_expand, kConsumerThreads, K::expand_launch_smem(af), st, af, blob);
+        *launches += 2;
+        return e;
+    }
     if ((phases & 4) && K::has_fused && a.gc_sync) {   // one grid: shrink units, then expand units
         const int es = K::expand_launch_smem(a);
         e = launch_pdl(K::fused, pl.n_shrink + pl.n_expand, kConsumerThreads, K::shrink_smem > es ? K::shrink_smem : es, st,

@@ -53,7 +53,7 @@ struct lora_pool {
     size_t meta_cap = 0;                 // words
     int32_t* gc_sync = nullptr;          // fused decode: [0] timeout flag, then 2 counters per gc (zeroed)
     size_t gc_sync_cap = 0;
-    bool fused_decode = false;           // LORA_OPT_DECODE_FUSED
+    int fused_decode = 0;                // LORA_OPT_DECODE_FUSED: 0 pair, 1 one grid, 2 flag-chained pair
     int decode_path = 0;                 // LORA_OPT_DECODE_PATH: 0 kernel pair, 1 cluster-span kernel (bf16)
     bool pad_max_rank = false;           // LORA_OPT_PAD_MAX_RANK: BGMV-style padded decode work (comparison)
     Plan plan;
@@ -430,7 +430,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
                        p->esz, p->num_sms};
         L.phases = mode == 0 ? 3 : mode;
         if (fused) {
-            L.phases |= 4;
+            L.phases |= p->fused_decode == 2 ? 8 : 4;
             L.gc_sync = p->gc_sync + 1;
         }
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
@@ -540,7 +540,7 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         L.n_jobs = n_pools;
         if (p0->fused_decode && p0->esz == 2) {
             if ((s = grow(p0->gc_sync, p0->gc_sync_cap, (size_t)(1 + 2 * fz.n_gc), true, "gc_sync")) != LORA_OK) return s;
-            L.phases |= 4;
+            L.phases |= p0->fused_decode == 2 ? 8 : 4;
             L.gc_sync = p0->gc_sync + 1;
         }
         for (int i = 1; i < n_pools; ++i)
@@ -599,8 +599,8 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             p->decode_path = (int)value;
             return LORA_OK;
         case LORA_OPT_DECODE_FUSED:
-            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_FUSED takes 0 or 1");
-            p->fused_decode = value == 1;
+            if (value < 0 || value > 2) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_FUSED takes 0, 1 or 2");
+            p->fused_decode = (int)value;
             return LORA_OK;
         default:
             return fail(LORA_ERR_ARG, "unknown option " + std::to_string(option));

@@ -83,6 +83,14 @@ with torch.cuda.stream(st):
 torch.cuda.synchronize()
 fused = run(lambda: [p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st) for p, y in zip(pools, ys)])
 for p in pools:
+    p.set_option(L.binding.LORA_OPT_DECODE_FUSED, 2)
+with torch.cuda.stream(st):
+    for p, y in zip(pools, ys):
+        p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+torch.cuda.synchronize()
+flagc = run(lambda: [p.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st) for p, y in zip(pools, ys)])
+print("c2 x %d pools: us/apply  flag-chained pair %.2f" % (NP, flagc))
+for p in pools:
     p.set_option(L.binding.LORA_OPT_DECODE_FUSED, 0)
 # q/k/v style: 3 pools per lora_apply_multi launch pair
 trip = [(pools[i:i + 3], ys[i:i + 3]) for i in range(0, NP - 2, 3)]

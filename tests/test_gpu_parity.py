@@ -356,7 +356,7 @@ def test_apply_multi_qkv_fused_equals_separate(L):
         p.close()
 
 
-def test_fused_decode_grid_equals_kernel_pair(L):
+def test_fused_decode_grid_and_flag_chain_equal_kernel_pair(L):
     """LORA_OPT_DECODE_FUSED: one grid per apply (expand units wait on per-gc counters) is bit
     for bit the PDL kernel pair, over many back-to-back applies on one pool with changing batches
     (the counters must re-arm after every apply), eagerly and inside a CUDA graph."""
@@ -369,15 +369,28 @@ def test_fused_decode_grid_equals_kernel_pair(L):
         pool = make_pool(b, L, L_tc=1 << 30)
         x = to_torch(b.x, "cuda")
         outs = {}
-        for fused in (0, 1):
+        for fused in (0, 1, 2):
             pool.set_option(B.LORA_OPT_DECODE_FUSED, fused)
             y = to_torch(b.y_in, "cuda")
             for _ in range(7):   # y accumulates 7 deltas
                 pool.apply(x, y, b.seg_indptr, b.adapter_ids)
             torch.cuda.synchronize()
             outs[fused] = y.clone()
-        assert torch.equal(outs[0], outs[1])
-        # graph replays of the fused apply
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+        # graph replays of the fused apply and of the flag-chained pair
+        for mode in (1, 2):
+            pool.set_option(B.LORA_OPT_DECODE_FUSED, mode)
+            y = to_torch(b.y_in, "cuda")
+            st = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+            y.copy_(to_torch(b.y_in, "cuda"))
+            with torch.cuda.stream(st):
+                for _ in range(7):
+                    g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(y, outs[1])
         pool.set_option(B.LORA_OPT_DECODE_FUSED, 1)
         y = to_torch(b.y_in, "cuda")
         st = torch.cuda.Stream()
