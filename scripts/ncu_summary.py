@@ -43,6 +43,8 @@ def main():
     if raw:
         hr = raw[0]
         rix = {n: i for i, n in enumerate(hr)}
+        units = raw[1] if len(raw) > 1 else [""] * len(hr)
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         for r in raw[2:]:
             if len(r) != len(hr):
                 continue
@@ -51,7 +53,8 @@ def main():
                 continue
             for m in RAW:
                 if m in rix:
-                    k[m] = _f(r[rix[m]])
+                    # byte counters are stored in bytes (ncu picks a unit per value)
+                    k[m] = _f(r[rix[m]]) * scale.get(units[rix[m]], 1.0) if "bytes" in m else _f(r[rix[m]])
     for kid, k in kern.items():
         print("[%s] %s" % (kid, k["name"][:110]))
         for m in WANT + RAW:

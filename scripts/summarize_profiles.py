@@ -49,7 +49,7 @@ def launches():
         a[3] += d.get("dram__bytes_write.sum", 0)
     tot = sum(a[1] for a in agg.values())
     lines = ["ncu launch list (--clock-control none, serialised, cold caches: compare SHARES, not absolutes)",
-             "command: bench.py --layers 4 --steps 10 --prefill-layers 1 (see scripts/profile_round.sh)", "",
+             "command: bench.py --layers 4 --steps 10 --prefill-layers 1 --c4-steps 0 --c5-reps 0 (scripts/profile_round.sh)", "",
              "%-34s %6s %10s %8s %14s %14s" % ("kernel", "count", "mean_us", "share", "dram_rd/launch", "dram_wr/launch")]
     for name, (n, t, rd, wr) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append("%-34s %6d %10.2f %7.1f%% %14.0f %14.0f" % (name, n, t / n, 100 * t / tot, rd / n, wr / n))
@@ -72,15 +72,15 @@ if __name__ == "__main__":
     agg = launches()
     dec = full("decode")
     pf = full("prefill")
-    # traffic per decode apply (shrink + expand launch pair) and per prefill launch, for bench.py
-    shr = [v for v in dec.values() if "shrink" in v["name"]]
-    exp = [v for v in dec.values() if "expand" in v["name"]]
-    mb = 1e6   # ncu raw page reports dram bytes in Mbyte
-    rd = lambda v: (v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)) * mb  # noqa
+    # decode capture = one c2 layer step (scripts/ncu_decode_step.py): the q/k/v lora_apply_multi pair and
+    # the o pair, i.e. 4 projection applies -> DRAM bytes per projection apply for bench.py's roofline
+    rd = lambda v: v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)  # noqa  (bytes)
+    dec_k = [v for v in dec.values() if "shrink" in v["name"] or "expand" in v["name"]]
     summ = {"tag": TAG,
-            "dram_bytes_per_launch": round(sum(map(rd, shr)) / len(shr) + sum(map(rd, exp)) / len(exp)) if shr and exp else None,
-            "note": "decode apply = shrink + expand launch pair; ncu --set full, one capture each; writes to y "
-                    "can remain in L2 at kernel end",
+            "dram_bytes_per_launch": round(sum(map(rd, dec_k)) / 4) if len(dec_k) == 4 else None,
+            "decode_kernels_captured": [v["name"] for v in dec_k],
+            "note": "DRAM bytes per projection apply = (q/k/v lora_apply_multi pair + o pair) / 4, ncu --set full, "
+                    "cold caches; writes to y can remain in L2 at kernel end",
             "prefill_dram_bytes_per_launch": round(sum(map(rd, pf.values())) / len(pf)) if pf else None}
     json.dump(summ, open(os.path.join(OUT, "ncu_decode_summary.json"), "w"), indent=1)
     print(summ)
