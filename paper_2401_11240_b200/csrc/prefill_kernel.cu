@@ -37,6 +37,7 @@ constexpr int kPfShrinkStages = 7;     // shrink-phase ring: the 3 ring stages +
 constexpr int kPfStageBytes = 32768;   // X chunk 16 KB + A chunk <= 16 KB, or one B tile (<= 32 KB)
 constexpr int kPfVBytes = 128 * 128 * 2;   // one V part (hi or lo): 128 tokens x r16 <= 128, bf16
 constexpr int kPfYBytes = 128 * 128 * 2;   // one staged y tile (128 tokens x 128 columns, bf16)
+constexpr int kPfYSlots = 3;               // staged y tiles in flight (the third lives in the unused V-lo space)
 constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 2 * kPfYBytes + 256;
 constexpr int kPfNTile = 128;          // expand columns per tile
 constexpr int kPfTileWords = 8;        // per-tile record in the metadata blob
@@ -149,9 +150,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const uint32_t vhi = base + kPfStages * kPfStageBytes;
     const uint32_t vlo = vhi + kPfVBytes;
     uint8_t* gv = gbase + kPfStages * kPfStageBytes;   // generic pointer to vhi
-    const uint32_t yring = vlo + kPfVBytes;             // 2 x 32 KB staged y tiles
+    // v goes to the expand as bf16 (SURVEY §8(c) reading 4 allows it on the tcgen05 expand; rel-L2
+    // budget in DESIGN.md), so the lo-part buffer serves as a third staged y tile: 3 x 32 KB at vlo
+    const uint32_t yring = vlo;
     uint8_t* gy = gbase + (yring - base);
-    const uint32_t bars = yring + 2 * kPfYBytes;        // 14 mbarriers + tmem slot
+    const uint32_t bars = vlo + kPfVBytes + 2 * kPfYBytes;   // mbarriers + tmem slot
     // barriers: shrink ring full/empty [7] x 2, expand ring full/empty [3] x 2, then the rest
     auto full = [&](int s) { return bars + 8u * s; };
     auto empty = [&](int s) { return bars + 8u * (kPfShrinkStages + s); };
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
     auto y_full = [&](int b) { return v_ready + 40u + 8u * b; };
     uint32_t* tmem_slot =
-        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 8) - base));
+        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 9) - base));
 
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -191,8 +194,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         for (int b = 0; b < 2; ++b) {
             pf_bar_init(tm_full(b), 1);
             pf_bar_init(tm_empty(b), 128);
-            pf_bar_init(y_full(b), 1);
         }
+        for (int b = 0; b < kPfYSlots; ++b) pf_bar_init(y_full(b), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {   // TMEM: D1 at columns [0,128), D2 buffers at [128,256) and [256,384)
@@ -313,7 +316,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                     const uint32_t voff = (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u;
                     const uint64_t bd = umma_desc(sb + (uint32_t)ks * 2048u, lbo, 1024);
                     umma_f16(dcol, umma_desc(vhi + voff, 16, 1024), bd, id2, ks != 0);
-                    umma_f16(dcol, umma_desc(vlo + voff, 16, 1024), bd, id2, 1);
                 }
                 umma_commit(empty2(stage));
                 umma_commit(tm_full(b));
@@ -354,7 +356,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 const uint32_t off = (uint32_t)kk * 16384u + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
                                      (uint32_t)((chunk ^ (row & 7)) * 16);
                 *reinterpret_cast<uint4*>(gv + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                *reinterpret_cast<uint4*>(gv + kPfVBytes + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
@@ -368,22 +369,22 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         const bool valid = row < nvalid;
         const bool leader = (tid == 64);
         auto issue_y = [&](int nt) {
-            const int b = nt & 1;
+            const int b = nt % kPfYSlots;
             const uint32_t dst = yring + (uint32_t)b * kPfYBytes;
             pf_arrive_tx(y_full(b), (uint32_t)kPfYBytes);
             tma_2d(dst, &a.tm_y, nt * kPfNTile, tok0, y_full(b));
             tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(b));
         };
         if (leader) {
-            issue_y(0);
-            if (nnt > 1) issue_y(1);
+            for (int q = 0; q < kPfYSlots && q < nnt; ++q) issue_y(q);
         }
         for (int nt = 0; nt < nnt; ++nt) {
             const int b = nt & 1;
             pf_wait(tm_full(b), (nt >> 1) & 1);
-            pf_wait(y_full(b), (nt >> 1) & 1);
+            const int yb = nt % kPfYSlots;
+            pf_wait(y_full(yb), (nt / kPfYSlots) & 1);
             tc_fence_after();
-            uint8_t* ys = gy + b * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
+            uint8_t* ys = gy + yb * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll 1
             for (int c0 = 0; c0 < kPfNTile; c0 += 32) {
                 float d[32];
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             // STG.128 instruction (a thread-per-row store touches 32 rows per instruction)
             __syncwarp();
             {
-                const uint8_t* yslot = gy + b * kPfYBytes;
+                const uint8_t* yslot = gy + yb * kPfYBytes;
 #pragma unroll 4
                 for (int i = 0; i < 16; ++i) {
                     const int rr = sub * 32 + i * 2 + (lane >> 4), c16 = lane & 15;
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             }
             // every epilogue thread is done with y slot b -> refill it with tile nt + 2
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (leader && nt + 2 < nnt) issue_y(nt + 2);
+            if (leader && nt + kPfYSlots < nnt) issue_y(nt + kPfYSlots);
         }
     }
     tc_fence_before();
