@@ -19,6 +19,8 @@ LIB = os.path.join(LIB_DIR, "liblora.so")
 OBJ_DIR = os.path.join(HERE, "lib", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# extra -D flags for experiment builds (both compilers; part of the build digest)
+DEFS = os.environ.get("LORA_BUILD_DEFS", "").split()
 NVCC_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                         "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 CXX_FLAGS = ["-O2", "-fPIC", "-std=c++17", "-Wall", "-I/usr/local/cuda/include", "-I" + os.path.join(ROOT, "include")]
@@ -37,6 +39,7 @@ def _digest():
     files = _sources() + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h")]
     files.append(os.path.join(ROOT, "include", "lora_delta.h"))
     files.append(os.path.abspath(__file__))
+    h.update(" ".join(DEFS).encode())
     for f in files:
         h.update(f.encode())
         with open(f, "rb") as fh:
@@ -54,9 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in _sources():
         obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
-            cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+            cmd = [NVCC] + NVCC_FLAGS + DEFS + ["-c", src, "-o", obj]
         else:
-            cmd = ["g++"] + CXX_FLAGS + ["-c", src, "-o", obj]
+            cmd = ["g++"] + CXX_FLAGS + DEFS + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

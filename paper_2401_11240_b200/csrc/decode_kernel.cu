@@ -624,7 +624,7 @@ constexpr int kShrinkMmaSmem = 1024 + kShrinkRowsMma * kAPitch + kConsumerWarps 
 // at 4 shrink CTAs per SM, so a shrink grid spreads over more SMs (more HBM request streams)
 // and leaves room for the expand CTAs it overlaps with (c2 sweep, scripts/occ_sweep.sh:
 // 39 KB -> 88.3K tok/s, 50-57 KB -> 91.8K, >= 66 KB -> 70K).
-constexpr int kShrinkMmaLaunchSmem = 52 * 1024;
+constexpr int kShrinkMmaLaunchSmem = kShrinkMmaSmem > 52 * 1024 ? kShrinkMmaSmem : 52 * 1024;
 
 // FUSED: the unit runs inside lora_decode_fused_kernel and publishes its v partials to the
 // gc's expand units with a release-increment of the gc's counter (see that kernel).
@@ -718,7 +718,15 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         float* pw = part + warp * kShrinkRowsMma * kTokChunkMma;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const float v = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
+            // fixed-order pairwise sum of the warp's k-blocks (kKBlocks = 4 for a 1024-wide k-slice)
+            float kb[kKBlocks];
+#pragma unroll
+            for (int b = 0; b < kKBlocks; ++b) kb[b] = acc[b][q];
+#pragma unroll
+            for (int w = 1; w < kKBlocks; w *= 2)
+#pragma unroll
+                for (int b = 0; b + w < kKBlocks; b += 2 * w) kb[b] += kb[b + w];
+            const float v = kb[0];
             const int row = g + ((q & 2) ? 8 : 0), t = 2 * c + (q & 1);
             pw[row * kTokChunkMma + t] = v;
         }

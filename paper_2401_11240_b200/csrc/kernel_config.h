@@ -19,8 +19,11 @@ constexpr int kTokChunkMma = 8;                   // bf16 tensor-core kernels: t
 constexpr int kMaxTokChunk = 8;
 constexpr int kShrinkRows = 8;                    // fp32: A rows per shrink unit
 constexpr int kShrinkRowsMma = 16;                // bf16: A rows per shrink unit (MMA M = 16)
-constexpr int kKSlice = 1024;                     // k elements per shrink unit (both element types)
-constexpr int kSliceBytes = 4096;                 // fp32 smem row slice (kKSlice * 4)
+#ifndef LORA_KSLICE
+#define LORA_KSLICE 1024                          // experiment builds: LORA_BUILD_DEFS=-DLORA_KSLICE=2048
+#endif
+constexpr int kKSlice = LORA_KSLICE;              // k elements per shrink unit (both element types)
+constexpr int kSliceBytes = kKSlice * 4;          // fp32 smem row slice
 constexpr int kExpandBytes = 32768;               // B bytes per expand unit (r * ncols * esz)
 constexpr int kMaxNcols = 1024;                   // columns per expand unit
 
