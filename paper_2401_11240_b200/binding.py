@@ -81,16 +81,16 @@ def _load() -> ctypes.CDLL:
         "lora_load_adapter": [vp, c_i32, c_int, vp, vp, ctypes.c_float],
         "lora_unload_adapter": [vp, c_i32],
         "lora_adapter_ready": [vp, c_i32, P(c_int)],
-        "lora_apply": [vp, vp, vp, _P32, _P32, c_int, vp],
-        "lora_plan": [vp, _P32, _P32, c_int],
+        "lora_apply": [vp, vp, vp, vp, vp, c_int, vp],          # seg_indptr / adapter_ids as addresses
+        "lora_plan": [vp, vp, vp, c_int],
         "lora_set_option": [vp, c_int, c_i64],
         "lora_pool_info": [vp, P(PoolInfo)],
         "lora_debug_metadata": [vp, P(MetadataView)],
         "lora_debug_adapter_pages": [vp, c_i32, _P32, c_int, P(c_int)],
         "lora_debug_read_pages": [vp, c_i32, vp, vp],
         "lora_debug_set_trace": [vp, vp],
-        "lora_apply_shrink": [vp, vp, _P32, _P32, c_int, vp, c_i64, vp],
-        "lora_apply_multi": [P(vp), P(vp), P(vp), c_int, _P32, _P32, c_int, vp],
+        "lora_apply_shrink": [vp, vp, vp, vp, c_int, vp, c_i64, vp],
+        "lora_apply_multi": [P(vp), P(vp), P(vp), c_int, vp, vp, c_int, vp],
         "lora_apply_expand": [vp, vp, vp, vp],
     }
     for name, args in sig.items():
@@ -113,17 +113,42 @@ def _check(rc: int) -> None:
 
 
 def _i32(a) -> np.ndarray:
+    if type(a) is np.ndarray and a.dtype == np.int32 and a.flags.c_contiguous:
+        return a   # the per-apply fast path: no copy, no conversion
     return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+_ADDR_CACHE: list = []   # (array, address) of the last few int32 arrays (kept alive by the cache)
+
+
+def _addr(a: np.ndarray) -> int:
+    """a.ctypes.data without building a ctypes helper per call (the same seg_indptr / adapter_ids
+    arrays are passed to every pool of a decode step)."""
+    for arr, ad in _ADDR_CACHE:
+        if arr is a:
+            return ad
+    ad = a.__array_interface__["data"][0]
+    _ADDR_CACHE.insert(0, (a, ad))
+    del _ADDR_CACHE[8:]
+    return ad
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream)
+    return stream if isinstance(stream, int) else int(stream.cuda_stream)
 
 
 def _ptr_of(t) -> int:
     """device/host address of a torch tensor, numpy array or int."""
     if t is None:
         return 0
+    dp = getattr(t, "data_ptr", None)
+    if dp is not None:
+        return int(dp())
     if isinstance(t, int):
         return t
-    if hasattr(t, "data_ptr"):
-        return int(t.data_ptr())
     if isinstance(t, np.ndarray):
         return int(t.ctypes.data)
     raise TypeError(type(t))
@@ -133,15 +158,12 @@ def apply_multi(pools, xs, ys, seg_indptr, adapter_ids, stream=None) -> None:
     """lora_apply_multi: pools[i] applies to (xs[i], ys[i]) in one fused launch pair."""
     n = len(pools)
     ip, ids = _i32(seg_indptr), _i32(adapter_ids)
-    if stream is None:
-        import torch
-        stream = torch.cuda.current_stream()
-    sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
+    sp = _stream_ptr(stream)
     VP = ctypes.c_void_p * n
     hp = VP(*[p.handle.value for p in pools])
     xp = VP(*[_ptr_of(x) for x in xs])
     yp = VP(*[_ptr_of(y) for y in ys])
-    _check(LIB.lora_apply_multi(hp, xp, yp, n, ip.ctypes.data_as(_P32), ids.ctypes.data_as(_P32), int(ids.shape[0]), sp))
+    _check(LIB.lora_apply_multi(hp, xp, yp, n, _addr(ip), _addr(ids), int(ids.shape[0]), sp))
 
 
 class LoraPool:
@@ -190,35 +212,23 @@ class LoraPool:
         """x, y: device tensors (or raw pointers); seg_indptr / adapter_ids: host int32 arrays;
         stream: a torch.cuda.Stream, a raw cudaStream_t int, or None (current torch stream)."""
         ip, ids = _i32(seg_indptr), _i32(adapter_ids)
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream()
-        sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
-        _check(LIB.lora_apply(self.handle, _ptr_of(x), _ptr_of(y), ip.ctypes.data_as(_P32),
-                              ids.ctypes.data_as(_P32), int(ids.shape[0]), sp))
+        _check(LIB.lora_apply(self.handle, _ptr_of(x), _ptr_of(y), _addr(ip), _addr(ids),
+                              int(ids.shape[0]), _stream_ptr(stream)))
 
     def apply_shrink(self, x, seg_indptr, adapter_ids, v_out, stream=None) -> None:
         """Tensor-parallel first half: partial v (fp32, caller-owned device buffer v_out) over
         this pool's H_in shard.  The caller sums v_out across TP ranks, then calls apply_expand."""
         ip, ids = _i32(seg_indptr), _i32(adapter_ids)
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream()
-        sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
         cap = int(v_out.numel()) if hasattr(v_out, "numel") else 0
-        _check(LIB.lora_apply_shrink(self.handle, _ptr_of(x), ip.ctypes.data_as(_P32), ids.ctypes.data_as(_P32),
-                                     int(ids.shape[0]), _ptr_of(v_out), cap, sp))
+        _check(LIB.lora_apply_shrink(self.handle, _ptr_of(x), _addr(ip), _addr(ids),
+                                     int(ids.shape[0]), _ptr_of(v_out), cap, _stream_ptr(stream)))
 
     def apply_expand(self, y, v_in, stream=None) -> None:
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream()
-        sp = stream if isinstance(stream, int) else int(stream.cuda_stream)
-        _check(LIB.lora_apply_expand(self.handle, _ptr_of(y), _ptr_of(v_in), sp))
+        _check(LIB.lora_apply_expand(self.handle, _ptr_of(y), _ptr_of(v_in), _stream_ptr(stream)))
 
     def plan(self, seg_indptr, adapter_ids) -> None:
         ip, ids = _i32(seg_indptr), _i32(adapter_ids)
-        _check(LIB.lora_plan(self.handle, ip.ctypes.data_as(_P32), ids.ctypes.data_as(_P32), int(ids.shape[0])))
+        _check(LIB.lora_plan(self.handle, _addr(ip), _addr(ids), int(ids.shape[0])))
 
     def set_option(self, option: int, value: int) -> None:
         _check(LIB.lora_set_option(self.handle, int(option), int(value)))

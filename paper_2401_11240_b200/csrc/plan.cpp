@@ -25,15 +25,26 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     if (S < 0) { err = "num_segments < 0"; return LORA_ERR_ARG; }
     if (S > 0 && (ip == nullptr || ids == nullptr)) { err = "seg_indptr/adapter_ids is NULL"; return LORA_ERR_ARG; }
     if (S > 0 && ip[0] != 0) { err = "seg_indptr[0] != 0"; return LORA_ERR_ARG; }
+    // one hash lookup per segment (runs of one id reuse it); the records are used below
+    static thread_local std::vector<const AdapterRec*> seg_rec;
+    seg_rec.assign(S, nullptr);
     for (int i = 0; i < S; ++i) {
         if (ip[i + 1] < ip[i]) { err = "seg_indptr not non-decreasing at segment " + std::to_string(i); return LORA_ERR_ARG; }
-        if (ids[i] >= 0 && table.find(ids[i]) == table.end()) {
-            err = "adapter_ids[" + std::to_string(i) + "] = " + std::to_string(ids[i]) + " is not loaded";
-            return LORA_ERR_UNKNOWN_ADAPTER;
+        if (ids[i] >= 0) {
+            if (i > 0 && ids[i] == ids[i - 1]) {
+                seg_rec[i] = seg_rec[i - 1];
+                continue;
+            }
+            auto it = table.find(ids[i]);
+            if (it == table.end()) {
+                err = "adapter_ids[" + std::to_string(i) + "] = " + std::to_string(ids[i]) + " is not loaded";
+                return LORA_ERR_UNKNOWN_ADAPTER;
+            }
+            seg_rec[i] = &it->second;
         }
     }
     const int T = S > 0 ? ip[S] : 0;
-    pl = Plan();
+    pl.reset();
     pl.T = T; pl.S = S; pl.L_tc = L_tc;
 
     // M1 token -> segment
@@ -42,7 +53,8 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         for (int t = ip[i]; t < ip[i + 1]; ++t) pl.tok_seg[t] = i;
 
     // M2 groups (ids >= 0 owning >= 1 token), ascending
-    std::vector<int32_t> gids;
+    static thread_local std::vector<int32_t> gids;
+    gids.clear();
     for (int i = 0; i < S; ++i)
         if (ids[i] >= 0 && ip[i + 1] > ip[i]) gids.push_back(ids[i]);
     std::sort(gids.begin(), gids.end());
@@ -53,13 +65,17 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
 
     // M5 seg kinds and M6 features
     pl.seg_kind.resize(S);
-    std::vector<int32_t> seg_group(S, -1);
+    static thread_local std::vector<int32_t> seg_group;
+    seg_group.assign(S, -1);
+    static thread_local std::vector<const AdapterRec*> group_rec;
+    group_rec.assign(G, nullptr);
     for (int i = 0; i < S; ++i) {
         const int len = ip[i + 1] - ip[i];
         if (ids[i] < 0 || len == 0) { pl.seg_kind[i] = LORA_KIND_NONE; continue; }
         pl.seg_kind[i] = len >= L_tc ? LORA_KIND_PREFILL : LORA_KIND_DECODE;
         seg_group[i] = gidx(ids[i]);
-        const int64_t r = table.at(ids[i]).rank;
+        group_rec[seg_group[i]] = seg_rec[i];
+        const int64_t r = seg_rec[i]->rank;
         pl.n_seg += 1;
         pl.max_rank = std::max(pl.max_rank, r);
         pl.sum_rank_seg += r;
@@ -72,7 +88,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     pl.group_rank.resize(G); pl.group_scale.resize(G); pl.group_ntok.assign(G, 0);
     pl.group_page_off.resize(G); pl.group_tok_off.resize(G);
     for (int g = 0; g < G; ++g) {
-        const AdapterRec& a = table.at(gids[g]);
+        const AdapterRec& a = *group_rec[g];
         pl.group_rank[g] = a.rank;
         pl.group_scale[g] = a.scale;
         pl.group_page_off[g] = (int32_t)pl.pages.size();
@@ -95,11 +111,12 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     }
 
     // ---- kernel work ----
-    // tokens of the SIMT path per group (ascending), and tensor-core segments
-    std::vector<std::vector<int32_t>> simt(G);
+    // tokens of the SIMT path per group (ascending; flat, counting-sorted by group), and
+    // tensor-core segments
     // tensor-core routing: PREFILL segments of rank <= kPfMaxRank while the tile records and
     // page lists fit the kernel-parameter blob; everything else takes the decode kernels
-    std::vector<uint8_t> on_tc(S, 0);
+    static thread_local std::vector<uint8_t> on_tc;
+    on_tc.assign(S, 0);
     if (tc_enabled) {
         std::vector<int32_t> group_pf_off(G, -1);
         std::vector<int32_t> pages_words;
@@ -144,21 +161,37 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         }
         std::copy(pages_words.begin(), pages_words.end(), pl.pf_blob.begin() + (size_t)tiles * 8);
     }
+    static thread_local std::vector<int32_t> simt_off, simt_tok;
+    simt_off.assign(G + 1, 0);
     for (int t = 0; t < T; ++t) {
         const int i = pl.tok_seg[t];
         const int g = seg_group[i];
-        if (g < 0 || on_tc[i]) continue;
-        simt[g].push_back(t);
+        if (g >= 0 && !on_tc[i]) simt_off[g + 1] += 1;
+    }
+    for (int g = 0; g < G; ++g) simt_off[g + 1] += simt_off[g];
+    simt_tok.resize(simt_off[G]);
+    {
+        static thread_local std::vector<int32_t> fill;
+        fill.assign(simt_off.begin(), simt_off.end() - 1);
+        for (int t = 0; t < T; ++t) {
+            const int i = pl.tok_seg[t];
+            const int g = seg_group[i];
+            if (g >= 0 && !on_tc[i]) simt_tok[fill[g]++] = t;
+        }
     }
     const int ksplit = ksplit_of(H_in, esz);
     // gc = (group, token chunk)
     struct Gc { int g, tok_off, ntok; };
-    std::vector<Gc> gcs;
-    std::vector<int32_t> blob_pages, blob_toks, group_blob_page(G, -1);
+    static thread_local std::vector<Gc> gcs;
+    static thread_local std::vector<int32_t> blob_pages, blob_toks, group_blob_page, gp;
+    gcs.clear();
+    blob_pages.clear();
+    blob_toks.clear();
+    group_blob_page.assign(G, -1);
     for (int g = 0; g < G; ++g) {
-        if (simt[g].empty()) continue;
-        std::vector<int32_t> gp(pl.pages.begin() + pl.group_page_off[g],
-                                pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
+        const int n_simt = simt_off[g + 1] - simt_off[g];
+        if (n_simt == 0) continue;
+        gp.assign(pl.pages.begin() + pl.group_page_off[g], pl.pages.begin() + pl.group_page_off[g] + pl.group_rank[g]);
         // padded-BGMV comparison mode (NEXT f4): every group's rank rows are padded to
         // the batch's max rank with the pool's all-zero page -- the work Punica's BGMV does
         if (pad_zero_page >= 0) gp.insert(gp.end(), (size_t)(pl.max_rank - pl.group_rank[g]), pad_zero_page);
@@ -170,11 +203,12 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
             group_blob_page[g] = (int32_t)blob_pages.size();
             blob_pages.insert(blob_pages.end(), gp.begin(), gp.end());
         }
-        const size_t tc = (size_t)tok_chunk(esz);
-        for (size_t c = 0; c < simt[g].size(); c += tc) {
-            const int n = (int)std::min<size_t>(tc, simt[g].size() - c);
+        const int tc = tok_chunk(esz);
+        const int32_t* st = simt_tok.data() + simt_off[g];
+        for (int c = 0; c < n_simt; c += tc) {
+            const int n = std::min(tc, n_simt - c);
             gcs.push_back({g, (int)blob_toks.size(), n});
-            blob_toks.insert(blob_toks.end(), simt[g].begin() + c, simt[g].begin() + c + n);
+            blob_toks.insert(blob_toks.end(), st + c, st + c + n);
         }
     }
     const int n_gc = (int)gcs.size();

@@ -56,6 +56,24 @@ struct Plan {
     int32_t n_span_cta = 0;          // multiple of the cluster size (idle CTAs pad the last cluster)
     int32_t span_cluster = 0;        // cluster size the records were packed for (0 = not built)
     int32_t span_max_rank = 0, span_max_sk = 0, span_max_sn = 0;
+
+    // back to the default state but keeping every vector's capacity (one plan per apply: the
+    // host planner is on the per-call path, so it should not reallocate)
+    void reset() {
+        std::vector<int32_t>* iv[] = {&tok_seg, &group_id, &group_rank, &group_ntok, &group_page_off, &group_tok_off,
+                                      &group_tokens, &pages, &seg_kind, &blob, &pf_blob, &span_blob};
+        for (auto* v : iv) v->clear();
+        group_scale.clear();
+        prefill.clear();
+        Plan d;   // scalar defaults (its vectors are empty: no allocation)
+        T = d.T; S = d.S; G = d.G; L_tc = d.L_tc;
+        n_seg = max_rank = nseg_x_maxrank = sum_rank_seg = sum_rank_groups = sum_rank_tokens = 0;
+        n_gc = n_shrink = n_expand = 0;
+        unit_tab = 0; unit_words = d.unit_words; blob_esz = d.blob_esz; vbuf_floats = 0; n_jobs = 1;
+        for (int i = 0; i < 4; ++i) job_shrink_base[i] = job_expand_base[i] = 0;
+        n_prefill_tiles = n_pf_tiles = 0;
+        n_span_cta = span_cluster = span_max_rank = span_max_sk = span_max_sn = 0;
+    }
 };
 
 // Span-path parameters (per pool; fixed for a device so the result of a token is a fixed
