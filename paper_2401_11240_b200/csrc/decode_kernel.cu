@@ -772,6 +772,9 @@ constexpr int kExpandMmaSmemMax = 320 + 2 * kTokChunkMma * ((LORA_MAX_RANK + 8) 
                                   LORA_MAX_RANK * kPitchPad + kTokChunkMma * (kMaxNcols * 2 + kPitchPad) +
                                   kTokChunkMma * (kMaxNcols + 4) * 4 + LORA_MAX_RANK * 4;
 constexpr int kBulkMinBytes = 2048;   // B row slices at least this long go through cp.async.bulk
+#ifndef LORA_EXPAND_MINB
+#define LORA_EXPAND_MINB 3                // expand CTAs per SM the register budget allows (experiments)
+#endif
 
 // FUSED: v comes from shrink units of the same grid; thread 0 acquires the gc's counter
 // (all n_s shrink units released) instead of a grid dependency, and the gc's last expand unit
@@ -1001,7 +1004,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
 }
 
 template <int W, bool FLAG>
-__global__ void __launch_bounds__(kConsumerThreads, 3)   /* <= 85 registers: 3 CTAs per SM */
+__global__ void __launch_bounds__(kConsumerThreads, LORA_EXPAND_MINB)   /* <= 85 registers: 3 CTAs per SM */
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;

@@ -28,6 +28,8 @@ pools, batches = [], []
 for i in range(NP):
     b = mk(i)
     pool = L.LoraPool(b.H_in, b.H_out, 64, b.dtype, max_total_rank=sum(a.rank for a in b.adapters))
+    if os.environ.get("LORA_TRACE_FUSED"):   # hand-off variant (LORA_OPT_DECODE_FUSED 1 or 2)
+        pool.set_option(L.binding.LORA_OPT_DECODE_FUSED, int(os.environ["LORA_TRACE_FUSED"]))
     for a in b.adapters:
         pool.load_adapter(a.id, a.rank, tt(a.A, True), tt(a.B, True), a.scale)
     pools.append(pool)
