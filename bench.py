@@ -366,6 +366,7 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
     gen_s = _t.perf_counter() - t0
     budget = sum(gen.c4_rank(a) for a in range(n_ad)) // 5
     pool = L.LoraPool(H, H, n_ad, "bf16", max_total_rank=budget)
+    pool.set_option(L.binding.LORA_OPT_LOAD_KERNEL, 1)   # the cold-start path by the zero-copy gather kernel
     cache = AdapterCache(pool, repo, budget, n_ad)
     st = torch.cuda.Stream(device=dev)
     T = 64 + 512
@@ -452,6 +453,7 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
     out = {"workload": "c4: Llama-2-13B 5120->5120 bf16, 1000 adapters ranks 8..128 in pinned host memory, pool = 20%% "
                        "of their ranks, Zipf(1.0), 64 decode + 1x512 prefill tokens/step, LRU, rank %d/%d" % (rank, world),
            "value": round(T / (ms * 1e-3), 1), "unit": "tokens/s per GPU (loads included)", "ms_per_step": round(ms, 4),
+           "load_path": "zero-copy gather kernel (LORA_OPT_LOAD_KERNEL=1)",
            "ms_per_step_all_resident": round(ms_noload, 4),
            "overlap": round(ms_noload / ms, 3),   # 1.0 = the cold-start loads cost nothing
            "steps": steps, "hit_rate": round(hits / max(1, hits + misses), 4), "loads_per_step": round(misses / steps, 2),

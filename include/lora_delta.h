@@ -93,6 +93,16 @@ typedef enum {
                                       with MBGMV (§3.1).  Same result (zero rows
                                       add 0); more bytes and time.  Not for production. */
 
+#define LORA_OPT_LOAD_KERNEL 6     /* 1: lora_load_adapter copies the rank rows with a zero-copy gather
+                                      kernel on the side stream (SMs read the UVA-mapped pinned host
+                                      rows over PCIe): c4 cold-start loads 26 -> ~41 GB/s effective,
+                                      one 1 MB adapter in 18 us (56 GB/s).  0 (default): cudaMemcpyAsync
+                                      per run of pages (also the fallback when the host rows have no
+                                      device mapping).  Same bytes (tested bitwise), same ready-event
+                                      semantics.  Not the default: in 2 of 4 c2 bench runs of pools
+                                      loaded this way the steady-state decode apply was 7 % slower
+                                      (unexplained). */
+
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.
  *   hidden_in, hidden_out  H_in, H_out of the adapted projection (Eq. 1's H1, H2).

@@ -149,6 +149,9 @@ typedef struct CUstream_st* lora_cuda_stream;
 namespace lora {
 int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
 int launch_span(const Plan& pl, const SpanLaunchDesc& L, lora_cuda_stream st, int* launches);
+// zero-copy cold-start copy of one adapter (load_kernel.cu): sA/sB device-visible pinned host rows
+int launch_load(char* dA, char* dB, const void* sA, const void* sB, int64_t ra, int64_t rb, int rank,
+                const int32_t* pages, int num_sms, lora_cuda_stream st);
 bool span_fits(const Plan& pl);           // the launch's smem layout fits one CTA
 const SpanParams& span_params();          // process-wide (env knobs LORA_SPAN_* for sweeps)
 int span_max_blob_words();

@@ -55,6 +55,7 @@ struct lora_pool {
     size_t gc_sync_cap = 0;
     int fused_decode = 0;                // LORA_OPT_DECODE_FUSED: 0 pair, 1 one grid, 2 flag-chained pair
     int decode_path = 0;                 // LORA_OPT_DECODE_PATH: 0 kernel pair, 1 cluster-span kernel (bf16)
+    bool load_kernel = false;            // LORA_OPT_LOAD_KERNEL: cold-start copies by a zero-copy gather kernel
     bool pad_max_rank = false;           // LORA_OPT_PAD_MAX_RANK: BGMV-style padded decode work (comparison)
     Plan plan;
     Plan fused;                          // merged kernel work of the last lora_apply_multi led by this pool
@@ -90,12 +91,13 @@ lora_status cuda_fail(cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(_e, what); \
     } while (0)
 
-bool is_pinned(const void* p) {
+bool is_pinned(const void* p, const void** dev_ptr = nullptr) {
     cudaPointerAttributes attr;
     if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
+    if (dev_ptr) *dev_ptr = attr.devicePointer;   // UVA-mapped address for zero-copy reads (or null)
     return attr.type == cudaMemoryTypeHost;
 }
 
@@ -221,10 +223,12 @@ lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_
     if (p->free_pages < rank)
         return fail(LORA_ERR_POOL_FULL, "page budget exhausted: need " + std::to_string(rank) + ", free " +
                                             std::to_string(p->free_pages));
+    const void* devA = nullptr;
+    const void* devB = nullptr;
     if (!p->host_only) {
         if (!A_host || !B_host) return fail(LORA_ERR_ARG, "A_host/B_host is NULL");
-        if (!is_pinned(A_host)) return fail(LORA_ERR_NOT_PINNED, "A_host is not pinned host memory");
-        if (!is_pinned(B_host)) return fail(LORA_ERR_NOT_PINNED, "B_host is not pinned host memory");
+        if (!is_pinned(A_host, &devA)) return fail(LORA_ERR_NOT_PINNED, "A_host is not pinned host memory");
+        if (!is_pinned(B_host, &devB)) return fail(LORA_ERR_NOT_PINNED, "B_host is not pinned host memory");
     }
     // lowest free pages, ascending (reading R9)
     AdapterRec rec;
@@ -244,6 +248,12 @@ lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_
             p->fence_pending = false;
         }
         const size_t ra = (size_t)p->H_in * p->esz, rb = (size_t)p->H_out * p->esz;
+        if (p->load_kernel && devA && devB && ((uintptr_t)devA % 16) == 0 && ((uintptr_t)devB % 16) == 0) {
+            // zero-copy gather kernel (LORA_OPT_LOAD_KERNEL)
+            cudaError_t e = (cudaError_t)launch_load(p->dA, p->dB, devA, devB, (int64_t)ra, (int64_t)rb, rank,
+                                                     rec.pages.data(), p->num_sms, p->side);
+            if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: load kernel"); }
+        } else
         // one copy per run of consecutive pages
         for (int j = 0; j < rank;) {
             int k = j + 1;
@@ -590,6 +600,10 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             if (s == LORA_OK) s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
             return s;
         }
+        case LORA_OPT_LOAD_KERNEL:
+            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_LOAD_KERNEL takes 0 or 1");
+            p->load_kernel = value == 1;
+            return LORA_OK;
         case LORA_OPT_PAD_MAX_RANK:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_PAD_MAX_RANK takes 0 or 1");
             p->pad_max_rank = value == 1;

@@ -20,6 +20,8 @@ for a in range(n_ad):
              torch.from_numpy(ad.B.view(np.int16)).pin_memory())
 budget = sum(gen.c4_rank(a) for a in range(n_ad)) // 5
 pool = L.LoraPool(H, H, n_ad, "bf16", max_total_rank=budget)
+if os.environ.get("LORA_LOAD_KERNEL"):
+    pool.set_option(L.binding.LORA_OPT_LOAD_KERNEL, 1)
 cache = AdapterCache(pool, repo, budget, n_ad)
 st = torch.cuda.Stream()
 x = torch.randn(576, H).to(torch.bfloat16).cuda()

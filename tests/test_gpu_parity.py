@@ -427,3 +427,33 @@ def test_pad_max_rank_bgmv_mode(L, name):
     assert rel_l2(outs[1], ref, b.dtype) <= TOL[b.dtype]
     if b.dtype == "bf16":
         assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("kernel", [1, 0], ids=["gather_kernel", "memcpy"])
+def test_load_paths_land_exact_bytes(L, kernel):
+    """LORA_OPT_LOAD_KERNEL 1 (zero-copy gather kernel, default) and 0 (cudaMemcpyAsync) land the
+    adapter bytes in its pages bitwise (read back, pin P12), including fragmented page runs, and the
+    apply matches the oracle."""
+    import torch
+    from paper_2401_11240_b200 import binding as B
+    b = gen.config_c2(y_zero=False)
+    pool = L.LoraPool(b.H_in, b.H_out, 64, "bf16", max_total_rank=sum(a.rank for a in b.adapters) + 64)
+    pool.set_option(B.LORA_OPT_LOAD_KERNEL, kernel)
+    # fragment the free list: load and unload a filler between adapters
+    keep = []
+    for i, a in enumerate(b.adapters):
+        pool.load_adapter(a.id, a.rank, to_torch(a.A, pin=True), to_torch(a.B, pin=True), a.scale)
+        if i == 3:
+            filler = gen.make_adapter(1, 2, 999, 24, b.H_in, b.H_out, "bf16")
+            pool.load_adapter(999, 24, to_torch(filler.A, pin=True), to_torch(filler.B, pin=True), 1.0)
+            keep.append(filler)
+        if i == 6:
+            pool.unload_adapter(999)
+    torch.cuda.synchronize()
+    for a in b.adapters:
+        A, Bm = pool.read_pages(a.id, a.rank)
+        assert np.array_equal(A, a.A) and np.array_equal(Bm, a.B), a.id
+    y, _ = run_gpu(b, L, pool=pool)
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+    pool.close()
