@@ -81,7 +81,10 @@ for trial in range(36):
     rng.shuffle(ids)
     sum_r = int(sum(rank_of[int(a)] for a in ads))
     max_r = int(max(rank_of[int(a)] for a in ads))
-    row = {"G": G, "sum_rank_groups": sum_r, "max_rank": max_r, "nseg_x_maxrank": T * max_r,
+    # the kernel reads every adapter once per 8-token chunk: sum over chunks of r
+    n_tok = {int(a): int((ids == a).sum()) for a in ads}
+    sum_gc = int(sum(rank_of[a] * -(-n_tok[a] // 8) for a in n_tok))
+    row = {"G": G, "sum_rank_groups": sum_r, "sum_rank_gc": sum_gc, "max_rank": max_r, "nseg_x_maxrank": T * max_r,
            "sum_rank_tokens": int(sum(rank_of[int(a)] for a in ids)), "G_x_maxrank": G * max_r,
            "t_mbgmv_us": t_apply(ip, ids, 0), "t_bgmv_us": t_apply(ip, ids, 1)}
     rows.append(row)
@@ -99,6 +102,7 @@ for r in RANKS:
 out = {
     "workload": "64 one-token decode segments, 4096->4096 bf16, adapters ranks {8..128}, %d random compositions" % len(rows),
     "mbgmv_time_vs_sum_rank_groups": fit([r["sum_rank_groups"] for r in rows], [r["t_mbgmv_us"] for r in rows]),
+    "mbgmv_time_vs_sum_rank_gc": fit([r["sum_rank_gc"] for r in rows], [r["t_mbgmv_us"] for r in rows]),
     "mbgmv_time_vs_nseg_x_maxrank": fit([r["nseg_x_maxrank"] for r in rows], [r["t_mbgmv_us"] for r in rows]),
     "bgmv_time_vs_G_x_maxrank": fit([r["G_x_maxrank"] for r in rows], [r["t_bgmv_us"] for r in rows]),
     "bgmv_time_vs_sum_rank_groups": fit([r["sum_rank_groups"] for r in rows], [r["t_bgmv_us"] for r in rows]),
