@@ -14,9 +14,10 @@ one lora_apply for o (its input is the attention output); --qkv-mode serial issu
 
 value   tokens/s = (64 tokens x ranks) / step time, device-timed with CUDA events around K
         replays of a CUDA graph of one step (inputs resident in HBM), max over ranks.
-e2e     the same metric through the public API (LoraPool.apply -> lora_apply) with host
-        buffers: every step copies that step's x (pinned host -> device), runs the 128
-        applies eagerly and reads all y back (device -> pinned host).
+e2e     the same metric through the public API (LoraPool.apply / lora_apply_multi) with host
+        buffers: every step copies that step's x (pinned host -> device), runs the applies
+        eagerly and reads all y back (device -> pinned host), pipelined in 4 layer chunks on two
+        copy streams.
 roofline  the decode kernel (the only kernel in the step): algorithmic bytes per launch
         (adapter rows once + x once + y read and write) / average launch time.
 cpu_baseline  the fp64 oracle (oracle/, C, OpenMP over tokens) on a bounded sample.
@@ -593,16 +594,23 @@ def main():
 
     # ---- activations: x per layer (attention input for q/k/v, o-proj input), y per projection
     g = torch.Generator(device="cpu").manual_seed(gen.BASE_SEED + 100 + rank)
-    xs = [[torch.randn(T_DECODE, H, generator=g).to(torch.bfloat16).to(dev) for _ in range(2)] for _ in range(layers)]
-    ys = [[torch.zeros(T_DECODE, H, dtype=torch.bfloat16, device=dev) for _ in PROJS] for _ in range(layers)]
+    # one contiguous buffer per kind (per-layer views go to the API), so the e2e step moves the whole
+    # step's x in one H2D and all y in one D2H copy
+    xs_all = torch.empty(layers, 2, T_DECODE, H, dtype=torch.bfloat16, device=dev)
+    for l in range(layers):
+        for i in range(2):
+            xs_all[l, i].copy_(torch.randn(T_DECODE, H, generator=g).to(torch.bfloat16))
+    ys_all = torch.zeros(layers, len(PROJS), T_DECODE, H, dtype=torch.bfloat16, device=dev)
+    xs = [[xs_all[l, i] for i in range(2)] for l in range(layers)]
+    ys = [[ys_all[l, p] for p in range(len(PROJS))] for l in range(layers)]
     stream = torch.cuda.Stream(device=dev)
 
     mode = args.qkv_mode
     fuse = mode == "fused"
     side = [torch.cuda.Stream(device=dev) for _ in range(2)]
 
-    def step(st):
-        for l in range(layers):
+    def step(st, only=None):
+        for l in (range(layers) if only is None else [only]):
             if mode == "fused":   # q, k, v share x and the batch: one fused launch pair (lora_apply_multi), then o
                 L.apply_multi(pools[l][:3], [xs[l][0]] * 3, ys[l][:3], ip, ids, stream=st)
                 pools[l][3].apply(xs[l][1], ys[l][3], ip, ids, stream=st)
@@ -666,23 +674,39 @@ def main():
                         "read+write per projection apply (profiles/ncu_decode_summary.json)"}
 
     # ---- e2e through the public API with host buffers
-    x_host = [[torch.empty(T_DECODE, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)] for _ in range(layers)]
-    for l in range(layers):
-        for i in range(2):
-            x_host[l][i].copy_(xs[l][i].cpu())
-    y_host = [[torch.empty(T_DECODE, H, dtype=torch.bfloat16).pin_memory() for _ in PROJS] for _ in range(layers)]
-    h2d = sum(t.numel() * 2 for row in x_host for t in row)
-    d2h = sum(t.numel() * 2 for row in y_host for t in row)
+    x_host = xs_all.cpu().pin_memory()
+    y_host = torch.empty(tuple(ys_all.shape), dtype=torch.bfloat16).pin_memory()
+    h2d = x_host.numel() * 2
+    d2h = y_host.numel() * 2
+
+    # pipelined in NCH layer chunks on two copy streams (PCIe is full duplex): chunk k's x H2D, its
+    # applies, its y D2H; the next step's x may land while this step's y is still leaving
+    NCH = 4 if layers % 4 == 0 else 1
+    LPC = layers // NCH
+    h2d_st = torch.cuda.Stream(device=dev)
+    d2h_st = torch.cuda.Stream(device=dev)
+    ev_x = [torch.cuda.Event() for _ in range(NCH)]
+    ev_y = [torch.cuda.Event() for _ in range(NCH)]
 
     def e2e_step():
-        with torch.cuda.stream(stream):
-            for l in range(layers):
-                for i in range(2):
-                    xs[l][i].copy_(x_host[l][i], non_blocking=True)
-            step(stream)
-            for l in range(layers):
-                for p in range(len(PROJS)):
-                    y_host[l][p].copy_(ys[l][p], non_blocking=True)
+        h2d_st.wait_stream(stream)      # previous step's applies have read x
+        stream.wait_stream(d2h_st)      # previous step's y has left before y is updated again
+        for k in range(NCH):
+            sl = slice(k * LPC, (k + 1) * LPC)
+            with torch.cuda.stream(h2d_st):
+                xs_all[sl].copy_(x_host[sl], non_blocking=True)
+                ev_x[k].record(h2d_st)
+        for k in range(NCH):
+            sl = slice(k * LPC, (k + 1) * LPC)
+            stream.wait_event(ev_x[k])
+            with torch.cuda.stream(stream):
+                for l in range(k * LPC, (k + 1) * LPC):
+                    step(stream, only=l)
+                ev_y[k].record(stream)
+            d2h_st.wait_event(ev_y[k])
+            with torch.cuda.stream(d2h_st):
+                y_host[sl].copy_(ys_all[sl], non_blocking=True)
+        stream.wait_stream(d2h_st)      # the step ends when its last y has landed
 
     for _ in range(3):
         e2e_step()
