@@ -230,6 +230,16 @@ def cpu_oracle_tokens_per_s(n_layers_sample: int, world_rank: int = 0, n_threads
     return T_DECODE * frac / dt, n_threads, dt
 
 
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     """--impl reference: the oracle (fp64 C, OpenMP) as the reference arm, same metric."""
     world, rank, local = dist_env()
@@ -249,7 +259,7 @@ def run_reference(args):
             "data": "synthetic (workloads.gen, seeded)",
             "config": {"workload": WORKLOAD, "layers": LAYERS, "tokens_per_step": T_DECODE, "adapters": 32,
                        "parallelism": "dp%d" % world},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
                              "sample": "1 of 32 layers (4 applies x 64 tokens) per step, extrapolated x32; %.1f s" % secs},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -748,6 +758,7 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": "%d of 32 layers x 4 projections (64 tokens), fp64 C oracle, OpenMP over tokens, "
                          "extrapolated to 32 layers; %.1f s of CPU work" % (args.cpu_sample_layers, dt),
+               "cpu_model": _cpu_model(),
                "single_thread_value": v1,
                "single_thread_sample": "1 layer x 4 projections, 1 thread, extrapolated; %.1f s" % dt1}
 
