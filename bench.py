@@ -77,10 +77,16 @@ def parse():
 
 
 # ---------------------------------------------------------------- distributed plumbing
+# test-only: LORA_BENCH_SHARE_GPU=1 runs every rank on cuda:0 with gloo plumbing, so the N > 1
+# control flow (barriers, max over ranks, rank-0 line, request partitioning) can be exercised on a
+# one-GPU box (NCCL refuses two ranks on one device).  Never used for reported numbers.
+SHARE_GPU = os.environ.get("LORA_BENCH_SHARE_GPU") == "1"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
@@ -89,7 +95,10 @@ def init_dist(world, local):
     import torch.distributed as dist
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world > 1
 
 
@@ -98,7 +107,7 @@ def max_over_ranks(v: float, use_dist: bool) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
