@@ -620,11 +620,20 @@ constexpr int kKPerWarp = kKSlice / kConsumerWarps;   // 128
 constexpr int kKBlocks = kKPerWarp / 32;              // 4
 constexpr int kAPitch = kKSlice * 2 + 64;             // bf16 row pitch: rows g, g+1 land 16 banks apart
 constexpr int kShrinkMmaSmem = 1024 + kShrinkRowsMma * kAPitch + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
-// Launch size of the bf16 shrink CTA: 52 KB instead of the ~39 KB it touches caps co-residency
-// at 4 shrink CTAs per SM, so a shrink grid spreads over more SMs (more HBM request streams)
-// and leaves room for the expand CTAs it overlaps with (c2 sweep, scripts/occ_sweep.sh:
-// 39 KB -> 88.3K tok/s, 50-57 KB -> 91.8K, >= 66 KB -> 70K).
-constexpr int kShrinkMmaLaunchSmem = kShrinkMmaSmem > 52 * 1024 ? kShrinkMmaSmem : 52 * 1024;
+// Launch size of the bf16 shrink CTA (>= the ~39 KB it touches) sets how many shrink CTAs share an
+// SM.  One pool per launch prefers 52 KB (4/SM: the grid spreads over more SMs; serial sweep
+// 40 KB 89.9K, 52 KB 94.3K tok/s); grids of more than 4 CTAs per SM (q/k/v in one
+// lora_apply_multi launch, 3x the units) prefer 40 KB (5/SM: more of the grid in one wave).
+#ifndef LORA_SHRINK_LAUNCH_KB
+#define LORA_SHRINK_LAUNCH_KB 52                 // grids of <= 4 shrink CTAs per SM (one pool)
+#endif
+#ifndef LORA_SHRINK_LAUNCH_KB_BIG
+#define LORA_SHRINK_LAUNCH_KB_BIG 40             // larger grids (q/k/v multi: 40 KB 99.3K vs 52 KB 98.1K tok/s)
+#endif
+constexpr int kShrinkMmaLaunchSmem =
+    kShrinkMmaSmem > LORA_SHRINK_LAUNCH_KB * 1024 ? kShrinkMmaSmem : LORA_SHRINK_LAUNCH_KB * 1024;
+constexpr int kShrinkMmaLaunchSmemBig =
+    kShrinkMmaSmem > LORA_SHRINK_LAUNCH_KB_BIG * 1024 ? kShrinkMmaSmem : LORA_SHRINK_LAUNCH_KB_BIG * 1024;
 
 // FUSED: the unit runs inside lora_decode_fused_kernel and publishes its v partials to the
 // gc's expand units with a release-increment of the gc's counter (see that kernel).
@@ -1130,7 +1139,16 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         return e;
     }
     if (phases & 1) {
-        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, K::shrink_smem > pad_s ? K::shrink_smem : pad_s, st, a, blob);
+        static int n_sms = 0;
+        if (n_sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        // bf16: a grid of more than 4 shrink CTAs per SM (e.g. q/k/v in one multi launch) fits better
+        // at 5 per SM (DESIGN.md §6 N1 occupancy)
+        const int ss = (sizeof(T) == 2 && pl.n_shrink > 4 * n_sms) ? kShrinkMmaLaunchSmemBig : K::shrink_smem;
+        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, ss > pad_s ? ss : pad_s, st, a, blob);
         if (e != cudaSuccess) return e;
         *launches += 1;
     }
