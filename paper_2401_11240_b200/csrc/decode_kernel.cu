@@ -1012,8 +1012,10 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     }
 }
 
-template <int W, bool FLAG>
-__global__ void __launch_bounds__(kConsumerThreads, LORA_EXPAND_MINB)   /* <= 85 registers: 3 CTAs per SM */
+// MINB: CTAs per SM the register budget allows (3: <= 85 registers; 4: <= 64, no spills) -- the
+// launcher takes 4 only for grids of more than 3 expand CTAs per SM (q/k/v multi launches)
+template <int W, bool FLAG, int MINB = LORA_EXPAND_MINB>
+__global__ void __launch_bounds__(kConsumerThreads, MINB)
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
@@ -1079,12 +1081,14 @@ struct DecodeKernels {
     static constexpr bool has_fused = false;
     static constexpr auto fused = lora_shrink_kernel<T, W>;   // unused
     static constexpr auto shrink_flag = lora_shrink_kernel<T, W>;   // unused
+    static constexpr auto expand_big = lora_expand_kernel<T, W>;    // unused (== expand)
     static constexpr auto expand_flag = lora_expand_kernel<T, W>;   // unused
 };
 template <int W>
 struct DecodeKernels<__nv_bfloat16, W> {
     static constexpr auto shrink = lora_shrink_mma_kernel<W, false>;
     static constexpr auto expand = lora_expand_mma_kernel<W, false>;
+    static constexpr auto expand_big = lora_expand_mma_kernel<W, false, 4>;
     static constexpr auto shrink_flag = lora_shrink_mma_kernel<W, true>;
     static constexpr auto expand_flag = lora_expand_mma_kernel<W, true>;
     static constexpr int shrink_smem = kShrinkMmaLaunchSmem;
@@ -1103,6 +1107,7 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         constexpr int kMaxOptin = 227 * 1024;
         cudaError_t e = cudaFuncSetAttribute(K::shrink, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand_big, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
         if (e == cudaSuccess && K::has_fused) {
             e = cudaFuncSetAttribute(K::fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
             if (e == cudaSuccess) e = cudaFuncSetAttribute(K::shrink_flag, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
@@ -1153,7 +1158,15 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         *launches += 1;
     }
     if (phases & 2) {
-        e = launch_pdl(K::expand, pl.n_expand, kConsumerThreads,
+        static int n_sms_e = 0;
+        if (n_sms_e == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n_sms_e, cudaDevAttrMultiProcessorCount, dev);
+        }
+        static const bool big_ok = getenv("LORA_EXP_NO_EXPAND_BIG") == nullptr;
+        const bool big = big_ok && sizeof(T) == 2 && pl.n_expand > 3 * n_sms_e;
+        e = launch_pdl(big ? K::expand_big : K::expand, pl.n_expand, kConsumerThreads,
                        K::expand_launch_smem(a) > pad_e ? K::expand_launch_smem(a) : pad_e, st, a, blob);
         *launches += 1;
     }
