@@ -784,6 +784,9 @@ constexpr int kBulkMinBytes = 2048;   // B row slices at least this long go thro
 #ifndef LORA_EXPAND_MINB
 #define LORA_EXPAND_MINB 3                // expand CTAs per SM the register budget allows (experiments)
 #endif
+#ifndef LORA_EXPAND_BIG_MINB
+#define LORA_EXPAND_BIG_MINB 4            // ... for grids of more than 3 expand CTAs per SM
+#endif
 
 // FUSED: v comes from shrink units of the same grid; thread 0 acquires the gc's counter
 // (all n_s shrink units released) instead of a grid dependency, and the gc's last expand unit
@@ -1088,7 +1091,7 @@ template <int W>
 struct DecodeKernels<__nv_bfloat16, W> {
     static constexpr auto shrink = lora_shrink_mma_kernel<W, false>;
     static constexpr auto expand = lora_expand_mma_kernel<W, false>;
-    static constexpr auto expand_big = lora_expand_mma_kernel<W, false, 4>;
+    static constexpr auto expand_big = lora_expand_mma_kernel<W, false, LORA_EXPAND_BIG_MINB>;
     static constexpr auto shrink_flag = lora_shrink_mma_kernel<W, true>;
     static constexpr auto expand_flag = lora_expand_mma_kernel<W, true>;
     static constexpr int shrink_smem = kShrinkMmaLaunchSmem;
@@ -1152,7 +1155,8 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         }
         // bf16: a grid of more than 4 shrink CTAs per SM (e.g. q/k/v in one multi launch) fits better
         // at 5 per SM (DESIGN.md §6 N1 occupancy)
-        const int ss = (sizeof(T) == 2 && pl.n_shrink > 4 * n_sms) ? kShrinkMmaLaunchSmemBig : K::shrink_smem;
+        static const bool force_big = getenv("LORA_EXP_FORCE_BIG") != nullptr;   // experiments
+        const int ss = (sizeof(T) == 2 && (force_big || pl.n_shrink > 4 * n_sms)) ? kShrinkMmaLaunchSmemBig : K::shrink_smem;
         e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, ss > pad_s ? ss : pad_s, st, a, blob);
         if (e != cudaSuccess) return e;
         *launches += 1;
@@ -1165,7 +1169,8 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
             cudaDeviceGetAttribute(&n_sms_e, cudaDevAttrMultiProcessorCount, dev);
         }
         static const bool big_ok = getenv("LORA_EXP_NO_EXPAND_BIG") == nullptr;
-        const bool big = big_ok && sizeof(T) == 2 && pl.n_expand > 3 * n_sms_e;
+        static const bool force_big_e = getenv("LORA_EXP_FORCE_BIG") != nullptr;   // experiments
+        const bool big = big_ok && sizeof(T) == 2 && (force_big_e || pl.n_expand > 3 * n_sms_e);
         e = launch_pdl(big ? K::expand_big : K::expand, pl.n_expand, kConsumerThreads,
                        K::expand_launch_smem(a) > pad_e ? K::expand_launch_smem(a) : pad_e, st, a, blob);
         *launches += 1;
