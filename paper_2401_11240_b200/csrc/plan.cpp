@@ -21,7 +21,7 @@ static lora_status append_unit_table(Plan& pl, std::string& err);
 
 lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, int H_in, int H_out,
                        int esz, int L_tc, bool tc_enabled, const AdapterTable& table, std::string& err,
-                       int pad_zero_page) {
+                       int pad_zero_page, int pf_sms) {
     if (S < 0) { err = "num_segments < 0"; return LORA_ERR_ARG; }
     if (S > 0 && (ip == nullptr || ids == nullptr)) { err = "seg_indptr/adapter_ids is NULL"; return LORA_ERR_ARG; }
     if (S > 0 && ip[0] != 0) { err = "seg_indptr[0] != 0"; return LORA_ERR_ARG; }
@@ -137,17 +137,30 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
             tiles += nt;
             pl.prefill.push_back({ip[i], len, g});
         }
-        pl.n_pf_tiles = tiles;
+        // few token tiles (e.g. 70B prefill, 32 tiles): split each tile's expand columns over
+        // `split` CTAs so more SMs stream; every CTA of a tile recomputes its shrink (x re-read
+        // from L2/HBM), and every y element is still produced by the same arithmetic (bitwise)
+        const int nct = H_out / 128;
+        int split = 1;
+        if (tiles > 0 && pf_sms > 0) {
+            split = std::max(1, std::min(nct, pf_sms / tiles));
+            while (split > 1 && (tiles * split + (int)pages_words.size()) * 8 > kPfMaxBlobWords) --split;
+        }
+        const int ctas = tiles * split;
+        pl.n_pf_tiles = ctas;
         pl.n_prefill_tiles = tiles;
-        pl.pf_blob.assign((size_t)tiles * 8 + pages_words.size(), 0);
+        pl.pf_blob.assign((size_t)ctas * 8 + pages_words.size(), 0);
         int tix = 0;
         for (const PrefillSeg& sg : pl.prefill) {
-            for (int t0 = 0; t0 < sg.len; t0 += 128) {
+            for (int t0 = 0; t0 < sg.len; t0 += 128)
+            for (int sp = 0; sp < split; ++sp) {
                 int32_t* rec = pl.pf_blob.data() + (size_t)tix * 8;
+                rec[6] = sp * nct / split;
+                rec[7] = (sp + 1) * nct / split;
                 rec[0] = sg.tok0 + t0;
                 rec[1] = std::min(128, sg.len - t0);
                 rec[2] = pl.group_rank[sg.group];
-                rec[3] = tiles * 8 + group_pf_off[sg.group];
+                rec[3] = ctas * 8 + group_pf_off[sg.group];
                 rec[4] = f32_bits(pl.group_scale[sg.group]);
                 // rec[5]: first page when the adapter's pages are one run (2D TMA boxes), else -1
                 {
@@ -159,7 +172,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
                 ++tix;
             }
         }
-        std::copy(pages_words.begin(), pages_words.end(), pl.pf_blob.begin() + (size_t)tiles * 8);
+        std::copy(pages_words.begin(), pages_words.end(), pl.pf_blob.begin() + (size_t)ctas * 8);
     }
     static thread_local std::vector<int32_t> simt_off, simt_tok;
     simt_off.assign(G + 1, 0);

@@ -48,9 +48,10 @@ struct Plan {
     int32_t job_expand_base[4] = {0, 0, 0, 0};
     // ---- tcgen05 prefill work (N2) ----
     std::vector<PrefillSeg> prefill;
-    int32_t n_prefill_tiles = 0;     // == n_pf_tiles (128-token tiles on the tensor-core path)
-    std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] tile records {tok0, nvalid, rank, page_off, scale_bits, first_page|-1}, then pages
-    int32_t n_pf_tiles = 0;
+    int32_t n_prefill_tiles = 0;     // 128-token tiles on the tensor-core path (canonical count)
+    std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] CTA records {tok0, nvalid, rank, page_off, scale_bits,
+                                     // first_page|-1, first column tile, end column tile}, then pages
+    int32_t n_pf_tiles = 0;          // prefill CTAs (tiles x column split)
     // ---- cluster-span decode work (N1c, span_kernel.cu): one grid per apply ----
     std::vector<int32_t> span_blob;  // [n_span_cta][kSpanRecWords] CTA records, then pages, then tokens
     int32_t n_span_cta = 0;          // multiple of the cluster size (idle CTAs pad the last cluster)
@@ -97,7 +98,7 @@ bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanPara
 // Returns LORA_OK or an error status with `err` naming the offending operand.
 lora_status build_plan(Plan& plan, const int32_t* seg_indptr, const int32_t* adapter_ids, int S,
                        int H_in, int H_out, int esz, int L_tc, bool tc_enabled,
-                       const AdapterTable& table, std::string& err, int pad_zero_page = -1);
+                       const AdapterTable& table, std::string& err, int pad_zero_page = -1, int pf_sms = 0);
 
 // ---- kernel launch descriptors (pool.cpp -> *_kernel.cu) ----
 struct DecodeLaunch {

@@ -323,7 +323,7 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     std::string err;
     const bool tc = !p->host_only ? p->tc_prefill : prefill_supported(p->H_in, p->H_out, p->esz);
     lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
-                               p->L_tc, tc, p->table, err, p->pad_max_rank ? p->n_pages : -1);
+                               p->L_tc, tc, p->table, err, p->pad_max_rank ? p->n_pages : -1, p->num_sms);
     if (s != LORA_OK) return fail(s, err);
     return LORA_OK;
 }
@@ -384,7 +384,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         std::string err;
         const bool tc = p->tc_prefill && mode == 0;   // the split path keeps every token on the decode kernels
         s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, tc, p->table,
-                       err, p->pad_max_rank ? p->n_pages : -1);
+                       err, p->pad_max_rank ? p->n_pages : -1, p->num_sms);
         if (s != LORA_OK) return fail(s, err);
         if (mode == 1 && p->plan.vbuf_floats > v_cap)
             return fail(LORA_ERR_ARG, "v buffer too small: need " + std::to_string(p->plan.vbuf_floats) + " floats");
@@ -494,7 +494,7 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
         lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
-                                   p->tc_prefill, p->table, err);
+                                   p->tc_prefill, p->table, err, -1, p->num_sms);
         if (s != LORA_OK) return fail(s, "pool " + std::to_string(i) + ": " + err);
         p->split_ready = false;
     }

@@ -177,7 +177,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const int first_page = rec[5];   // >= 0: rank rows are pages [first_page, first_page + r)
     const int rp = (r + 15) & ~15;                      // rank padded to the MMA N/K granularity
     const int nkc = a.H_in / 64;                        // shrink K chunks
-    const int nnt = a.H_out / kPfNTile;                 // expand column tiles
+    // expand column tiles of this CTA: [nt_lo, nt_lo + nnt) -- a tile's columns may be split over
+    // several CTAs (each recomputes the tile's shrink) when the batch has fewer tiles than SMs
+    const int nt_lo = rec[6];
+    const int nnt = (rec[7] > 0 ? rec[7] : a.H_out / kPfNTile) - nt_lo;
     if (a.trace && tid == 0) a.trace[(size_t)tile * 4 + 0] = pf_gtime();
 
     if (tid == 0) {
@@ -258,7 +261,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         phase = 0;
         // expand: B rows of each 128-column tile, MN-major SW128 atoms (8 rank rows x 64 cols);
         // atom (kg, ng) at (ng * rp/8 + kg) * 1 KB; a gather4 fills 4 rows of one atom
-        for (int nt = 0; nt < nnt; ++nt) {
+        for (int q = 0; q < nnt; ++q) {
+            const int nt = nt_lo + q;
             pf_wait(empty2(stage), phase ^ 1u);
             const uint32_t sb = ring + stage * kPfStageBytes;
             if (lane == 0) {
@@ -303,9 +307,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         pf_wait(v_ready, 0);
         tc_fence_after();
         const int ksteps = rp / 16;
-        for (int nt = 0; nt < nnt; ++nt) {
-            const int b = nt & 1;
-            pf_wait(tm_empty(b), ((nt >> 1) & 1) ^ 1u);
+        for (int q = 0; q < nnt; ++q) {
+            const int b = q & 1;
+            pf_wait(tm_empty(b), ((q >> 1) & 1) ^ 1u);
             pf_wait(full2(stage), phase);
             tc_fence_after();
             if (lane == 0) {
@@ -368,8 +372,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         //      (rows past the segment belong to other segments' tiles).
         const bool valid = row < nvalid;
         const bool leader = (tid == 64);
-        auto issue_y = [&](int nt) {
-            const int b = nt % kPfYSlots;
+        auto issue_y = [&](int q) {   // q: this CTA's column-tile index
+            const int b = q % kPfYSlots;
+            const int nt = nt_lo + q;
             const uint32_t dst = yring + (uint32_t)b * kPfYBytes;
             pf_arrive_tx(y_full(b), (uint32_t)kPfYBytes);
             tma_2d(dst, &a.tm_y, nt * kPfNTile, tok0, y_full(b));
@@ -378,11 +383,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         if (leader) {
             for (int q = 0; q < kPfYSlots && q < nnt; ++q) issue_y(q);
         }
-        for (int nt = 0; nt < nnt; ++nt) {
-            const int b = nt & 1;
-            pf_wait(tm_full(b), (nt >> 1) & 1);
-            const int yb = nt % kPfYSlots;
-            pf_wait(y_full(yb), (nt / kPfYSlots) & 1);
+        for (int q = 0; q < nnt; ++q) {
+            const int nt = nt_lo + q;
+            const int b = q & 1;
+            pf_wait(tm_full(b), (q >> 1) & 1);
+            const int yb = q % kPfYSlots;
+            pf_wait(y_full(yb), (q / kPfYSlots) & 1);
             tc_fence_after();
             uint8_t* ys = gy + yb * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll 1
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             }
             // every epilogue thread is done with y slot b -> refill it with tile nt + 2
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (leader && nt + kPfYSlots < nnt) issue_y(nt + kPfYSlots);
+            if (leader && q + kPfYSlots < nnt) issue_y(q + kPfYSlots);
         }
     }
     tc_fence_before();

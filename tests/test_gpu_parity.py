@@ -509,3 +509,15 @@ def test_two_pools_on_two_streams_concurrently(L):
     assert torch.equal(ys[0], ser[0]) and torch.equal(ys[1], ser[1])
     p1.close()
     p2.close()
+
+
+@pytest.mark.parametrize("proj", ["q", "down"])
+def test_c5_prefill_column_split(L, proj):
+    """c5 prefill (8 x 512 tokens, 70B shapes): only 32 token tiles, so the planner splits every
+    tile's expand columns over several CTAs (each recomputes the shrink); full output vs the oracle,
+    and the tcgen05 path is really taken."""
+    b = gen.config_c5(proj, prefill=True, y_zero=False)
+    y, md = run_gpu(b, L)
+    assert md["n_prefill_tiles"] == 32
+    ref = O.delta_for_batch(b, n_threads=16)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
