@@ -567,8 +567,52 @@ def bench_c5(L, dev, reps: int, hbm_peak: float):
         for tp in (2, 4, 8):
             row["tp%d" % tp]["speedup_vs_tp1"] = round(row["tp1"]["us_per_apply"] / row["tp%d" % tp]["us_per_apply"], 2)
         out[name] = row
+    # prefill 8 x 512 tokens (32 token tiles: the planner splits each tile's columns over SMs/tiles CTAs)
+    pf = {}
+    for proj in ("q", "gate", "down"):
+        b = gen.config_c5(proj, prefill=True)
+        pools = []
+        for _ in range(2):
+            pool = L.LoraPool(b.H_in, b.H_out, 16, "bf16", max_total_rank=sum(a_.rank for a_ in b.adapters))
+            for a_ in b.adapters:
+                pool.load_adapter(a_.id, a_.rank, torch.from_numpy(a_.A.view(np.int16)).pin_memory(),
+                                  torch.from_numpy(a_.B.view(np.int16)).pin_memory(), a_.scale)
+            pools.append(pool)
+        torch.cuda.synchronize()
+        x = torch.from_numpy(b.x.view(np.int16)).to(dev)
+        ys = [torch.zeros(b.T, b.H_out, dtype=torch.int16, device=dev) for _ in pools]
+
+        def body():
+            for pool, y in zip(pools, ys):
+                pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
+
+        with torch.cuda.stream(st):
+            body()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            body()
+        ts = []
+        for _ in range(max(1, reps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            with torch.cuda.stream(st):
+                g.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / len(pools))
+        us = float(np.median(ts))
+        sum_r = sum(a_.rank for a_ in b.adapters)
+        byts = 2 * (sum_r * (b.H_in + b.H_out) + b.T * b.H_in + 2 * b.T * b.H_out)
+        pf[proj] = {"shape": [b.H_in, b.H_out], "tokens": b.T, "us_per_apply": round(us, 2),
+                    "roofline_frac": round(byts / (us * 1e-6) / 1e9 / hbm_peak, 4)}
+        for pool in pools:
+            pool.close()
+        del pools, ys
     return {"workload": "c5: Llama-2-70B projection shapes, decode 64 tokens over 32 adapters ranks 16..128, bf16; "
-                        "tp>1 = one rank's shard kernels (shrink + expand), v all-reduce excluded",
+                        "tp>1 = one rank's shard kernels (shrink + expand), v all-reduce excluded; prefill_tp1: 8 x 512 "
+                        "tokens over 8 adapters on the tcgen05 kernel",
+            "prefill_tp1": pf,
             "shapes": {k: list(v) for k, v in shapes.items()}, "per_shape": out}
 
 
