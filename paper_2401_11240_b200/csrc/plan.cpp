@@ -137,15 +137,22 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
             tiles += nt;
             pl.prefill.push_back({ip[i], len, g});
         }
-        // few token tiles (e.g. 70B prefill, 32 tiles): split each tile's expand columns over
-        // `split` CTAs so more SMs stream; every CTA of a tile recomputes its shrink (x re-read
-        // from L2/HBM), and every y element is still produced by the same arithmetic (bitwise)
+        // few token tiles (e.g. 70B prefill, 32 tiles): `split` CTAs per tile, each expanding a
+        // share of the columns.  If the shrink dominates (H_in > H_out, e.g. a down projection) the
+        // CTAs form a cluster that also splits the shrink's K, exchanging fp32 partials over DSMEM
+        // (summed in rank order); otherwise each CTA recomputes the tile's shrink (x re-read, mostly
+        // from L2) -- the DSMEM exchange of full partials costs more than that when H_in <= H_out
+        // (c5 prefill: q 44 % vs 39 %, down 51 % vs 36 % of HBM roofline).  Every y element is
+        // produced by the same arithmetic either way within a mode.
         const int nct = H_out / 128;
         int split = 1;
+        const bool splitk = H_in > H_out;
         if (tiles > 0 && pf_sms > 0) {
             split = std::max(1, std::min(nct, pf_sms / tiles));
+            if (splitk) split = std::min(split, std::min(8, H_in / 64));
             while (split > 1 && (tiles * split + (int)pages_words.size()) * 8 > kPfMaxBlobWords) --split;
         }
+        pl.pf_cs = splitk ? split : 1;
         const int ctas = tiles * split;
         pl.n_pf_tiles = ctas;
         pl.n_prefill_tiles = tiles;

@@ -51,7 +51,8 @@ struct Plan {
     int32_t n_prefill_tiles = 0;     // 128-token tiles on the tensor-core path (canonical count)
     std::vector<int32_t> pf_blob;    // [n_pf_tiles][8] CTA records {tok0, nvalid, rank, page_off, scale_bits,
                                      // first_page|-1, first column tile, end column tile}, then pages
-    int32_t n_pf_tiles = 0;          // prefill CTAs (tiles x column split)
+    int32_t n_pf_tiles = 0;          // prefill CTAs (tiles x pf_cs)
+    int32_t pf_cs = 1;               // CTAs per token tile (a cluster: split-K shrink + column split)
     // ---- cluster-span decode work (N1c, span_kernel.cu): one grid per apply ----
     std::vector<int32_t> span_blob;  // [n_span_cta][kSpanRecWords] CTA records, then pages, then tokens
     int32_t n_span_cta = 0;          // multiple of the cluster size (idle CTAs pad the last cluster)
@@ -73,6 +74,7 @@ struct Plan {
         unit_tab = 0; unit_words = d.unit_words; blob_esz = d.blob_esz; vbuf_floats = 0; n_jobs = 1;
         for (int i = 0; i < 4; ++i) job_shrink_base[i] = job_expand_base[i] = 0;
         n_prefill_tiles = n_pf_tiles = 0;
+        pf_cs = 1;
         n_span_cta = span_cluster = span_max_rank = span_max_sk = span_max_sn = 0;
     }
 };

@@ -48,6 +48,7 @@ struct PrefillArgs {
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads; writes go per row)
     const char* box_maps;   // pool page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), SW128
+    int cs;                 // cluster size: the cs CTAs of a token tile split its shrink K and its columns
     char* y;
     const int32_t* meta_global;
     unsigned long long* trace;
@@ -93,6 +94,38 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm,
         "%5, %6}], [%7];" ::"r"(dst),
         "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
         : "memory");
+}
+// ---- cluster split-K helpers
+__device__ __forceinline__ uint32_t pf_cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t pf_mapa(uint32_t addr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void pf_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void pf_wait_cluster(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_PFWC:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LAB_PFWC;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ float4 pf_ld_dsmem_v4(uint32_t cluster_addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(cluster_addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void pf_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1 (sm_100)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -165,8 +198,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     auto tm_full = [&](int b) { return v_ready + 8u + 8u * b; };
     auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
     auto y_full = [&](int b) { return v_ready + 40u + 8u * b; };
+    // split-K exchange (cs > 1): all cs partials of the tile are in the CTAs' SMEM / all peers read mine
+    const uint32_t pready = bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 9);
+    const uint32_t pconsumed = pready + 8u;
     uint32_t* tmem_slot =
-        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 9) - base));
+        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 11) - base));
+    static_assert(8 * (2 * kPfShrinkStages + 2 * kPfStages + 11) + 4 <= 256, "barrier region");
 
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -176,7 +213,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const float scale = __int_as_float(rec[4]);
     const int first_page = rec[5];   // >= 0: rank rows are pages [first_page, first_page + r)
     const int rp = (r + 15) & ~15;                      // rank padded to the MMA N/K granularity
-    const int nkc = a.H_in / 64;                        // shrink K chunks
+    const int nkc_all = a.H_in / 64;                    // shrink K chunks of the tile
+    const int cs = a.cs;
+    const int ck = cs > 1 ? (int)pf_cluster_rank() : 0;  // this CTA's share of K: [kc_lo, kc_lo + nkc)
+    const int kc_lo = ck * nkc_all / cs;
+    const int nkc = (ck + 1) * nkc_all / cs - kc_lo;
     // expand column tiles of this CTA: [nt_lo, nt_lo + nnt) -- a tile's columns may be split over
     // several CTAs (each recomputes the tile's shrink) when the batch has fewer tiles than SMs
     const int nt_lo = rec[6];
@@ -194,6 +235,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         }
         pf_bar_init(d1_full, 1);
         pf_bar_init(v_ready, 128);
+        pf_bar_init(pready, (uint32_t)cs);
+        pf_bar_init(pconsumed, (uint32_t)cs);
         for (int b = 0; b < 2; ++b) {
             pf_bar_init(tm_full(b), 1);
             pf_bar_init(tm_empty(b), 128);
@@ -207,6 +250,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (cs > 1) pf_cluster_sync();   // every peer's barriers are initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // x and y may be produced by the preceding kernel in the stream
@@ -242,7 +286,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             }
         };
         const bool use_box = first_page >= 0 && a.box_maps != nullptr;
-        for (int kc = 0; kc < nkc; ++kc) {
+        for (int kq = 0; kq < nkc; ++kq) {
+            const int kc = kc_lo + kq;
             pf_wait(empty(stage), phase ^ 1u);
             const uint32_t sb = ring + stage * kPfStageBytes;
             if (lane == 0) {
@@ -337,9 +382,49 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         pf_wait(d1_full, 0);
         tc_fence_after();
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 2] = pf_gtime();
+        // split-K (cs > 1): this CTA's D1 is a partial over its K share.  Partials go to the CTA's
+        // (now idle) y area as fp32 [row][rp] (+16-B pad); once every peer's partial is ready, each
+        // CTA sums all cs of them over distributed shared memory in rank order (deterministic).
+        const int ppitch = rp * 4 + 16;
+        const uint32_t pbase = yring;
+        if (cs > 1) {
+            for (int c0 = 0; c0 < rp; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
+                const int nv = rp - c0 < 32 ? (rp - c0) / 4 : 8;   // only the row's rp columns (rp % 16 == 0)
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (i < nv)
+                        *reinterpret_cast<float4*>(gy + row * ppitch + (c0 + 4 * i) * 4) =
+                            make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 64)
+                for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(pready, (uint32_t)c));
+            pf_wait_cluster(pready, 0);
+        }
         for (int c0 = 0; c0 < rp; c0 += 32) {
             float v[32];
-            tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
+            if (cs > 1) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                const int nv = rp - c0 < 32 ? (rp - c0) / 4 : 8;
+                for (int c = 0; c < cs; ++c) {
+                    const uint32_t src = pf_mapa(pbase + (uint32_t)(row * ppitch + c0 * 4), (uint32_t)c);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if (i >= nv) break;
+                        const float4 f = pf_ld_dsmem_v4(src + 16u * i);
+                        v[4 * i] += f.x;
+                        v[4 * i + 1] += f.y;
+                        v[4 * i + 2] += f.z;
+                        v[4 * i + 3] += f.w;
+                    }
+                }
+            } else {
+                tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
+            }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {   // four 16-B chunks of 8 columns
                 uint32_t hw[4], lw[4];
@@ -362,6 +447,11 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 *reinterpret_cast<uint4*>(gv + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
             }
         }
+        if (cs > 1) {   // done reading every peer's partial
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 64)
+                for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(pconsumed, (uint32_t)c));
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
         tc_fence_before();
         pf_arrive(v_ready);
@@ -381,6 +471,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(b));
         };
         if (leader) {
+            if (cs > 1) pf_wait_cluster(pconsumed, 0);   // peers no longer read the partial in the y area
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             for (int q = 0; q < kPfYSlots && q < nnt; ++q) issue_y(q);
         }
         for (int q = 0; q < nnt; ++q) {
@@ -502,11 +594,15 @@ static cudaError_t launch_pf(const PrefillArgs& a, const Plan& pl, cudaStream_t 
     cfg.blockDim = dim3(kPfThreads);
     cfg.dynamicSmemBytes = kPfSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = a.cs > 1 ? a.cs : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, lora_prefill_tc_kernel<W>, a, blob);
 }
 
@@ -526,6 +622,7 @@ int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int*
     a.H_in = L.H_in;
     a.H_out = L.H_out;
     a.n_tiles = pl.n_pf_tiles;
+    a.cs = pl.pf_cs > 1 ? pl.pf_cs : 1;
     a.zero_page = L.zero_page;
     const size_t n = pl.pf_blob.size();
     cudaError_t r;

@@ -1,5 +1,5 @@
-"""Per-CTA phase timeline of the tcgen05 prefill kernel on config 3 (lora_debug_set_trace).
-usage: python scripts/trace_prefill.py"""
+"""Per-CTA phase timeline of the tcgen05 prefill kernel (lora_debug_set_trace): config 3, or a c5
+prefill shape (32 token tiles: split-K clusters).  usage: python scripts/trace_prefill.py [c3|c5q|c5down]"""
 import os
 import sys
 
@@ -16,7 +16,9 @@ def tt(a, pin=False):
     return t.pin_memory() if pin else t
 
 
-b = gen.config_c3()
+which = sys.argv[1] if len(sys.argv) > 1 else "c3"
+b = {"c3": lambda: gen.config_c3(), "c5q": lambda: gen.config_c5("q", prefill=True),
+     "c5down": lambda: gen.config_c5("down", prefill=True)}[which]()
 pool = L.LoraPool(b.H_in, b.H_out, 64, b.dtype, max_total_rank=sum(a.rank for a in b.adapters))
 for a in b.adapters:
     pool.load_adapter(a.id, a.rank, tt(a.A, True), tt(a.B, True), a.scale)
@@ -26,8 +28,8 @@ for _ in range(3):
     pool.apply(x, y, b.seg_indptr, b.adapter_ids)
 torch.cuda.synchronize()
 md = pool.metadata()
-nt = md["n_prefill_tiles"]
-buf = torch.zeros(4 * nt + 64, dtype=torch.int64, device="cuda")
+nt = md["n_prefill_tiles"] * (1 if which == "c3" else 4)   # CTAs (c5: 4-CTA clusters per tile)
+buf = torch.zeros(4 * nt * 2 + 64, dtype=torch.int64, device="cuda")
 pool.set_trace(buf)
 flush = torch.empty(512 * 2 ** 20, dtype=torch.int8, device="cuda")
 flush.zero_()
@@ -46,7 +48,7 @@ for lab, a_, b_ in (("start->shrink done", 0, 2), ("shrink done->V ready", 2, 3)
     print("  %-22s med %.2f p10 %.2f p90 %.2f max %.2f us" % (lab, np.median(d), np.percentile(d, 10),
                                                               np.percentile(d, 90), d.max()))
 print("  start spread %.2f us" % ((U[:, 0].max() - t0) / 1e3))
-ranks = np.array([gen.C3_RANKS[(t // 4) % 5] for t in range(nt)])
+ranks = np.array([gen.C3_RANKS[(t // 4) % 5] for t in range(nt)]) if which == "c3" else np.zeros(nt, int)
 for r in sorted(set(ranks.tolist())):
     m = ranks == r
     print("  rank %3d: shrink %.1f us, expand %.1f us, total %.1f us (%d tiles)" % (
