@@ -5,6 +5,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernel_config.h"
@@ -137,18 +138,19 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
             tiles += nt;
             pl.prefill.push_back({ip[i], len, g});
         }
-        // few token tiles (e.g. 70B prefill, 32 tiles): `split` CTAs per tile, each expanding a
-        // share of the columns.  If the shrink dominates (H_in > H_out, e.g. a down projection) the
-        // CTAs form a cluster that also splits the shrink's K, exchanging fp32 partials over DSMEM
-        // (summed in rank order); otherwise each CTA recomputes the tile's shrink (x re-read, mostly
-        // from L2) -- the DSMEM exchange of full partials costs more than that when H_in <= H_out
-        // (c5 prefill: q 44 % vs 39 %, down 51 % vs 36 % of HBM roofline).  Every y element is
-        // produced by the same arithmetic either way within a mode.
+        // few token tiles (e.g. 70B prefill, 32 tiles): `split` CTAs per tile, each expanding a share
+        // of the columns.  Split-K: the CTAs form a cluster (<= 8) that also splits the shrink's K,
+        // exchanging fp32 partial D1 tiles through an L2 scratch (summed in rank order, deterministic)
+        // -- nothing is read twice.  Used when <= 8 CTAs per tile are wanted or when the shrink
+        // dominates (H_in > H_out); beyond 8 (very few tiles, e.g. one 512-token segment) the other
+        // CTAs of a tile each recompute its shrink (column split; x re-read, mostly from L2).
         const int nct = H_out / 128;
         int split = 1;
-        const bool splitk = H_in > H_out;
+        bool splitk = false;
         if (tiles > 0 && pf_sms > 0) {
+            static const bool force_splitk = getenv("LORA_EXP_PF_SPLITK") != nullptr;   // experiments
             split = std::max(1, std::min(nct, pf_sms / tiles));
+            splitk = force_splitk || split <= 8 || H_in > H_out;
             if (splitk) split = std::min(split, std::min(8, H_in / 64));
             while (split > 1 && (tiles * split + (int)pages_words.size()) * 8 > kPfMaxBlobWords) --split;
         }

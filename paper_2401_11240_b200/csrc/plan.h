@@ -140,6 +140,7 @@ struct PrefillLaunch {
     const int32_t* meta_dev;
     unsigned long long* trace;
     int T, H_in, H_out, zero_page, num_sms;
+    float* pscratch = nullptr;   // split-K partials: [CTA][128 rows][128] fp32 (L2-resident exchange)
 };
 
 // Concatenates the SIMT work lists of plans[0..n) (one per fused pool = job index) into merged

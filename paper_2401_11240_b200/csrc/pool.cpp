@@ -48,6 +48,8 @@ struct lora_pool {
     bool fence_pending = false;
     std::vector<cudaStream_t> apply_streams;   // streams applied on since the last unload
     float* vbuf = nullptr;
+    float* pf_scratch = nullptr;         // prefill split-K partials (grown on demand)
+    size_t pf_scratch_cap = 0;
     size_t vbuf_cap = 0;                 // floats
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
@@ -202,6 +204,7 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->span_tmaps) cudaFree(p->span_tmaps);
         if (p->dB) cudaFree(p->dB);
         if (p->vbuf) cudaFree(p->vbuf);
+        if (p->pf_scratch) cudaFree(p->pf_scratch);
         if (p->gc_sync) cudaFree(p->gc_sync);
         if (p->meta_dev) cudaFree(p->meta_dev);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
@@ -447,7 +450,11 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
     if (pl.n_pf_tiles > 0 && mode == 0) {
+        if (pl.pf_cs > 1 &&
+            (s = grow(p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
+            return s;
         PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
+        L.pscratch = p->pf_scratch;
         cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
     }
@@ -561,8 +568,13 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
         if (p->plan.n_pf_tiles == 0) continue;
+        if (p->plan.pf_cs > 1 &&
+            (s = grow(p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * 128, false, "pf_scratch")) !=
+                LORA_OK)
+            return s;
         PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
                         p->num_sms};
+        L.pscratch = p->pf_scratch;
         cudaError_t e = (cudaError_t)launch_prefill(p->plan, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: prefill kernel launch");
     }

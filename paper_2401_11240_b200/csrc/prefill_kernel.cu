@@ -49,6 +49,7 @@ struct PrefillArgs {
     CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads; writes go per row)
     const char* box_maps;   // pool page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), SW128
     int cs;                 // cluster size: the cs CTAs of a token tile split its shrink K and its columns
+    float* pscratch;        // split-K partials [CTA][128][128] fp32 (L2-resident exchange)
     char* y;
     const int32_t* meta_global;
     unsigned long long* trace;
@@ -382,11 +383,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         pf_wait(d1_full, 0);
         tc_fence_after();
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 2] = pf_gtime();
-        // split-K (cs > 1): this CTA's D1 is a partial over its K share.  Partials go to the CTA's
-        // (now idle) y area as fp32 [row][rp] (+16-B pad); once every peer's partial is ready, each
-        // CTA sums all cs of them over distributed shared memory in rank order (deterministic).
-        const int ppitch = rp * 4 + 16;
-        const uint32_t pbase = yring;
+        // split-K (cs > 1): this CTA's D1 is a partial over its K share.  Partials go to an
+        // L2-resident scratch as fp32 [CTA][row][128]; once every peer's partial is released (remote
+        // mbarrier arrive, cluster scope), each CTA sums all cs of them in rank order (deterministic).
+        float* pmine = a.pscratch + ((size_t)blockIdx.x * 128 + row) * 128;
         if (cs > 1) {
             for (int c0 = 0; c0 < rp; c0 += 32) {
                 float v[32];
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                     if (i < nv)
-                        *reinterpret_cast<float4*>(gy + row * ppitch + (c0 + 4 * i) * 4) =
+                        *reinterpret_cast<float4*>(pmine + c0 + 4 * i) =
                             make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
             asm volatile("fence.acq_rel.cluster;" ::: "memory");
@@ -411,15 +411,19 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 for (int i = 0; i < 32; ++i) v[i] = 0.f;
                 const int nv = rp - c0 < 32 ? (rp - c0) / 4 : 8;
                 for (int c = 0; c < cs; ++c) {
-                    const uint32_t src = pf_mapa(pbase + (uint32_t)(row * ppitch + c0 * 4), (uint32_t)c);
+                    // partials of the cluster's CTAs (L2): blockIdx.x - ck + c, this row, columns c0..;
+                    // all 8 loads of a peer are in flight before the first add consumes one
+                    const float* src = a.pscratch + ((size_t)(blockIdx.x - ck + c) * 128 + row) * 128 + c0;
+                    float4 f[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        f[i] = i < nv ? __ldcg(reinterpret_cast<const float4*>(src) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        if (i >= nv) break;
-                        const float4 f = pf_ld_dsmem_v4(src + 16u * i);
-                        v[4 * i] += f.x;
-                        v[4 * i + 1] += f.y;
-                        v[4 * i + 2] += f.z;
-                        v[4 * i + 3] += f.w;
+                        v[4 * i] += f[i].x;
+                        v[4 * i + 1] += f[i].y;
+                        v[4 * i + 2] += f[i].z;
+                        v[4 * i + 3] += f[i].w;
                     }
                 }
             } else {
@@ -447,11 +451,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 *reinterpret_cast<uint4*>(gv + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
             }
         }
-        if (cs > 1) {   // done reading every peer's partial
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (tid == 64)
-                for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(pconsumed, (uint32_t)c));
-        }
+
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
         tc_fence_before();
         pf_arrive(v_ready);
@@ -471,7 +471,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(b));
         };
         if (leader) {
-            if (cs > 1) pf_wait_cluster(pconsumed, 0);   // peers no longer read the partial in the y area
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             for (int q = 0; q < kPfYSlots && q < nnt; ++q) issue_y(q);
         }
@@ -623,6 +622,8 @@ int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int*
     a.H_out = L.H_out;
     a.n_tiles = pl.n_pf_tiles;
     a.cs = pl.pf_cs > 1 ? pl.pf_cs : 1;
+    a.pscratch = L.pscratch;
+    if (a.cs > 1 && !a.pscratch) return (int)cudaErrorInvalidValue;
     a.zero_page = L.zero_page;
     const size_t n = pl.pf_blob.size();
     cudaError_t r;
