@@ -119,12 +119,6 @@ __device__ __forceinline__ void pf_wait_cluster(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ float4 pf_ld_dsmem_v4(uint32_t cluster_addr) {
-    float4 v;
-    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(cluster_addr) : "memory");
-    return v;
-}
 __device__ __forceinline__ void pf_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -199,9 +193,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     auto tm_full = [&](int b) { return v_ready + 8u + 8u * b; };
     auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
     auto y_full = [&](int b) { return v_ready + 40u + 8u * b; };
-    // split-K exchange (cs > 1): all cs partials of the tile are in the CTAs' SMEM / all peers read mine
+    // split-K exchange (cs > 1): every peer's partial of the tile is in the L2 scratch
     const uint32_t pready = bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 9);
-    const uint32_t pconsumed = pready + 8u;
     uint32_t* tmem_slot =
         reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 11) - base));
     static_assert(8 * (2 * kPfShrinkStages + 2 * kPfStages + 11) + 4 <= 256, "barrier region");
@@ -237,7 +230,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         pf_bar_init(d1_full, 1);
         pf_bar_init(v_ready, 128);
         pf_bar_init(pready, (uint32_t)cs);
-        pf_bar_init(pconsumed, (uint32_t)cs);
         for (int b = 0; b < 2; ++b) {
             pf_bar_init(tm_full(b), 1);
             pf_bar_init(tm_empty(b), 128);
