@@ -521,3 +521,14 @@ def test_c5_prefill_column_split(L, proj):
     assert md["n_prefill_tiles"] == 32
     ref = O.delta_for_batch(b, n_threads=16)
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+def test_prefill_rank_above_tcgen05_limit_falls_back(L):
+    """Prefill-length segments of rank > 128 (the tcgen05 path's limit) run on the decode kernel pair
+    in 8-token chunks, next to rank <= 128 segments on the tensor-core path, in one apply."""
+    b = gen.build_batch("r200", 4711, "bf16", 512, 512, [300, 150, 1, 1], [0, 1, 0, 1], {0: 200, 1: 96},
+                        y_zero=False)
+    y, md = run_gpu(b, L)
+    assert md["n_prefill_tiles"] == 2          # only the rank-96 segment (150 tokens) is on tcgen05
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
