@@ -4,6 +4,7 @@ partial v is an elementwise add); a world-size-1 NCCL group exercises TPLoraLaye
 collective path.  Multi-process coverage of the decomposition runs on CPU with gloo
 (tests/test_tp_gloo.py)."""
 import os
+import socket
 
 import numpy as np
 import pytest
@@ -57,7 +58,11 @@ def test_tp_layer_nccl_world1(torch_cuda):
     from paper_2401_11240_b200.tp import TPLoraLayer
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
+        if "MASTER_PORT" not in os.environ:
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            sk.close()
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     b = gen.config_c5("q", y_zero=False)
     ref = O.delta_for_batch(b, n_threads=8)
