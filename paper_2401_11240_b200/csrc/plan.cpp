@@ -149,7 +149,8 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         bool splitk = false;
         if (tiles > 0 && pf_sms > 0) {
             static const bool force_splitk = getenv("LORA_EXP_PF_SPLITK") != nullptr;   // experiments
-            split = std::max(1, std::min(nct, pf_sms / tiles));
+            static const int force_split = getenv("LORA_EXP_PF_SPLIT") ? atoi(getenv("LORA_EXP_PF_SPLIT")) : 0;
+            split = force_split > 0 ? std::min(nct, force_split) : std::max(1, std::min(nct, pf_sms / tiles));
             splitk = force_splitk || split <= 8 || H_in > H_out;
             if (splitk) split = std::min(split, std::min(8, H_in / 64));
             while (split > 1 && (tiles * split + (int)pages_words.size()) * 8 > kPfMaxBlobWords) --split;
