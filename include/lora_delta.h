@@ -247,6 +247,9 @@ typedef struct {
     int64_t v_floats;                          /* size of the partial-v buffer (lora_apply_shrink) */
     int32_t n_span_ctas, span_cluster;         /* cluster-span decode grid of the last apply (0 if the
                                                   kernel pair ran): CTAs and cluster size */
+    int32_t n_prefill_ctas, prefill_cluster;   /* tcgen05 prefill grid of the last apply: CTAs
+                                                  (tiles x CTAs per tile) and split-K cluster size
+                                                  (1 = no split-K) */
 } lora_metadata_view;
 
 lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* out);

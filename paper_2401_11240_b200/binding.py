@@ -59,7 +59,8 @@ class MetadataView(ctypes.Structure):
                 ("sum_rank_tokens", ctypes.c_int64),
                 ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32),
                 ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32),
-                ("v_floats", ctypes.c_int64), ("n_span_ctas", ctypes.c_int32), ("span_cluster", ctypes.c_int32)]
+                ("v_floats", ctypes.c_int64), ("n_span_ctas", ctypes.c_int32), ("span_cluster", ctypes.c_int32),
+                ("n_prefill_ctas", ctypes.c_int32), ("prefill_cluster", ctypes.c_int32)]
 
 
 def header_symbols() -> List[str]:
@@ -258,7 +259,7 @@ class LoraPool:
                "pages": arr(m.pages, int(m.sum_rank_groups)), "seg_kind": arr(m.seg_kind, m.S)}
         for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens",
                   "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units", "v_floats",
-                  "n_span_ctas", "span_cluster"):
+                  "n_span_ctas", "span_cluster", "n_prefill_ctas", "prefill_cluster"):
             out[k] = int(getattr(m, k))
         return out
 

@@ -678,6 +678,8 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
     o->n_span_ctas = pl.n_span_cta;
     o->span_cluster = pl.span_cluster;
     o->n_prefill_tiles = pl.n_prefill_tiles;
+    o->n_prefill_ctas = pl.n_pf_tiles;
+    o->prefill_cluster = pl.pf_cs;
     return LORA_OK;
 }
 

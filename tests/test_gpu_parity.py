@@ -513,12 +513,13 @@ def test_two_pools_on_two_streams_concurrently(L):
 
 @pytest.mark.parametrize("proj", ["q", "down"])
 def test_c5_prefill_column_split(L, proj):
-    """c5 prefill (8 x 512 tokens, 70B shapes): only 32 token tiles, so the planner splits every
-    tile's expand columns over several CTAs (each recomputes the shrink); full output vs the oracle,
-    and the tcgen05 path is really taken."""
+    """c5 prefill (8 x 512 tokens, 70B shapes): only 32 token tiles, so the planner gives every tile
+    a split-K cluster of 4 CTAs (shrink K and expand columns split); full output vs the oracle, and
+    the tcgen05 path is really taken."""
     b = gen.config_c5(proj, prefill=True, y_zero=False)
     y, md = run_gpu(b, L)
     assert md["n_prefill_tiles"] == 32
+    assert md["prefill_cluster"] > 1 and md["n_prefill_ctas"] == 32 * md["prefill_cluster"]
     ref = O.delta_for_batch(b, n_threads=16)
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
 
@@ -531,4 +532,49 @@ def test_prefill_rank_above_tcgen05_limit_falls_back(L):
     y, md = run_gpu(b, L)
     assert md["n_prefill_tiles"] == 2          # only the rank-96 segment (150 tokens) is on tcgen05
     ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+def _few_tile_batch(name, seed, H_in, H_out, n_tiles):
+    """Prefill segments (ragged lengths 65..400, ranks incl. 1 / 24 / 128) totalling exactly n_tiles
+    128-token tiles, plus three decode tokens."""
+    rng = np.random.default_rng(seed)
+    lens, tiles = [], 0
+    while tiles < n_tiles:
+        ln = int(rng.integers(65, 401))
+        t = -(-ln // 128)
+        if tiles + t > n_tiles:
+            ln = int(rng.integers(65, 129)) + 128 * (n_tiles - tiles - 1)
+            t = n_tiles - tiles
+        lens.append(ln)
+        tiles += t
+    ranks_cycle = (1, 8, 24, 128, 16, 64)
+    n_ad = min(len(lens), 6)
+    ids = [i % n_ad for i in range(len(lens))] + [0, 1 % n_ad, 0]
+    lens = lens + [1, 1, 1]
+    ranks = {a: ranks_cycle[a] for a in range(n_ad)}
+    return gen.build_batch(name, seed, "bf16", H_in, H_out, lens, ids, ranks, y_zero=False)
+
+
+@pytest.mark.parametrize("H_in,H_out,n_tiles", [
+    (1024, 1024, 3), (1024, 1024, 20), (1024, 1024, 24), (1024, 1024, 27), (1024, 1024, 30),
+    (1024, 1024, 40), (1024, 1024, 60), (1024, 4096, 2), (4096, 1024, 2)])
+def test_prefill_few_tile_splits(L, H_in, H_out, n_tiles):
+    """Few token tiles: the planner gives each tile `split` CTAs (N2 few-tile rule):
+    split = min(H_out/128, SMs // tiles). For split <= 8, or when H_in > H_out, the tile's CTAs form a
+    split-K cluster, capped at min(8, H_in/64); partial D1 tiles are summed in rank order. Otherwise
+    every CTA recomputes the shrink for its share of the columns. Each case hits a different cluster
+    size (8, 7, 6, 5, 4, 3, 2 on 148 SMs) or the recompute path. Full output vs the oracle."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    b = _few_tile_batch("few%d_%d_%d" % (H_in, H_out, n_tiles), 100 + n_tiles, H_in, H_out, n_tiles)
+    y, md = run_gpu(b, L)
+    assert md["n_prefill_tiles"] == n_tiles
+    split = max(1, min(H_out // 128, sms // n_tiles))
+    splitk = split <= 8 or H_in > H_out
+    if splitk:
+        split = min(split, 8, H_in // 64)
+    assert md["n_prefill_ctas"] == n_tiles * split
+    assert md["prefill_cluster"] == (split if splitk else 1)
+    ref = O.delta_for_batch(b, n_threads=16)
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
