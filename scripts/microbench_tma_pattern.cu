@@ -1,0 +1,162 @@
+// DRAM access pattern of the prefill shrink's x stream, in isolation.
+// Each CTA (one per SM, 16-KB ring stages) reads 128 rows x 4096 bf16 (1 MB):
+//   A  strided : 64 boxes {64 cols, 128 rows} SW128, k-chunk order   (what the prefill kernel does)
+//   B  contig  : the same bytes as 64 contiguous 16-KB boxes          (ideal streaming)
+//   C  grouped : 4 stages at a time, boxes {64, 16} in row-block-major order, so each row's 4
+//                adjacent 128-B pieces (512 B) are requested back to back
+//   D  4 lanes : each stage as 4 boxes {64, 32} issued by 4 lanes of the producer warp
+// and the same at 2 CTAs per SM (grid 2 x SMs, <= 6 stages each).
+// The consumer only waits and frees stages (no compute).
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/microbench_tma_pattern scripts/microbench_tma_pattern.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint32_t b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c) : "memory"); }
+__device__ __forceinline__ void arrive_tx(uint32_t b, uint32_t tx) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(tx) : "memory"); }
+__device__ __forceinline__ void arrive(uint32_t b) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory"); }
+__device__ __forceinline__ void wait(uint32_t b, uint32_t ph) {
+    asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W_%=;\n}" ::"r"(b), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(dst), "l"(tm), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+
+constexpr int kStageBytes = 16384;
+constexpr int kMaxStages = 12;
+
+__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                                       const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
+                                                       int mode, int nst) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const uint32_t base = (su32(sm) + 1023u) & ~1023u;
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) { bar_init(su32(&full[s]), 1); bar_init(su32(&empty[s]), 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int row0 = blockIdx.x * 128;
+    if (mode == 3 && tid < 32) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kc = 0; kc < 64; ++kc) {
+            wait(su32(&empty[s]), ph ^ 1u);
+            if (tid == 0) arrive_tx(su32(&full[s]), kStageBytes);
+            __syncwarp();
+            if (tid < 4) tma2d(base + s * kStageBytes + tid * 4096, &tmD, kc * 64, row0 + tid * 32, su32(&full[s]));
+            if (++s == nst) { s = 0; ph ^= 1u; }
+        }
+    } else if (tid == 0) {
+        if (mode == 2) {
+            // groups of 4 stages; every stage of a group gets 8 boxes of 16 rows
+            int s0 = 0;
+            uint32_t ph = 0;
+            for (int g = 0; g < 16; ++g) {
+                for (int j = 0; j < 4; ++j) {
+                    wait(su32(&empty[s0 + j]), ph ^ 1u);
+                    arrive_tx(su32(&full[s0 + j]), kStageBytes);
+                }
+                for (int rb = 0; rb < 8; ++rb)
+                    for (int j = 0; j < 4; ++j)
+                        tma2d(base + (s0 + j) * kStageBytes + rb * 2048, &tmC, (g * 4 + j) * 64, row0 + rb * 16,
+                              su32(&full[s0 + j]));
+                s0 += 4;
+                if (s0 == nst) { s0 = 0; ph ^= 1u; }
+            }
+        } else {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int kc = 0; kc < 64; ++kc) {
+                wait(su32(&empty[s]), ph ^ 1u);
+                arrive_tx(su32(&full[s]), kStageBytes);
+                if (mode == 0) tma2d(base + s * kStageBytes, &tmA, kc * 64, row0, su32(&full[s]));
+                else tma2d(base + s * kStageBytes, &tmB, 0, blockIdx.x * 8192 + kc * 128, su32(&full[s]));
+                if (++s == nst) { s = 0; ph ^= 1u; }
+            }
+        }
+    } else if (tid == 32) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kc = 0; kc < 64; ++kc) {
+            wait(su32(&full[s]), ph);
+            arrive(su32(&empty[s]));
+            if (++s == nst) { s = 0; ph ^= 1u; }
+        }
+    }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+}
+
+static int make(CUtensorMap* m, void* ptr, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return (int)enc()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const char* names[4] = {"A strided {64,128}", "B contiguous 16KB", "C grouped 4x{64,16}", "D 4 lanes {64,32}"};
+    const int grids[4] = {64, 128, sms, 2 * sms};
+    void* flush;
+    CK(cudaMalloc(&flush, 512u << 20));
+    for (int gi = 0; gi < 4; ++gi) {
+        const int grid = grids[gi];
+        const uint64_t rows = (uint64_t)grid * 128;
+        void* x;
+        CK(cudaMalloc(&x, rows * 4096 * 2));
+        CK(cudaMemset(x, 1, rows * 4096 * 2));
+        CUtensorMap tA, tB, tC, tD;
+        if (make(&tA, x, 4096, rows, 128) || make(&tB, x, 64, rows * 64, 128) || make(&tC, x, 4096, rows, 16) ||
+            make(&tD, x, 4096, rows, 32)) {
+            printf("tensor map failed\n");
+            return 1;
+        }
+        const bool two = grid > sms;   // 2 CTAs per SM: <= 6 stages each
+        const int smem = (two ? 6 : kMaxStages) * kStageBytes + 1024;
+        CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (int mode = 0; mode < 4; ++mode)
+            for (int nst : {4, 8, 12}) {
+                if (two && nst > 6) nst = (mode == 2 ? 4 : 6);
+                std::vector<float> ts;
+                for (int it = 0; it < 7; ++it) {
+                    CK(cudaMemset(flush, it, 512u << 20));
+                    cudaEvent_t e0, e1;
+                    cudaEventCreate(&e0);
+                    cudaEventCreate(&e1);
+                    cudaEventRecord(e0);
+                    stream_kernel<<<grid, 64, smem>>>(tA, tB, tC, tD, mode, nst);
+                    cudaEventRecord(e1);
+                    CK(cudaEventSynchronize(e1));
+                    float ms;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    ts.push_back(ms * 1000.f);
+                }
+                std::sort(ts.begin(), ts.end());
+                const float us = ts[3];
+                const double bytes = (double)rows * 4096 * 2;
+                printf("grid %3d  %-22s stages %2d: %7.1f us  %6.0f GB/s chip  %5.1f GB/s per CTA\n", grid, names[mode], nst,
+                       us, bytes / us / 1e3, bytes / grid / us / 1e3);
+            }
+        CK(cudaFree(x));
+    }
+    return 0;
+}
