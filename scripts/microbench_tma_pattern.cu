@@ -35,7 +35,7 @@ constexpr int kMaxStages = 12;
 
 __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                                        const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
-                                                       int mode, int nst) {
+                                                       int mode, int nst, int nk = 64) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const uint32_t base = (su32(sm) + 1023u) & ~1023u;
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
@@ -76,18 +76,18 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
         } else {
             int s = 0;
             uint32_t ph = 0;
-            for (int kc = 0; kc < 64; ++kc) {
+            for (int kc = 0; kc < nk; ++kc) {
                 wait(su32(&empty[s]), ph ^ 1u);
                 arrive_tx(su32(&full[s]), kStageBytes);
                 if (mode == 0) tma2d(base + s * kStageBytes, &tmA, kc * 64, row0, su32(&full[s]));
-                else tma2d(base + s * kStageBytes, &tmB, 0, blockIdx.x * 8192 + kc * 128, su32(&full[s]));
+                else tma2d(base + s * kStageBytes, &tmB, 0, blockIdx.x * 128 * nk + kc * 128, su32(&full[s]));
                 if (++s == nst) { s = 0; ph ^= 1u; }
             }
         }
     } else if (tid == 32) {
         int s = 0;
         uint32_t ph = 0;
-        for (int kc = 0; kc < 64; ++kc) {
+        for (int kc = 0; kc < nk; ++kc) {
             wait(su32(&full[s]), ph);
             arrive(su32(&empty[s]));
             if (++s == nst) { s = 0; ph ^= 1u; }
@@ -156,6 +156,40 @@ int main() {
                 printf("grid %3d  %-22s stages %2d: %7.1f us  %6.0f GB/s chip  %5.1f GB/s per CTA\n", grid, names[mode], nst,
                        us, bytes / us / 1e3, bytes / grid / us / 1e3);
             }
+        CK(cudaFree(x));
+    }
+    // equal bytes (sms x 2 MB, contiguous 16-KB boxes): one CTA per SM streaming 2 MB vs two CTAs
+    // per SM streaming 1 MB each
+    {
+        const uint64_t rows = (uint64_t)sms * 256;
+        void* x;
+        CK(cudaMalloc(&x, rows * 4096 * 2));
+        CK(cudaMemset(x, 1, rows * 4096 * 2));
+        CUtensorMap tB;
+        if (make(&tB, x, 64, rows * 64, 128)) { printf("tensor map failed\n"); return 1; }
+        for (int two = 0; two < 2; ++two) {
+            const int grid = two ? 2 * sms : sms, nst = two ? 6 : 12, nk = two ? 64 : 128;
+            const int smem = nst * kStageBytes + 1024;
+            CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            std::vector<float> ts;
+            for (int it = 0; it < 7; ++it) {
+                CK(cudaMemset(flush, it, 512u << 20));
+                cudaEvent_t e0, e1;
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                stream_kernel<<<grid, 64, smem>>>(tB, tB, tB, tB, 1, nst, nk);
+                cudaEventRecord(e1);
+                CK(cudaEventSynchronize(e1));
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                ts.push_back(ms * 1000.f);
+            }
+            std::sort(ts.begin(), ts.end());
+            const double bytes = (double)rows * 4096 * 2;
+            printf("equal bytes %.0f MB: %s: %7.1f us  %6.0f GB/s chip\n", bytes / 1e6,
+                   two ? "2 CTAs/SM x 1 MB, 6 stages " : "1 CTA/SM x 2 MB, 12 stages", ts[3], bytes / ts[3] / 1e3);
+        }
         CK(cudaFree(x));
     }
     return 0;
