@@ -198,7 +198,8 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
  *   Every token takes the decode kernels (the tcgen05 prefill path fuses shrink and expand).
  * lora_apply_expand -- y[:, this rank's H_out slice] += s · (Σ v) · B_shard for the batch of the
  *   immediately preceding lora_apply_shrink on this pool, reading the (all-reduced) v_in.
- * Errors: as lora_apply; ARG if v_capacity is too small or expand has no pending shrink.
+ * Errors: as lora_apply; ARG if v_capacity is too small or expand has no pending shrink; ALIGN if
+ *   v_out / v_in is not 4-byte aligned.
  */
 lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_indptr, const int32_t* adapter_ids,
                               int num_segments, float* v_out, int64_t v_capacity, void* stream);

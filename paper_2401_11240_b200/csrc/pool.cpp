@@ -377,6 +377,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if (xs < ys + yb && ys < xs + xb) return fail(LORA_ERR_ARG, "x and y overlap");
     }
     if (mode != 0 && !v_ext) return fail(LORA_ERR_ARG, "v buffer is NULL");
+    if (mode != 0 && ((uintptr_t)v_ext & 3)) return fail(LORA_ERR_ALIGN, "v buffer must be 4-byte aligned");
     DeviceGuard g(p->device);
     cudaStream_t st = (cudaStream_t)stream_ptr;
     {

@@ -328,6 +328,33 @@ def test_unknown_adapter_on_apply_has_no_side_effect(L):
     pool.close()
 
 
+def test_misaligned_pointers_rejected_without_side_effects(L):
+    """x / y not 16-B aligned and a TP v buffer not 4-B aligned are refused (LORA_ERR_ALIGN) before
+    any launch: y is unchanged, no CUDA error is left pending, and the next valid apply is exact."""
+    import torch
+    b = gen.config_c2(y_zero=False)
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    y = to_torch(b.y_in, "cuda")
+    v = torch.zeros(1 << 20, dtype=torch.float32, device="cuda")
+    cases = [
+        lambda: pool.apply(x.data_ptr() + 2, y, b.seg_indptr, b.adapter_ids),
+        lambda: pool.apply(x, y.data_ptr() + 8, b.seg_indptr, b.adapter_ids),
+        lambda: pool.apply_shrink(x, b.seg_indptr, b.adapter_ids, v.data_ptr() + 2),
+    ]
+    for fn in cases:
+        with pytest.raises(L.LoraError) as ei:
+            fn()
+        assert ei.value.name == "LORA_ERR_ALIGN", str(ei.value)
+    torch.cuda.synchronize()
+    assert np.array_equal(from_torch(y, "bf16"), b.y_in)
+    pool.apply(x, y, b.seg_indptr, b.adapter_ids)
+    torch.cuda.synchronize()
+    ref = O.delta_for_batch(b, n_threads=8)
+    assert rel_l2(from_torch(y, "bf16"), ref, "bf16") <= TOL["bf16"]
+    pool.close()
+
+
 def test_apply_multi_qkv_fused_equals_separate(L):
     """lora_apply_multi over 3 pools (q, k, v of one layer; k/v with GQA-like narrower output) in
     one launch pair == three separate lora_apply calls, bit for bit, and within tolerance of the oracle."""
