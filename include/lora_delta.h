@@ -162,8 +162,14 @@ lora_status lora_adapter_ready(lora_pool* p, int32_t id, int* ready);
  * Builds the canonical metadata on the host, makes `stream` wait for any adapter whose
  * load is still in flight, and launches the decode (SIMT) and prefill (tcgen05) kernels on
  * `stream`.  Never synchronises the host.  seg_indptr/adapter_ids are consumed before
- * return.  T = 0 or num_segments = 0 is a no-op.  Graph capture of `stream` is supported.
- * Errors: ARG, ALIGN, UNKNOWN_ADAPTER, UNSUPPORTED (host-only pool), CUDA.
+ * return.  T = 0 or num_segments = 0 is a no-op.  Graph capture of `stream` is supported: inside
+ * a capture nothing is allocated, synchronised or queried, and loads still in flight become
+ * external event waits.  A batch that needs more scratch than the pool holds is refused there
+ * (UNSUPPORTED, the capture stays valid): run that batch shape once outside the capture, or pre-size
+ * with LORA_OPT_RESERVE_TOKENS.  Outgrown scratch is kept until lora_pool_destroy, so graphs captured
+ * earlier stay valid when a later apply grows it.  The pool's scratch is shared by its applies: one
+ * pool serves one stream (or graph) at a time.
+ * Errors: ARG, ALIGN, UNKNOWN_ADAPTER, UNSUPPORTED (host-only pool; scratch growth during capture), CUDA.
  */
 lora_status lora_apply(lora_pool* p, const void* x, void* y,
                        const int32_t* seg_indptr, const int32_t* adapter_ids,

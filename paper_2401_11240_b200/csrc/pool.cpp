@@ -65,6 +65,8 @@ struct lora_pool {
     int64_t launches = 0;
     bool split_ready = false;             // a lora_apply_shrink awaits its lora_apply_expand
     unsigned long long* trace = nullptr;   // lora_debug_set_trace
+    bool capturing = false;               // the current apply's stream is being captured into a graph
+    std::vector<void*> retired;           // outgrown scratch buffers: a captured graph may still use them
 };
 
 namespace {
@@ -105,21 +107,45 @@ bool is_pinned(const void* p, const void** dev_ptr = nullptr) {
 
 // grow a device buffer (rare; synchronises the device so no in-flight kernel uses the old one)
 template <typename T>
-lora_status grow(T*& buf, size_t& cap, size_t need, bool zero, const char* what) {
+lora_status grow(lora_pool* p, T*& buf, size_t& cap, size_t need, bool zero, const char* what) {
     if (need <= cap) return LORA_OK;
+    // no allocation, synchronisation or free inside a capture: that would invalidate the caller's graph
+    if (p->capturing)
+        return fail(LORA_ERR_UNSUPPORTED, std::string(what) +
+                                              " scratch must grow inside a CUDA graph capture: run this batch shape "
+                                              "once outside the capture, or pre-size it with LORA_OPT_RESERVE_TOKENS");
     size_t n = std::max(need, cap * 2);
-    if (buf) {
-        CUDA_TRY(cudaDeviceSynchronize(), what);
-        CUDA_TRY(cudaFree(buf), what);
-        buf = nullptr;
-        cap = 0;
-    }
-    CUDA_TRY(cudaMalloc((void**)&buf, n * sizeof(T)), what);
+    T* nb = nullptr;
+    CUDA_TRY(cudaMalloc((void**)&nb, n * sizeof(T)), what);
     if (zero) {
-        CUDA_TRY(cudaMemset(buf, 0, n * sizeof(T)), what);
+        CUDA_TRY(cudaMemset(nb, 0, n * sizeof(T)), what);
         CUDA_TRY(cudaDeviceSynchronize(), what);
     }
+    // the old buffer is not freed: in-flight kernels and graphs captured earlier keep its address
+    // (freed with the pool; geometric growth bounds the total at twice the final size)
+    if (buf) p->retired.push_back(buf);
+    buf = nb;
     cap = n;
+    return LORA_OK;
+}
+
+// order `st` after an adapter's cold-start load.  While `st` is being captured no event may be
+// queried (cudaEventQuery invalidates a capture), so the wait becomes an external event-wait node
+// (a no-op at replay once the load has completed).
+lora_status wait_loaded(AdapterRec& a, cudaStream_t st, bool capturing, const char* what) {
+    if (a.ready_known) return LORA_OK;
+    if (capturing) {
+        CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a.ready, cudaEventWaitExternal), what);
+        return LORA_OK;
+    }
+    cudaError_t e = cudaEventQuery((cudaEvent_t)a.ready);
+    if (e == cudaSuccess) {
+        a.ready_known = true;
+        return LORA_OK;
+    }
+    if (e != cudaErrorNotReady) return cuda_fail(e, what);
+    cudaGetLastError();
+    CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a.ready, 0), what);
     return LORA_OK;
 }
 
@@ -207,6 +233,7 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->pf_scratch) cudaFree(p->pf_scratch);
         if (p->gc_sync) cudaFree(p->gc_sync);
         if (p->meta_dev) cudaFree(p->meta_dev);
+        for (void* b : p->retired) cudaFree(b);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
         if (p->side) cudaStreamDestroy(p->side);
     }
@@ -403,23 +430,16 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     // order after in-flight loads of the adapters this batch reads
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply: capture query");
-    for (int gi = 0; gi < pl.G; ++gi) {
-        AdapterRec& a = p->table.at(pl.group_id[gi]);
-        if (a.ready_known) continue;
-        cudaError_t e = cudaEventQuery((cudaEvent_t)a.ready);
-        if (e == cudaSuccess) { a.ready_known = true; continue; }
-        if (e != cudaErrorNotReady) return cuda_fail(e, "lora_apply: load event");
-        cudaGetLastError();
-        CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a.ready,
-                                     cap == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0),
-                 "lora_apply: wait load");
-    }
+    p->capturing = cap != cudaStreamCaptureStatusNone;
+    for (int gi = 0; gi < pl.G; ++gi)
+        if ((s = wait_loaded(p->table.at(pl.group_id[gi]), st, p->capturing, "lora_apply: wait load")) != LORA_OK)
+            return s;
     // scratch
     if (pl.n_gc > 0 && mode == 0) {
-        if ((s = grow(p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
+        if ((s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
     }
     if (pl.n_gc > 0 && mode != 2) {
-        if ((s = grow(p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
+        if ((s = grow(p, p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
     }
     int launches = 0;
     bool span = false;
@@ -438,7 +458,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: span decode kernel launch");
     }
     const bool fused = !span && mode == 0 && p->fused_decode && p->esz == 2 && pl.n_gc > 0;
-    if (fused && (s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync")) != LORA_OK) return s;
+    if (fused && (s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync")) != LORA_OK) return s;
     if (pl.n_gc > 0 && !span) {
         DecodeLaunch L{x, y, p->dA, p->dB, mode == 0 ? p->vbuf : v_ext, p->meta_dev, p->trace, p->H_in, p->H_out,
                        p->esz, p->num_sms};
@@ -452,7 +472,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     }
     if (pl.n_pf_tiles > 0 && mode == 0) {
         if (pl.pf_cs > 1 &&
-            (s = grow(p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
+            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
             return s;
         PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
         L.pscratch = p->pf_scratch;
@@ -513,19 +533,13 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     if (s != LORA_OK) return fail(s, err);
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply_multi: capture query");
+    for (int i = 0; i < n_pools; ++i) pools[i]->capturing = cap != cudaStreamCaptureStatusNone;
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
-        for (int gi = 0; gi < p->plan.G; ++gi) {
-            AdapterRec& a = p->table.at(p->plan.group_id[gi]);
-            if (a.ready_known) continue;
-            cudaError_t e = cudaEventQuery((cudaEvent_t)a.ready);
-            if (e == cudaSuccess) { a.ready_known = true; continue; }
-            if (e != cudaErrorNotReady) return cuda_fail(e, "lora_apply_multi: load event");
-            cudaGetLastError();
-            CUDA_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)a.ready,
-                                         cap == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0),
-                     "lora_apply_multi: wait load");
-        }
+        for (int gi = 0; gi < p->plan.G; ++gi)
+            if ((s = wait_loaded(p->table.at(p->plan.group_id[gi]), st, cap != cudaStreamCaptureStatusNone,
+                                 "lora_apply_multi: wait load")) != LORA_OK)
+                return s;
     }
     Plan& fz = p0->fused;
     int launches = 0;
@@ -551,13 +565,13 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: span decode kernel launch");
     }
     if (fz.n_gc > 0 && !span) {
-        if ((s = grow(p0->vbuf, p0->vbuf_cap, (size_t)std::max<int64_t>(fz.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
-        if ((s = grow(p0->meta_dev, p0->meta_cap, fz.blob.size(), false, "meta")) != LORA_OK) return s;
+        if ((s = grow(p0, p0->vbuf, p0->vbuf_cap, (size_t)std::max<int64_t>(fz.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
+        if ((s = grow(p0, p0->meta_dev, p0->meta_cap, fz.blob.size(), false, "meta")) != LORA_OK) return s;
         DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
                        p0->num_sms};
         L.n_jobs = n_pools;
         if (p0->fused_decode && p0->esz == 2) {
-            if ((s = grow(p0->gc_sync, p0->gc_sync_cap, (size_t)(1 + 2 * fz.n_gc), true, "gc_sync")) != LORA_OK) return s;
+            if ((s = grow(p0, p0->gc_sync, p0->gc_sync_cap, (size_t)(1 + 2 * fz.n_gc), true, "gc_sync")) != LORA_OK) return s;
             L.phases |= p0->fused_decode == 2 ? 8 : 4;
             L.gc_sync = p0->gc_sync + 1;
         }
@@ -570,7 +584,7 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         lora_pool* p = pools[i];
         if (p->plan.n_pf_tiles == 0) continue;
         if (p->plan.pf_cs > 1 &&
-            (s = grow(p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * 128, false, "pf_scratch")) !=
+            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * 128, false, "pf_scratch")) !=
                 LORA_OK)
             return s;
         PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
@@ -606,11 +620,12 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             if (value < 0) return fail(LORA_ERR_ARG, "reserve must be >= 0");
             if (p->host_only) return LORA_OK;
             DeviceGuard g(p->device);
+            p->capturing = false;   // a host call, not stream-ordered
             const int64_t ks = ksplit_of(p->H_in, p->esz);
-            lora_status s = grow(p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(1, value * ks * LORA_MAX_RANK), false, "vbuf");
+            lora_status s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(1, value * ks * LORA_MAX_RANK), false, "vbuf");
             if (s == LORA_OK)
-                s = grow(p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
-            if (s == LORA_OK) s = grow(p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
+                s = grow(p, p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
+            if (s == LORA_OK) s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
             return s;
         }
         case LORA_OPT_LOAD_KERNEL:

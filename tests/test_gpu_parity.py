@@ -274,6 +274,46 @@ def test_cuda_graph_capture_replay(L):
     pool.close()
 
 
+def test_graph_capture_scratch_growth(L):
+    """Scratch growth and CUDA graphs: an apply that would have to grow the pool's scratch inside a
+    capture is refused (LORA_ERR_UNSUPPORTED, nothing allocated or synchronised, so the caller's
+    capture stays valid); a graph captured before an eager apply grew the scratch still replays
+    exactly (outgrown buffers are retired, not freed)."""
+    import torch
+    big = gen.config_c2(T=256, y_zero=False)
+    small = gen.config_c2(T=16, y_zero=False, tag=3)
+    used = set(int(a) for a in small.adapter_ids)
+    small.adapters = [a for a in big.adapters if a.id in used]   # the pool holds big's adapters
+    pool = make_pool(big, L)
+    s = torch.cuda.Stream()
+    xs, ys = to_torch(small.x, "cuda"), to_torch(small.y_in, "cuda")
+    xb, yb = to_torch(big.x, "cuda"), to_torch(big.y_in, "cuda")
+    y0s, y0b = ys.clone(), yb.clone()
+    with torch.cuda.stream(s):
+        pool.apply(xs, ys, small.seg_indptr, small.adapter_ids, stream=s)   # sizes scratch for 16 tokens
+    torch.cuda.synchronize()
+    g1 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1, stream=s):
+        pool.apply(xs, ys, small.seg_indptr, small.adapter_ids, stream=s)
+    g2 = torch.cuda.CUDAGraph()
+    with pytest.raises(L.LoraError) as ei:
+        with torch.cuda.graph(g2, stream=s):
+            pool.apply(xb, yb, big.seg_indptr, big.adapter_ids, stream=s)
+    assert ei.value.name == "LORA_ERR_UNSUPPORTED" and "capture" in str(ei.value)
+    torch.cuda.synchronize()
+    yb.copy_(y0b)
+    with torch.cuda.stream(s):
+        pool.apply(xb, yb, big.seg_indptr, big.adapter_ids, stream=s)       # grows the scratch
+    torch.cuda.synchronize()
+    assert rel_l2(from_torch(yb, "bf16"), O.delta_for_batch(big, n_threads=8), "bf16") <= TOL["bf16"]
+    ys.copy_(y0s)
+    with torch.cuda.stream(s):
+        g1.replay()                                                            # captured before the growth
+    torch.cuda.synchronize()
+    assert rel_l2(from_torch(ys, "bf16"), O.delta_for_batch(small, n_threads=8), "bf16") <= TOL["bf16"]
+    pool.close()
+
+
 def test_async_load_then_apply_orders_on_event(L):
     """lora_load_adapter returns before the copy lands; an apply issued right after must see
     the adapter (the stream waits on the load's ready event)."""
