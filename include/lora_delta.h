@@ -211,6 +211,26 @@ lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_in
                               int num_segments, float* v_out, int64_t v_capacity, void* stream);
 lora_status lora_apply_expand(lora_pool* p, void* y, const float* v_in, void* stream);
 
+/* lora_apply_fused_base -- the delta fused into the base projection GEMM (
+ * PAPER.md §4.1 P:548-550 "incorporate the operators of GPU LoRA computation into the base LLM
+ * inference process"; Eq. 1 P:276-280 with the adapter scale):
+ *     y_t = x_t · W + s_a · (x_t · A_a) · B_a      (id < 0: y_t = x_t · W)
+ * in one tcgen05 kernel: every K stage's x tile feeds both x·W and x·A; V = s·(x·A) is rounded once
+ * to bf16 and its expand accumulates into the base accumulator in TMEM; y is written once (never
+ * read).  fp32 accumulation, one bf16 rounding of y.
+ *   x    device [T][hidden_in] bf16, 16-B aligned.
+ *   W    device [hidden_in][hidden_out] bf16 row-major (the base projection), 16-B aligned; not owned.
+ *   y    device [T][hidden_out] bf16, 16-B aligned, OVERWRITTEN (not accumulated); must not overlap
+ *        x or W.
+ *   seg_indptr / adapter_ids / num_segments / stream: as lora_apply.  Every segment's tokens are
+ *   covered by 128-token tiles of that segment (short segments waste tile rows: this path is for
+ *   prefill batches).
+ * Errors: ARG, ALIGN, UNKNOWN_ADAPTER, CUDA; UNSUPPORTED for an fp32 pool, hidden_in % 64 != 0,
+ * hidden_out % 128 != 0, an adapter of rank > 128, or a batch whose tile records and page lists
+ * exceed the 7,680-word parameter blob of one launch. */
+lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, void* y, const int32_t* seg_indptr,
+                                  const int32_t* adapter_ids, int num_segments, void* stream);
+
 /* lora_plan -- build (and keep for lora_debug_metadata) the canonical metadata of a batch
  * without launching anything.  Pure host code; works on host-only pools. */
 lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* adapter_ids,

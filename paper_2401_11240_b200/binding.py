@@ -93,6 +93,7 @@ def _load() -> ctypes.CDLL:
         "lora_apply_shrink": [vp, vp, vp, vp, c_int, vp, c_i64, vp],
         "lora_apply_multi": [P(vp), P(vp), P(vp), c_int, vp, vp, c_int, vp],
         "lora_apply_expand": [vp, vp, vp, vp],
+        "lora_apply_fused_base": [vp, vp, vp, vp, vp, vp, c_int, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -226,6 +227,13 @@ class LoraPool:
 
     def apply_expand(self, y, v_in, stream=None) -> None:
         _check(LIB.lora_apply_expand(self.handle, _ptr_of(y), _ptr_of(v_in), _stream_ptr(stream)))
+
+    def apply_fused_base(self, x, W, y, seg_indptr, adapter_ids, stream=None) -> None:
+        """y = x·W + s·(x·A)·B in one kernel (lora_apply_fused_base): W [H_in][H_out] bf16, y
+        overwritten."""
+        ip, ids = _i32(seg_indptr), _i32(adapter_ids)
+        _check(LIB.lora_apply_fused_base(self.handle, _ptr_of(x), _ptr_of(W), _ptr_of(y), _addr(ip), _addr(ids),
+                                         int(ids.shape[0]), _stream_ptr(stream)))
 
     def plan(self, seg_indptr, adapter_ids) -> None:
         ip, ids = _i32(seg_indptr), _i32(adapter_ids)

@@ -1,0 +1,336 @@
+// fused_base_kernel.cu -- SURVEY §8(f) NEXT row 2: the LoRA delta fused into the base projection
+// GEMM (§4.1: "incorporate the operators of GPU LoRA computation into the base
+// LLM inference process"; Eq. 1: y = x·W + x·A·B, with the per-adapter scale s).
+//
+// One CTA per (128-token tile of one segment, 128-column tile of y):
+//     D_base[t][n]  = Σ_k X[t][k] · W[k][n]          base GEMM, TMEM columns [0, 128)
+//     D1[t][j]      = Σ_k X[t][k] · A_g[k][j]        shrink,    TMEM columns [128, 128 + r16)
+//     D_base[t][n] += Σ_j bf16(s_g·D1[t][j]) · B_g[j][n]   expand into the base accumulator
+//     y[t][n]       = bf16(D_base[t][n])             one rounding, y written once
+// Each K stage's x chunk feeds both the base MMA and the shrink MMA, so x is read once for both
+// and y is never read: the separate delta pass's y read + write disappear.
+// First version: the shrink is recomputed per column tile (r16/128 extra MMA work), tiles never
+// span segments, and rank <= 128 (the N2 limits).  Layouts are N2's (prefill_kernel.cu): x box
+// {64,128} SW128 K-major, A / B rank rows gathered from the paged pool with tile::gather4, B and
+// W tiles MN-major SW128 atoms (8 K-rows x 64 columns), V K-major SW128.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
+#include "kernel_config.h"
+#include "plan.h"
+
+namespace lora {
+
+constexpr int kFbThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
+constexpr int kFbStages = 3;
+constexpr int kFbStageBytes = 49152;   // X chunk 16 KB + W chunk 16 KB + A chunk <= 16 KB
+constexpr int kFbVBytes = 32768;       // V: 128 tokens x r16 <= 128, bf16, K-major SW128
+constexpr int kFbBBytes = 32768;       // B tile: r16 <= 128 rank rows x 128 columns, MN-major SW128
+constexpr int kFbSmem = 1024 + kFbStages * kFbStageBytes + kFbVBytes + kFbBBytes + 256;
+constexpr int kFbTileWords = 8;
+static_assert(kFbSmem <= 227 * 1024, "shared memory");
+
+struct FusedBaseArgs {
+    CUtensorMap tm_x;   // x [T][H_in], box {64, 128}
+    CUtensorMap tm_w;   // W [H_in][H_out], box {64, 64}
+    CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1} (gather4)
+    CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1} (gather4)
+    char* y;
+    int H_in, H_out, zero_page;
+};
+
+struct FbBlob {
+    int32_t w[kFusedBaseMaxWords];   // [n_tiles][8] {tok0, nvalid, rank, page_off, scale_bits}, then pages
+};
+
+namespace {
+__device__ __forceinline__ uint32_t fb_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void fb_bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fb_arrive_tx(uint32_t bar, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void fb_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fb_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_FBW:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LAB_FBW;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fb_tma_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tm), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void fb_gather4(uint32_t dst, const CUtensorMap* tm, int col, int r0, int r1, int r2, int r3,
+                                           uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5, %6}], [%7];" ::"r"(dst),
+        "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1 (sm_100)
+__device__ __forceinline__ uint64_t fb_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor: D fp32, A/B bf16, M=128, N=n, B K-major (0) or MN-major (1)
+__device__ __forceinline__ uint32_t fb_idesc(int n, int b_mn_major) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void fb_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void fb_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fb_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fb_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fb_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kFbThreads, 1)
+    lora_fused_base_kernel(const __grid_constant__ FusedBaseArgs a, const __grid_constant__ FbBlob blob) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = fb_smem(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* gbase = smem_raw + (base - raw);
+    const uint32_t ring = base;
+    const uint32_t vbuf = base + kFbStages * kFbStageBytes;
+    uint8_t* gv = gbase + (vbuf - base);
+    const uint32_t bbuf = vbuf + kFbVBytes;
+    const uint32_t bars = bbuf + kFbBBytes;
+    auto full = [&](int s) { return bars + 8u * s; };
+    auto empty = [&](int s) { return bars + 8u * (kFbStages + s); };
+    const uint32_t d_full = bars + 8u * (2 * kFbStages);
+    const uint32_t v_ready = d_full + 8u;
+    const uint32_t b_full = d_full + 16u;
+    const uint32_t d2_full = d_full + 24u;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (d_full + 32u - base));
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int32_t* rec = blob.w + blockIdx.x * kFbTileWords;
+    const int tok0 = rec[0], nvalid = rec[1], r = rec[2], poff = rec[3];
+    const float scale = __int_as_float(rec[4]);
+    const int rp = r > 0 ? (r + 15) & ~15 : 0;
+    const int n0 = blockIdx.y * 128;
+    const int nkc = a.H_in / 64;
+
+    if (tid == 0) {
+        for (int s = 0; s < kFbStages; ++s) {
+            fb_bar_init(full(s), 1);
+            fb_bar_init(empty(s), 1);
+        }
+        fb_bar_init(d_full, 1);
+        fb_bar_init(v_ready, 128);
+        fb_bar_init(b_full, 1);
+        fb_bar_init(d2_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {   // TMEM: D_base at columns [0,128), D1 at [128,256)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(fb_smem(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fb_fence_before();
+    __syncthreads();
+    fb_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        const int ngr = rp / 4;
+        int pg[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = lane * 4 + q;
+            pg[q] = j < r ? blob.w[poff + j] : a.zero_page;
+        }
+        if (r > 0) {   // the expand's B tile up front (its own buffer)
+            if (lane == 0) fb_arrive_tx(b_full, (uint32_t)(rp * 128 * 2));
+            __syncwarp();
+            if (lane < ngr)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t dst = bbuf + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
+                    fb_gather4(dst, &a.tm_b, n0 + h * 64, pg[0], pg[1], pg[2], pg[3], b_full);
+                }
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kc = 0; kc < nkc; ++kc) {
+            fb_wait(empty(stage), phase ^ 1u);
+            const uint32_t sb = ring + stage * kFbStageBytes;
+            if (lane == 0) {
+                fb_arrive_tx(full(stage), (uint32_t)(16384 + 16384 + rp * 128));
+                fb_tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
+                // W rows [64kc, 64kc+64) x columns [n0, n0+128): two MN-major atom columns of 8 KB
+                fb_tma_2d(sb + 16384, &a.tm_w, n0, kc * 64, full(stage));
+                fb_tma_2d(sb + 16384 + 8192, &a.tm_w, n0 + 64, kc * 64, full(stage));
+            }
+            __syncwarp();
+            if (lane < ngr)
+                fb_gather4(sb + 32768 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
+            if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        const uint32_t id_base = fb_idesc(128, 1);
+        const uint32_t id1 = rp > 0 ? fb_idesc(rp, 0) : 0u;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kc = 0; kc < nkc; ++kc) {
+            fb_wait(full(stage), phase);
+            fb_fence_after();
+            if (lane == 0) {
+                const uint32_t sb = ring + stage * kFbStageBytes;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t xd = fb_desc(sb + kk * 32, 16, 1024);
+                    fb_mma(tmem, xd, fb_desc(sb + 16384 + kk * 2048, 8192, 1024), id_base, (kc | kk) != 0);
+                    if (rp > 0) fb_mma(tmem + 128u, xd, fb_desc(sb + 32768 + kk * 32, 16, 1024), id1, (kc | kk) != 0);
+                }
+                fb_commit(empty(stage));
+                if (kc == nkc - 1) fb_commit(d_full);
+            }
+            __syncwarp();
+            if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
+        }
+        if (rp > 0) {
+            fb_wait(v_ready, 0);
+            fb_wait(b_full, 0);
+            fb_fence_after();
+            if (lane == 0) {
+                const uint32_t lbo = (uint32_t)(rp / 8) * 1024u;
+                for (int ks = 0; ks < rp / 16; ++ks) {
+                    const uint32_t voff = (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u;
+                    fb_mma(tmem, fb_desc(vbuf + voff, 16, 1024), fb_desc(bbuf + (uint32_t)ks * 2048u, lbo, 1024), id_base, 1u);
+                }
+            }
+        }
+        if (lane == 0) fb_commit(d2_full);
+        __syncwarp();
+    } else {
+        // ===================== epilogue: warps 2..5 -> TMEM lanes 32*(warp%4) .. +32 =====================
+        const int sub = warp & 3;
+        const int row = sub * 32 + lane;
+        const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
+        if (rp > 0) {
+            // V = s · D1 -> bf16, K-major SW128 (atom kk = columns [64kk, 64kk+64)); columns >= r are 0
+            fb_wait(d_full, 0);
+            fb_fence_after();
+            for (int c0 = 0; c0 < rp; c0 += 32) {
+                float v[32];
+                fb_ld32(tmem + lane_addr + 128u + (uint32_t)c0, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t hw[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int j0 = c0 + q * 8 + 2 * e;
+                        const float f0 = j0 < r ? v[q * 8 + 2 * e] * scale : 0.f;
+                        const float f1 = j0 + 1 < r ? v[q * 8 + 2 * e + 1] * scale : 0.f;
+                        __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+                        hw[e] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    const int col = c0 + q * 8;
+                    const int kk = col >> 6, chunk = (col & 63) >> 3;
+                    const uint32_t off = (uint32_t)kk * 16384u + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
+                                         (uint32_t)((chunk ^ (row & 7)) * 16);
+                    *reinterpret_cast<uint4*>(gv + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
+            fb_fence_before();
+            fb_arrive(v_ready);
+        }
+        // y[tok0 + row][n0 .. n0+128) = bf16(D_base): valid rows only (rows past the segment belong
+        // to other tiles)
+        fb_wait(d2_full, 0);
+        fb_fence_after();
+        char* yrow = a.y + ((size_t)(tok0 + row) * a.H_out + n0) * 2;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+            float d[32];
+            fb_ld32(tmem + lane_addr + (uint32_t)c0, d);
+            if (row < nvalid) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 hb = __floats2bfloat162_rn(d[q * 8 + 2 * e], d[q * 8 + 2 * e + 1]);
+                        o[e] = *reinterpret_cast<uint32_t*>(&hb);
+                    }
+                    *reinterpret_cast<uint4*>(yrow + (c0 + q * 8) * 2) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+            }
+        }
+    }
+    fb_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fb_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
+}
+
+int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);   // prefill_kernel.cu
+
+int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_tiles, lora_cuda_stream st) {
+    if (n_words > kFusedBaseMaxWords || n_tiles <= 0) return (int)cudaErrorInvalidValue;
+    FusedBaseArgs a;
+    std::memset(&a, 0, sizeof(a));
+    int e = make_tmap_bf16(&a.tm_x, L.x, L.T, L.H_in, 128);
+    if (!e) e = make_tmap_bf16(&a.tm_w, L.w, L.H_in, L.H_out, 64);
+    if (e) return e;
+    std::memcpy(&a.tm_a, L.tm_a, sizeof(CUtensorMap));
+    std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
+    a.y = static_cast<char*>(L.y);
+    a.H_in = L.H_in;
+    a.H_out = L.H_out;
+    a.zero_page = L.zero_page;
+    FbBlob blob;   // the kernel-parameter blob (copied into the launch)
+    std::memcpy(blob.w, words, (size_t)n_words * 4);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t ce = cudaFuncSetAttribute(lora_fused_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFbSmem);
+        if (ce != cudaSuccess) return (int)ce;
+        configured = true;
+    }
+    lora_fused_base_kernel<<<dim3(n_tiles, L.H_out / 128), kFbThreads, kFbSmem, st>>>(a, blob);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace lora

@@ -162,6 +162,18 @@ int span_max_blob_words();
 // writes the 2 * kSpanBoxKinds CUtensorMaps (128 B each) of a bf16 pool to host_out; 0 on success
 int span_make_tmaps(void* host_out, const void* dA, const void* dB, int n_rows, int H_in, int H_out);
 int launch_prefill(const Plan& pl, const PrefillLaunch& L, lora_cuda_stream st, int* launches);
+
+// NEXT f2: the delta fused into the base projection GEMM (fused_base_kernel.cu)
+constexpr int kFusedBaseMaxWords = 7680;   // parameter blob: [tiles][8] records + page lists
+struct FusedBaseLaunch {
+    const void* x;      // [T][H_in] bf16
+    const void* w;      // [H_in][H_out] bf16 (the base projection)
+    void* y;            // [T][H_out] bf16, written
+    const void* tm_a;   // the pool's gather4 maps
+    const void* tm_b;
+    int T, H_in, H_out, zero_page;
+};
+int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_tiles, lora_cuda_stream st);
 bool prefill_supported(int H_in, int H_out, int esz);
 int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);
 constexpr int kPfMaxRank = 128;        // tensor-core prefill path handles ranks up to this

@@ -609,6 +609,94 @@ lora_status lora_apply_expand(lora_pool* p, void* y, const float* v_in, void* st
     return apply_impl(p, nullptr, y, nullptr, nullptr, 0, stream, 2, const_cast<float*>(v_in), 0);
 }
 
+lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, void* y, const int32_t* seg_indptr,
+                                  const int32_t* adapter_ids, int num_segments, void* stream) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "apply on a host-only pool");
+    if (p->esz != 2 || !p->tc_prefill || p->H_in % 64 || p->H_out % 128)
+        return fail(LORA_ERR_UNSUPPORTED,
+                    "the fused base GEMM needs a bf16 pool with hidden_in % 64 == 0 and hidden_out % 128 == 0");
+    if (num_segments < 0) return fail(LORA_ERR_ARG, "num_segments < 0");
+    if (num_segments == 0) return LORA_OK;
+    if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
+    std::string err;
+    lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
+                               false, p->table, err);   // validates the CSR and the ids (canonical metadata)
+    if (s != LORA_OK) return fail(s, err);
+    const int T = seg_indptr[num_segments];
+    if (T == 0) return LORA_OK;
+    if (!x || !W || !y) return fail(LORA_ERR_ARG, "x/W/y is NULL");
+    if (((uintptr_t)x & 15) || ((uintptr_t)W & 15) || ((uintptr_t)y & 15))
+        return fail(LORA_ERR_ALIGN, "x, W and y must be 16-byte aligned");
+    {
+        const char *xs = (const char*)x, *ws = (const char*)W, *ys = (const char*)y;
+        const size_t xb = (size_t)T * p->H_in * 2, wb = (size_t)p->H_in * p->H_out * 2, yb = (size_t)T * p->H_out * 2;
+        if ((xs < ys + yb && ys < xs + xb) || (ws < ys + yb && ys < ws + wb)) return fail(LORA_ERR_ARG, "y overlaps x or W");
+    }
+    // parameter blob: [tiles][8] {tok0, nvalid, rank, page_off, scale_bits, 0, 0, 0}, then each used
+    // adapter's pages once; segments with id < 0 get base-only tiles (rank 0)
+    int n_tiles = 0;
+    for (int i = 0; i < num_segments; ++i) n_tiles += (seg_indptr[i + 1] - seg_indptr[i] + 127) / 128;
+    static thread_local std::vector<int32_t> words;
+    static thread_local std::vector<std::pair<int32_t, int32_t>> offs;   // (id, page offset)
+    words.assign((size_t)n_tiles * 8, 0);
+    offs.clear();
+    int tix = 0;
+    for (int i = 0; i < num_segments; ++i) {
+        const int len = seg_indptr[i + 1] - seg_indptr[i];
+        if (len <= 0) continue;
+        const int32_t id = adapter_ids[i];
+        int rank = 0, off = 0;
+        float scale = 0.f;
+        if (id >= 0) {
+            const AdapterRec& a = p->table.at(id);
+            if (a.rank > 128) return fail(LORA_ERR_UNSUPPORTED, "the fused base GEMM supports rank <= 128");
+            rank = a.rank;
+            scale = a.scale;
+            off = -1;
+            for (const auto& o : offs)
+                if (o.first == id) off = o.second;
+            if (off < 0) {
+                off = (int)words.size();
+                offs.emplace_back(id, off);
+                words.insert(words.end(), a.pages.begin(), a.pages.end());
+            }
+        }
+        int32_t sb;
+        std::memcpy(&sb, &scale, 4);
+        for (int t0 = 0; t0 < len; t0 += 128, ++tix) {
+            int32_t* rec = words.data() + (size_t)tix * 8;
+            rec[0] = seg_indptr[i] + t0;
+            rec[1] = std::min(128, len - t0);
+            rec[2] = rank;
+            rec[3] = off;
+            rec[4] = sb;
+        }
+    }
+    if ((int)words.size() > kFusedBaseMaxWords)
+        return fail(LORA_ERR_UNSUPPORTED, "batch too large for one fused launch (tiles and page lists exceed " +
+                                              std::to_string(kFusedBaseMaxWords) + " words)");
+    DeviceGuard g(p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_fused_base: pending CUDA error");
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply_fused_base: capture query");
+    p->capturing = cap != cudaStreamCaptureStatusNone;
+    for (const auto& o : offs)
+        if ((s = wait_loaded(p->table.at(o.first), st, p->capturing, "lora_apply_fused_base: wait load")) != LORA_OK)
+            return s;
+    FusedBaseLaunch L{x, W, y, p->tm_a, p->tm_b, T, p->H_in, p->H_out, p->n_pages};
+    cudaError_t e = (cudaError_t)launch_fused_base(L, words.data(), (int)words.size(), n_tiles, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lora_apply_fused_base: kernel launch");
+    p->launches += 1;
+    if (std::find(p->apply_streams.begin(), p->apply_streams.end(), st) == p->apply_streams.end())
+        p->apply_streams.push_back(st);
+    return LORA_OK;
+}
+
 lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
     if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
     switch (option) {

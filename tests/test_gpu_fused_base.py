@@ -1,0 +1,86 @@
+"""NEXT f2 on the GPU: lora_apply_fused_base, y = x·W + s·(x·A)·B in one tcgen05 kernel, against the
+fp64 oracle's delta plus x·W in fp64 (numpy on the same bf16 values).  PAPER.md Eq. 1,
+§4.1 P:548-550.  The delta is checked on its own as well (y − x·W vs the oracle delta), so a large
+base term cannot hide a wrong adapter contribution."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from workloads import gen
+
+from gpu_util import TOL, from_torch, make_pool, rel_l2, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2401_11240_b200 as lib
+    return lib
+
+
+def _weight(seed, H_in, H_out):
+    w = gen.storage_to_f64(gen.make_rows(seed, 77, 0, H_in, H_out, "bf16"), "bf16") / np.sqrt(H_in)
+    return gen.f32_to_storage(w.astype(np.float32), "bf16")
+
+
+def _check(L, b, W):
+    import torch
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    Wd = to_torch(W, "cuda")
+    y = torch.full((b.T, b.H_out), 0x7fc0, dtype=torch.int16, device="cuda")   # NaN: every row must be written
+    pool.apply_fused_base(x, Wd, y, b.seg_indptr, b.adapter_ids)
+    torch.cuda.synchronize()
+    got = gen.storage_to_f64(from_torch(y, "bf16"), "bf16").reshape(b.T, b.H_out)
+    base = gen.storage_to_f64(b.x, "bf16").reshape(b.T, b.H_in) @ gen.storage_to_f64(W, "bf16").reshape(b.H_in, b.H_out)
+    delta = O.delta_for_batch(b, n_threads=16).reshape(b.T, b.H_out)   # y_in = 0: the delta alone
+    assert np.isfinite(got).all()
+    full = np.linalg.norm(got - (base + delta)) / np.linalg.norm(base + delta)
+    assert full <= TOL["bf16"], full
+    # the delta alone: bf16 rounding of y (~2^-9 |y|) is the floor here, so the bound is looser
+    d_err = np.linalg.norm((got - base) - delta) / np.linalg.norm(delta)
+    assert d_err <= 2e-2, d_err
+    # tokens without an adapter get exactly the base product (up to its one rounding)
+    ids = np.repeat(b.adapter_ids, np.diff(b.seg_indptr))
+    if (ids < 0).any():
+        m = ids < 0
+        assert np.linalg.norm(got[m] - base[m]) / np.linalg.norm(base[m]) <= TOL["bf16"]
+    pool.close()
+    return full, d_err
+
+
+def test_fused_base_ragged_small(L):
+    """Ragged segments (1..300 tokens, tails inside a tile), ranks 1 / 8 / 128, an id < 0 segment,
+    an adapter used by two segments, 3 column tiles."""
+    b = gen.build_batch("fb_small", 811, "bf16", 256, 384, [300, 1, 128, 50, 129], [0, -1, 1, 2, 0],
+                        {0: 8, 1: 128, 2: 1}, y_zero=True)
+    W = _weight(5, 256, 384)
+    _check(L, b, W)
+
+
+def test_fused_base_prefill_mix(L):
+    """8 prompts of 512 tokens at H = 1024 -> 2048 (16 column tiles), ranks 8..128."""
+    ranks = {i: (8, 16, 32, 64, 128)[i % 5] for i in range(8)}
+    b = gen.build_batch("fb_mix", 812, "bf16", 1024, 2048, [512] * 8, list(range(8)), ranks, y_zero=True)
+    W = _weight(6, 1024, 2048)
+    _check(L, b, W)
+
+
+def test_fused_base_rejects_unsupported(L):
+    import torch
+    b = gen.build_batch("fb_r200", 813, "bf16", 256, 256, [200], [0], {0: 200}, y_zero=True)
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    y = torch.zeros((b.T, b.H_out), dtype=torch.int16, device="cuda")
+    W = to_torch(_weight(7, 256, 256), "cuda")
+    with pytest.raises(L.LoraError) as ei:
+        pool.apply_fused_base(x, W, y, b.seg_indptr, b.adapter_ids)
+    assert ei.value.name == "LORA_ERR_UNSUPPORTED"
+    with pytest.raises(L.LoraError) as ei:
+        pool.apply_fused_base(x, W, x, b.seg_indptr, b.adapter_ids)   # y overlaps x
+    assert ei.value.name == "LORA_ERR_ARG"
+    pool.close()
