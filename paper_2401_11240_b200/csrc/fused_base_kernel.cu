@@ -27,12 +27,13 @@ namespace lora {
 
 constexpr int kFbThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
 constexpr int kFbStages = 3;
-constexpr int kFbStageBytes = 49152;   // X chunk 16 KB + W chunk 16 KB + A chunk <= 16 KB
+// ring stage: X chunk 16 KB + W chunk (64 x NT columns) + A chunk <= 16 KB; after the mainloop
+// stage 0 holds the expand's B tile (r16 <= 128 rank rows x NT columns <= 64 KB)
+constexpr int fb_stage_bytes(int nt) { return 16384 + nt * 128 + 16384; }
 constexpr int kFbVBytes = 32768;       // V: 128 tokens x r16 <= 128, bf16, K-major SW128
-constexpr int kFbBBytes = 32768;       // B tile: r16 <= 128 rank rows x 128 columns, MN-major SW128
-constexpr int kFbSmem = 1024 + kFbStages * kFbStageBytes + kFbVBytes + kFbBBytes + 256;
+constexpr int fb_smem_bytes(int nt) { return 1024 + kFbStages * fb_stage_bytes(nt) + kFbVBytes + 256; }
 constexpr int kFbTileWords = 8;
-static_assert(kFbSmem <= 227 * 1024, "shared memory");
+static_assert(fb_smem_bytes(256) <= 227 * 1024, "shared memory");
 
 struct FusedBaseArgs {
     CUtensorMap tm_x;   // x [T][H_in], box {64, 128}
@@ -121,17 +122,20 @@ __device__ __forceinline__ void fb_ld32(uint32_t taddr, float (&v)[32]) {
 }
 }  // namespace
 
+template <int NT>   // output columns per CTA (128 or 256 = the MMA N of the base GEMM)
 __global__ void __launch_bounds__(kFbThreads, 1)
     lora_fused_base_kernel(const __grid_constant__ FusedBaseArgs a, const __grid_constant__ FbBlob blob) {
+    constexpr int kStage = fb_stage_bytes(NT);
+    constexpr uint32_t kTmemCols = NT == 256 ? 512u : 256u;   // D_base [0, NT), D1 [NT, NT + 128)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = fb_smem(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
     const uint32_t ring = base;
-    const uint32_t vbuf = base + kFbStages * kFbStageBytes;
+    const uint32_t vbuf = base + kFbStages * kStage;
     uint8_t* gv = gbase + (vbuf - base);
-    const uint32_t bbuf = vbuf + kFbVBytes;
-    const uint32_t bars = bbuf + kFbBBytes;
+    const uint32_t bbuf = ring;   // stage 0, once every mainloop MMA has completed (d_full)
+    const uint32_t bars = vbuf + kFbVBytes;
     auto full = [&](int s) { return bars + 8u * s; };
     auto empty = [&](int s) { return bars + 8u * (kFbStages + s); };
     const uint32_t d_full = bars + 8u * (2 * kFbStages);
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     const int tok0 = rec[0], nvalid = rec[1], r = rec[2], poff = rec[3];
     const float scale = __int_as_float(rec[4]);
     const int rp = r > 0 ? (r + 15) & ~15 : 0;
-    const int n0 = blockIdx.y * 128;
+    const int n0 = blockIdx.y * NT;
     const int nkc = a.H_in / 64;
 
     if (tid == 0) {
@@ -159,8 +163,9 @@ __global__ void __launch_bounds__(kFbThreads, 1)
         fb_bar_init(d2_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {   // TMEM: D_base at columns [0,128), D1 at [128,256)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(fb_smem(tmem_slot)));
+    if (warp == 1) {   // TMEM: D_base at columns [0, NT), D1 at [NT, NT + 128)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(fb_smem(tmem_slot)),
+                     "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fb_fence_before();
@@ -177,36 +182,37 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             const int j = lane * 4 + q;
             pg[q] = j < r ? blob.w[poff + j] : a.zero_page;
         }
-        if (r > 0) {   // the expand's B tile up front (its own buffer)
-            if (lane == 0) fb_arrive_tx(b_full, (uint32_t)(rp * 128 * 2));
-            __syncwarp();
-            if (lane < ngr)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t dst = bbuf + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
-                    fb_gather4(dst, &a.tm_b, n0 + h * 64, pg[0], pg[1], pg[2], pg[3], b_full);
-                }
-        }
         int stage = 0;
         uint32_t phase = 0;
         for (int kc = 0; kc < nkc; ++kc) {
             fb_wait(empty(stage), phase ^ 1u);
-            const uint32_t sb = ring + stage * kFbStageBytes;
+            const uint32_t sb = ring + stage * kStage;
             if (lane == 0) {
-                fb_arrive_tx(full(stage), (uint32_t)(16384 + 16384 + rp * 128));
+                fb_arrive_tx(full(stage), (uint32_t)(16384 + NT * 128 + rp * 128));
                 fb_tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
-                // W rows [64kc, 64kc+64) x columns [n0, n0+128): two MN-major atom columns of 8 KB
-                fb_tma_2d(sb + 16384, &a.tm_w, n0, kc * 64, full(stage));
-                fb_tma_2d(sb + 16384 + 8192, &a.tm_w, n0 + 64, kc * 64, full(stage));
+                // W rows [64kc, 64kc+64) x columns [n0, n0+NT): NT/64 MN-major atom columns of 8 KB
+#pragma unroll
+                for (int h = 0; h < NT / 64; ++h) fb_tma_2d(sb + 16384 + h * 8192, &a.tm_w, n0 + h * 64, kc * 64, full(stage));
             }
             __syncwarp();
             if (lane < ngr)
-                fb_gather4(sb + 32768 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
+                fb_gather4(sb + 16384 + NT * 128 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
             if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
+        }
+        if (r > 0) {   // the expand's B tile into stage 0 once every mainloop MMA has read the ring
+            fb_wait(d_full, 0);
+            if (lane == 0) fb_arrive_tx(b_full, (uint32_t)(rp * NT * 2));
+            __syncwarp();
+            if (lane < ngr)
+#pragma unroll
+                for (int h = 0; h < NT / 64; ++h) {
+                    const uint32_t dst = bbuf + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
+                    fb_gather4(dst, &a.tm_b, n0 + h * 64, pg[0], pg[1], pg[2], pg[3], b_full);
+                }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
-        const uint32_t id_base = fb_idesc(128, 1);
+        const uint32_t id_base = fb_idesc(NT, 1);
         const uint32_t id1 = rp > 0 ? fb_idesc(rp, 0) : 0u;
         int stage = 0;
         uint32_t phase = 0;
@@ -214,12 +220,13 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             fb_wait(full(stage), phase);
             fb_fence_after();
             if (lane == 0) {
-                const uint32_t sb = ring + stage * kFbStageBytes;
+                const uint32_t sb = ring + stage * kStage;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                     const uint64_t xd = fb_desc(sb + kk * 32, 16, 1024);
                     fb_mma(tmem, xd, fb_desc(sb + 16384 + kk * 2048, 8192, 1024), id_base, (kc | kk) != 0);
-                    if (rp > 0) fb_mma(tmem + 128u, xd, fb_desc(sb + 32768 + kk * 32, 16, 1024), id1, (kc | kk) != 0);
+                    if (rp > 0)
+                        fb_mma(tmem + (uint32_t)NT, xd, fb_desc(sb + 16384 + NT * 128 + kk * 32, 16, 1024), id1, (kc | kk) != 0);
                 }
                 fb_commit(empty(stage));
                 if (kc == nkc - 1) fb_commit(d_full);
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             fb_fence_after();
             for (int c0 = 0; c0 < rp; c0 += 32) {
                 float v[32];
-                fb_ld32(tmem + lane_addr + 128u + (uint32_t)c0, v);
+                fb_ld32(tmem + lane_addr + (uint32_t)NT + (uint32_t)c0, v);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint32_t hw[4];
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
         fb_fence_after();
         char* yrow = a.y + ((size_t)(tok0 + row) * a.H_out + n0) * 2;
 #pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+        for (int c0 = 0; c0 < NT; c0 += 32) {
             float d[32];
             fb_ld32(tmem + lane_addr + (uint32_t)c0, d);
             if (row < nvalid) {
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     __syncthreads();
     if (warp == 1) {
         fb_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
 }
 
@@ -325,11 +332,18 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
     std::memcpy(blob.w, words, (size_t)n_words * 4);
     static bool configured = false;
     if (!configured) {
-        cudaError_t ce = cudaFuncSetAttribute(lora_fused_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFbSmem);
+        cudaError_t ce = cudaFuncSetAttribute(lora_fused_base_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              fb_smem_bytes(128));
+        if (ce == cudaSuccess)
+            ce = cudaFuncSetAttribute(lora_fused_base_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      fb_smem_bytes(256));
         if (ce != cudaSuccess) return (int)ce;
         configured = true;
     }
-    lora_fused_base_kernel<<<dim3(n_tiles, L.H_out / 128), kFbThreads, kFbSmem, st>>>(a, blob);
+    if (L.H_out % 256 == 0)
+        lora_fused_base_kernel<256><<<dim3(n_tiles, L.H_out / 256), kFbThreads, fb_smem_bytes(256), st>>>(a, blob);
+    else
+        lora_fused_base_kernel<128><<<dim3(n_tiles, L.H_out / 128), kFbThreads, fb_smem_bytes(128), st>>>(a, blob);
     return (int)cudaGetLastError();
 }
 
