@@ -145,11 +145,14 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (d_full + 32u - base));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int32_t* rec = blob.w + blockIdx.x * kFbTileWords;
+    // grid: x = column tile (fast), y = token tile -- a token tile's column CTAs run together and
+    // share its x tiles through L2 (W stays L2-resident); the transposed order re-streams x from HBM
+    // once per column tile
+    const int32_t* rec = blob.w + blockIdx.y * kFbTileWords;
     const int tok0 = rec[0], nvalid = rec[1], r = rec[2], poff = rec[3];
     const float scale = __int_as_float(rec[4]);
     const int rp = r > 0 ? (r + 15) & ~15 : 0;
-    const int n0 = blockIdx.y * NT;
+    const int n0 = blockIdx.x * NT;
     const int nkc = a.H_in / 64;
 
     if (tid == 0) {
@@ -341,9 +344,9 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
         configured = true;
     }
     if (L.H_out % 256 == 0)
-        lora_fused_base_kernel<256><<<dim3(n_tiles, L.H_out / 256), kFbThreads, fb_smem_bytes(256), st>>>(a, blob);
+        lora_fused_base_kernel<256><<<dim3(L.H_out / 256, n_tiles), kFbThreads, fb_smem_bytes(256), st>>>(a, blob);
     else
-        lora_fused_base_kernel<128><<<dim3(n_tiles, L.H_out / 128), kFbThreads, fb_smem_bytes(128), st>>>(a, blob);
+        lora_fused_base_kernel<128><<<dim3(L.H_out / 128, n_tiles), kFbThreads, fb_smem_bytes(128), st>>>(a, blob);
     return (int)cudaGetLastError();
 }
 
