@@ -40,6 +40,7 @@ struct FusedBaseArgs {
     CUtensorMap tm_w;   // W [H_in][H_out], box {64, 64}
     CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1} (gather4)
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1} (gather4)
+    const char* box_maps;   // the pool's page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), or null
     char* y;
     int H_in, H_out, zero_page;
 };
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     // once per column tile
     const int32_t* rec = blob.w + blockIdx.y * kFbTileWords;
     const int tok0 = rec[0], nvalid = rec[1], r = rec[2], poff = rec[3];
+    const int first_page = rec[5];   // >= 0: the rank rows are pages [first_page, first_page + r)
     const float scale = __int_as_float(rec[4]);
     const int rp = r > 0 ? (r + 15) & ~15 : 0;
     const int n0 = blockIdx.x * NT;
@@ -179,6 +181,22 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     if (warp == 0) {
         // ===================== TMA producer =====================
         const int ngr = rp / 4;
+        // contiguous adapters: the rp rank rows as 2D boxes of 128/64/32/16 rows (one TMA request
+        // instead of rp/4 gather4s); rows r..rp-1 then hold neighbouring pages, which meet V's
+        // zero columns (shrink: V columns >= r are zeroed; expand: they multiply those zeros)
+        const bool use_box = first_page >= 0 && a.box_maps != nullptr;
+        auto boxes = [&](uint32_t dst, int map_base, int col, uint32_t bar) {
+            int row = 0;
+            for (int k = 4; k >= 1; --k) {
+                const int R = 8 << k;
+                while (rp - row >= R) {
+                    fb_tma_2d(dst + (uint32_t)row * 128u,
+                              reinterpret_cast<const CUtensorMap*>(a.box_maps + (map_base + k) * 128), col,
+                              first_page + row, bar);
+                    row += R;
+                }
+            }
+        };
         int pg[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -196,17 +214,23 @@ __global__ void __launch_bounds__(kFbThreads, 1)
                 // W rows [64kc, 64kc+64) x columns [n0, n0+NT): NT/64 MN-major atom columns of 8 KB
 #pragma unroll
                 for (int h = 0; h < NT / 64; ++h) fb_tma_2d(sb + 16384 + h * 8192, &a.tm_w, n0 + h * 64, kc * 64, full(stage));
+                if (use_box && r > 0) boxes(sb + 16384 + NT * 128, 0, kc * 64, full(stage));
             }
             __syncwarp();
-            if (lane < ngr)
+            if (!use_box && lane < ngr)
                 fb_gather4(sb + 16384 + NT * 128 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
             if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
         }
         if (r > 0) {   // the expand's B tile into stage 0 once every mainloop MMA has read the ring
             fb_wait(d_full, 0);
-            if (lane == 0) fb_arrive_tx(b_full, (uint32_t)(rp * NT * 2));
+            if (lane == 0) {
+                fb_arrive_tx(b_full, (uint32_t)(rp * NT * 2));
+                if (use_box)
+                    for (int h = 0; h < NT / 64; ++h)
+                        boxes(bbuf + (uint32_t)(h * (rp / 8)) * 1024u, kSpanBoxKinds, n0 + h * 64, b_full);
+            }
             __syncwarp();
-            if (lane < ngr)
+            if (!use_box && lane < ngr)
 #pragma unroll
                 for (int h = 0; h < NT / 64; ++h) {
                     const uint32_t dst = bbuf + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
@@ -327,6 +351,7 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
     if (e) return e;
     std::memcpy(&a.tm_a, L.tm_a, sizeof(CUtensorMap));
     std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
+    a.box_maps = static_cast<const char*>(L.box_maps);
     a.y = static_cast<char*>(L.y);
     a.H_in = L.H_in;
     a.H_out = L.H_out;

@@ -172,6 +172,7 @@ struct FusedBaseLaunch {
     const void* tm_a;   // the pool's gather4 maps
     const void* tm_b;
     int T, H_in, H_out, zero_page;
+    const void* box_maps = nullptr;   // device: the pool's 2D box maps (contiguous adapters)
 };
 int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_tiles, lora_cuda_stream st);
 bool prefill_supported(int H_in, int H_out, int esz);

@@ -664,6 +664,13 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
         }
         int32_t sb;
         std::memcpy(&sb, &scale, 4);
+        int first_page = -1;   // the adapter's pages as one run: 2D box loads
+        if (rank > 0) {
+            const int32_t* gp = words.data() + off;
+            bool run = true;
+            for (int j = 1; j < rank && run; ++j) run = gp[j] == gp[0] + j;
+            first_page = run ? gp[0] : -1;
+        }
         for (int t0 = 0; t0 < len; t0 += 128, ++tix) {
             int32_t* rec = words.data() + (size_t)tix * 8;
             rec[0] = seg_indptr[i] + t0;
@@ -671,6 +678,7 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
             rec[2] = rank;
             rec[3] = off;
             rec[4] = sb;
+            rec[5] = first_page;
         }
     }
     if ((int)words.size() > kFusedBaseMaxWords)
@@ -689,6 +697,7 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
         if ((s = wait_loaded(p->table.at(o.first), st, p->capturing, "lora_apply_fused_base: wait load")) != LORA_OK)
             return s;
     FusedBaseLaunch L{x, W, y, p->tm_a, p->tm_b, T, p->H_in, p->H_out, p->n_pages};
+    L.box_maps = p->span_tmaps;
     cudaError_t e = (cudaError_t)launch_fused_base(L, words.data(), (int)words.size(), n_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "lora_apply_fused_base: kernel launch");
     p->launches += 1;

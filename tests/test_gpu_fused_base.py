@@ -27,9 +27,23 @@ def _weight(seed, H_in, H_out):
     return gen.f32_to_storage(w.astype(np.float32), "bf16")
 
 
-def _check(L, b, W):
+def _fragmented_pool(b, L):
+    """Adapters whose pages are NOT one run (the kernel's gather4 path): a rank-4 filler is loaded
+    first and unloaded after the first adapter, so the next adapter's pages wrap around it."""
+    pool = L.LoraPool(b.H_in, b.H_out, len(b.adapters) + 4, b.dtype,
+                      max_total_rank=sum(a.rank for a in b.adapters) + 8)
+    filler = np.zeros((4, b.H_in), np.uint16), np.zeros((4, b.H_out), np.uint16)
+    pool.load_adapter(999, 4, to_torch(filler[0], pin=True), to_torch(filler[1], pin=True), 1.0)
+    for i, a in enumerate(b.adapters):
+        pool.load_adapter(a.id, a.rank, to_torch(a.A, pin=True), to_torch(a.B, pin=True), a.scale)
+        if i == 0:
+            pool.unload_adapter(999)
+    return pool
+
+
+def _check(L, b, W, fragmented=False):
     import torch
-    pool = make_pool(b, L)
+    pool = _fragmented_pool(b, L) if fragmented else make_pool(b, L)
     x = to_torch(b.x, "cuda")
     Wd = to_torch(W, "cuda")
     y = torch.full((b.T, b.H_out), 0x7fc0, dtype=torch.int16, device="cuda")   # NaN: every row must be written
@@ -53,13 +67,16 @@ def _check(L, b, W):
     return full, d_err
 
 
-def test_fused_base_ragged_small(L):
+@pytest.mark.parametrize("fragmented", [False, True], ids=["box_loads", "gather4_loads"])
+@pytest.mark.parametrize("H_out", [384, 512], ids=["nt128", "nt256"])
+def test_fused_base_ragged_small(L, fragmented, H_out):
     """Ragged segments (1..300 tokens, tails inside a tile), ranks 1 / 8 / 128, an id < 0 segment,
-    an adapter used by two segments, 3 column tiles."""
-    b = gen.build_batch("fb_small", 811, "bf16", 256, 384, [300, 1, 128, 50, 129], [0, -1, 1, 2, 0],
+    an adapter used by two segments; 128- and 256-column tiles; adapters in one page run (2D box
+    loads) or fragmented (gather4 loads)."""
+    b = gen.build_batch("fb_small", 811, "bf16", 256, H_out, [300, 1, 128, 50, 129], [0, -1, 1, 2, 0],
                         {0: 8, 1: 128, 2: 1}, y_zero=True)
-    W = _weight(5, 256, 384)
-    _check(L, b, W)
+    W = _weight(5, 256, H_out)
+    _check(L, b, W, fragmented)
 
 
 def test_fused_base_prefill_mix(L):
