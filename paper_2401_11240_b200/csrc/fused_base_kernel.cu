@@ -135,7 +135,9 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     const uint32_t ring = base;
     const uint32_t vbuf = base + kFbStages * kStage;
     uint8_t* gv = gbase + (vbuf - base);
-    const uint32_t bbuf = ring;   // stage 0, once every mainloop MMA has completed (d_full)
+    // the expand's B tile goes into the ring stage the producer would fill next (nkc % stages): the
+    // first one released at the end of the mainloop, so its load overlaps the last stages' MMAs
+    const uint32_t bbuf = ring + (uint32_t)((a.H_in / 64) % kFbStages) * kStage;
     const uint32_t bars = vbuf + kFbVBytes;
     auto full = [&](int s) { return bars + 8u * s; };
     auto empty = [&](int s) { return bars + 8u * (kFbStages + s); };
@@ -221,8 +223,8 @@ __global__ void __launch_bounds__(kFbThreads, 1)
                 fb_gather4(sb + 16384 + NT * 128 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
             if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
         }
-        if (r > 0) {   // the expand's B tile into stage 0 once every mainloop MMA has read the ring
-            fb_wait(d_full, 0);
+        if (r > 0) {   // the expand's B tile into the next ring stage, once its last mainloop MMAs are done
+            fb_wait(empty(stage), phase ^ 1u);
             if (lane == 0) {
                 fb_arrive_tx(b_full, (uint32_t)(rp * NT * 2));
                 if (use_box)
