@@ -73,6 +73,8 @@ def parse():
                          "o (input = attention output) is always its own lora_apply")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
     ap.add_argument("--c5-reps", type=int, default=5, help="config 5 (70B shapes, tp 1/2/4/8 shards) timing reps; 0 = skip")
+    ap.add_argument("--fused-base-reps", type=int, default=5,
+                    help="NEXT f2 (delta fused into the base GEMM) timing reps on c3 shapes; 0 = skip")
     return ap.parse_args()
 
 
@@ -492,6 +494,61 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
 
 
 # ---------------------------------------------------------------- config 5: Llama-2-70B shapes, TP shards
+def bench_fused_base(L, dev, reps: int, tc_peak: float):
+    """NEXT f2: y = x·W + s·(x·A)·B on c3 shapes (32 x 512 tokens, 4096 -> 4096, ranks 8..128).
+    fused = lora_apply_fused_base (one tcgen05 kernel); unfused = cuBLAS x·W then lora_apply (the
+    delta pass reads and writes y again); base = cuBLAS x·W alone.  CUDA graphs of 4 calls, L2
+    flushed before each replay, median of `reps`."""
+    import torch
+    b = gen.config_c3()
+    pool = L.LoraPool(b.H_in, b.H_out, 64, "bf16", max_total_rank=sum(a.rank for a in b.adapters))
+    for a in b.adapters:
+        pool.load_adapter(a.id, a.rank, torch.from_numpy(a.A.view(np.int16)).pin_memory(),
+                          torch.from_numpy(a.B.view(np.int16)).pin_memory(), a.scale)
+    g = torch.Generator(device="cpu").manual_seed(gen.BASE_SEED + 300)
+    x = torch.from_numpy(b.x.view(np.int16)).to(dev).view(torch.bfloat16)
+    W = (torch.randn(b.H_in, b.H_out, generator=g) / b.H_in ** 0.5).to(torch.bfloat16).to(dev)
+    y = torch.empty(b.T, b.H_out, dtype=torch.bfloat16, device=dev)
+    st = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)
+    NP = 4
+    calls = {
+        "fused": lambda: pool.apply_fused_base(x, W, y, b.seg_indptr, b.adapter_ids, stream=st),
+        "unfused": lambda: (torch.matmul(x, W, out=y), pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)),
+        "base": lambda: torch.matmul(x, W, out=y),
+    }
+    sum_tr = sum(int(b.seg_indptr[i + 1] - b.seg_indptr[i]) * gen.C3_RANKS[i % 5] for i in range(len(b.adapter_ids)))
+    flops = 2.0 * b.T * b.H_in * b.H_out + 2.0 * sum_tr * (b.H_in + b.H_out)
+    out = {"workload": "c3 shapes: 32 x 512 tokens, 4096 -> 4096, 32 adapters ranks 8..128, W random bf16",
+           "tflop_per_call": round(flops / 1e12, 4), "peak_tflops": tc_peak}
+    for name, fn in calls.items():
+        with torch.cuda.stream(st):
+            fn()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            for _ in range(NP):
+                fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            with torch.cuda.stream(st):
+                graph.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / NP)
+        us = float(np.median(ts))
+        out[name] = {"us": round(us, 1), "tflops": round(flops / (us * 1e-6) / 1e12, 1),
+                     "frac_tc_peak": round(flops / (us * 1e-6) / 1e12 / tc_peak, 3)}
+        del graph
+    out["fused_vs_unfused"] = round(out["unfused"]["us"] / out["fused"]["us"], 3)
+    pool.close()
+    return out
+
+
 def bench_c5(L, dev, reps: int, hbm_peak: float):
     """c5: Llama-2-70B per-layer projection shapes (q/o 8192^2, k/v 8192->1024, gate/up 8192->28672,
     down 28672->8192), decode 64 tokens over 32 adapters of ranks [16,32,64,128][a mod 4].  tp = 1:
@@ -800,6 +857,10 @@ def main():
     if args.c5_reps > 0:
         c5 = bench_c5(L, dev, args.c5_reps, hbm_peak)
 
+    fused_base = None
+    if args.fused_base_reps > 0 and rank == 0:
+        fused_base = bench_fused_base(L, dev, args.fused_base_reps, tc_peak)
+
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -832,6 +893,7 @@ def main():
                 "prefill": prefill,
                 "c4": c4,
                 "c5": c5,
+                "fused_base": fused_base,
                 "setup_s": round(t_gen, 1)}
         s = json.dumps(line)
         print(s, flush=True)
