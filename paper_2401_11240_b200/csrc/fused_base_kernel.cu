@@ -26,14 +26,15 @@
 namespace lora {
 
 constexpr int kFbThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
-constexpr int kFbStages = 3;
+constexpr int kFbMaxStages = 4;   // the ring holds as many stages as fit (3 or 4, by the tile's rank)
 // ring stage: X chunk 16 KB + W chunk (64 x NT columns) + A chunk <= 16 KB; after the mainloop
 // stage 0 holds the expand's B tile (r16 <= 128 rank rows x NT columns <= 64 KB)
 constexpr int fb_stage_bytes(int nt) { return 16384 + nt * 128 + 16384; }
-constexpr int kFbVBytes = 32768;       // V: 128 tokens x r16 <= 128, bf16, K-major SW128
-constexpr int fb_smem_bytes(int nt) { return 1024 + kFbStages * fb_stage_bytes(nt) + kFbVBytes + 256; }
+// V: 128 tokens x r16 <= 128, bf16, K-major SW128 (32 KB), in a ring stage after the mainloop
+constexpr int kFbSmem = 227 * 1024;                  // the whole opt-in maximum: the ring takes what the rank allows
+constexpr int kFbRingBytes = kFbSmem - 1024 - 256;   // minus alignment slack and the barrier block
 constexpr int kFbTileWords = 8;
-static_assert(fb_smem_bytes(256) <= 227 * 1024, "shared memory");
+static_assert(3 * fb_stage_bytes(256) <= kFbRingBytes, "three stages at rank 128");
 
 struct FusedBaseArgs {
     CUtensorMap tm_x;   // x [T][H_in], box {64, 128}
@@ -126,26 +127,22 @@ __device__ __forceinline__ void fb_ld32(uint32_t taddr, float (&v)[32]) {
 template <int NT>   // output columns per CTA (128 or 256 = the MMA N of the base GEMM)
 __global__ void __launch_bounds__(kFbThreads, 1)
     lora_fused_base_kernel(const __grid_constant__ FusedBaseArgs a, const __grid_constant__ FbBlob blob) {
-    constexpr int kStage = fb_stage_bytes(NT);
+    // stage = X 16 KB + W (64 x NT) + A (r16 rows x 128 B): 4 stages fit up to rank 64 at NT = 256
     constexpr uint32_t kTmemCols = NT == 256 ? 512u : 256u;   // D_base [0, NT), D1 [NT, NT + 128)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = fb_smem(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
     const uint32_t ring = base;
-    const uint32_t vbuf = base + kFbStages * kStage;
-    uint8_t* gv = gbase + (vbuf - base);
-    // the expand's B tile goes into the ring stage the producer would fill next (nkc % stages): the
-    // first one released at the end of the mainloop, so its load overlaps the last stages' MMAs
-    const uint32_t bbuf = ring + (uint32_t)((a.H_in / 64) % kFbStages) * kStage;
-    const uint32_t bars = vbuf + kFbVBytes;
+    const uint32_t bars = base + kFbRingBytes;
     auto full = [&](int s) { return bars + 8u * s; };
-    auto empty = [&](int s) { return bars + 8u * (kFbStages + s); };
-    const uint32_t d_full = bars + 8u * (2 * kFbStages);
+    auto empty = [&](int s) { return bars + 8u * (kFbMaxStages + s); };
+    const uint32_t d_full = bars + 8u * (2 * kFbMaxStages);
     const uint32_t v_ready = d_full + 8u;
     const uint32_t b_full = d_full + 16u;
     const uint32_t d2_full = d_full + 24u;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (d_full + 32u - base));
+    static_assert(8 * (2 * kFbMaxStages + 4) + 4 <= 256, "barrier block");
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // grid: x = column tile (fast), y = token tile -- a token tile's column CTAs run together and
@@ -158,9 +155,17 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     const int rp = r > 0 ? (r + 15) & ~15 : 0;
     const int n0 = blockIdx.x * NT;
     const int nkc = a.H_in / 64;
+    const uint32_t kStage = (uint32_t)(16384 + NT * 128 + rp * 128);   // multiple of 2 KB
+    const int nst = min(kFbMaxStages, (int)(kFbRingBytes / kStage));
+    // after the mainloop: the expand's B tile goes into the ring stage the producer would fill next
+    // (nkc % nst, the first one released, so its load overlaps the last stages' MMAs) and V into the
+    // one after it (free once every mainloop MMA has completed)
+    const uint32_t bbuf = ring + (uint32_t)(nkc % nst) * kStage;
+    const uint32_t vbuf = ring + (uint32_t)((nkc + 1) % nst) * kStage;
+    uint8_t* gv = gbase + (vbuf - base);
 
     if (tid == 0) {
-        for (int s = 0; s < kFbStages; ++s) {
+        for (int s = 0; s < kFbMaxStages; ++s) {
             fb_bar_init(full(s), 1);
             fb_bar_init(empty(s), 1);
         }
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             __syncwarp();
             if (!use_box && lane < ngr)
                 fb_gather4(sb + 16384 + NT * 128 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
-            if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
+            if (++stage == nst) { stage = 0; phase ^= 1u; }
         }
         if (r > 0) {   // the expand's B tile into the next ring stage, once its last mainloop MMAs are done
             fb_wait(empty(stage), phase ^ 1u);
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
                 if (kc == nkc - 1) fb_commit(d_full);
             }
             __syncwarp();
-            if (++stage == kFbStages) { stage = 0; phase ^= 1u; }
+            if (++stage == nst) { stage = 0; phase ^= 1u; }
         }
         if (rp > 0) {
             fb_wait(v_ready, 0);
@@ -362,18 +367,16 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
     std::memcpy(blob.w, words, (size_t)n_words * 4);
     static bool configured = false;
     if (!configured) {
-        cudaError_t ce = cudaFuncSetAttribute(lora_fused_base_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              fb_smem_bytes(128));
+        cudaError_t ce = cudaFuncSetAttribute(lora_fused_base_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFbSmem);
         if (ce == cudaSuccess)
-            ce = cudaFuncSetAttribute(lora_fused_base_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      fb_smem_bytes(256));
+            ce = cudaFuncSetAttribute(lora_fused_base_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFbSmem);
         if (ce != cudaSuccess) return (int)ce;
         configured = true;
     }
     if (L.H_out % 256 == 0)
-        lora_fused_base_kernel<256><<<dim3(L.H_out / 256, n_tiles), kFbThreads, fb_smem_bytes(256), st>>>(a, blob);
+        lora_fused_base_kernel<256><<<dim3(L.H_out / 256, n_tiles), kFbThreads, kFbSmem, st>>>(a, blob);
     else
-        lora_fused_base_kernel<128><<<dim3(L.H_out / 128, n_tiles), kFbThreads, fb_smem_bytes(128), st>>>(a, blob);
+        lora_fused_base_kernel<128><<<dim3(L.H_out / 128, n_tiles), kFbThreads, kFbSmem, st>>>(a, blob);
     return (int)cudaGetLastError();
 }
 
