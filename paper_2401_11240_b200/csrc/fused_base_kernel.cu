@@ -44,6 +44,7 @@ struct FusedBaseArgs {
     const char* box_maps;   // the pool's page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), or null
     char* y;
     int H_in, H_out, zero_page;
+    int ring_bytes;   // dynamic shared memory for the ring (the launch's smem minus 1280 B)
 };
 
 struct FbBlob {
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
     const uint32_t ring = base;
-    const uint32_t bars = base + kFbRingBytes;
+    const uint32_t bars = base + (uint32_t)a.ring_bytes;
     auto full = [&](int s) { return bars + 8u * s; };
     auto empty = [&](int s) { return bars + 8u * (kFbMaxStages + s); };
     const uint32_t d_full = bars + 8u * (2 * kFbMaxStages);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     const int n0 = blockIdx.x * NT;
     const int nkc = a.H_in / 64;
     const uint32_t kStage = (uint32_t)(16384 + NT * 128 + rp * 128);   // multiple of 2 KB
-    const int nst = min(kFbMaxStages, (int)(kFbRingBytes / kStage));
+    const int nst = min(kFbMaxStages, (int)((uint32_t)a.ring_bytes / kStage));
     // after the mainloop: the expand's B tile goes into the ring stage the producer would fill next
     // (nkc % nst, the first one released, so its load overlaps the last stages' MMAs) and V into the
     // one after it (free once every mainloop MMA has completed)
@@ -373,6 +374,7 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
         if (ce != cudaSuccess) return (int)ce;
         configured = true;
     }
+    a.ring_bytes = kFbRingBytes;
     if (L.H_out % 256 == 0)
         lora_fused_base_kernel<256><<<dim3(L.H_out / 256, n_tiles), kFbThreads, kFbSmem, st>>>(a, blob);
     else
