@@ -2,17 +2,19 @@
 // GEMM (§4.1: "incorporate the operators of GPU LoRA computation into the base
 // LLM inference process"; Eq. 1: y = x·W + x·A·B, with the per-adapter scale s).
 //
-// One CTA per (128-token tile of one segment, 128-column tile of y):
-//     D_base[t][n]  = Σ_k X[t][k] · W[k][n]          base GEMM, TMEM columns [0, 128)
-//     D1[t][j]      = Σ_k X[t][k] · A_g[k][j]        shrink,    TMEM columns [128, 128 + r16)
+// One CTA per (128-token tile of one segment, NT-column tile of y; NT = 256, or 128 when
+// H_out % 256 != 0), column tiles the fast grid dimension so a token tile's CTAs share x in L2:
+//     D_base[t][n]  = Σ_k X[t][k] · W[k][n]          base GEMM, TMEM columns [0, NT)
+//     D1[t][j]      = Σ_k X[t][k] · A_g[k][j]        shrink,    TMEM columns [NT, NT + r16)
 //     D_base[t][n] += Σ_j bf16(s_g·D1[t][j]) · B_g[j][n]   expand into the base accumulator
 //     y[t][n]       = bf16(D_base[t][n])             one rounding, y written once
 // Each K stage's x chunk feeds both the base MMA and the shrink MMA, so x is read once for both
 // and y is never read: the separate delta pass's y read + write disappear.
-// First version: the shrink is recomputed per column tile (r16/128 extra MMA work), tiles never
-// span segments, and rank <= 128 (the N2 limits).  Layouts are N2's (prefill_kernel.cu): x box
-// {64,128} SW128 K-major, A / B rank rows gathered from the paged pool with tile::gather4, B and
-// W tiles MN-major SW128 atoms (8 K-rows x 64 columns), V K-major SW128.
+// First version: the shrink is recomputed per column tile (r16/NT extra MMA work), tiles never
+// span segments, and rank <= 128 (the N2 limits).  The ring holds 3-4 stages sized by the tile's
+// rank.  Layouts are N2's (prefill_kernel.cu): x box {64,128} SW128 K-major; A / B rank rows as 2D
+// boxes when the adapter's pages are one run, else tile::gather4; B and W tiles MN-major SW128
+// atoms (8 K-rows x 64 columns); V K-major SW128.  Measurements: DESIGN.md §10.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
