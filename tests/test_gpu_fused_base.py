@@ -101,3 +101,37 @@ def test_fused_base_rejects_unsupported(L):
         pool.apply_fused_base(x, W, x, b.seg_indptr, b.adapter_ids)   # y overlaps x
     assert ei.value.name == "LORA_ERR_ARG"
     pool.close()
+
+
+def test_fused_base_graph_capture_matches_eager(L):
+    """The fused path allocates nothing and queries no event on a captured stream: a graph of it
+    replays bitwise-equal to the eager call."""
+    import torch
+    b = gen.build_batch("fb_graph", 815, "bf16", 256, 512, [200, 64, 1], [0, 1, -1], {0: 16, 1: 64}, y_zero=True)
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    W = to_torch(_weight(8, 256, 512), "cuda")
+    y_eager = torch.zeros((b.T, b.H_out), dtype=torch.int16, device="cuda")
+    y_graph = torch.zeros_like(y_eager)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pool.apply_fused_base(x, W, y_eager, b.seg_indptr, b.adapter_ids, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        pool.apply_fused_base(x, W, y_graph, b.seg_indptr, b.adapter_ids, stream=s)
+    with torch.cuda.stream(s):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_eager, y_graph)
+    pool.close()
+
+
+def test_fused_base_rejects_fp32_pool(L):
+    import torch
+    pool = L.LoraPool(256, 256, 2, "f32", max_total_rank=8)
+    x = torch.zeros((4, 256), dtype=torch.float32, device="cuda")
+    with pytest.raises(L.LoraError) as ei:
+        pool.apply_fused_base(x, x, torch.zeros_like(x), [0, 4], [-1])
+    assert ei.value.name == "LORA_ERR_UNSUPPORTED"
+    pool.close()
