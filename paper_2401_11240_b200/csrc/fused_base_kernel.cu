@@ -319,27 +319,36 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             fb_fence_before();
             fb_arrive(v_ready);
         }
-        // y[tok0 + row][n0 .. n0+128) = bf16(D_base): valid rows only (rows past the segment belong
-        // to other tiles)
+        // y[tok0 + row][n0 .. n0+NT) = bf16(D_base): valid rows only (rows past the segment belong
+        // to other tiles).  Each 32-column chunk of the warp's 32 rows is staged in the (now idle)
+        // ring, 64 B per row with its four 16-B pieces rotated by row (bank spread), then leaves as
+        // 8 rows x 64 contiguous bytes per store instruction instead of 32 rows x 16 B.
         fb_wait(d2_full, 0);
         fb_fence_after();
-        char* yrow = a.y + ((size_t)(tok0 + row) * a.H_out + n0) * 2;
+        uint8_t* stg = gbase + (ring - base) + sub * 2048;
 #pragma unroll 1
         for (int c0 = 0; c0 < NT; c0 += 32) {
             float d[32];
             fb_ld32(tmem + lane_addr + (uint32_t)c0, d);
-            if (row < nvalid) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t o[4];
+            for (int q = 0; q < 4; ++q) {
+                uint32_t o[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 hb = __floats2bfloat162_rn(d[q * 8 + 2 * e], d[q * 8 + 2 * e + 1]);
-                        o[e] = *reinterpret_cast<uint32_t*>(&hb);
-                    }
-                    *reinterpret_cast<uint4*>(yrow + (c0 + q * 8) * 2) = make_uint4(o[0], o[1], o[2], o[3]);
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 hb = __floats2bfloat162_rn(d[q * 8 + 2 * e], d[q * 8 + 2 * e + 1]);
+                    o[e] = *reinterpret_cast<uint32_t*>(&hb);
                 }
+                *reinterpret_cast<uint4*>(stg + lane * 64 + ((q + lane) & 3) * 16) = make_uint4(o[0], o[1], o[2], o[3]);
             }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int idx = i * 32 + lane, rr = idx >> 2, qq = idx & 3;
+                const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 64 + ((qq + rr) & 3) * 16);
+                if (sub * 32 + rr < nvalid)
+                    *reinterpret_cast<uint4*>(a.y + ((size_t)(tok0 + sub * 32 + rr) * a.H_out + n0 + c0 + qq * 8) * 2) = v;
+            }
+            __syncwarp();
         }
     }
     fb_fence_before();
