@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define LORA_ABI_VERSION 1
+#define LORA_ABI_VERSION 2
 #define LORA_MAX_RANK 256          /* 1 <= rank <= min(LORA_MAX_RANK, hidden_in, hidden_out) */
 
 typedef struct lora_pool lora_pool;   /* opaque; bound to the CUDA device current at create */
@@ -74,18 +74,14 @@ typedef enum {
 #define LORA_OPT_TC_THRESHOLD 1    /* L_tc (default 64); segments with len >= L_tc take the tcgen05 path.
                                       A value larger than any segment forces the SIMT path everywhere. */
 #define LORA_OPT_RESERVE_TOKENS 2  /* pre-size scratch for this many tokens (avoids a cudaMalloc in apply) */
-#define LORA_OPT_DECODE_FUSED 3    /* bf16 decode hand-off: 0 (default) = PDL-chained shrink/expand kernel
-                                      pair; 1 = ONE grid per apply (expand units wait on per-gc counters);
-                                      2 = flag-chained pair (two grids, the expand grid acquires the per-gc
-                                      counters instead of waiting for the whole shrink grid).  Same
-                                      arithmetic, bitwise equal. */
-#define LORA_OPT_DECODE_PATH 4     /* bf16 decode tokens: 0 (default) = the PDL-chained shrink/expand
-                                      kernel pair; 1 = EXPERIMENTAL one-grid cluster-span kernel
-                                      (csrc/span_kernel.cu: shrink partials reduced over distributed
-                                      shared memory, adapter rows by 2D TMA boxes; DESIGN.md §6 N1c
-                                      records why it is slower on B200 today).  Batches it cannot
-                                      take (fragmented pages, > 8 tokens per chunk, slices > 2048)
-                                      fall back to the pair.  The two sum in different orders. */
+#define LORA_OPT_DECODE_KERNEL 3   /* bf16 decode tokens of lora_apply / lora_apply_multi: 0 (default) = the
+                                      persistent streaming kernel (one grid per apply, one CTA per SM, adapter
+                                      rows streamed through an SMEM ring, shrink -> expand hand-off per
+                                      (adapter, token chunk) through counters; DESIGN.md §6 N1s); 1 = the
+                                      PDL-chained shrink/expand kernel pair (also used by the TP split calls,
+                                      fp32 pools and batches whose metadata exceeds one launch).  Bitwise equal. */
+#define LORA_OPT_DECODE_STAGES 4   /* ring stages (52 KB each: adapter rows + the unit's x / y rows) of the
+                                      streaming kernel: 2 (default) or 3 */
 
 #define LORA_OPT_PAD_MAX_RANK 5    /* comparison mode: 1 pads every adapter's
                                       decode work to the batch's max rank with the pool's all-zero
@@ -272,8 +268,8 @@ typedef struct {
     int32_t n_decode_units, n_prefill_tiles;   /* kernel work of the last apply (informational) */
     int32_t n_shrink_units, n_expand_units;    /* split of n_decode_units (shrink units come first) */
     int64_t v_floats;                          /* size of the partial-v buffer (lora_apply_shrink) */
-    int32_t n_span_ctas, span_cluster;         /* cluster-span decode grid of the last apply (0 if the
-                                                  kernel pair ran): CTAs and cluster size */
+    int32_t decode_ctas, decode_stages;        /* bf16 decode of the last apply: persistent streaming
+                                                  kernel CTAs and ring stages (0 = kernel pair) */
     int32_t n_prefill_ctas, prefill_cluster;   /* tcgen05 prefill grid of the last apply: CTAs
                                                   (tiles x CTAs per tile) and split-K cluster size
                                                   (1 = no split-K) */

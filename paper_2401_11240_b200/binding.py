@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "lora_delta.h")
 LORA_F32, LORA_BF16 = 0, 1
 LORA_POOL_HOST_ONLY = 1
 LORA_KIND_NONE, LORA_KIND_DECODE, LORA_KIND_PREFILL = -1, 0, 1
-LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS, LORA_OPT_DECODE_FUSED, LORA_OPT_DECODE_PATH = 1, 2, 3, 4
+LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS, LORA_OPT_DECODE_KERNEL, LORA_OPT_DECODE_STAGES = 1, 2, 3, 4
 LORA_OPT_PAD_MAX_RANK, LORA_OPT_LOAD_KERNEL = 5, 6
 LORA_MAX_RANK = 256
 
@@ -59,7 +59,7 @@ class MetadataView(ctypes.Structure):
                 ("sum_rank_tokens", ctypes.c_int64),
                 ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32),
                 ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32),
-                ("v_floats", ctypes.c_int64), ("n_span_ctas", ctypes.c_int32), ("span_cluster", ctypes.c_int32),
+                ("v_floats", ctypes.c_int64), ("decode_ctas", ctypes.c_int32), ("decode_stages", ctypes.c_int32),
                 ("n_prefill_ctas", ctypes.c_int32), ("prefill_cluster", ctypes.c_int32)]
 
 
@@ -267,7 +267,7 @@ class LoraPool:
                "pages": arr(m.pages, int(m.sum_rank_groups)), "seg_kind": arr(m.seg_kind, m.S)}
         for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens",
                   "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units", "v_floats",
-                  "n_span_ctas", "span_cluster", "n_prefill_ctas", "prefill_cluster"):
+                  "decode_ctas", "decode_stages", "n_prefill_ctas", "prefill_cluster"):
             out[k] = int(getattr(m, k))
         return out
 

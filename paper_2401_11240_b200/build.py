@@ -53,14 +53,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == dig:
         return LIB
     os.makedirs(OBJ_DIR, exist_ok=True)
-    objs = []
+    jobs = []
     for src in _sources():
         obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
             cmd = [NVCC] + NVCC_FLAGS + DEFS + ["-c", src, "-o", obj]
         else:
             cmd = ["g++"] + CXX_FLAGS + DEFS + ["-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        jobs.append((cmd, obj))
+    # the translation units compile independently: in parallel
+    import concurrent.futures as cf
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[0], capture_output=True, text=True), jobs))
+    objs = []
+    for (cmd, obj), r in zip(jobs, results):
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("compile failed: " + " ".join(cmd))

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstring>
 
 #include "kernel_config.h"
@@ -191,15 +192,18 @@ __global__ void __launch_bounds__(kFbThreads, 1)
     if (warp == 0) {
         // ===================== TMA producer =====================
         const int ngr = rp / 4;
-        // contiguous adapters: the rp rank rows as 2D boxes of 128/64/32/16 rows (one TMA request
-        // instead of rp/4 gather4s); rows r..rp-1 then hold neighbouring pages, which meet V's
-        // zero columns (shrink: V columns >= r are zeroed; expand: they multiply those zeros)
+        // contiguous adapters: the first rb = r & ~7 rank rows as 2D boxes of 128/64/32/16/8 rows
+        // (one TMA request instead of rb/4 gather4s); rows [rb, rp) by gather4 with the pool's zero
+        // page past r -- never the pages after the adapter's run (another tenant's or freed rows,
+        // where an Inf would turn 0 * B into NaN)
         const bool use_box = first_page >= 0 && a.box_maps != nullptr;
+        const int rb = use_box ? (r & ~7) : 0;
+        const bool gat = lane >= rb / 4 && lane < ngr;
         auto boxes = [&](uint32_t dst, int map_base, int col, uint32_t bar) {
             int row = 0;
-            for (int k = 4; k >= 1; --k) {
+            for (int k = 4; k >= 0; --k) {
                 const int R = 8 << k;
-                while (rp - row >= R) {
+                while (rb - row >= R) {
                     fb_tma_2d(dst + (uint32_t)row * 128u,
                               reinterpret_cast<const CUtensorMap*>(a.box_maps + (map_base + k) * 128), col,
                               first_page + row, bar);
@@ -224,10 +228,10 @@ __global__ void __launch_bounds__(kFbThreads, 1)
                 // W rows [64kc, 64kc+64) x columns [n0, n0+NT): NT/64 MN-major atom columns of 8 KB
 #pragma unroll
                 for (int h = 0; h < NT / 64; ++h) fb_tma_2d(sb + 16384 + h * 8192, &a.tm_w, n0 + h * 64, kc * 64, full(stage));
-                if (use_box && r > 0) boxes(sb + 16384 + NT * 128, 0, kc * 64, full(stage));
+                if (rb > 0) boxes(sb + 16384 + NT * 128, 0, kc * 64, full(stage));
             }
             __syncwarp();
-            if (!use_box && lane < ngr)
+            if (gat)
                 fb_gather4(sb + 16384 + NT * 128 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
             if (++stage == nst) { stage = 0; phase ^= 1u; }
         }
@@ -235,12 +239,12 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             fb_wait(empty(stage), phase ^ 1u);
             if (lane == 0) {
                 fb_arrive_tx(b_full, (uint32_t)(rp * NT * 2));
-                if (use_box)
+                if (rb > 0)
                     for (int h = 0; h < NT / 64; ++h)
-                        boxes(bbuf + (uint32_t)(h * (rp / 8)) * 1024u, kSpanBoxKinds, n0 + h * 64, b_full);
+                        boxes(bbuf + (uint32_t)(h * (rp / 8)) * 1024u, kBoxKinds, n0 + h * 64, b_full);
             }
             __syncwarp();
-            if (!use_box && lane < ngr)
+            if (gat)
 #pragma unroll
                 for (int h = 0; h < NT / 64; ++h) {
                     const uint32_t dst = bbuf + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
@@ -377,13 +381,17 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
     a.zero_page = L.zero_page;
     FbBlob blob;   // the kernel-parameter blob (copied into the launch)
     std::memcpy(blob.w, words, (size_t)n_words * 4);
-    static bool configured = false;
-    if (!configured) {
+    // cudaFuncSetAttribute is per device: one bit per device
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return (int)cudaErrorInvalidDevice;
+    const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
+    if (!bit || !(configured.load(std::memory_order_acquire) & bit)) {
         cudaError_t ce = cudaFuncSetAttribute(lora_fused_base_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFbSmem);
         if (ce == cudaSuccess)
             ce = cudaFuncSetAttribute(lora_fused_base_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFbSmem);
         if (ce != cudaSuccess) return (int)ce;
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     a.ring_bytes = kFbRingBytes;
     if (L.H_out % 256 == 0)

@@ -45,16 +45,7 @@ constexpr int kGcFields = 9;     // rank, page_off, tok_off, ntok, shrink_base, 
 enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB };
 constexpr int kMaxJobs = 4;      // pools fused into one launch pair by lora_apply_multi (e.g. q, k, v)
 
-// cluster-span decode kernel (span_kernel.cu): CTA record of kSpanRecWords int32 words
-//   [0] job | span << 4 | index in span << 12 | span leader's rank in the cluster << 20
-//   [1] rank | ntok << 16      (rank 0: idle CTA padding the last cluster)
-//   [2] first page of the gc's (contiguous) rank rows   [3] blob word of the gc's first token
-//   [4] scale (fp32 bits)      [5] kc | nc << 16 (ring chunk widths, powers of two)
-//   [6] k0 | nk << 16          [7] n0 | nn << 16 (this CTA's slices of H_in and H_out)
-constexpr int kSpanRecWords = 8;
-constexpr int kSpanTok = 8;                       // tokens per group-chunk (MMA N)
-constexpr int kSpanMaxStages = 12;
-constexpr int kSpanBoxKinds = 5;                  // TMA boxes {64 columns, 8 << k rows}, k < 5 (<= 128 rows)
+constexpr int kBoxKinds = 5;                      // 2D TMA boxes {64 columns, 8 << k page rows}, k < 5
 
 LORA_HD int vec_elems(int esz) { return 16 / esz; }             // elements per 16-B vector
 LORA_HD int tok_chunk(int esz) { return esz == 2 ? kTokChunkMma : kTokChunk; }
@@ -67,6 +58,9 @@ LORA_HD int expand_ncols(int r, int esz) {
     int c = pow2floor(kExpandBytes / (r * esz));
     return c < kMaxNcols ? c : kMaxNcols;
 }
+// row stride of a gc's rank-r intermediate in the v scratch: r rounded up to 4 floats, so every
+// [k-slice][token] row starts 16-B aligned (float4 loads) -- layout [ksplit][ntok][v_stride(r)]
+LORA_HD int v_stride(int r) { return (r + 3) & ~3; }
 LORA_HD int shrink_jblocks(int r, int esz) { return (r + shrink_rows(esz) - 1) / shrink_rows(esz); }
 
 }  // namespace lora

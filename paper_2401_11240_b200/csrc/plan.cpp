@@ -10,6 +10,13 @@
 
 #include "kernel_config.h"
 
+#ifndef LORA_EXP_PF_SPLIT
+#define LORA_EXP_PF_SPLIT 0
+#endif
+#ifndef LORA_EXP_PF_SPLITK
+#define LORA_EXP_PF_SPLITK 0
+#endif
+
 namespace lora {
 
 static inline int32_t f32_bits(float f) {
@@ -148,10 +155,11 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         int split = 1;
         bool splitk = false;
         if (tiles > 0 && pf_sms > 0) {
-            static const bool force_splitk = getenv("LORA_EXP_PF_SPLITK") != nullptr;   // experiments
-            static const int force_split = getenv("LORA_EXP_PF_SPLIT") ? atoi(getenv("LORA_EXP_PF_SPLIT")) : 0;
+            // experiment builds only (LORA_BUILD_DEFS): -DLORA_EXP_PF_SPLIT=s forces s CTAs per tile,
+            // -DLORA_EXP_PF_SPLITK=1 forces the split-K cluster mode
+            const int force_split = LORA_EXP_PF_SPLIT;
             split = force_split > 0 ? std::min(nct, force_split) : std::max(1, std::min(nct, pf_sms / tiles));
-            splitk = force_splitk || split <= 8 || H_in > H_out;
+            splitk = LORA_EXP_PF_SPLITK || split <= 8 || H_in > H_out;
             if (splitk) split = std::min(split, std::min(8, H_in / 64));
             while (split > 1 && (tiles * split + (int)pages_words.size()) * 8 > kPfMaxBlobWords) --split;
         }
@@ -258,7 +266,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         shrink += ksplit * shrink_jblocks(r, esz);
         const int nc = expand_ncols(r, esz);
         expand += (H_out + nc - 1) / nc;
-        voff += (int64_t)ksplit * gcs[c].ntok * r;
+        voff += (int64_t)ksplit * gcs[c].ntok * v_stride(r);
     }
     if (voff > INT32_MAX) { err = "batch too large for the SIMT scratch"; return LORA_ERR_ARG; }
     std::copy(blob_pages.begin(), blob_pages.end(), pl.blob.begin() + pages_base);
@@ -375,93 +383,6 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
     m.vbuf_floats = voff;
     m.blob_esz = plans[0]->blob_esz;
     return append_unit_table(m, err);
-}
-
-}  // namespace lora
-
-namespace lora {
-
-static int pow2ceil(int v) { int p = 1; while (p < v) p *= 2; return p; }
-
-int span_of(int r, int H_in, int H_out, const SpanParams& sp) {
-    // the span aims at target_bytes of adapter rows per CTA (more streams through the ring)
-    const int64_t bytes = (int64_t)r * (H_in + H_out) * 2;
-    int s = pow2ceil((int)std::min<int64_t>(1 << 20, std::max<int64_t>(1, (bytes + sp.target_bytes - 1) / sp.target_bytes)));
-    s = std::min(s, sp.cluster);
-    // every CTA of the span owns >= 16 columns of H_in and of H_out (one MMA k-step / tile)
-    while (s > 1 && (H_in / s < 16 || H_out / s < 16)) s /= 2;
-    // x / y staging ([8][slice]) bounds the slices: hard limit
-    const int hmax = std::max(H_in, H_out);
-    const int smin = pow2ceil((hmax + sp.max_slice - 1) / sp.max_slice);
-    if (smin > sp.cluster) return 0;
-    return std::max(s, smin);
-}
-
-bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanParams& sp) {
-    pl.span_blob.clear();
-    pl.n_span_cta = 0;
-    pl.span_cluster = 0;
-    pl.span_max_rank = pl.span_max_sk = pl.span_max_sn = 0;
-    if (pl.blob.empty() || pl.n_gc == 0) return false;
-    const int32_t* h = pl.blob.data();
-    const int n_gc = h[0], n_pages = h[3], n_toks = h[4];
-    const int pages_base = kHdrWords + kGcFields * n_gc, toks_base = pages_base + n_pages;
-    struct G { int gc, s; };
-    std::vector<G> order;
-    order.reserve(n_gc);
-    for (int c = 0; c < n_gc; ++c) {
-        const int32_t* e = h + kHdrWords + kGcFields * c;
-        const int job = e[GC_JOB];
-        const int s = span_of(e[GC_RANK], H_in[job], H_out[job], sp);
-        if (s == 0 || e[GC_NTOK] > kSpanTok) return false;
-        // TMA boxes need the rank rows as one run of consecutive pages (page reference < 0)
-        if (e[GC_PAGE_OFF] >= 0) return false;
-        order.push_back({c, s});
-    }
-    // spans are powers of two: placed in descending size, each starts at a multiple of its size,
-    // so none crosses a cluster boundary (perfect packing but for the last cluster)
-    std::stable_sort(order.begin(), order.end(), [](const G& a, const G& b) { return a.s > b.s; });
-    int n_cta = 0;
-    for (const G& g : order) n_cta += g.s;
-    n_cta = (n_cta + sp.cluster - 1) / sp.cluster * sp.cluster;
-    const int rec_words = kSpanRecWords * n_cta;
-    pl.span_blob.assign((size_t)rec_words + n_pages + n_toks, 0);
-    int32_t* out = pl.span_blob.data();
-    std::copy(h + pages_base, h + pages_base + n_pages, out + rec_words);
-    std::copy(h + toks_base, h + toks_base + n_toks, out + rec_words + n_pages);
-    int cta = 0;
-    for (const G& g : order) {
-        const int32_t* e = h + kHdrWords + kGcFields * g.gc;
-        const int job = e[GC_JOB], r = e[GC_RANK], s = g.s;
-        const int hi = H_in[job], ho = H_out[job];
-        const int sk = ((hi + s - 1) / s + 15) / 16 * 16, sn = ((ho + s - 1) / s + 15) / 16 * 16;
-        // chunk widths: powers of two >= 64 (the TMA box width) filling a stage of rows8 rows
-        const int rows8 = (r + 7) & ~7;
-        int kc = std::max(64, pow2floor(std::max(1, sp.stage_bytes / (2 * rows8))));
-        int nc = kc;
-        kc = std::max(64, std::min(kc, pow2ceil(sk)));
-        nc = std::max(64, std::min(nc, pow2ceil(sn)));
-        const int leader = cta % sp.cluster;
-        for (int i = 0; i < s; ++i, ++cta) {
-            int32_t* w = out + (size_t)kSpanRecWords * cta;
-            const int k0 = i * sk, n0 = i * sn;
-            const int nk = std::max(0, std::min(sk, hi - k0)), nn = std::max(0, std::min(sn, ho - n0));
-            w[0] = job | (s << 4) | (i << 12) | (leader << 20);
-            w[1] = r | (e[GC_NTOK] << 16);
-            w[2] = ~e[GC_PAGE_OFF];   // first page of the contiguous run
-            w[3] = rec_words + n_pages + (e[GC_TOK_OFF] - toks_base);
-            w[4] = e[GC_SCALE];
-            w[5] = kc | (nc << 16);
-            w[6] = std::min(k0, 0xffff) | (nk << 16);
-            w[7] = std::min(n0, 0xffff) | (nn << 16);
-        }
-        pl.span_max_rank = std::max(pl.span_max_rank, r);
-        pl.span_max_sk = std::max(pl.span_max_sk, sk);
-        pl.span_max_sn = std::max(pl.span_max_sn, sn);
-    }
-    pl.n_span_cta = n_cta;
-    pl.span_cluster = sp.cluster;
-    return true;
 }
 
 }  // namespace lora

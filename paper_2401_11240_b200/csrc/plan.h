@@ -46,6 +46,7 @@ struct Plan {
     int32_t n_jobs = 1;                          // pools fused by lora_apply_multi
     int32_t job_shrink_base[4] = {0, 0, 0, 0};   // first shrink / expand unit of each job
     int32_t job_expand_base[4] = {0, 0, 0, 0};
+
     // ---- tcgen05 prefill work (N2) ----
     std::vector<PrefillSeg> prefill;
     int32_t n_prefill_tiles = 0;     // 128-token tiles on the tensor-core path (canonical count)
@@ -53,17 +54,13 @@ struct Plan {
                                      // first_page|-1, first column tile, end column tile}, then pages
     int32_t n_pf_tiles = 0;          // prefill CTAs (tiles x pf_cs)
     int32_t pf_cs = 1;               // CTAs per token tile (a cluster: split-K shrink + column split)
-    // ---- cluster-span decode work (N1c, span_kernel.cu): one grid per apply ----
-    std::vector<int32_t> span_blob;  // [n_span_cta][kSpanRecWords] CTA records, then pages, then tokens
-    int32_t n_span_cta = 0;          // multiple of the cluster size (idle CTAs pad the last cluster)
-    int32_t span_cluster = 0;        // cluster size the records were packed for (0 = not built)
-    int32_t span_max_rank = 0, span_max_sk = 0, span_max_sn = 0;
+    int32_t stream_ctas = 0, stream_ns = 0;   // bf16 decode on the streaming kernel (0 = kernel pair)
 
     // back to the default state but keeping every vector's capacity (one plan per apply: the
     // host planner is on the per-call path, so it should not reallocate)
     void reset() {
         std::vector<int32_t>* iv[] = {&tok_seg, &group_id, &group_rank, &group_ntok, &group_page_off, &group_tok_off,
-                                      &group_tokens, &pages, &seg_kind, &blob, &pf_blob, &span_blob};
+                                      &group_tokens, &pages, &seg_kind, &blob, &pf_blob};
         for (auto* v : iv) v->clear();
         group_scale.clear();
         prefill.clear();
@@ -75,24 +72,9 @@ struct Plan {
         for (int i = 0; i < 4; ++i) job_shrink_base[i] = job_expand_base[i] = 0;
         n_prefill_tiles = n_pf_tiles = 0;
         pf_cs = 1;
-        n_span_cta = span_cluster = span_max_rank = span_max_sk = span_max_sn = 0;
+        stream_ctas = stream_ns = 0;
     }
 };
-
-// Span-path parameters (per pool; fixed for a device so the result of a token is a fixed
-// function of (x_t, adapter): the span of a rank depends only on r, H_in, H_out and these).
-struct SpanParams {
-    int cluster = 16;          // thread-block cluster size (CTAs); spans are powers of two <= cluster
-    int target_bytes = 65536;  // adapter bytes per CTA the span size aims at
-    int stage_bytes = 16384;   // bytes of one ring stage (A or B chunk: r rows x kc|nc columns)
-    int n_stages = 4;          // ring stages (all issued before griddepcontrol.wait)
-    int max_slice = 2048;      // largest per-CTA k or n slice (x / y staging is [8][slice])
-};
-// span (CTAs per group-chunk) for rank r, or 0 if the shape needs more than `cluster` CTAs
-int span_of(int r, int H_in, int H_out, const SpanParams& sp);
-// Builds pl.span_blob from the gc records of pl.blob (a build_plan or merge_plans result);
-// H_in/H_out per job.  Returns false (pl.span_cluster = 0) if some gc does not fit the span path.
-bool build_span_work(Plan& pl, const int* H_in, const int* H_out, const SpanParams& sp);
 
 // Builds `plan`.  tc_enabled=false routes every token through the SIMT kernel.  pad_zero_page >= 0
 // pads every group's decode work to the batch's max rank with that (all-zero) page (BGMV mode;
@@ -112,8 +94,11 @@ struct DecodeLaunch {
     int32_t* meta_dev;     // device scratch for metadata too large for kernel parameters
     unsigned long long* trace;   // optional per-unit timestamps (lora_debug_set_trace), or null
     int H_in, H_out, esz, num_sms;
-    int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel, bit 2: one fused grid (bf16)
-    int* gc_sync = nullptr;      // fused mode: pool's zeroed counter buffer + 1 (2 * n_gc words)
+    int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel
+    int stream_ctas = 0;         // > 0 (bf16, phases 3): the persistent streaming kernel with this grid
+    int stream_ns = 2;           //   ... and this many ring stages
+    int* gc_cnt = nullptr;       //   ... and the pool's counters (2 * n_gc words, zero; [-1] timeout flag)
+    const Plan* plan = nullptr;   // the plan being launched (set by launch_decode)
     struct More {                // jobs 1.. of a fused multi-pool apply (job 0 = the fields above)
         const void* x;
         void* y;
@@ -123,20 +108,12 @@ struct DecodeLaunch {
     } more[3];
     int n_jobs = 1;
 };
-struct SpanLaunchDesc {     // the cluster-span decode kernel's operands, per fused job
-    const void* x[4];
-    void* y[4];
-    const void* tmaps[4];    // device copy of the pool's span tensor maps (span_make_tmaps)
-    int H_in[4], H_out[4];
-    int n_jobs;
-    unsigned long long* trace;
-};
 struct PrefillLaunch {
     const void* x;
     void* y;
     const void* tm_a;      // 128-B CUtensorMap of the A pages (gather4 box {64, 1})
     const void* tm_b;      // 128-B CUtensorMap of the B pages
-    const void* box_maps;  // device: the pool's 2D box maps (span_make_tmaps: A boxes {64, 8<<k}, then B)
+    const void* box_maps;  // device: the pool's 2D box maps (make_box_tmaps: A boxes {64, 8<<k}, then B)
     const int32_t* meta_dev;
     unsigned long long* trace;
     int T, H_in, H_out, zero_page, num_sms;
@@ -152,15 +129,12 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& merged, std::stri
 typedef struct CUstream_st* lora_cuda_stream;
 namespace lora {
 int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
-int launch_span(const Plan& pl, const SpanLaunchDesc& L, lora_cuda_stream st, int* launches);
 // zero-copy cold-start copy of one adapter (load_kernel.cu): sA/sB device-visible pinned host rows
 int launch_load(char* dA, char* dB, const void* sA, const void* sB, int64_t ra, int64_t rb, int rank,
                 const int32_t* pages, int num_sms, lora_cuda_stream st);
-bool span_fits(const Plan& pl);           // the launch's smem layout fits one CTA
-const SpanParams& span_params();          // process-wide (env knobs LORA_SPAN_* for sweeps)
-int span_max_blob_words();
-// writes the 2 * kSpanBoxKinds CUtensorMaps (128 B each) of a bf16 pool to host_out; 0 on success
-int span_make_tmaps(void* host_out, const void* dA, const void* dB, int n_rows, int H_in, int H_out);
+// writes the 2 * kBoxKinds CUtensorMaps (128 B each; A maps then B maps, box {64, 8 << k}) of a
+// bf16 pool's page arrays to host_out; 0 on success
+int make_box_tmaps(void* host_out, const void* dA, const void* dB, int n_rows, int H_in, int H_out);
 int launch_prefill(const Plan& pl, const PrefillLaunch& L, lora_cuda_stream st, int* launches);
 
 // NEXT f2: the delta fused into the base projection GEMM (fused_base_kernel.cu)

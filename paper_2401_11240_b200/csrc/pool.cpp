@@ -39,7 +39,7 @@ struct lora_pool {
     bool tc_prefill = false;             // tensor-core prefill path available for this pool
     alignas(64) unsigned char tm_a[128]; // TMA maps of the page arrays (gather4 boxes {64, 1})
     alignas(64) unsigned char tm_b[128];
-    void* span_tmaps = nullptr;          // device: 2 x kSpanBoxKinds tensor maps of the page arrays (span kernel)
+    void* box_maps = nullptr;            // device: 2 x kBoxKinds 2D box tensor maps of the page arrays (TMA boxes)
     std::vector<uint8_t> page_used;
     int free_pages = 0;
     AdapterTable table;
@@ -53,10 +53,10 @@ struct lora_pool {
     size_t vbuf_cap = 0;                 // floats
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
-    int32_t* gc_sync = nullptr;          // fused decode: [0] timeout flag, then 2 counters per gc (zeroed)
+    int32_t* gc_sync = nullptr;          // streaming decode: [0] spin-timeout flag, then 2 counters per gc (zero)
     size_t gc_sync_cap = 0;
-    int fused_decode = 0;                // LORA_OPT_DECODE_FUSED: 0 pair, 1 one grid, 2 flag-chained pair
-    int decode_path = 0;                 // LORA_OPT_DECODE_PATH: 0 kernel pair, 1 cluster-span kernel (bf16)
+    int decode_kernel = 0;               // LORA_OPT_DECODE_KERNEL: 0 streaming kernel (bf16), 1 kernel pair
+    int decode_stages = 2;               // LORA_OPT_DECODE_STAGES: ring stages of the streaming kernel
     bool load_kernel = false;            // LORA_OPT_LOAD_KERNEL: cold-start copies by a zero-copy gather kernel
     bool pad_max_rank = false;           // LORA_OPT_PAD_MAX_RANK: BGMV-style padded decode work (comparison)
     Plan plan;
@@ -194,11 +194,11 @@ lora_status lora_pool_create_ex(int hidden_in, int hidden_out, int max_adapters,
         // page contents start zeroed (rows a TMA box loads past an adapter are then finite)
         if (e == cudaSuccess) e = cudaMemset(p->dA, 0, (size_t)(p->n_pages + 1) * hidden_in * esz);
         if (e == cudaSuccess) e = cudaMemset(p->dB, 0, (size_t)(p->n_pages + 1) * hidden_out * esz);
-        if (e == cudaSuccess && esz == 2) {
-            alignas(64) unsigned char maps[2 * kSpanBoxKinds * 128];
-            if (span_make_tmaps(maps, p->dA, p->dB, p->n_pages + 1, hidden_in, hidden_out) == 0) {
-                e = cudaMalloc(&p->span_tmaps, sizeof(maps));
-                if (e == cudaSuccess) e = cudaMemcpy(p->span_tmaps, maps, sizeof(maps), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && p->tc_prefill) {
+            alignas(64) unsigned char maps[2 * kBoxKinds * 128];
+            if (make_box_tmaps(maps, p->dA, p->dB, p->n_pages + 1, hidden_in, hidden_out) == 0) {
+                e = cudaMalloc(&p->box_maps, sizeof(maps));
+                if (e == cudaSuccess) e = cudaMemcpy(p->box_maps, maps, sizeof(maps), cudaMemcpyHostToDevice);
             }
         }
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
@@ -227,11 +227,11 @@ lora_status lora_pool_destroy(lora_pool* p) {
         for (auto& kv : p->table)
             if (kv.second.ready) cudaEventDestroy((cudaEvent_t)kv.second.ready);
         if (p->dA) cudaFree(p->dA);
-        if (p->span_tmaps) cudaFree(p->span_tmaps);
+        if (p->box_maps) cudaFree(p->box_maps);
+        if (p->gc_sync) cudaFree(p->gc_sync);
         if (p->dB) cudaFree(p->dB);
         if (p->vbuf) cudaFree(p->vbuf);
         if (p->pf_scratch) cudaFree(p->pf_scratch);
-        if (p->gc_sync) cudaFree(p->gc_sync);
         if (p->meta_dev) cudaFree(p->meta_dev);
         for (void* b : p->retired) cudaFree(b);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
@@ -358,6 +358,21 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     return LORA_OK;
 }
 
+// bf16 decode work of a full apply goes to the persistent streaming kernel (one grid, one CTA per SM)
+// unless the pool asks for the kernel pair or the metadata exceeds one launch's parameters
+static lora_status use_stream(lora_pool* p, Plan& pl, DecodeLaunch& L) {
+    pl.stream_ctas = pl.stream_ns = 0;
+    if (p->esz != 2 || p->decode_kernel != 0 || pl.n_gc == 0 || pl.blob.size() > (size_t)kMaxParamBlobWords) return LORA_OK;
+    lora_status s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync");
+    if (s != LORA_OK) return s;
+    pl.stream_ctas = std::min(p->num_sms, std::max(pl.n_shrink, pl.n_expand));
+    pl.stream_ns = p->decode_stages;
+    L.stream_ctas = pl.stream_ctas;
+    L.stream_ns = pl.stream_ns;
+    L.gc_cnt = p->gc_sync + 1;
+    return LORA_OK;
+}
+
 // mode 0: full apply; 1: shrink only (partial v -> v_ext); 2: expand only (v_ext -> y, plan of the
 // last shrink).  Modes 1/2 serve tensor parallelism: the caller all-reduces v in between.
 static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr,
@@ -442,31 +457,11 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if ((s = grow(p, p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
     }
     int launches = 0;
-    bool span = false;
-    if (mode == 0 && p->esz == 2 && p->decode_path == 1 && p->span_tmaps && pl.n_gc > 0) {
-        const int hi[1] = {p->H_in}, ho[1] = {p->H_out};
-        span = build_span_work(p->plan, hi, ho, span_params()) && span_fits(pl) &&
-               (int)pl.span_blob.size() <= span_max_blob_words();
-        if (!span) p->plan.n_span_cta = p->plan.span_cluster = 0;
-    }
-    if (span) {
-        SpanLaunchDesc L{};
-        L.x[0] = x; L.y[0] = y; L.tmaps[0] = p->span_tmaps; L.H_in[0] = p->H_in; L.H_out[0] = p->H_out;
-        L.n_jobs = 1;
-        L.trace = p->trace;
-        cudaError_t e = (cudaError_t)launch_span(pl, L, st, &launches);
-        if (e != cudaSuccess) return cuda_fail(e, "lora_apply: span decode kernel launch");
-    }
-    const bool fused = !span && mode == 0 && p->fused_decode && p->esz == 2 && pl.n_gc > 0;
-    if (fused && (s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync")) != LORA_OK) return s;
-    if (pl.n_gc > 0 && !span) {
+    if (pl.n_gc > 0) {
         DecodeLaunch L{x, y, p->dA, p->dB, mode == 0 ? p->vbuf : v_ext, p->meta_dev, p->trace, p->H_in, p->H_out,
                        p->esz, p->num_sms};
         L.phases = mode == 0 ? 3 : mode;
-        if (fused) {
-            L.phases |= p->fused_decode == 2 ? 8 : 4;
-            L.gc_sync = p->gc_sync + 1;
-        }
+        if (mode == 0 && (s = use_stream(p, p->plan, L)) != LORA_OK) return s;
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
@@ -474,7 +469,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if (pl.pf_cs > 1 &&
             (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
             return s;
-        PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
+        PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
         L.pscratch = p->pf_scratch;
         cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
@@ -543,38 +538,15 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     }
     Plan& fz = p0->fused;
     int launches = 0;
-    bool span = false;
-    bool maps_ok = true;
-    for (int i = 0; i < n_pools; ++i) maps_ok = maps_ok && pools[i]->span_tmaps;
-    if (p0->esz == 2 && p0->decode_path == 1 && maps_ok && fz.n_gc > 0) {
-        int hi[kMaxJobs], ho[kMaxJobs];
-        for (int i = 0; i < n_pools; ++i) { hi[i] = pools[i]->H_in; ho[i] = pools[i]->H_out; }
-        span = build_span_work(fz, hi, ho, span_params()) && span_fits(fz) &&
-               (int)fz.span_blob.size() <= span_max_blob_words();
-        if (!span) fz.n_span_cta = fz.span_cluster = 0;
-    }
-    if (span) {
-        SpanLaunchDesc L{};
-        for (int i = 0; i < n_pools; ++i) {
-            L.x[i] = xs[i]; L.y[i] = ys[i]; L.tmaps[i] = pools[i]->span_tmaps;
-            L.H_in[i] = pools[i]->H_in; L.H_out[i] = pools[i]->H_out;
-        }
-        L.n_jobs = n_pools;
-        L.trace = p0->trace;
-        cudaError_t e = (cudaError_t)launch_span(fz, L, st, &launches);
-        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: span decode kernel launch");
-    }
-    if (fz.n_gc > 0 && !span) {
+    if (fz.n_gc > 0) {
         if ((s = grow(p0, p0->vbuf, p0->vbuf_cap, (size_t)std::max<int64_t>(fz.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
         if ((s = grow(p0, p0->meta_dev, p0->meta_cap, fz.blob.size(), false, "meta")) != LORA_OK) return s;
         DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
                        p0->num_sms};
         L.n_jobs = n_pools;
-        if (p0->fused_decode && p0->esz == 2) {
-            if ((s = grow(p0, p0->gc_sync, p0->gc_sync_cap, (size_t)(1 + 2 * fz.n_gc), true, "gc_sync")) != LORA_OK) return s;
-            L.phases |= p0->fused_decode == 2 ? 8 : 4;
-            L.gc_sync = p0->gc_sync + 1;
-        }
+        if ((s = use_stream(p0, fz, L)) != LORA_OK) return s;
+        p0->plan.stream_ctas = fz.stream_ctas;   // lora_debug_metadata reports the leader's plan
+        p0->plan.stream_ns = fz.stream_ns;
         for (int i = 1; i < n_pools; ++i)
             L.more[i - 1] = DecodeLaunch::More{xs[i], ys[i], pools[i]->dA, pools[i]->dB, pools[i]->H_in, pools[i]->H_out};
         cudaError_t e = (cudaError_t)launch_decode(fz, L, st, &launches);
@@ -587,7 +559,7 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
             (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * 128, false, "pf_scratch")) !=
                 LORA_OK)
             return s;
-        PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->span_tmaps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
+        PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
                         p->num_sms};
         L.pscratch = p->pf_scratch;
         cudaError_t e = (cudaError_t)launch_prefill(p->plan, L, st, &launches);
@@ -619,15 +591,18 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
     if (num_segments < 0) return fail(LORA_ERR_ARG, "num_segments < 0");
     if (num_segments == 0) return LORA_OK;
     if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
-    std::string err;
-    lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
-                               false, p->table, err);   // validates the CSR and the ids (canonical metadata)
-    if (s != LORA_OK) return fail(s, err);
-    const int T = seg_indptr[num_segments];
-    if (T == 0) return LORA_OK;
     if (!x || !W || !y) return fail(LORA_ERR_ARG, "x/W/y is NULL");
     if (((uintptr_t)x & 15) || ((uintptr_t)W & 15) || ((uintptr_t)y & 15))
         return fail(LORA_ERR_ALIGN, "x, W and y must be 16-byte aligned");
+    // validates the CSR and the ids into a scratch plan: the pool's own plan (the canonical metadata
+    // of the last lora_apply, and a pending lora_apply_shrink's work) is left untouched
+    std::string err;
+    static thread_local Plan check;
+    lora_status s = build_plan(check, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, false,
+                               p->table, err);
+    if (s != LORA_OK) return fail(s, err);
+    const int T = seg_indptr[num_segments];
+    if (T == 0) return LORA_OK;
     {
         const char *xs = (const char*)x, *ws = (const char*)W, *ys = (const char*)y;
         const size_t xb = (size_t)T * p->H_in * 2, wb = (size_t)p->H_in * p->H_out * 2, yb = (size_t)T * p->H_out * 2;
@@ -697,7 +672,7 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
         if ((s = wait_loaded(p->table.at(o.first), st, p->capturing, "lora_apply_fused_base: wait load")) != LORA_OK)
             return s;
     FusedBaseLaunch L{x, W, y, p->tm_a, p->tm_b, T, p->H_in, p->H_out, p->n_pages};
-    L.box_maps = p->span_tmaps;
+    L.box_maps = p->box_maps;
     cudaError_t e = (cudaError_t)launch_fused_base(L, words.data(), (int)words.size(), n_tiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "lora_apply_fused_base: kernel launch");
     p->launches += 1;
@@ -723,8 +698,21 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             if (s == LORA_OK)
                 s = grow(p, p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
             if (s == LORA_OK) s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
+            // prefill split-K partials: at most one 128 x 128 fp32 tile per CTA, and the planner keeps
+            // split-K grids within the SM count
+            const int64_t pf_ctas = std::min<int64_t>((value + 127) / 128 * 8, p->num_sms);
+            if (s == LORA_OK && p->tc_prefill && value > 0)
+                s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pf_ctas * 128 * 128, false, "pf_scratch");
             return s;
         }
+        case LORA_OPT_DECODE_KERNEL:
+            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_KERNEL takes 0 or 1");
+            p->decode_kernel = (int)value;
+            return LORA_OK;
+        case LORA_OPT_DECODE_STAGES:
+            if (value < 2 || value > 3) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_STAGES takes 2 or 3");
+            p->decode_stages = (int)value;
+            return LORA_OK;
         case LORA_OPT_LOAD_KERNEL:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_LOAD_KERNEL takes 0 or 1");
             p->load_kernel = value == 1;
@@ -732,14 +720,6 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
         case LORA_OPT_PAD_MAX_RANK:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_PAD_MAX_RANK takes 0 or 1");
             p->pad_max_rank = value == 1;
-            return LORA_OK;
-        case LORA_OPT_DECODE_PATH:
-            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_PATH takes 0 or 1");
-            p->decode_path = (int)value;
-            return LORA_OK;
-        case LORA_OPT_DECODE_FUSED:
-            if (value < 0 || value > 2) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_FUSED takes 0, 1 or 2");
-            p->fused_decode = (int)value;
             return LORA_OK;
         default:
             return fail(LORA_ERR_ARG, "unknown option " + std::to_string(option));
@@ -788,8 +768,8 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
     o->n_shrink_units = pl.n_shrink;
     o->n_expand_units = pl.n_expand;
     o->v_floats = pl.vbuf_floats;
-    o->n_span_ctas = pl.n_span_cta;
-    o->span_cluster = pl.span_cluster;
+    o->decode_ctas = pl.stream_ctas;
+    o->decode_stages = pl.stream_ns;
     o->n_prefill_tiles = pl.n_prefill_tiles;
     o->n_prefill_ctas = pl.n_pf_tiles;
     o->prefill_cluster = pl.pf_cs;

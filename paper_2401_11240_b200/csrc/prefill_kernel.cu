@@ -12,11 +12,10 @@
 //   all-zero page, in SMEM only.
 // * One elected thread issues tcgen05.mma (M=128, kind::f16, bf16 inputs, fp32 accumulate);
 //   tcgen05.commit releases ring slots and signals the epilogue.
-// * The epilogue (4 warps = the 128 TMEM lanes) reads D1, applies s_g, splits v into bf16
-//   hi + lo parts written as the expand's A operand (K-major SW128) -- so the expand keeps
-//   v's fp32 accuracy with two MMAs per k-step -- then, per expand tile, reads D2 and adds it
-//   to y with one rounding.  D2 is double-buffered in TMEM so the epilogue of tile n overlaps
-//   the MMAs of tile n+1.
+// * The epilogue (4 warps = the 128 TMEM lanes) reads D1, applies s_g and rounds v once to
+//   bf16, written as the expand's A operand (K-major SW128; reading R4) -- then, per
+//   expand tile, reads D2 and adds it to y with one rounding.  D2 is double-buffered in TMEM so
+//   the epilogue of tile n overlaps the MMAs of tile n+1.
 // The path is HBM-bound (x read once, y read+written once per tile; adapter rows mostly
 // from L2), so tensor-pipe utilisation is reported next to the HBM roofline.
 #include <cuda.h>
@@ -24,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstring>
 
 #include "kernel_config.h"
@@ -263,14 +263,18 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             const int j = lane * 4 + q;
             pg[q] = j < r ? M[poff + j] : a.zero_page;
         }
-        // contiguous adapters: rp rank rows as 2D boxes of 128/64/32/16 rows (one TMA request
-        // instead of rp/4 gather4s; the request rate bounded the rank-128 tiles); rows r..rp-1
-        // then hold neighbouring pages, which the epilogue neutralises by zeroing V there
+        // contiguous adapters: the first rb = r & ~7 rank rows as 2D boxes of 128/64/32/16/8 rows
+        // (one TMA request instead of rb/4 gather4s; the request rate bounded the rank-128 tiles).
+        // Rows [rb, rp) come by gather4 with the pool's zero page past r, never from the pages
+        // after the adapter's run (another tenant's rows, or freed ones: an Inf there would turn
+        // 0 * B into NaN in this tenant's y)
+        const bool use_box = first_page >= 0 && a.box_maps != nullptr;
+        const int rb = use_box ? (r & ~7) : 0;
         auto boxes = [&](uint32_t dst, int map_base, int col, uint32_t bar) {
             int row = 0;
-            for (int k = 4; k >= 1; --k) {
+            for (int k = 4; k >= 0; --k) {
                 const int R = 8 << k;
-                while (rp - row >= R) {
+                while (rb - row >= R) {
                     tma_2d(dst + (uint32_t)row * 128u,
                            reinterpret_cast<const CUtensorMap*>(a.box_maps + (map_base + k) * 128), col,
                            first_page + row, bar);
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 }
             }
         };
-        const bool use_box = first_page >= 0 && a.box_maps != nullptr;
+        const bool gat = lane >= rb / 4 && lane < ngr;   // this lane's gather4 group (rows 4 lane .. 4 lane + 3)
         for (int kq = 0; kq < nkc; ++kq) {
             const int kc = kc_lo + kq;
             pf_wait(empty(stage), phase ^ 1u);
@@ -286,10 +290,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             if (lane == 0) {
                 pf_arrive_tx(full(stage), (uint32_t)(128 * 128 + rp * 128));
                 tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
-                if (use_box) boxes(sb + 16384, 0, kc * 64, full(stage));
+                if (rb > 0) boxes(sb + 16384, 0, kc * 64, full(stage));
             }
             __syncwarp();
-            if (!use_box && lane < ngr)
+            if (gat)
                 tma_gather4(sb + 16384 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
             if (++stage == kPfShrinkStages) { stage = 0; phase ^= 1u; }
         }
@@ -305,12 +309,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             const uint32_t sb = ring + stage * kPfStageBytes;
             if (lane == 0) {
                 pf_arrive_tx(full2(stage), (uint32_t)(rp * kPfNTile * 2));
-                if (use_box)
+                if (rb > 0)
                     for (int h = 0; h < 2; ++h)
-                        boxes(sb + (uint32_t)(h * (rp / 8)) * 1024u, kSpanBoxKinds, nt * kPfNTile + h * 64, full2(stage));
+                        boxes(sb + (uint32_t)(h * (rp / 8)) * 1024u, kBoxKinds, nt * kPfNTile + h * 64, full2(stage));
             }
             __syncwarp();
-            if (!use_box && lane < ngr) {
+            if (gat) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t dst = sb + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
@@ -423,18 +427,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {   // four 16-B chunks of 8 columns
-                uint32_t hw[4], lw[4];
+                uint32_t hw[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    // columns >= r are exact zeros (they may come from neighbouring pages on the box path)
+                    // columns >= r are exact zeros (the zero page's rows; kept explicit)
                     const int j0 = c0 + q * 8 + 2 * e;
                     const float f0 = j0 < r ? v[q * 8 + 2 * e] * scale : 0.f;
                     const float f1 = j0 + 1 < r ? v[q * 8 + 2 * e + 1] * scale : 0.f;
                     __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
-                    const float2 hf = __bfloat1622float2(h);
-                    __nv_bfloat162 l = __floats2bfloat162_rn(f0 - hf.x, f1 - hf.y);
                     hw[e] = *reinterpret_cast<uint32_t*>(&h);
-                    lw[e] = *reinterpret_cast<uint32_t*>(&l);
                 }
                 const int col = c0 + q * 8;
                 const int kk = col >> 6, chunk = (col & 63) >> 3;
@@ -568,14 +569,27 @@ int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, i
     return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+int make_box_tmaps(void* host_out, const void* dA, const void* dB, int n_rows, int H_in, int H_out) {
+    char* o = static_cast<char*>(host_out);
+    for (int k = 0; k < kBoxKinds; ++k) {
+        if (make_tmap_bf16(o + k * 128, dA, n_rows, H_in, 8 << k)) return 1;
+        if (make_tmap_bf16(o + (kBoxKinds + k) * 128, dB, n_rows, H_out, 8 << k)) return 1;
+    }
+    return 0;
+}
+
 template <int W>
 static cudaError_t launch_pf(const PrefillArgs& a, const Plan& pl, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
+    // cudaFuncSetAttribute is per device: one bit per device
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
+    if (!bit || !(configured.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(lora_prefill_tc_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kPfSmem);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     PfBlob<W> blob;
     if (W > 1)

@@ -58,9 +58,27 @@ def run_gpu(batch, L, pool=None, y_in=None, stream=None, L_tc=None, seg_indptr=N
 
 
 def rel_l2(y_gpu: np.ndarray, y_ref: np.ndarray, dtype: str) -> float:
-    g = gen.storage_to_f64(y_gpu, dtype).reshape(y_ref.shape)
-    den = np.linalg.norm(y_ref)
-    return float(np.linalg.norm(g - y_ref) / (den if den > 0 else 1.0))
+    """max(global rel-L2 over all elements, every token row's own rel-L2).  The per-token term keeps
+    one wrong row (or one wrong column chunk of a row) from hiding inside a large batch's global
+    norm.  A row's denominator is max(its reference norm, 10 % of the batch's RMS row norm): a row
+    whose delta nearly cancels (||x·A|| << ||x||·||A||, e.g. H_out = 8, rank 1) amplifies the
+    fp32 / bf16 rounding of its shrink sum by that condition number -- arithmetic, not a fault
+    (per-token reading).  A row whose reference is all zero must match exactly
+    (reading R6): inf otherwise."""
+    ref = np.asarray(y_ref, dtype=np.float64)
+    g = gen.storage_to_f64(y_gpu, dtype).reshape(ref.shape)
+    den = np.linalg.norm(ref)
+    err = float(np.linalg.norm(g - ref) / (den if den > 0 else 1.0))
+    if ref.ndim == 2 and ref.shape[0] > 0:
+        dif = np.linalg.norm(g - ref, axis=1)
+        rn = np.linalg.norm(ref, axis=1)
+        zero = rn == 0
+        if np.any(dif[zero] != 0):
+            return float("inf")
+        if np.any(~zero):
+            floor = 0.1 * float(np.sqrt(np.mean(rn[~zero] ** 2)))
+            err = max(err, float(np.max(dif[~zero] / np.maximum(rn[~zero], floor))))
+    return err
 
 
 TOL = {"f32": 1e-5, "bf16": 5e-3}   # BASELINE.json north_star

@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     for n in names:
         assert hasattr(L.LIB, n), n
         assert ctypes.cast(getattr(L.LIB, n), ctypes.c_void_p).value
-    assert L.LIB.lora_abi_version() == 1
+    assert L.LIB.lora_abi_version() == 2
 
 
 def _compare_md(md, ref):

@@ -107,19 +107,18 @@ def test_c3_prefill_reduced(L):
     _check_md(md, _md_ref(b))
 
 
-def test_c3_full_size_sampled(L):
-    """config 3 at full size (32 x 512 tokens): every token of the GPU result vs the oracle on a
-    sampled subset of tokens (the oracle computes them one by one)."""
-    b = gen.config_c3(y_zero=False)
-    y, md = run_gpu(b, L)
-    rng = np.random.default_rng(3)
-    mask = np.zeros(b.T, np.uint8)
-    mask[rng.choice(b.T, 96, replace=False)] = 1
-    mask[[0, 511, 512, b.T - 1]] = 1
-    ref = O.delta_for_batch(b, token_mask=mask, n_threads=8)
-    sel = mask.astype(bool)
-    assert rel_l2(y.reshape(b.T, -1)[sel], ref[sel], "bf16") <= TOL["bf16"]
-    _check_md(md, _md_ref(b))
+def test_c3_full_size_every_token(L):
+    """config 3 at full size (32 x 512 tokens = 128 token tiles, the bench's launch configuration):
+    every one of the 16,384 tokens against the oracle (OpenMP over tokens), global and per-token
+    rel-L2 (gpu_util.rel_l2), run A (delta alone) and run B (accumulate)."""
+    import os
+    for y_zero in (True, False):
+        b = gen.config_c3(y_zero=y_zero)
+        y, md = run_gpu(b, L)
+        assert md["n_prefill_tiles"] == 128
+        ref = O.delta_for_batch(b, n_threads=len(os.sched_getaffinity(0)))
+        assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+        _check_md(md, _md_ref(b))
 
 
 @pytest.mark.parametrize("proj", ["k", "q", "down"])
@@ -423,57 +422,44 @@ def test_apply_multi_qkv_fused_equals_separate(L):
         p.close()
 
 
-def test_fused_decode_grid_and_flag_chain_equal_kernel_pair(L):
-    """LORA_OPT_DECODE_FUSED: one grid per apply (expand units wait on per-gc counters) is bit
-    for bit the PDL kernel pair, over many back-to-back applies on one pool with changing batches
-    (the counters must re-arm after every apply), eagerly and inside a CUDA graph."""
+def test_box_path_never_reads_neighbour_pages(L):
+    """Tenant isolation on the TMA-box path (prefill and fused base GEMM): an adapter of rank 24
+    (not a multiple of 16) whose page run is followed by another adapter whose A and B hold Inf /
+    NaN.  Rows past the rank must come from the zero page: y stays finite and matches the oracle."""
     import torch
-    from paper_2401_11240_b200 import binding as B
-    batches = [gen.config_c2(y_zero=False), gen.config_c2(zipf=True, y_zero=False, tag=3),
-               gen.random_batch(4242, "bf16", 4096, 4096, max_seg=40, max_rank=128, max_len=5, n_adapters=32,
-                                y_zero=False)]
-    for b in batches:
-        pool = make_pool(b, L, L_tc=1 << 30)
-        x = to_torch(b.x, "cuda")
-        outs = {}
-        for fused in (0, 1, 2):
-            pool.set_option(B.LORA_OPT_DECODE_FUSED, fused)
-            y = to_torch(b.y_in, "cuda")
-            for _ in range(7):   # y accumulates 7 deltas
-                pool.apply(x, y, b.seg_indptr, b.adapter_ids)
-            torch.cuda.synchronize()
-            outs[fused] = y.clone()
-        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
-        # graph replays of the fused apply and of the flag-chained pair
-        for mode in (1, 2):
-            pool.set_option(B.LORA_OPT_DECODE_FUSED, mode)
-            y = to_torch(b.y_in, "cuda")
-            st = torch.cuda.Stream()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=st):
-                pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
-            y.copy_(to_torch(b.y_in, "cuda"))
-            with torch.cuda.stream(st):
-                for _ in range(7):
-                    g.replay()
-            torch.cuda.synchronize()
-            assert torch.equal(y, outs[1])
-        pool.set_option(B.LORA_OPT_DECODE_FUSED, 1)
-        y = to_torch(b.y_in, "cuda")
-        st = torch.cuda.Stream()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=st):
-            pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
-        y.copy_(to_torch(b.y_in, "cuda"))
-        with torch.cuda.stream(st):
-            for _ in range(7):
-                g.replay()
-        torch.cuda.synchronize()
-        assert torch.equal(y, outs[1])
-        ref = O.delta_for_batch(b, n_threads=8)
-        y1, _ = run_gpu(b, L, pool=pool)
-        assert rel_l2(y1, ref, "bf16") <= TOL["bf16"]
-        pool.close()
+    rng = np.random.default_rng(11)
+    b = gen.build_batch("iso", 2424, "bf16", 256, 512, [300, 129], [0, 2], {0: 24, 2: 8}, y_zero=False)
+    pool = L.LoraPool(b.H_in, b.H_out, 8, "bf16", max_total_rank=64)
+    pool.set_option(L.binding.LORA_OPT_TC_THRESHOLD, 16)
+    by_id = {a.id: a for a in b.adapters}
+    a0 = by_id[0]
+    pool.load_adapter(0, a0.rank, to_torch(a0.A, pin=True), to_torch(a0.B, pin=True), a0.scale)
+    # neighbour: pages right after adapter 0's run, full of Inf / NaN
+    bad_A = np.full((16, b.H_in), 0x7F80, np.uint16)   # +Inf
+    bad_B = np.full((16, b.H_out), 0x7FC0, np.uint16)  # NaN
+    bad_A[::2] = 0x7FC0
+    pool.load_adapter(1, 16, to_torch(bad_A, pin=True), to_torch(bad_B, pin=True), 1.0)
+    a2 = by_id[2]
+    pool.load_adapter(2, a2.rank, to_torch(a2.A, pin=True), to_torch(a2.B, pin=True), a2.scale)
+    assert pool.adapter_pages(0) == list(range(24)) and pool.adapter_pages(1)[0] == 24
+    ref = O.delta_for_batch(b, n_threads=8)
+    y, md = run_gpu(b, L, pool=pool)
+    assert md["n_prefill_tiles"] == 3 + 2
+    yf = gen.storage_to_f64(y, "bf16")
+    assert np.isfinite(yf).all()
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+    # fused base GEMM: y = x·W + delta, the same pool
+    w = rng.standard_normal((b.H_in, b.H_out)).astype(np.float32) / np.sqrt(b.H_in)
+    W = gen.f32_to_storage(w, "bf16")
+    yb = torch.zeros((b.T, b.H_out), dtype=torch.int16, device="cuda")
+    pool.apply_fused_base(to_torch(b.x, "cuda"), to_torch(W, "cuda"), yb, b.seg_indptr, b.adapter_ids)
+    torch.cuda.synchronize()
+    got = gen.storage_to_f64(from_torch(yb, "bf16"), "bf16").reshape(b.T, b.H_out)
+    base = gen.storage_to_f64(b.x, "bf16").reshape(b.T, b.H_in) @ gen.storage_to_f64(W, "bf16").reshape(b.H_in, b.H_out)
+    want = base + (ref.reshape(b.T, b.H_out) - gen.storage_to_f64(b.y_in, "bf16").reshape(b.T, b.H_out))
+    assert np.isfinite(got).all()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= TOL["bf16"]
+    pool.close()
 
 
 @pytest.mark.parametrize("name", ["c2", "c2_zipf", "c1"])
@@ -644,4 +630,54 @@ def test_prefill_few_tile_splits(L, H_in, H_out, n_tiles):
     assert md["n_prefill_ctas"] == n_tiles * split
     assert md["prefill_cluster"] == (split if splitk else 1)
     ref = O.delta_for_batch(b, n_threads=16)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("stages", [2, 3])
+def test_stream_kernel_bitwise_equals_pair(L, stages):
+    """The persistent streaming decode kernel (default, LORA_OPT_DECODE_KERNEL 0) and the PDL kernel
+    pair (1) run the same arithmetic in the same fixed orders: bitwise-equal y, over single-pool and
+    q/k/v-multi applies, uniform / Zipf / random batches (ranks 1..256, up to 8 tokens per chunk),
+    repeated applies (the per-gc counters must re-arm) and a CUDA graph replay."""
+    import torch
+    from paper_2401_11240_b200 import binding as B
+    batches = [gen.config_c2(y_zero=False), gen.config_c2(zipf=True, y_zero=False, tag=3),
+               gen.random_batch(4242, "bf16", 4096, 1024, max_seg=40, max_rank=256, max_len=5, n_adapters=24,
+                                y_zero=False),
+               gen.random_batch(4343, "bf16", 1000, 3000, max_seg=60, max_rank=200, max_len=12, n_adapters=16,
+                                y_zero=False)]
+    for b in batches:
+        pools = [make_pool(b, L, L_tc=1 << 30) for _ in range(3)]
+        x = to_torch(b.x, "cuda")
+        outs = {}
+        for kern in (1, 0):
+            for p in pools:
+                p.set_option(B.LORA_OPT_DECODE_KERNEL, kern)
+                p.set_option(B.LORA_OPT_DECODE_STAGES, stages)
+            ys = [to_torch(b.y_in, "cuda") for _ in range(4)]
+            for _ in range(3):
+                pools[0].apply(x, ys[0], b.seg_indptr, b.adapter_ids)
+                L.apply_multi(pools, [x] * 3, ys[1:], b.seg_indptr, b.adapter_ids)
+            torch.cuda.synchronize()
+            md = pools[0].metadata()
+            assert (md["decode_ctas"] > 0) == (kern == 0) and (kern == 1 or md["decode_stages"] == stages)
+            st = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                pools[0].apply(x, ys[0], b.seg_indptr, b.adapter_ids, stream=st)
+                L.apply_multi(pools, [x] * 3, ys[1:], b.seg_indptr, b.adapter_ids, stream=st)
+            with torch.cuda.stream(st):
+                for _ in range(2):
+                    g.replay()
+            torch.cuda.synchronize()
+            outs[kern] = [y.clone() for y in ys]
+        for a_, c_ in zip(outs[0], outs[1]):
+            assert torch.equal(a_, c_)
+        for p in pools:
+            p.close()
+    # and one fresh apply against the oracle
+    b = batches[2]
+    ref = O.delta_for_batch(b, n_threads=8)
+    y, md = run_gpu(b, L, L_tc=1 << 30)
+    assert md["decode_ctas"] > 0
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
