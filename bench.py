@@ -71,9 +71,6 @@ def parse():
                     help="q/k/v (same x, independent deltas; the paper adapts W_Q/W_K/W_V together, P:875): one "
                          "lora_apply_multi (default), one lora_apply each in stream order, or forked onto 3 streams; "
                          "o (input = attention output) is always its own lora_apply")
-    ap.add_argument("--decode-kernel", type=int, choices=[0, 1], default=0,
-                    help="LORA_OPT_DECODE_KERNEL: 0 = persistent streaming kernel (default), 1 = PDL kernel pair")
-    ap.add_argument("--decode-stages", type=int, choices=[2, 3], default=2, help="LORA_OPT_DECODE_STAGES")
     ap.add_argument("--min-window-ms", type=float, default=200.0,
                     help="repeat the K-step timed window until this much device time is covered (median reported)")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
@@ -704,8 +701,6 @@ def main():
             for p in range(len(PROJS)):
                 ads = futs[(l, p)].result()
                 pool = L.LoraPool(H, H, 32, "bf16", max_total_rank=sum(a.rank for a in ads))
-                pool.set_option(L.binding.LORA_OPT_DECODE_KERNEL, args.decode_kernel)
-                pool.set_option(L.binding.LORA_OPT_DECODE_STAGES, args.decode_stages)
                 for a in ads:
                     A = torch.from_numpy(a.A.view(np.int16)).pin_memory()
                     B = torch.from_numpy(a.B.view(np.int16)).pin_memory()
@@ -909,8 +904,7 @@ def main():
                                  (layers * len(PROJS) * ranks_sum * 2 * H * 2 / 1e9),
                            "timing": "CUDA graph of one step, K replays per window, CUDA events, max over ranks; "
                                      "median of %d windows" % len(windows),
-                           "qkv_mode": mode, "decode_kernel": ["streaming", "pair"][args.decode_kernel],
-                           "decode_stages": args.decode_stages},
+                           "qkv_mode": mode},
                 "windows": {"n": len(windows), "ms_per_step_min": round(min(windows) / args.steps, 5),
                             "ms_per_step_max": round(max(windows) / args.steps, 5),
                             "covered_ms": round(sum(windows), 1)},

@@ -42,6 +42,8 @@ extern "C" {
 #define LORA_MAX_RANK 256          /* 1 <= rank <= min(LORA_MAX_RANK, hidden_in, hidden_out) */
 
 typedef struct lora_pool lora_pool;   /* opaque; bound to the CUDA device current at create */
+typedef struct lora_tp_comm lora_tp_comm;   /* opaque; one tensor-parallel group's NCCL communicator */
+#define LORA_TP_UNIQUE_ID_BYTES 128          /* size of the group's rendezvous id (ncclUniqueId) */
 
 typedef enum { LORA_F32 = 0, LORA_BF16 = 1 } lora_dtype;
 
@@ -74,14 +76,8 @@ typedef enum {
 #define LORA_OPT_TC_THRESHOLD 1    /* L_tc (default 64); segments with len >= L_tc take the tcgen05 path.
                                       A value larger than any segment forces the SIMT path everywhere. */
 #define LORA_OPT_RESERVE_TOKENS 2  /* pre-size scratch for this many tokens (avoids a cudaMalloc in apply) */
-#define LORA_OPT_DECODE_KERNEL 3   /* bf16 decode tokens of lora_apply / lora_apply_multi: 0 (default) = the
-                                      persistent streaming kernel (one grid per apply, one CTA per SM, adapter
-                                      rows streamed through an SMEM ring, shrink -> expand hand-off per
-                                      (adapter, token chunk) through counters; DESIGN.md §6 N1s); 1 = the
-                                      PDL-chained shrink/expand kernel pair (also used by the TP split calls,
-                                      fp32 pools and batches whose metadata exceeds one launch).  Bitwise equal. */
-#define LORA_OPT_DECODE_STAGES 4   /* ring stages (52 KB each: adapter rows + the unit's x / y rows) of the
-                                      streaming kernel: 2 (default) or 3 */
+/* options 3 and 4 (round-1 decode hand-off / cluster-span experiments) are retired in ABI 2; DESIGN.md
+   §6 keeps their measurements and that of the round-2 persistent streaming kernel */
 
 #define LORA_OPT_PAD_MAX_RANK 5    /* comparison mode: 1 pads every adapter's
                                       decode work to the batch's max rank with the pool's all-zero
@@ -185,24 +181,60 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
                              const int32_t* seg_indptr, const int32_t* adapter_ids, int num_segments, void* stream);
 
 /*
- * Tensor-parallel split of lora_apply (BASELINE.json north_star: "splits B's output dimension
- * (and A's input dimension, with an NCCL all-reduce of the tiny rank-r intermediate)").
- * A TP rank's pool holds the shards A[:, its H_in slice] and B[:, its H_out slice], so the pool's
- * hidden_in / hidden_out are the shard widths.
+ * Tensor parallelism (BASELINE.json north_star: "A tensor-parallel variant splits B's output
+ * dimension (and A's input dimension, with an NCCL all-reduce of the tiny rank-r intermediate over
+ * NVLink) for 70B-sized projections").  The paper's own scheme replicates
+ * A and splits only B, with no communication (§4.2 "Support model parallelism");
+ * splitting A's input dimension too makes every GPU's adapter bytes scale as 1/tp at the cost of one
+ * all-reduce of v = s-less x·A, [T x r] fp32 (c5 decode: 64 tokens x ranks 16..128 = 15,360 B).
+ * A TP rank's pool holds the shards A[:, its H_in slice] and B[:, its H_out slice]: the pool's
+ * hidden_in / hidden_out are the shard widths.  Column-parallel layers (q/k/v/gate/up: x replicated)
+ * pass the rank's x columns as a strided view (x_ld = full width) and their own y shard;
+ * row-parallel layers (o/down: x already sharded) pass their x shard and a strided view of the
+ * partial, pre-all-reduce y (y_ld = full width), which the base layer's own all-reduce completes.
  *
- * lora_apply_shrink -- partial v over this rank's H_in slice:
- *   x           device [T][hidden_in] (the rank's x columns), pool dtype.
- *   v_out       device fp32 buffer of v_capacity floats; receives the partial intermediate in the
- *               library's internal layout (per group-chunk [k_slice][token][rank], unscaled); its
- *               size is lora_metadata_view.v_floats of the same batch (lora_plan).  Identical
- *               batches on every TP rank give identical layouts, so an elementwise SUM all-reduce
- *               of v_out across ranks (NCCL, done by the caller) yields the full-H_in partials.
- *   Every token takes the decode kernels (the tcgen05 prefill path fuses shrink and expand).
- * lora_apply_expand -- y[:, this rank's H_out slice] += s · (Σ v) · B_shard for the batch of the
- *   immediately preceding lora_apply_shrink on this pool, reading the (all-reduced) v_in.
+ * lora_tp_unique_id -- ncclGetUniqueId into id_out[LORA_TP_UNIQUE_ID_BYTES]: rank 0 of the group calls
+ *   it and hands the bytes to the other ranks (the Python binding broadcasts them through the
+ *   torch.distributed process group).  Errors: ARG, NCCL (libnccl.so.2 is resolved at run time).
+ * lora_tp_comm_create -- ncclCommInitRank for (tp_rank, tp_size) on the CUDA device current at the
+ *   call; collective over the group.  The caller owns the handle and destroys it after the pools
+ *   bound to it.  Errors: ARG, NCCL.
+ * lora_tp_comm_destroy -- ncclCommDestroy.  NULL is a no-op.
+ * lora_tp_init -- binds pool p to the group's communicator (NULL unbinds).  Errors: ARG (other device),
+ *   UNSUPPORTED (host-only pool).
+ * lora_apply_tp -- y[:, this rank's out slice] += s·(Σ_ranks x_k·A_k)·B_shard for one batch, all on
+ *   `stream` without host synchronisation: the shrink kernel (partials over this rank's
+ *   H_in slice, per 1,024-wide k-slice), the k-reduce kernel (slices summed in fixed order into the
+ *   compact v [Σ_gc ntok x round_up(r, 4)] fp32), ncclAllReduce(SUM) of that compact v in place
+ *   over the group, the expand kernel.  Every token takes the decode kernels.  Capturable in a CUDA
+ *   graph (NCCL calls are).
+ *     x   device, T rows of hidden_in elements, row stride x_ld elements (0 = hidden_in), 16-B aligned.
+ *     y   device, T rows of hidden_out elements, row stride y_ld elements (0 = hidden_out), 16-B aligned.
+ *   Errors: as lora_apply; ARG without lora_tp_init or with x_ld/y_ld below the widths; NCCL.
+ * lora_load_adapter_shard -- lora_load_adapter of this rank's shard straight from the FULL pinned
+ *   adapter: rows j of A_host [rank][a_ld] columns [a_col0, a_col0 + hidden_in) and of B_host
+ *   [rank][b_ld] columns [b_col0, b_col0 + hidden_out), one cudaMemcpy2DAsync per run of pages on the
+ *   pool's side stream (no host-side slice or re-pin).  Errors: as lora_load_adapter; SHAPE (columns
+ *   outside the full rows), ALIGN (pitch or first column not 16-B aligned).
+ *
+ * The split calls for callers that run their own collective:
+ * lora_apply_shrink -- shrink + k-reduce of this rank's partial v into v_out (device fp32, v_capacity
+ *   floats, 4-B aligned): the compact layout above, size lora_metadata_view.v_floats of the same
+ *   batch (lora_plan).  Identical batches on every rank give identical layouts, so an elementwise
+ *   SUM all-reduce of v_out yields the full-H_in v.  Every token takes the decode kernels.
+ * lora_apply_expand -- y[:, this rank's H_out slice] += s · v · B_shard for the batch of the
+ *   immediately preceding lora_apply_shrink on this pool, reading the (all-reduced) compact v_in.
  * Errors: as lora_apply; ARG if v_capacity is too small or expand has no pending shrink; ALIGN if
  *   v_out / v_in is not 4-byte aligned.
  */
+lora_status lora_tp_unique_id(void* id_out);
+lora_status lora_tp_comm_create(const void* id, int tp_rank, int tp_size, lora_tp_comm** out);
+lora_status lora_tp_comm_destroy(lora_tp_comm* comm);
+lora_status lora_tp_init(lora_pool* p, lora_tp_comm* comm);
+lora_status lora_apply_tp(lora_pool* p, const void* x, int64_t x_ld, void* y, int64_t y_ld, const int32_t* seg_indptr,
+                          const int32_t* adapter_ids, int num_segments, void* stream);
+lora_status lora_load_adapter_shard(lora_pool* p, int32_t id, int rank, const void* A_host, int64_t a_ld, int64_t a_col0,
+                                    const void* B_host, int64_t b_ld, int64_t b_col0, float scale);
 lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_indptr, const int32_t* adapter_ids,
                               int num_segments, float* v_out, int64_t v_capacity, void* stream);
 lora_status lora_apply_expand(lora_pool* p, void* y, const float* v_in, void* stream);
@@ -267,9 +299,8 @@ typedef struct {
     int64_t sum_rank_tokens;         /*     Σ_t r_{a(t)} (flops / 2(H_in+H_out)) */
     int32_t n_decode_units, n_prefill_tiles;   /* kernel work of the last apply (informational) */
     int32_t n_shrink_units, n_expand_units;    /* split of n_decode_units (shrink units come first) */
-    int64_t v_floats;                          /* size of the partial-v buffer (lora_apply_shrink) */
-    int32_t decode_ctas, decode_stages;        /* bf16 decode of the last apply: persistent streaming
-                                                  kernel CTAs and ring stages (0 = kernel pair) */
+    int64_t v_floats;                          /* size of the compact k-reduced v (lora_apply_shrink) */
+    int32_t reserved0, reserved1;
     int32_t n_prefill_ctas, prefill_cluster;   /* tcgen05 prefill grid of the last apply: CTAs
                                                   (tiles x CTAs per tile) and split-K cluster size
                                                   (1 = no split-K) */

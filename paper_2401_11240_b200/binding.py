@@ -21,7 +21,7 @@ HEADER = os.path.join(ROOT, "include", "lora_delta.h")
 LORA_F32, LORA_BF16 = 0, 1
 LORA_POOL_HOST_ONLY = 1
 LORA_KIND_NONE, LORA_KIND_DECODE, LORA_KIND_PREFILL = -1, 0, 1
-LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS, LORA_OPT_DECODE_KERNEL, LORA_OPT_DECODE_STAGES = 1, 2, 3, 4
+LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS = 1, 2
 LORA_OPT_PAD_MAX_RANK, LORA_OPT_LOAD_KERNEL = 5, 6
 LORA_MAX_RANK = 256
 
@@ -59,7 +59,7 @@ class MetadataView(ctypes.Structure):
                 ("sum_rank_tokens", ctypes.c_int64),
                 ("n_decode_units", ctypes.c_int32), ("n_prefill_tiles", ctypes.c_int32),
                 ("n_shrink_units", ctypes.c_int32), ("n_expand_units", ctypes.c_int32),
-                ("v_floats", ctypes.c_int64), ("decode_ctas", ctypes.c_int32), ("decode_stages", ctypes.c_int32),
+                ("v_floats", ctypes.c_int64), ("reserved0", ctypes.c_int32), ("reserved1", ctypes.c_int32),
                 ("n_prefill_ctas", ctypes.c_int32), ("prefill_cluster", ctypes.c_int32)]
 
 
@@ -94,6 +94,12 @@ def _load() -> ctypes.CDLL:
         "lora_apply_multi": [P(vp), P(vp), P(vp), c_int, vp, vp, c_int, vp],
         "lora_apply_expand": [vp, vp, vp, vp],
         "lora_apply_fused_base": [vp, vp, vp, vp, vp, vp, c_int, vp],
+        "lora_tp_unique_id": [vp],
+        "lora_tp_comm_create": [vp, c_int, c_int, P(vp)],
+        "lora_tp_comm_destroy": [vp],
+        "lora_tp_init": [vp, vp],
+        "lora_apply_tp": [vp, vp, c_i64, vp, c_i64, vp, vp, c_int, vp],
+        "lora_load_adapter_shard": [vp, c_i32, c_int, vp, c_i64, c_i64, vp, c_i64, c_i64, ctypes.c_float],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -154,6 +160,55 @@ def _ptr_of(t) -> int:
     if isinstance(t, np.ndarray):
         return int(t.ctypes.data)
     raise TypeError(type(t))
+
+
+TP_UNIQUE_ID_BYTES = 128
+
+
+def tp_unique_id() -> bytes:
+    """lora_tp_unique_id: the TP group's rendezvous id (rank 0 creates it, the others receive it)."""
+    buf = ctypes.create_string_buffer(TP_UNIQUE_ID_BYTES)
+    _check(LIB.lora_tp_unique_id(buf))
+    return buf.raw
+
+
+class TPComm:
+    """lora_tp_comm: one tensor-parallel group's NCCL communicator, owned by the library."""
+
+    def __init__(self, unique_id: bytes, tp_rank: int, tp_size: int):
+        if len(unique_id) != TP_UNIQUE_ID_BYTES:
+            raise ValueError("unique id must be %d bytes" % TP_UNIQUE_ID_BYTES)
+        h = ctypes.c_void_p()
+        _check(LIB.lora_tp_comm_create(ctypes.create_string_buffer(unique_id, TP_UNIQUE_ID_BYTES), int(tp_rank),
+                                       int(tp_size), ctypes.byref(h)))
+        self.handle, self.rank, self.size = h, tp_rank, tp_size
+
+    @classmethod
+    def from_process_group(cls, group=None):
+        """Rank 0 of `group` (torch.distributed) creates the id and broadcasts it; collective."""
+        import torch
+        import torch.distributed as dist
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.zeros(TP_UNIQUE_ID_BYTES, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(tp_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return cls(bytes(t.cpu().numpy().tobytes()), rank, size)
+
+    def close(self) -> None:
+        if self.handle:
+            _check(LIB.lora_tp_comm_destroy(self.handle))
+            self.handle = None
+
+
+def _ld_of(t, width: int) -> int:
+    """row stride (elements) of a 2D torch tensor view whose rows hold `width` contiguous elements."""
+    if hasattr(t, "stride") and t.dim() == 2:
+        if t.stride(1) != 1:
+            raise ValueError("rows must be contiguous")
+        return int(t.stride(0))
+    return int(width)
 
 
 def apply_multi(pools, xs, ys, seg_indptr, adapter_ids, stream=None) -> None:
@@ -228,6 +283,27 @@ class LoraPool:
     def apply_expand(self, y, v_in, stream=None) -> None:
         _check(LIB.lora_apply_expand(self.handle, _ptr_of(y), _ptr_of(v_in), _stream_ptr(stream)))
 
+    def tp_init(self, comm) -> None:
+        """lora_tp_init: bind this (shard) pool to the TP group's communicator (None unbinds)."""
+        _check(LIB.lora_tp_init(self.handle, comm.handle if comm is not None else None))
+        self._tp_comm = comm   # the communicator must outlive the binding
+
+    def apply_tp(self, x, y, seg_indptr, adapter_ids, stream=None) -> None:
+        """lora_apply_tp: shrink -> k-reduce -> NCCL all-reduce of the compact v -> expand, on `stream`.
+        x / y may be strided 2D views (e.g. x[:, k0:k1] of the replicated activations)."""
+        ip, ids = _i32(seg_indptr), _i32(adapter_ids)
+        _check(LIB.lora_apply_tp(self.handle, _ptr_of(x), _ld_of(x, self.hidden_in), _ptr_of(y),
+                                 _ld_of(y, self.hidden_out), _addr(ip), _addr(ids), int(ids.shape[0]),
+                                 _stream_ptr(stream)))
+
+    def load_adapter_shard(self, aid: int, rank: int, A_full, a_col0: int, B_full, b_col0: int, scale: float) -> None:
+        """lora_load_adapter_shard: A_full [rank][H_in_full] / B_full [rank][H_out_full] pinned host tensors of
+        the whole adapter; this pool keeps columns [a_col0, a_col0 + hidden_in) / [b_col0, b_col0 + hidden_out)."""
+        _check(LIB.lora_load_adapter_shard(self.handle, int(aid), int(rank), _ptr_of(A_full), int(A_full.shape[1]),
+                                           int(a_col0), _ptr_of(B_full), int(B_full.shape[1]), int(b_col0),
+                                           float(scale)))
+        self._keep[int(aid)] = (A_full, B_full)
+
     def apply_fused_base(self, x, W, y, seg_indptr, adapter_ids, stream=None) -> None:
         """y = x·W + s·(x·A)·B in one kernel (lora_apply_fused_base): W [H_in][H_out] bf16, y
         overwritten."""
@@ -267,7 +343,7 @@ class LoraPool:
                "pages": arr(m.pages, int(m.sum_rank_groups)), "seg_kind": arr(m.seg_kind, m.S)}
         for k in ("n_seg", "max_rank", "nseg_x_maxrank", "sum_rank_seg", "sum_rank_groups", "sum_rank_tokens",
                   "n_decode_units", "n_prefill_tiles", "n_shrink_units", "n_expand_units", "v_floats",
-                  "decode_ctas", "decode_stages", "n_prefill_ctas", "prefill_cluster"):
+                  "n_prefill_ctas", "prefill_cluster"):
             out[k] = int(getattr(m, k))
         return out
 

@@ -38,7 +38,8 @@ struct DecodeJob {                // one pool's operands (lora_apply_multi fuses
     char* y;
     const char* A;                // pool page arrays
     const char* B;
-    int H_in, H_out, ksplit, pad;
+    int H_in, H_out, ksplit;
+    int x_ld, y_ld;               // row strides of x and y in elements (H_in / H_out unless a TP shard view)
 };
 
 struct DecodeArgs {
@@ -51,9 +52,9 @@ struct DecodeArgs {
     int unit_words;              // 3 (full unit records) or 1 (gc | local only: large batches)
     // bf16 expand smem layout, sized per launch from the batch (max rank / tokens / columns)
     int e_vpitch, e_boff, e_yoff, e_dtoff, e_pgoff, e_smem;
-    int* gc_cnt;                 // streaming kernel: [n_gc] shrink-done, [n_gc] expand-done counters (zero
-                                 // between applies); gc_cnt[-1] = spin-timeout flag
-    int ps_tab;                  // streaming kernel: unit records per CTA (SMEM table rows)
+    float* vred;                 // compact k-reduced v (TP split): written by lora_vreduce_kernel, read by
+                                 // the expand when v_compact is set
+    int v_compact;
     int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
     int job_expand_base[kMaxJobs];
 };
@@ -100,10 +101,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 // per-thread 16-B async copy HBM -> SMEM (LDGSTS): no per-request copy-engine overhead, so it
 // keeps up with HBM for sub-2-KB row slices where cp.async.bulk does not (scripts/microbench_stream.cu)
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t policy) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "l"(policy)
-                 : "memory");
+// (no L2::cache_hint operand: with it, ptxas 12.9 emitted for some expand instantiations an LDGSTS
+// whose 64-bit descriptor sits in an odd uniform register -- "illegal instruction" at run time)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t /*policy*/) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 // L2 prefetch (no data returned to the SM).  Safe before griddepcontrol.wait even for lines a
 // preceding kernel still writes: L2 is the point of coherence, the later real read sees them.
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nk * E::kSize));
         __syncwarp();
         if (lane < ntok)
-            bulk_g2s(xbuf + lane * kSliceBytes, J.x + ((size_t)tok * J.H_in + k0) * E::kSize, (uint32_t)nk * E::kSize,
+            bulk_g2s(xbuf + lane * kSliceBytes, J.x + ((size_t)tok * J.x_ld + k0) * E::kSize, (uint32_t)nk * E::kSize,
                      &bars[1], policy_evict_normal());
     }
     // 3. partial dot products: warp -> (row, k-part)
@@ -455,16 +456,19 @@ __global__ void __launch_bounds__(kConsumerThreads)
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * E::kSize));
         __syncwarp();
         if (lane < ntok)
-            bulk_g2s(ybuf + lane * row_stride, J.y + ((size_t)tok * J.H_out + n0) * E::kSize, (uint32_t)nc * E::kSize,
+            bulk_g2s(ybuf + lane * row_stride, J.y + ((size_t)tok * J.y_ld + n0) * E::kSize, (uint32_t)nc * E::kSize,
                      &bars[1], policy_evict_normal());
     }
     {
-        const int voff = sh->voff;
+        // v: the k-slice partials summed in slice order, or the compact k-reduced v (TP split)
+        const int voff = a.v_compact ? gc_field(M, sh->gc, GC_VRED) : sh->voff;
+        const int ksplit = a.v_compact ? 1 : J.ksplit;
+        const float* vsrc = a.v_compact ? a.vred : a.vbuf;
         const float scale = sh->scale;
         for (int i = tid; i < ntok * r; i += kConsumerThreads) {
             const int t = i / r, j = i - t * r;
             float v = 0.f;
-            for (int k = 0; k < J.ksplit; ++k) v += ld_cg_f32(a.vbuf + voff + (k * ntok + t) * v_stride(r) + j);
+            for (int k = 0; k < ksplit; ++k) v += ld_cg_f32(vsrc + voff + (k * ntok + t) * v_stride(r) + j);
             vsm[t * r + j] = v * scale;
         }
     }
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             for (int t = 0; t < kTokChunk; ++t) {
                 if (t < ntok) {
                     const uint4 yo = lds128(ybuf + t * row_stride + ci * 16);
-                    stg128_na(J.y + ((size_t)sh->tok[t] * J.H_out + n0 + ci * V) * E::kSize, E::add_round(yo, acc[t]));
+                    stg128_na(J.y + ((size_t)sh->tok[t] * J.y_ld + n0 + ci * V) * E::kSize, E::add_round(yo, acc[t]));
                 }
             }
         }
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
                 for (int i = 0; i < V; ++i) d[i] += src[i];
             }
             const uint4 yo = lds128(ybuf + t * row_stride + c2 * 16);
-            stg128_na(J.y + ((size_t)sh->tok[t] * J.H_out + n0 + c2 * V) * E::kSize, E::add_round(yo, d));
+            stg128_na(J.y + ((size_t)sh->tok[t] * J.y_ld + n0 + c2 * V) * E::kSize, E::add_round(yo, d));
         }
     }
     if (a.trace && tid == 0) {
@@ -649,7 +653,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         const int voff = gc_field(M, gc, GC_VOFF);
         if (a.trace) { asm volatile("" ::"r"(page), "r"(tokv)); if (lane == 0) a.trace[(size_t)u * 8 + 7] = gtime(); }
         if (lane < kTokChunkMma) sh->tok[lane] = tokv;
-        if (tokv >= 0) prefetch_l2(J.x + ((size_t)tokv * J.H_in + k0) * ES, (uint32_t)(nk * ES));
+        if (tokv >= 0) prefetch_l2(J.x + ((size_t)tokv * J.x_ld + k0) * ES, (uint32_t)(nk * ES));
         if (lane == 0) {
             mbar_arrive_expect_tx(&bars[0], (uint32_t)(nj * nk * ES));
             sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
@@ -674,7 +678,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
     uint4 xr[kKBlocks];
     {
         const int tk = g < ntok ? sh->tok[g] : -1;
-        const char* xrow = J.x + ((size_t)(tk < 0 ? 0 : tk) * J.H_in + k0) * ES;
+        const char* xrow = J.x + ((size_t)(tk < 0 ? 0 : tk) * J.x_ld + k0) * ES;
 #pragma unroll
         for (int b = 0; b < kKBlocks; ++b) {
             const int k = warp * kKPerWarp + b * 32 + c * 8;
@@ -807,7 +811,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         }
         if (lane < ntok) {
             sh->tok[lane] = tok;
-            prefetch_l2(J.y + ((size_t)tok * J.H_out + n0) * ES, row_bytes);
+            prefetch_l2(J.y + ((size_t)tok * J.y_ld + n0) * ES, row_bytes);
         }
         if (lane < 16) reinterpret_cast<uint32_t*>(zero)[lane] = 0u;
         __syncwarp();
@@ -850,25 +854,28 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * ES));
         __syncwarp();
         if (lane < ntok)
-            bulk_g2s(ybuf + lane * ypitch, J.y + ((size_t)tok * J.H_out + n0) * ES, (uint32_t)nc * ES, &bars[1],
+            bulk_g2s(ybuf + lane * ypitch, J.y + ((size_t)tok * J.y_ld + n0) * ES, (uint32_t)nc * ES, &bars[1],
                      policy_evict_normal());
     }
     // v (fp32, summed over k-slices, scaled) -> bf16 hi/lo tiles [8 tokens][r padded to 16]
     const int rp = (r + 15) & ~15;
     {
-        const int voff = sh->voff;
+        // v: the k-slice partials summed in slice order, or the compact k-reduced v (TP split)
+        const int voff = a.v_compact ? gc_field(M, sh->gc, GC_VRED) : sh->voff;
+        const int ksplit = a.v_compact ? 1 : J.ksplit;
+        const float* vsrc = a.v_compact ? a.vred : a.vbuf;
         const float scale = sh->scale;
         for (int i = tid; i < kTokChunkMma * rp; i += kConsumerThreads) {
             const int t = i / rp, j = i - t * rp;
             float v = 0.f;
             if (t < ntok && j < r) {
                 // k-slice partials: batches of 8 independent loads, summed in slice order
-                const float* src = a.vbuf + voff + t * v_stride(r) + j;
+                const float* src = vsrc + voff + t * v_stride(r) + j;
                 const int stride = ntok * v_stride(r);
-                for (int k0 = 0; k0 < J.ksplit; k0 += 8) {
+                for (int k0 = 0; k0 < ksplit; k0 += 8) {
                     float p[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) p[q] = k0 + q < J.ksplit ? ld_cg_f32(src + (k0 + q) * stride) : 0.f;
+                    for (int q = 0; q < 8; ++q) p[q] = k0 + q < ksplit ? ld_cg_f32(src + (k0 + q) * stride) : 0.f;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) v += p[q];
                 }
@@ -947,7 +954,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
             const float4 d1 = *reinterpret_cast<const float4*>(dt + t * dpitch + q * 8 + 4);
             const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
             const uint4 yo = lds128(ybuf + t * ypitch + q * 16);
-            stg128_na(J.y + ((size_t)sh->tok[t] * J.H_out + n0 + q * 8) * ES, Elem<__nv_bfloat16>::add_round(yo, d));
+            stg128_na(J.y + ((size_t)sh->tok[t] * J.y_ld + n0 + q * 8) * ES, Elem<__nv_bfloat16>::add_round(yo, d));
         }
     }
     if (a.trace && tid == 0) {
@@ -969,495 +976,25 @@ __global__ void __launch_bounds__(kConsumerThreads, MINB)
     expand_mma_body(a, M, blockIdx.x, smem);
 }
 
-// ------------------------------------------------------------------ N1s: persistent streaming decode (bf16)
-// ONE grid per apply of P CTAs (one per SM).  CTA c owns shrink units c, c+P, c+2P, ... and then
-// expand units c, c+P, ... (the unit tables are in gc order, so every CTA meets the early gcs first).
-// Warp roles:
-//  * warp 0, producer: streams each unit's operands HBM/L2 -> a ring of NS SMEM stages with
-//    cp.async.bulk -- the adapter rows (A rank rows of shrink units, B rank-row slices of expand
-//    units) from the first instruction (pool pages are immutable: nothing waits on the preceding
-//    grid), and after griddepcontrol.wait the x rows (shrink) / y rows (expand) of the same unit.
-//  * warps 4..11, consumers: a unit's MMAs with the arithmetic of shrink_mma_body / expand_mma_body
-//    (same fragment layouts and fixed summation orders: results are bitwise those of the kernel
-//    pair), all operands in SMEM; expand units add D to the staged y with one rounding and store it.
-//  * warp 3, publisher: sums a shrink unit's 8 warp partials (fixed order), stores its partial v and
-//    publishes it by a relaxed add to its gc's counter after a gpu-scope fence; consecutive units
-//    that are already reduced share one fence (the fence, an L2 round trip, is the hand-off's cost).
-//  * warps 1 and 2, v loaders (even / odd expand units): acquire the unit's gc counter (all of the
-//    gc's shrink units published), sum the k-slice partials in slice order, scale and split v into
-//    bf16 hi + lo in the warp's SMEM v slot.  The last expand unit of a gc to read v re-arms the gc's
-//    counters (zero) for the pool's next apply.
-// So the HBM stream never stops for a grid hand-off, and the expand of early gcs overlaps the shrink
-// of late ones.  Deadlock freedom: only expand units wait, only on shrink units of this grid, which
-// never wait; the dependent grid launches only after every CTA of this one has triggered (so is
-// resident), so no later grid can take the SM slot of a CTA this grid still needs.  The spin is
-// bounded (0.5 s, then a flag: a broken assumption gives a wrong result, never a hung GPU).
-constexpr int kPsWarps = 12;
-constexpr int kPsThreads = kPsWarps * 32;
-constexpr int kPsConsumer0 = 4;   // first consumer warp
-constexpr int kPsWBytes = 36864;  // weights: >= 16 rows x kAPitch (shrink), r x (ncols*2 + pad) (expand)
-constexpr int kPsXBytes = kTokChunkMma * kAPitch;   // x rows [8][kAPitch] (shrink) / y rows [8][ncols*2 + pad] (expand)
-constexpr int kPsStage = kPsWBytes + kPsXBytes;    // 53,760 B
-static_assert(kShrinkRowsMma * kAPitch <= kPsWBytes, "shrink unit must fit one stage");
-static_assert(kExpandBytes + LORA_MAX_RANK * kPitchPad <= kPsWBytes, "expand unit must fit one stage");
-static_assert(kMaxNcols * 2 + kPitchPad <= kAPitch, "y rows must fit the x/y region");
-constexpr int kPsPart = kConsumerWarps * kShrinkRowsMma * kTokChunkMma;   // floats per partial buffer
-constexpr int kPsMaxPend = 8;                                            // shrink units per publisher fence
-constexpr int kPsRecWords = 32;                                          // per-unit SMEM record (see below)
-
-// per-unit record, decoded once per CTA into SMEM by warp 0 (every role then reads it with LDS)
-enum {
-    R_KIND = 0, R_JOB, R_GC, R_R, R_NTOK, R_PREF, R_VOFF, R_RS,
-    R_J0 = 8, R_NJ, R_K0, R_NK, R_KS,                                        // shrink
-    R_N0 = 8, R_NC = 9, R_BPITCH = 10, R_NTILES = 11, R_NS = 12, R_NE = 13, R_SCALE = 14, R_KSPLIT = 15,   // expand
-    R_TOK = 16                                                               // [8] token rows
-};
-
-// smem: [0,512) barriers + publisher list | unit records [tab][kPsRecWords] | ring NS x kPsStage |
-//       partials [2][kPsPart] | v slots [2][hi,lo][8][vpitch] | 64 zero bytes
-__host__ __device__ constexpr int ps_ring_off(int tab) { return 512 + tab * kPsRecWords * 4; }
-__host__ __device__ constexpr int ps_part_off(int ns, int tab) { return ps_ring_off(tab) + ns * kPsStage; }
-__host__ __device__ constexpr int ps_vring_off(int ns, int tab) { return ps_part_off(ns, tab) + 2 * kPsPart * 4; }
-__host__ __device__ constexpr int ps_zero_off(int ns, int tab, int vpitch) {
-    return ps_vring_off(ns, tab) + 2 * 2 * kTokChunkMma * vpitch;
-}
-__host__ __device__ constexpr int ps_smem(int ns, int tab, int vpitch) { return ps_zero_off(ns, tab, vpitch) + 64; }
-
-__device__ __forceinline__ void ps_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ bool ps_test(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void red_relaxed_gpu(int* p, int v) {
-    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ float4 ld_cg_f4(const float* p) {
-    float4 v;
-    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds32(const void* p) {
-    uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
-    return v;
-}
-
-// decodes unit i of CTA c (shrink units c, c+P, ... then expand units c, c+P, ...) into rec
-__device__ __forceinline__ void ps_decode(const DecodeArgs& a, const int32_t* M, int c, int P, int ns_my, int i,
-                                          int32_t* rec) {
-    const bool shrink = i < ns_my;
-    const int uu = shrink ? c + i * P : c + (i - ns_my) * P;   // index within the unit kind
-    const UnitRec ur = load_unit(M, a.unit_tab, a.unit_words, shrink ? uu : a.n_shrink + uu, shrink);
-    const int job = job_of(uu, a.n_jobs, shrink ? a.job_shrink_base : a.job_expand_base);
-    const DecodeJob& J = a.jobs[job];
-    rec[R_KIND] = shrink ? 0 : 1;
-    rec[R_JOB] = job;
-    rec[R_GC] = ur.gc;
-    rec[R_R] = ur.r;
-    rec[R_NTOK] = ur.ntok;
-    rec[R_PREF] = ur.pref;
-    rec[R_VOFF] = gc_field(M, ur.gc, GC_VOFF);
-    rec[R_RS] = v_stride(ur.r);
-    for (int t = 0; t < kTokChunkMma; ++t) rec[R_TOK + t] = t < ur.ntok ? M[ur.toff + t] : 0;
-    if (shrink) {
-        const int njb = shrink_jblocks(ur.r, 2);
-        const int ks = ur.local / njb;
-        rec[R_KS] = ks;
-        rec[R_J0] = (ur.local - ks * njb) * kShrinkRowsMma;
-        rec[R_NJ] = min(kShrinkRowsMma, ur.r - rec[R_J0]);
-        rec[R_K0] = ks * kKSlice;
-        rec[R_NK] = min(kKSlice, J.H_in - ks * kKSlice);
-    } else {
-        const int cols = expand_ncols(ur.r, 2);
-        rec[R_N0] = ur.local * cols;
-        rec[R_NC] = min(cols, J.H_out - ur.local * cols);
-        rec[R_BPITCH] = cols * 2 + kPitchPad;
-        rec[R_NTILES] = (rec[R_NC] + 15) / 16;
-        const bool last_gc = ur.gc + 1 >= a.n_gc;
-        rec[R_NS] = (last_gc ? a.n_shrink : gc_field(M, ur.gc + 1, GC_SHRINK_BASE)) - gc_field(M, ur.gc, GC_SHRINK_BASE);
-        rec[R_NE] = (last_gc ? a.n_expand : gc_field(M, ur.gc + 1, GC_EXPAND_BASE)) - gc_field(M, ur.gc, GC_EXPAND_BASE);
-        rec[R_SCALE] = gc_field(M, ur.gc, GC_SCALE);
-        rec[R_KSPLIT] = J.ksplit;
+// TP split: the k-slice partials of every gc summed in slice order into the compact v
+// [gc][ntok][v_stride(r)] (GC_VRED offsets) -- the rank-r payload the TP ranks all-reduce
+// (c5 decode 64 tokens x ranks 16..128 = 15,360 B).  One CTA per gc.
+template <int W>
+__global__ void __launch_bounds__(256)
+    lora_vreduce_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    pdl_wait_cta();   // the partials of the shrink kernel
+    const int gc = blockIdx.x;
+    const int r = gc_field(M, gc, GC_RANK), ntok = gc_field(M, gc, GC_NTOK), rs = v_stride(r);
+    const int ksplit = a.jobs[gc_field(M, gc, GC_JOB)].ksplit;
+    const float* src = a.vbuf + gc_field(M, gc, GC_VOFF);
+    float* dst = a.vred + gc_field(M, gc, GC_VRED);
+    for (int e = threadIdx.x; e < ntok * rs; e += blockDim.x) {
+        float v = 0.f;
+        for (int k = 0; k < ksplit; ++k) v += ld_cg_f32(src + k * ntok * rs + e);
+        dst[e] = v;
     }
-}
-
-template <int W, int NS>
-__global__ void __launch_bounds__(kPsThreads, 1)
-    lora_decode_stream_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
-    constexpr int ES = 2;
-    extern __shared__ __align__(128) char smem[];
-    const int32_t* M = blob.w;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);   // [NS]  producer tx
-    uint64_t* empty = full + NS;                          // [NS]  8 consumer-warp arrivals
-    uint64_t* vfull = empty + NS;                         // [2]   v loader
-    uint64_t* vempty = vfull + 2;                         // [2]   8 consumer-warp arrivals
-    uint64_t* pfull = vempty + 2;                         // [2]   8 consumer-warp arrivals
-    uint64_t* pempty = pfull + 2;                         // [2]   publisher
-    int* pend = reinterpret_cast<int*>(smem + 256);       // publisher's unpublished gcs [kPsMaxPend]
-    int32_t* tab = reinterpret_cast<int32_t*>(smem + 512);
-    const int ntab = a.ps_tab;
-    char* ring = smem + ps_ring_off(ntab);
-    float* part = reinterpret_cast<float*>(smem + ps_part_off(NS, ntab));
-    const int vpitch = a.e_vpitch;
-    char* vring = smem + ps_vring_off(NS, ntab);
-    char* zero = smem + ps_zero_off(NS, ntab, vpitch);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int P = gridDim.x, c = blockIdx.x;
-    const int ns_my = c < a.n_shrink ? (a.n_shrink - 1 - c) / P + 1 : 0;
-    const int ne_my = c < a.n_expand ? (a.n_expand - 1 - c) / P + 1 : 0;
-    const int n_my = ns_my + ne_my;
-    int* cnt = a.gc_cnt;              // [n_gc] shrink units published, then [n_gc] expand units done
-    int* done = a.gc_cnt + a.n_gc;
-
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&vfull[s], 1);
-            mbar_init(&vempty[s], kConsumerWarps);
-            mbar_init(&pfull[s], kConsumerWarps);
-            mbar_init(&pempty[s], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (tid < 16) reinterpret_cast<uint32_t*>(zero)[tid] = 0u;
-    for (int i = tid; i < n_my; i += kPsThreads) ps_decode(a, M, c, P, ns_my, i, tab + i * kPsRecWords);
-    __syncthreads();
-    pdl_launch_dependents();   // every CTA of this grid is resident from here on (deadlock argument above)
-    auto R = [&](int i) -> const int32_t* { return tab + i * kPsRecWords; };
-    // lora_debug_set_trace: 16 words per unit (shrink units, then expand units): 0 smid, 2 operands in
-    // the stage, 3 expand: v ready, 5 consumers done, 6 expand: gc acquired, 7 producer issued,
-    // 10 shrink: publisher picked the partials, 11 shrink: published
-    auto T = [&](int i, int w) -> unsigned long long* {
-        return a.trace + (size_t)(i < ns_my ? c + i * P : a.n_shrink + c + (i - ns_my) * P) * 16 + w;
-    };
-
-    if (warp == 0) {
-        // ============ producer
-        const uint64_t pol_w = policy_evict_first(), pol_xy = policy_evict_normal();
-        auto issue = [&](int i, bool weights, bool xy) {
-            const int32_t* q = R(i);
-            char* st = ring + (i % NS) * kPsStage;
-            uint64_t* bar = &full[i % NS];
-            const DecodeJob& J = a.jobs[q[R_JOB]];
-            if (a.trace && weights && lane == 0) *T(i, 7) = gtime();
-            if (q[R_KIND] == 0) {
-                if (weights) {
-                    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)((q[R_NJ] + q[R_NTOK]) * q[R_NK] * ES));
-                    __syncwarp();
-                    if (lane < q[R_NJ])
-                        bulk_g2s(st + lane * kAPitch, J.A + ((size_t)page_at(M, q[R_PREF], lane) * J.H_in + q[R_K0]) * ES,
-                                 (uint32_t)(q[R_NK] * ES), bar, pol_w);
-                }
-                if (xy && lane < q[R_NTOK])
-                    bulk_g2s(st + kPsWBytes + lane * kAPitch, J.x + ((size_t)q[R_TOK + lane] * J.H_in + q[R_K0]) * ES,
-                             (uint32_t)(q[R_NK] * ES), bar, pol_xy);
-            } else {
-                const int nc = q[R_NC], n0 = q[R_N0], bpitch = q[R_BPITCH];
-                if (weights) {
-                    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)((q[R_R] + q[R_NTOK]) * nc * ES));
-                    __syncwarp();
-                    for (int j = lane; j < q[R_R]; j += 32)
-                        bulk_g2s(st + (size_t)j * bpitch, J.B + ((size_t)page_at(M, q[R_PREF], j) * J.H_out + n0) * ES,
-                                 (uint32_t)(nc * ES), bar, pol_w);
-                }
-                if (xy && lane < q[R_NTOK])
-                    bulk_g2s(st + kPsWBytes + lane * bpitch, J.y + ((size_t)q[R_TOK + lane] * J.H_out + n0) * ES,
-                             (uint32_t)(nc * ES), bar, pol_xy);
-            }
-        };
-        const int pre = n_my < NS ? n_my : NS;
-        for (int i = 0; i < pre; ++i) issue(i, true, false);   // before the preceding grid completes
-        if (n_my > 0) {
-            if (lane == 0) pdl_wait();   // x / y may be produced by the preceding grid
-            __syncwarp();
-        }
-        for (int i = 0; i < pre; ++i) issue(i, false, true);
-        for (int i = pre; i < n_my; ++i) {
-            mbar_wait(&empty[i % NS], ((i / NS) & 1) ^ 1);
-            issue(i, true, true);
-        }
-    } else if (warp == 1 || warp == 2) {
-        // ============ v loaders: warp 1 takes the even expand units (v slot 0), warp 2 the odd ones
-        const int slot = warp - 1;
-        if (ne_my > slot) {
-            if (lane == 0) pdl_wait();   // the v scratch and counters belong to this grid only after it
-            __syncwarp();
-        }
-        char* vhi = vring + slot * 2 * kTokChunkMma * vpitch;
-        char* vlo = vhi + kTokChunkMma * vpitch;
-        for (int k = slot; k < ne_my; k += 2) {
-            const int kk = k >> 1;   // this slot's use count
-            if (kk >= 1) mbar_wait(&vempty[slot], (kk & 1) ^ 1);
-            const int32_t* q = R(ns_my + k);
-            const int gc = q[R_GC], r = q[R_R], ntok = q[R_NTOK], rs = q[R_RS], ksplit = q[R_KSPLIT];
-            const int rq = rs >> 2, rp = (r + 15) & ~15;
-            const int voff = q[R_VOFF];
-            const float scale = __int_as_float(q[R_SCALE]);
-            if (lane == 0) {
-                const int n_s = q[R_NS];
-                if (ld_acquire_gpu(cnt + gc) < n_s) {
-                    const unsigned long long t0 = gtime_raw();
-                    while (ld_relaxed_gpu(cnt + gc) < n_s) {
-                        __nanosleep(64);
-                        if (gtime_raw() - t0 > 500000000ull) {
-                            atomicExch(a.gc_cnt - 1, 1);
-                            break;
-                        }
-                    }
-                    ld_acquire_gpu(cnt + gc);   // acquire the published partials
-                }
-                if (a.trace) *T(ns_my + k, 6) = gtime();
-            }
-            __syncwarp();
-            // (token t, rank quad jq) pairs; the k-slice partials of a pair are summed in slice order
-            const int npairs = ntok * rq;
-            for (int p0 = 0; p0 < npairs; p0 += 32 * 2) {
-                float4 acc[2];
-                int tq[2], jq[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int pp = p0 + h * 32 + lane;
-                    tq[h] = pp / rq;
-                    jq[h] = (pp - tq[h] * rq) * 4;
-                    acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-                for (int k0 = 0; k0 < ksplit; k0 += 4) {
-                    float4 pv[2][4];
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int s = 0; s < 4; ++s)
-                            pv[h][s] = (p0 + h * 32 + lane < npairs && k0 + s < ksplit)
-                                           ? ld_cg_f4(a.vbuf + voff + ((k0 + s) * ntok + tq[h]) * rs + jq[h])
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int s = 0; s < 4; ++s)
-                            if (k0 + s < ksplit) {
-                                acc[h].x += pv[h][s].x;
-                                acc[h].y += pv[h][s].y;
-                                acc[h].z += pv[h][s].z;
-                                acc[h].w += pv[h][s].w;
-                            }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (p0 + h * 32 + lane >= npairs) continue;
-                    const float f[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
-                    __nv_bfloat16 hb[4], lb[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float v = jq[h] + e < r ? f[e] * scale : 0.f;
-                        hb[e] = __float2bfloat16_rn(v);
-                        lb[e] = __float2bfloat16_rn(v - __bfloat162float(hb[e]));
-                    }
-                    *reinterpret_cast<uint2*>(vhi + tq[h] * vpitch + jq[h] * 2) = *reinterpret_cast<const uint2*>(hb);
-                    *reinterpret_cast<uint2*>(vlo + tq[h] * vpitch + jq[h] * 2) = *reinterpret_cast<const uint2*>(lb);
-                }
-            }
-            // zero the padded tail the MMAs read: tokens >= ntok, ranks rs .. rp
-            for (int t = 0; t < kTokChunkMma; ++t)
-                for (int j = (t < ntok ? rs : 0) + lane * 4; j < rp; j += 32 * 4) {
-                    *reinterpret_cast<uint2*>(vhi + t * vpitch + j * 2) = make_uint2(0u, 0u);
-                    *reinterpret_cast<uint2*>(vlo + t * vpitch + j * 2) = make_uint2(0u, 0u);
-                }
-            __syncwarp();
-            if (lane == 0) {
-                ps_arrive(&vfull[slot]);
-                if (a.trace) *T(ns_my + k, 3) = gtime();
-                // every v read of this unit is done: the gc's last expand unit re-arms its counters
-                if (atomicAdd(done + gc, 1) == q[R_NE] - 1) {
-                    cnt[gc] = 0;
-                    done[gc] = 0;
-                }
-            }
-        }
-    } else if (warp == 3) {
-        // ============ publisher: shrink partials -> v scratch -> gc counters
-        if (ns_my > 0) {
-            if (lane == 0) pdl_wait();
-            __syncwarp();
-        }
-        int npend = 0;
-        for (int i = 0; i < ns_my; ++i) {
-            const int32_t* q = R(i);
-            mbar_wait(&pfull[i & 1], (i >> 1) & 1);
-            if (a.trace && lane == 0) *T(i, 10) = gtime();
-            const float* pb = part + (i & 1) * kPsPart;
-            const int r = q[R_R], rs = q[R_RS], nj = q[R_NJ], j0 = q[R_J0], ntok = q[R_NTOK];
-            const int padr = j0 + nj == r ? rs - r : 0;   // the row stride's zero tail
-            float* vb = a.vbuf + q[R_VOFF] + q[R_KS] * ntok * rs + j0;
-            for (int e = lane; e < (nj + padr) * ntok; e += 32) {
-                const int row = e / ntok, t = e - row * ntok;
-                float v = 0.f;
-                if (row < nj) {
-#pragma unroll
-                    for (int w = 0; w < kConsumerWarps; ++w) v += pb[(w * kShrinkRowsMma + row) * kTokChunkMma + t];
-                }
-                vb[t * rs + row] = v;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                ps_arrive(&pempty[i & 1]);
-                pend[npend] = q[R_GC];
-            }
-            ++npend;
-            // publish now unless the next unit is already reduced (then one fence covers both)
-            bool more = i + 1 < ns_my && npend < kPsMaxPend;
-            if (more) more = __shfl_sync(0xffffffffu, lane == 0 && ps_test(&pfull[(i + 1) & 1], ((i + 1) >> 1) & 1) ? 1 : 0, 0) != 0;
-            if (!more) {
-                __threadfence();   // every lane's v stores, gpu scope (then the barrier and the adds)
-                __syncwarp();
-                if (lane < npend) red_relaxed_gpu(cnt + pend[lane], 1);
-                if (a.trace && lane < npend) *T(i - (npend - 1 - lane), 11) = gtime();
-                npend = 0;
-                __syncwarp();
-            }
-        }
-    } else {
-        // ============ consumers (warps 4..11)
-        const int cw = warp - kPsConsumer0;
-        const int g = lane >> 2, cc = lane & 3;
-        for (int i = 0; i < ns_my; ++i) {
-            const int32_t* q = R(i);
-            const int s = i % NS;
-            const int nj = q[R_NJ], nk = q[R_NK], ntok = q[R_NTOK];
-            mbar_wait(&full[s], (i / NS) & 1);
-            if (a.trace && tid == 128) { *T(i, 2) = gtime(); *T(i, 0) = smid(); }
-            const char* abuf = ring + s * kPsStage;
-            const char* xbuf = abuf + kPsWBytes;
-            uint4 ra[kKBlocks], rb[kKBlocks], xr[kKBlocks];
-#pragma unroll
-            for (int b = 0; b < kKBlocks; ++b) {
-                const int k = cw * kKPerWarp + b * 32 + cc * 8;
-                const bool kin = k < nk;
-                ra[b] = (g < nj && kin) ? lds128(abuf + g * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
-                rb[b] = (g + 8 < nj && kin) ? lds128(abuf + (g + 8) * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
-                xr[b] = (g < ntok && kin) ? lds128(xbuf + g * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
-            }
-            __syncwarp();
-            if (lane == 0) ps_arrive(&empty[s]);   // this warp is done with the stage
-            float acc[kKBlocks][4];
-#pragma unroll
-            for (int b = 0; b < kKBlocks; ++b) {
-                acc[b][0] = acc[b][1] = acc[b][2] = acc[b][3] = 0.f;
-                mma_bf16(acc[b], ra[b].x, rb[b].x, ra[b].y, rb[b].y, xr[b].x, xr[b].y);
-                mma_bf16(acc[b], ra[b].z, rb[b].z, ra[b].w, rb[b].w, xr[b].z, xr[b].w);
-            }
-            if (i >= 2) mbar_wait(&pempty[i & 1], ((i >> 1) & 1) ^ 1);
-            float* pw = part + (i & 1) * kPsPart + cw * kShrinkRowsMma * kTokChunkMma;
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-                float kb[kKBlocks];
-#pragma unroll
-                for (int b = 0; b < kKBlocks; ++b) kb[b] = acc[b][qq];
-#pragma unroll
-                for (int w = 1; w < kKBlocks; w *= 2)
-#pragma unroll
-                    for (int b = 0; b + w < kKBlocks; b += 2 * w) kb[b] += kb[b + w];
-                const int row = g + ((qq & 2) ? 8 : 0), t = 2 * cc + (qq & 1);
-                pw[row * kTokChunkMma + t] = kb[0];
-            }
-            __syncwarp();
-            if (lane == 0) ps_arrive(&pfull[i & 1]);
-            if (a.trace && tid == 128) *T(i, 5) = gtime();
-        }
-        // ---- expand units: per pass a warp takes two adjacent 16-column tiles
-        const int am = lane >> 3, ai = lane & 7;
-        const int aj = ai + ((am & 2) ? 8 : 0), an = (am & 1) * 8;
-        const int vt = lane & 7, vh = (lane >> 3) & 1;
-        const uint32_t zaddr = smem_u32(zero);
-        // this thread's output column pairs: even g -> token 2cc, columns (g, g+1) and (g+8, g+9);
-        // odd g -> token 2cc+1, columns (g-1, g) and (g+7, g+8) of each tile
-        const int tme = 2 * cc + (g & 1);
-        const int cpair = g & ~1;
-        for (int k = 0; k < ne_my; ++k) {
-            const int i = ns_my + k;
-            const int32_t* q = R(i);
-            const int s = i % NS, slot = k & 1;
-            const DecodeJob& J = a.jobs[q[R_JOB]];
-            const int r = q[R_R], ntok = q[R_NTOK], nc = q[R_NC], bpitch = q[R_BPITCH], ntiles = q[R_NTILES];
-            const int ksteps = (r + 15) >> 4;
-            const int tok = tme < ntok ? q[R_TOK + tme] : -1;
-            mbar_wait(&vfull[slot], (k >> 1) & 1);
-            mbar_wait(&full[s], (i / NS) & 1);
-            if (a.trace && tid == 128) { *T(i, 2) = gtime(); *T(i, 0) = smid(); }
-            const uint32_t vhi_base = smem_u32(vring + slot * 2 * kTokChunkMma * vpitch) + vt * vpitch + vh * 16;
-            const uint32_t vlo_base = vhi_base + kTokChunkMma * vpitch;
-            const char* stg = ring + s * kPsStage;
-            const uint32_t b_base = smem_u32(stg);
-            const char* ysm = stg + kPsWBytes + tme * bpitch;   // staged y row of this thread's token
-            char* yrow = J.y + ((size_t)(tok < 0 ? 0 : tok) * J.H_out + q[R_N0]) * ES;
-            for (int t0 = cw * 2; t0 < ntiles; t0 += 2 * kConsumerWarps) {
-                float d[2][4];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) d[h][0] = d[h][1] = d[h][2] = d[h][3] = 0.f;
-                for (int st = 0; st < ksteps; ++st) {
-                    const int j = st * 16 + aj;
-                    uint32_t h0, h1, l0, l1;
-                    ldsm_x2(h0, h1, vhi_base + st * 32);
-                    ldsm_x2(l0, l1, vlo_base + st * 32);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t af[4];
-                        ldsm_x4_trans(af[0], af[1], af[2], af[3],
-                                      (j < r && t0 + h < ntiles) ? b_base + j * bpitch + ((t0 + h) * 16 + an) * ES : zaddr);
-                        mma_bf16(d[h], af[0], af[1], af[2], af[3], h0, h1);
-                        mma_bf16(d[h], af[0], af[1], af[2], af[3], l0, l1);
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    // D (col g / g+8, tokens 2cc, 2cc+1) -> column pairs by one shuffle with the g^1 lane
-                    const float o0 = __shfl_xor_sync(0xffffffffu, d[h][0], 4);
-                    const float o1 = __shfl_xor_sync(0xffffffffu, d[h][1], 4);
-                    const float o2 = __shfl_xor_sync(0xffffffffu, d[h][2], 4);
-                    const float o3 = __shfl_xor_sync(0xffffffffu, d[h][3], 4);
-                    const float p0 = (g & 1) ? o1 : d[h][0], p1 = (g & 1) ? d[h][1] : o0;
-                    const float p2 = (g & 1) ? o3 : d[h][2], p3 = (g & 1) ? d[h][3] : o2;
-                    if (tok < 0 || t0 + h >= ntiles) continue;
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int col = (t0 + h) * 16 + cpair + e * 8;
-                        if (col >= nc) continue;
-                        const uint32_t w = lds32(ysm + col * ES);
-                        const __nv_bfloat162 out = __floats2bfloat162_rn(__uint_as_float(w << 16) + (e ? p2 : p0),
-                                                                         __uint_as_float(w & 0xffff0000u) + (e ? p3 : p1));
-                        *reinterpret_cast<__nv_bfloat162*>(yrow + col * ES) = out;
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                ps_arrive(&vempty[slot]);
-                ps_arrive(&empty[s]);   // B rows and the staged y of this stage are consumed
-            }
-            if (a.trace && tid == 128) *T(i, 5) = gtime();
-        }
-    }
+    pdl_launch_dependents();
 }
 
 // copies a metadata blob too large for one kernel's parameters into device memory,
@@ -1544,6 +1081,11 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, ss, st, a, blob);
         if (e != cudaSuccess) return e;
         *launches += 1;
+        if (a.vred && !a.v_compact) {   // TP split: k-reduce the partials into the compact v
+            e = launch_pdl(lora_vreduce_kernel<W>, pl.n_gc, 256, 0, st, a, blob);
+            if (e != cudaSuccess) return e;
+            *launches += 1;
+        }
     }
     if (phases & 2) {
         const bool big = pl.n_expand > 3 * num_sms;
@@ -1552,29 +1094,6 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         *launches += 1;
     }
     return e;
-}
-
-template <int W, int NS>
-static cudaError_t launch_stream_ns(const DecodeArgs& a, const Plan& pl, int grid, cudaStream_t st) {
-    static std::atomic<uint64_t> configured{0};
-    if (!configure_once(configured, [] {
-            return cudaFuncSetAttribute(lora_decode_stream_kernel<W, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        227 * 1024);
-        }))
-        return cudaErrorInvalidValue;
-    MetaBlob<W> blob;
-    const int n = (int)pl.blob.size();
-    for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
-    return launch_pdl(lora_decode_stream_kernel<W, NS>, grid, kPsThreads, ps_smem(NS, a.ps_tab, a.e_vpitch), st, a, blob);
-}
-
-template <int W>
-static cudaError_t launch_stream(const DecodeArgs& a, const DecodeLaunch& L, cudaStream_t st, int* launches) {
-    *launches += 1;
-    switch (L.stream_ns) {
-        case 3: return launch_stream_ns<W, 3>(a, *L.plan, L.stream_ctas, st);
-        default: return launch_stream_ns<W, 2>(a, *L.plan, L.stream_ctas, st);
-    }
 }
 
 template <typename T>
@@ -1587,10 +1106,13 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         const void* A = j == 0 ? L.poolA : L.more[j - 1].poolA;
         const void* B = j == 0 ? L.poolB : L.more[j - 1].poolB;
         const int hin = j == 0 ? L.H_in : L.more[j - 1].H_in, hout = j == 0 ? L.H_out : L.more[j - 1].H_out;
+        const int xld = j == 0 && L.x_ld > 0 ? (int)L.x_ld : hin, yld = j == 0 && L.y_ld > 0 ? (int)L.y_ld : hout;
         a.jobs[j] = DecodeJob{static_cast<const char*>(x), static_cast<char*>(y), static_cast<const char*>(A),
-                              static_cast<const char*>(B), hin, hout, ksplit_of(hin, (int)sizeof(T)), 0};
+                              static_cast<const char*>(B), hin, hout, ksplit_of(hin, (int)sizeof(T)), xld, yld};
     }
     a.vbuf = L.vbuf;
+    a.vred = L.vred;
+    a.v_compact = (L.phases == 2 && L.vred) ? 1 : 0;
     a.meta_global = L.meta_dev;
     a.trace = L.trace;
     a.n_shrink = pl.n_shrink;
@@ -1623,17 +1145,6 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         a.e_smem = a.e_pgoff + maxr * 4;
     }
     const int n = (int)pl.blob.size();
-    if (sizeof(T) == 2 && L.stream_ctas > 0 && L.phases == 3 && L.gc_cnt && n <= kUploadWords) {
-        a.gc_cnt = L.gc_cnt;
-        const int P = L.stream_ctas;
-        a.ps_tab = (pl.n_shrink + P - 1) / P + (pl.n_expand + P - 1) / P;
-        if (ps_smem(L.stream_ns, a.ps_tab, a.e_vpitch) > 227 * 1024) goto pair;   // unit table too large: the pair
-        if (n <= 1024) return launch_stream<1024>(a, L, st, launches);
-        if (n <= 2048) return launch_stream<2048>(a, L, st, launches);
-        if (n <= 4096) return launch_stream<4096>(a, L, st, launches);
-        return launch_stream<kUploadWords>(a, L, st, launches);
-    }
-pair:
     if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases, L.num_sms);
     if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases, L.num_sms);
     if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches, L.phases, L.num_sms);
@@ -1649,9 +1160,7 @@ pair:
     return launch_pair<T, 1>(a, pl, st, launches, L.phases, L.num_sms);
 }
 
-int launch_decode(const Plan& pl, const DecodeLaunch& L0, cudaStream_t st, int* launches) {
-    DecodeLaunch L = L0;
-    L.plan = &pl;
+int launch_decode(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {
     if (L.esz == 2) return (int)launch_typed<__nv_bfloat16>(pl, L, st, launches);
     return (int)launch_typed<float>(pl, L, st, launches);
 }

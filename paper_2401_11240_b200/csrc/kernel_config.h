@@ -41,8 +41,9 @@ LORA_HD int page_ref_add(int ref, int k) { return ref >= 0 ? ref + k : ~((~ref) 
 LORA_HD int unit_rank(uint32_t w) { return (int)(w & 0x1ffu); }
 LORA_HD int unit_ntok(uint32_t w) { return (int)((w >> 9) & 0xfu); }
 LORA_HD int unit_tok_off(uint32_t w) { return (int)(w >> 13); }
-constexpr int kGcFields = 9;     // rank, page_off, tok_off, ntok, shrink_base, expand_base, voff, scale_bits, job
-enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB };
+constexpr int kGcFields = 10;    // rank, page_off, tok_off, ntok, shrink_base, expand_base, voff, scale_bits, job,
+                                 // vred (offset of the gc's k-reduced v [ntok][v_stride(r)] in the compact v)
+enum { GC_RANK = 0, GC_PAGE_OFF, GC_TOK_OFF, GC_NTOK, GC_SHRINK_BASE, GC_EXPAND_BASE, GC_VOFF, GC_SCALE, GC_JOB, GC_VRED };
 constexpr int kMaxJobs = 4;      // pools fused into one launch pair by lora_apply_multi (e.g. q, k, v)
 
 constexpr int kBoxKinds = 5;                      // 2D TMA boxes {64 columns, 8 << k page rows}, k < 5

@@ -250,7 +250,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     const int pages_base = kHdrWords + kGcFields * n_gc;
     const int toks_base = pages_base + (int)blob_pages.size();
     int shrink = 0, expand = 0;
-    int64_t voff = 0;
+    int64_t voff = 0, vred = 0;
     for (int c = 0; c < n_gc; ++c) {
         const int g = gcs[c].g, r = pad_zero_page >= 0 ? (int)pl.max_rank : pl.group_rank[g];
         int32_t* e = gct + kGcFields * c;
@@ -263,17 +263,19 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         e[GC_VOFF] = (int32_t)voff;
         e[GC_SCALE] = f32_bits(pl.group_scale[g]);
         e[GC_JOB] = 0;
+        e[GC_VRED] = (int32_t)vred;
         shrink += ksplit * shrink_jblocks(r, esz);
         const int nc = expand_ncols(r, esz);
         expand += (H_out + nc - 1) / nc;
         voff += (int64_t)ksplit * gcs[c].ntok * v_stride(r);
+        vred += (int64_t)gcs[c].ntok * v_stride(r);
     }
     if (voff > INT32_MAX) { err = "batch too large for the SIMT scratch"; return LORA_ERR_ARG; }
     std::copy(blob_pages.begin(), blob_pages.end(), pl.blob.begin() + pages_base);
     std::copy(blob_toks.begin(), blob_toks.end(), pl.blob.begin() + toks_base);
     hdr[0] = n_gc; hdr[1] = shrink; hdr[2] = expand;
     hdr[3] = (int32_t)blob_pages.size(); hdr[4] = (int32_t)blob_toks.size(); hdr[5] = ksplit;
-    pl.n_shrink = shrink; pl.n_expand = expand; pl.vbuf_floats = voff;
+    pl.n_shrink = shrink; pl.n_expand = expand; pl.vbuf_floats = voff; pl.vred_floats = vred;
     pl.blob_esz = esz;
     return append_unit_table(pl, err);
 }
@@ -340,7 +342,7 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
     m.blob.assign(kHdrWords + (size_t)kGcFields * n_gc + n_pages + n_toks, 0);
     const int pages_base = kHdrWords + kGcFields * n_gc, toks_base = pages_base + n_pages;
     int gc = 0, pg = 0, tk = 0, shrink = 0, expand = 0;
-    int64_t voff = 0;
+    int64_t voff = 0, vred = 0;
     for (int p = 0; p < n; ++p) {
         const Plan& q = *plans[p];
         if (q.blob.empty() || q.n_gc == 0) continue;
@@ -357,6 +359,7 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
             o[GC_SHRINK_BASE] = e[GC_SHRINK_BASE] + shrink;
             o[GC_EXPAND_BASE] = e[GC_EXPAND_BASE] + expand;
             o[GC_VOFF] = (int32_t)(e[GC_VOFF] + voff);
+            o[GC_VRED] = (int32_t)(e[GC_VRED] + vred);
             o[GC_JOB] = p;
             ++gc;
         }
@@ -367,6 +370,7 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
         shrink += q.n_shrink;
         expand += q.n_expand;
         voff += q.vbuf_floats;
+        vred += q.vred_floats;
     }
     if (voff > INT32_MAX) { err = "fused batch too large for the SIMT scratch"; return LORA_ERR_ARG; }
     int32_t* h = m.blob.data();
@@ -381,6 +385,7 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& m, std::string& e
     m.n_shrink = shrink;
     m.n_expand = expand;
     m.vbuf_floats = voff;
+    m.vred_floats = vred;
     m.blob_esz = plans[0]->blob_esz;
     return append_unit_table(m, err);
 }

@@ -42,7 +42,8 @@ struct Plan {
     int32_t unit_tab = 0;                // blob word offset of the per-unit table
     int32_t unit_words = kUnitWords;     // words per unit record: kUnitWords, or 1 for large batches
     int32_t blob_esz = 2;                // element size the unit table was built for
-    int64_t vbuf_floats = 0;
+    int64_t vbuf_floats = 0;             // k-slice partials [gc][ksplit][ntok][v_stride(r)]
+    int64_t vred_floats = 0;             // compact k-reduced v [gc][ntok][v_stride(r)] (TP payload)
     int32_t n_jobs = 1;                          // pools fused by lora_apply_multi
     int32_t job_shrink_base[4] = {0, 0, 0, 0};   // first shrink / expand unit of each job
     int32_t job_expand_base[4] = {0, 0, 0, 0};
@@ -54,7 +55,6 @@ struct Plan {
                                      // first_page|-1, first column tile, end column tile}, then pages
     int32_t n_pf_tiles = 0;          // prefill CTAs (tiles x pf_cs)
     int32_t pf_cs = 1;               // CTAs per token tile (a cluster: split-K shrink + column split)
-    int32_t stream_ctas = 0, stream_ns = 0;   // bf16 decode on the streaming kernel (0 = kernel pair)
 
     // back to the default state but keeping every vector's capacity (one plan per apply: the
     // host planner is on the per-call path, so it should not reallocate)
@@ -68,11 +68,10 @@ struct Plan {
         T = d.T; S = d.S; G = d.G; L_tc = d.L_tc;
         n_seg = max_rank = nseg_x_maxrank = sum_rank_seg = sum_rank_groups = sum_rank_tokens = 0;
         n_gc = n_shrink = n_expand = 0;
-        unit_tab = 0; unit_words = d.unit_words; blob_esz = d.blob_esz; vbuf_floats = 0; n_jobs = 1;
+        unit_tab = 0; unit_words = d.unit_words; blob_esz = d.blob_esz; vbuf_floats = 0; vred_floats = 0; n_jobs = 1;
         for (int i = 0; i < 4; ++i) job_shrink_base[i] = job_expand_base[i] = 0;
         n_prefill_tiles = n_pf_tiles = 0;
         pf_cs = 1;
-        stream_ctas = stream_ns = 0;
     }
 };
 
@@ -95,10 +94,9 @@ struct DecodeLaunch {
     unsigned long long* trace;   // optional per-unit timestamps (lora_debug_set_trace), or null
     int H_in, H_out, esz, num_sms;
     int phases = 3;              // bit 0: shrink kernel, bit 1: expand kernel
-    int stream_ctas = 0;         // > 0 (bf16, phases 3): the persistent streaming kernel with this grid
-    int stream_ns = 2;           //   ... and this many ring stages
-    int* gc_cnt = nullptr;       //   ... and the pool's counters (2 * n_gc words, zero; [-1] timeout flag)
-    const Plan* plan = nullptr;   // the plan being launched (set by launch_decode)
+    float* vred = nullptr;       // phases 1: also reduce the partials over k-slices into this compact v;
+                                 // phases 2: the expand reads this compact (k-reduced) v instead of vbuf
+    int64_t x_ld = 0, y_ld = 0;  // row strides (elements) of x / y of job 0; 0 = H_in / H_out
     struct More {                // jobs 1.. of a fused multi-pool apply (job 0 = the fields above)
         const void* x;
         void* y;

@@ -8,6 +8,7 @@
 // management" borrowed from S-LoRA/LightLLM: one page = one rank
 // component (a_j ∈ R^{H_in}, b_j ∈ R^{H_out}) -- DESIGN.md reading R9.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -53,10 +54,6 @@ struct lora_pool {
     size_t vbuf_cap = 0;                 // floats
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
-    int32_t* gc_sync = nullptr;          // streaming decode: [0] spin-timeout flag, then 2 counters per gc (zero)
-    size_t gc_sync_cap = 0;
-    int decode_kernel = 0;               // LORA_OPT_DECODE_KERNEL: 0 streaming kernel (bf16), 1 kernel pair
-    int decode_stages = 2;               // LORA_OPT_DECODE_STAGES: ring stages of the streaming kernel
     bool load_kernel = false;            // LORA_OPT_LOAD_KERNEL: cold-start copies by a zero-copy gather kernel
     bool pad_max_rank = false;           // LORA_OPT_PAD_MAX_RANK: BGMV-style padded decode work (comparison)
     Plan plan;
@@ -67,6 +64,49 @@ struct lora_pool {
     unsigned long long* trace = nullptr;   // lora_debug_set_trace
     bool capturing = false;               // the current apply's stream is being captured into a graph
     std::vector<void*> retired;           // outgrown scratch buffers: a captured graph may still use them
+    float* vred = nullptr;                // TP: the compact k-reduced v all-reduced by lora_apply_tp
+    size_t vred_cap = 0;
+    lora_tp_comm* tp = nullptr;           // lora_tp_init: the TP group's communicator (not owned)
+};
+
+// ---- NCCL, resolved at run time (dlopen): the library loads without NCCL; only the TP calls need it.
+// The few types and constants used are NCCL's stable ABI (nccl.h 2.x: ncclUniqueId is 128 bytes,
+// ncclSuccess = 0, ncclSum = 0, ncclFloat32 = 7).
+namespace {
+typedef struct { char internal[LORA_TP_UNIQUE_ID_BYTES]; } nccl_uid;
+typedef void* nccl_comm;
+struct NcclApi {
+    int (*get_unique_id)(nccl_uid*) = nullptr;
+    int (*comm_init_rank)(nccl_comm*, int, nccl_uid, int) = nullptr;
+    int (*all_reduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+    int (*comm_destroy)(nccl_comm) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+};
+const NcclApi* nccl(std::string& err) {
+    static NcclApi api;
+    static bool tried = false, ok = false;
+    if (!tried) {
+        tried = true;
+        // the process's NCCL (torch loads libnccl.so.2), else the one beside the CUDA runtime
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.get_unique_id = (int (*)(nccl_uid*))dlsym(h, "ncclGetUniqueId");
+            api.comm_init_rank = (int (*)(nccl_comm*, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+            api.all_reduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+            api.comm_destroy = (int (*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+            api.error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+            ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.comm_destroy && api.error_string;
+        }
+    }
+    if (!ok) err = std::string("NCCL is not available (dlopen libnccl.so.2: ") + (dlerror() ? dlerror() : "symbols missing") + ")";
+    return ok ? &api : nullptr;
+}
+constexpr int kNcclSum = 0, kNcclFloat32 = 7;
+}  // namespace
+
+struct lora_tp_comm {
+    nccl_comm comm = nullptr;
+    int rank = 0, size = 1, device = 0;
 };
 
 namespace {
@@ -228,9 +268,9 @@ lora_status lora_pool_destroy(lora_pool* p) {
             if (kv.second.ready) cudaEventDestroy((cudaEvent_t)kv.second.ready);
         if (p->dA) cudaFree(p->dA);
         if (p->box_maps) cudaFree(p->box_maps);
-        if (p->gc_sync) cudaFree(p->gc_sync);
         if (p->dB) cudaFree(p->dB);
         if (p->vbuf) cudaFree(p->vbuf);
+        if (p->vred) cudaFree(p->vred);
         if (p->pf_scratch) cudaFree(p->pf_scratch);
         if (p->meta_dev) cudaFree(p->meta_dev);
         for (void* b : p->retired) cudaFree(b);
@@ -241,8 +281,10 @@ lora_status lora_pool_destroy(lora_pool* p) {
     return LORA_OK;
 }
 
-lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_host, const void* B_host,
-                              float scale) {
+// a_pitch / b_pitch: bytes between consecutive rank rows of the host buffers (0 = the pool's row
+// bytes, i.e. a contiguous [rank][hidden] buffer; larger for a TP shard of the full adapter)
+static lora_status load_impl(lora_pool* p, int32_t id, int rank, const void* A_host, size_t a_pitch, const void* B_host,
+                             size_t b_pitch, float scale) {
     if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
     if (id < 0) return fail(LORA_ERR_ARG, "id must be >= 0");
     const int rmax = std::min(LORA_MAX_RANK, std::min(p->H_in, p->H_out));
@@ -278,7 +320,24 @@ lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_
             p->fence_pending = false;
         }
         const size_t ra = (size_t)p->H_in * p->esz, rb = (size_t)p->H_out * p->esz;
-        if (p->load_kernel && devA && devB && ((uintptr_t)devA % 16) == 0 && ((uintptr_t)devB % 16) == 0) {
+        const bool strided = (a_pitch && a_pitch != ra) || (b_pitch && b_pitch != rb);
+        if (!a_pitch) a_pitch = ra;
+        if (!b_pitch) b_pitch = rb;
+        if (strided) {
+            // a TP shard: one 2D copy per run of consecutive pages, straight from the full pinned
+            // adapter (no host-side slice or re-pin on the cold-start path)
+            for (int j = 0; j < rank;) {
+                int k = j + 1;
+                while (k < rank && rec.pages[k] == rec.pages[k - 1] + 1) ++k;
+                cudaError_t e = cudaMemcpy2DAsync(p->dA + (size_t)rec.pages[j] * ra, ra, (const char*)A_host + j * a_pitch,
+                                                  a_pitch, ra, (size_t)(k - j), cudaMemcpyHostToDevice, p->side);
+                if (e == cudaSuccess)
+                    e = cudaMemcpy2DAsync(p->dB + (size_t)rec.pages[j] * rb, rb, (const char*)B_host + j * b_pitch, b_pitch,
+                                          rb, (size_t)(k - j), cudaMemcpyHostToDevice, p->side);
+                if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter_shard: copy"); }
+                j = k;
+            }
+        } else if (p->load_kernel && devA && devB && ((uintptr_t)devA % 16) == 0 && ((uintptr_t)devB % 16) == 0) {
             // zero-copy gather kernel (LORA_OPT_LOAD_KERNEL)
             cudaError_t e = (cudaError_t)launch_load(p->dA, p->dB, devA, devB, (int64_t)ra, (int64_t)rb, rank,
                                                      rec.pages.data(), p->num_sms, p->side);
@@ -307,6 +366,23 @@ lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_
     p->free_pages -= rank;
     p->table.emplace(id, std::move(rec));
     return LORA_OK;
+}
+
+lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank, const void* A_host, const void* B_host,
+                              float scale) {
+    return load_impl(p, id, rank, A_host, 0, B_host, 0, scale);
+}
+
+lora_status lora_load_adapter_shard(lora_pool* p, int32_t id, int rank, const void* A_host, int64_t a_ld, int64_t a_col0,
+                                    const void* B_host, int64_t b_ld, int64_t b_col0, float scale) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    if (a_col0 < 0 || b_col0 < 0 || a_ld < a_col0 + p->H_in || b_ld < b_col0 + p->H_out)
+        return fail(LORA_ERR_SHAPE, "shard columns outside the full adapter (a_ld/b_ld too small)");
+    if (((a_ld | a_col0) * p->esz) % 16 || ((b_ld | b_col0) * p->esz) % 16)
+        return fail(LORA_ERR_ALIGN, "shard row pitch and first column must be 16-B aligned");
+    const char* A = A_host ? (const char*)A_host + a_col0 * p->esz : nullptr;
+    const char* B = B_host ? (const char*)B_host + b_col0 * p->esz : nullptr;
+    return load_impl(p, id, rank, A, (size_t)a_ld * p->esz, B, (size_t)b_ld * p->esz, scale);
 }
 
 lora_status lora_unload_adapter(lora_pool* p, int32_t id) {
@@ -358,26 +434,11 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     return LORA_OK;
 }
 
-// bf16 decode work of a full apply goes to the persistent streaming kernel (one grid, one CTA per SM)
-// unless the pool asks for the kernel pair or the metadata exceeds one launch's parameters
-static lora_status use_stream(lora_pool* p, Plan& pl, DecodeLaunch& L) {
-    pl.stream_ctas = pl.stream_ns = 0;
-    if (p->esz != 2 || p->decode_kernel != 0 || pl.n_gc == 0 || pl.blob.size() > (size_t)kMaxParamBlobWords) return LORA_OK;
-    lora_status s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * pl.n_gc), true, "gc_sync");
-    if (s != LORA_OK) return s;
-    pl.stream_ctas = std::min(p->num_sms, std::max(pl.n_shrink, pl.n_expand));
-    pl.stream_ns = p->decode_stages;
-    L.stream_ctas = pl.stream_ctas;
-    L.stream_ns = pl.stream_ns;
-    L.gc_cnt = p->gc_sync + 1;
-    return LORA_OK;
-}
-
 // mode 0: full apply; 1: shrink only (partial v -> v_ext); 2: expand only (v_ext -> y, plan of the
 // last shrink).  Modes 1/2 serve tensor parallelism: the caller all-reduces v in between.
 static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr,
                               const int32_t* adapter_ids, int num_segments, void* stream_ptr, int mode, float* v_ext,
-                              int64_t v_cap) {
+                              int64_t v_cap, int64_t x_ld = 0, int64_t y_ld = 0) {
     if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
     if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "apply on a host-only pool");
     lora_status s = LORA_OK;
@@ -432,8 +493,8 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, tc, p->table,
                        err, p->pad_max_rank ? p->n_pages : -1, p->num_sms);
         if (s != LORA_OK) return fail(s, err);
-        if (mode == 1 && p->plan.vbuf_floats > v_cap)
-            return fail(LORA_ERR_ARG, "v buffer too small: need " + std::to_string(p->plan.vbuf_floats) + " floats");
+        if (mode == 1 && p->plan.vred_floats > v_cap)
+            return fail(LORA_ERR_ARG, "v buffer too small: need " + std::to_string(p->plan.vred_floats) + " floats");
         p->split_ready = false;
     }
     const Plan& pl = p->plan;
@@ -449,8 +510,8 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     for (int gi = 0; gi < pl.G; ++gi)
         if ((s = wait_loaded(p->table.at(pl.group_id[gi]), st, p->capturing, "lora_apply: wait load")) != LORA_OK)
             return s;
-    // scratch
-    if (pl.n_gc > 0 && mode == 0) {
+    // scratch (the k-slice partials live in the pool; the TP split's compact v is the caller's)
+    if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
     }
     if (pl.n_gc > 0 && mode != 2) {
@@ -458,10 +519,11 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     }
     int launches = 0;
     if (pl.n_gc > 0) {
-        DecodeLaunch L{x, y, p->dA, p->dB, mode == 0 ? p->vbuf : v_ext, p->meta_dev, p->trace, p->H_in, p->H_out,
-                       p->esz, p->num_sms};
+        DecodeLaunch L{x, y, p->dA, p->dB, p->vbuf, p->meta_dev, p->trace, p->H_in, p->H_out, p->esz, p->num_sms};
         L.phases = mode == 0 ? 3 : mode;
-        if (mode == 0 && (s = use_stream(p, p->plan, L)) != LORA_OK) return s;
+        L.vred = mode == 0 ? nullptr : v_ext;
+        L.x_ld = x_ld;
+        L.y_ld = y_ld;
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
@@ -544,9 +606,6 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
                        p0->num_sms};
         L.n_jobs = n_pools;
-        if ((s = use_stream(p0, fz, L)) != LORA_OK) return s;
-        p0->plan.stream_ctas = fz.stream_ctas;   // lora_debug_metadata reports the leader's plan
-        p0->plan.stream_ns = fz.stream_ns;
         for (int i = 1; i < n_pools; ++i)
             L.more[i - 1] = DecodeLaunch::More{xs[i], ys[i], pools[i]->dA, pools[i]->dB, pools[i]->H_in, pools[i]->H_out};
         cudaError_t e = (cudaError_t)launch_decode(fz, L, st, &launches);
@@ -579,6 +638,105 @@ lora_status lora_apply_shrink(lora_pool* p, const void* x, const int32_t* seg_in
 
 lora_status lora_apply_expand(lora_pool* p, void* y, const float* v_in, void* stream) {
     return apply_impl(p, nullptr, y, nullptr, nullptr, 0, stream, 2, const_cast<float*>(v_in), 0);
+}
+
+lora_status lora_tp_unique_id(void* id_out) {
+    if (!id_out) return fail(LORA_ERR_ARG, "id_out is NULL");
+    std::string err;
+    const NcclApi* n = nccl(err);
+    if (!n) return fail(LORA_ERR_NCCL, err);
+    nccl_uid id;
+    const int r = n->get_unique_id(&id);
+    if (r != 0) return fail(LORA_ERR_NCCL, std::string("ncclGetUniqueId: ") + n->error_string(r));
+    std::memcpy(id_out, &id, sizeof(id));
+    return LORA_OK;
+}
+
+lora_status lora_tp_comm_create(const void* id, int tp_rank, int tp_size, lora_tp_comm** out) {
+    if (!id || !out) return fail(LORA_ERR_ARG, "id/out is NULL");
+    *out = nullptr;
+    if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) return fail(LORA_ERR_ARG, "need 0 <= tp_rank < tp_size");
+    std::string err;
+    const NcclApi* n = nccl(err);
+    if (!n) return fail(LORA_ERR_NCCL, err);
+    lora_tp_comm* c = new lora_tp_comm();
+    c->rank = tp_rank;
+    c->size = tp_size;
+    cudaGetDevice(&c->device);
+    nccl_uid uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    const int r = n->comm_init_rank(&c->comm, tp_size, uid, tp_rank);
+    if (r != 0) {
+        delete c;
+        return fail(LORA_ERR_NCCL, std::string("ncclCommInitRank: ") + n->error_string(r));
+    }
+    *out = c;
+    return LORA_OK;
+}
+
+lora_status lora_tp_comm_destroy(lora_tp_comm* c) {
+    if (!c) return LORA_OK;
+    std::string err;
+    const NcclApi* n = nccl(err);
+    int r = 0;
+    if (n && c->comm) {
+        DeviceGuard g(c->device);
+        r = n->comm_destroy(c->comm);
+    }
+    delete c;
+    if (r != 0) return fail(LORA_ERR_NCCL, std::string("ncclCommDestroy: ") + n->error_string(r));
+    return LORA_OK;
+}
+
+lora_status lora_tp_init(lora_pool* p, lora_tp_comm* comm) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    if (p->host_only) return fail(LORA_ERR_UNSUPPORTED, "tensor parallelism on a host-only pool");
+    if (comm && comm->device != p->device) return fail(LORA_ERR_ARG, "communicator and pool are on different devices");
+    p->tp = comm;
+    return LORA_OK;
+}
+
+lora_status lora_apply_tp(lora_pool* p, const void* x, int64_t x_ld, void* y, int64_t y_ld, const int32_t* seg_indptr,
+                          const int32_t* adapter_ids, int num_segments, void* stream) {
+    if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    if (!p->tp) return fail(LORA_ERR_ARG, "lora_apply_tp needs lora_tp_init");
+    if (x_ld < 0 || y_ld < 0 || (x_ld && x_ld < p->H_in) || (y_ld && y_ld < p->H_out))
+        return fail(LORA_ERR_ARG, "x_ld / y_ld must be 0 or at least hidden_in / hidden_out");
+    if ((x_ld * p->esz) % 16 || (y_ld * p->esz) % 16) return fail(LORA_ERR_ALIGN, "x_ld / y_ld rows must be 16-B aligned");
+    std::string err;
+    const NcclApi* n = nccl(err);
+    if (!n) return fail(LORA_ERR_NCCL, err);
+    if (!y) return fail(LORA_ERR_ARG, "y is NULL");
+    if (((uintptr_t)y & 15)) return fail(LORA_ERR_ALIGN, "y must be 16-byte aligned");
+    // the compact v: planned first (every token on the decode kernels, as the split runs it) so its
+    // buffer can be sized before anything is enqueued
+    lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, false,
+                               p->table, err);
+    if (s != LORA_OK) return fail(s, err);
+    const size_t nv = (size_t)std::max<int64_t>(p->plan.vred_floats, 1);
+    {
+        DeviceGuard g(p->device);
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing((cudaStream_t)stream, &cap), "lora_apply_tp: capture query");
+        p->capturing = cap != cudaStreamCaptureStatusNone;
+        if ((s = grow(p, p->vred, p->vred_cap, nv, false, "vred")) != LORA_OK) return s;
+    }
+    s = apply_impl(p, x, nullptr, seg_indptr, adapter_ids, num_segments, stream, 1, p->vred, (int64_t)p->vred_cap, x_ld, 0);
+    if (s != LORA_OK) return s;
+    if (!p->split_ready || p->plan.n_gc == 0) {   // nothing to reduce or expand
+        p->split_ready = false;
+        return LORA_OK;
+    }
+    {
+        DeviceGuard g(p->device);
+        const int r = n->all_reduce(p->vred, p->vred, (size_t)p->plan.vred_floats, kNcclFloat32, kNcclSum, p->tp->comm,
+                                    (cudaStream_t)stream);
+        if (r != 0) {
+            p->split_ready = false;
+            return fail(LORA_ERR_NCCL, std::string("ncclAllReduce: ") + n->error_string(r));
+        }
+    }
+    return apply_impl(p, nullptr, y, nullptr, nullptr, 0, stream, 2, p->vred, 0, 0, y_ld);
 }
 
 lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, void* y, const int32_t* seg_indptr,
@@ -697,7 +855,6 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             lora_status s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(1, value * ks * LORA_MAX_RANK), false, "vbuf");
             if (s == LORA_OK)
                 s = grow(p, p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
-            if (s == LORA_OK) s = grow(p, p->gc_sync, p->gc_sync_cap, (size_t)(1 + 2 * value), true, "gc_sync");
             // prefill split-K partials: at most one 128 x 128 fp32 tile per CTA, and the planner keeps
             // split-K grids within the SM count
             const int64_t pf_ctas = std::min<int64_t>((value + 127) / 128 * 8, p->num_sms);
@@ -705,14 +862,6 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
                 s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pf_ctas * 128 * 128, false, "pf_scratch");
             return s;
         }
-        case LORA_OPT_DECODE_KERNEL:
-            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_KERNEL takes 0 or 1");
-            p->decode_kernel = (int)value;
-            return LORA_OK;
-        case LORA_OPT_DECODE_STAGES:
-            if (value < 2 || value > 3) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_STAGES takes 2 or 3");
-            p->decode_stages = (int)value;
-            return LORA_OK;
         case LORA_OPT_LOAD_KERNEL:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_LOAD_KERNEL takes 0 or 1");
             p->load_kernel = value == 1;
@@ -767,9 +916,7 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* o) {
     o->n_decode_units = pl.n_shrink + pl.n_expand;
     o->n_shrink_units = pl.n_shrink;
     o->n_expand_units = pl.n_expand;
-    o->v_floats = pl.vbuf_floats;
-    o->decode_ctas = pl.stream_ctas;
-    o->decode_stages = pl.stream_ns;
+    o->v_floats = pl.vred_floats;
     o->n_prefill_tiles = pl.n_prefill_tiles;
     o->n_prefill_ctas = pl.n_pf_tiles;
     o->prefill_cluster = pl.pf_cs;

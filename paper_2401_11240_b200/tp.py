@@ -1,25 +1,23 @@
-"""Tensor-parallel LoRA delta (BASELINE.json north_star; SURVEY.md §8(e)).
+"""Tensor-parallel LoRA delta (BASELINE.json north_star; SURVEY.md §8(a) a5, §8(e)).
 
 Scheme ("BJ scheme"): rank k of a tp-way group holds A[:, H_in slice k] and
-B[:, H_out slice k].  Per apply:
-    1. shrink    v_k = x[:, slice k] · A[slice k, :]          (library kernel, lora_apply_shrink)
-    2. all-reduce v = Σ_k v_k  (fp32, rank-r sized: c5 decode 15 KB)  -- torch.distributed / NCCL
-    3. expand    y[:, out slice k] += s · v · B[:, out slice k]    (library kernel, lora_apply_expand)
-so adapter bytes per GPU scale as 1/tp.  The paper's own scheme ("partition B like the base
-weight ... no extra communication") is the special case split_in=False (A replicated, no collective).
-Row-parallel layers (o/down: x already sharded on H_in) use split_in=True with the caller's x shard
-and add into the partial (pre-all-reduce) y of the base layer.
+B[:, H_out slice k].  One lora_apply_tp call per apply, entirely inside liblora.so on the caller's
+stream: shrink over the rank's H_in slice -> k-reduce into the compact fp32 v [Σ_gc ntok x r] ->
+ncclAllReduce(SUM) of v over the group (the library's own communicator; c5 decode: 15,360 B) ->
+expand into the rank's H_out slice.  Adapter bytes per GPU scale as 1/tp.  The paper's own scheme
+(partition B like the base weight, no extra communication) is split_in=False
+(A replicated, no collective: the pool's A holds all of H_in).
+Column-parallel layers (q/k/v/gate/up: x replicated) pass x[:, slice] as a strided view; row-parallel
+layers (o/down: x already sharded) pass their x shard and add into a strided view of the partial
+(pre-all-reduce) y of the base layer (y[:, out slice] of the full-width partial sum).
 
-PyTorch is plumbing here: device buffers and the NCCL all-reduce through torch.distributed.
-Every arithmetic step runs in liblora.so.
+Torch is plumbing here: tensors, and the process group that broadcasts the NCCL unique id.
 """
 from __future__ import annotations
 
 from typing import Optional, Tuple
 
-import numpy as np
-
-from .binding import LoraPool
+from .binding import LORA_OPT_TC_THRESHOLD, LoraPool, TPComm
 
 
 def shard_bounds(H: int, tp: int, rank: int) -> Tuple[int, int]:
@@ -35,52 +33,40 @@ class TPLoraLayer:
 
     def __init__(self, hidden_in: int, hidden_out: int, tp_rank: int, tp_size: int, max_adapters: int,
                  max_total_rank: int = 0, dtype: str = "bf16", split_in: bool = True, split_out: bool = True,
-                 group=None):
+                 comm: Optional[TPComm] = None):
         self.H_in, self.H_out = hidden_in, hidden_out
         self.tp_rank, self.tp_size = tp_rank, tp_size
         self.split_in, self.split_out = split_in, split_out
         self.in_lo, self.in_hi = shard_bounds(hidden_in, tp_size, tp_rank) if split_in else (0, hidden_in)
         self.out_lo, self.out_hi = shard_bounds(hidden_out, tp_size, tp_rank) if split_out else (0, hidden_out)
-        self.group = group
         self.pool = LoraPool(self.in_hi - self.in_lo, self.out_hi - self.out_lo, max_adapters, dtype,
                              max_total_rank=max_total_rank)
-        # the split (shrink | all-reduce | expand) runs every token on the decode kernels; keep
-        # lora_plan's sizing consistent with that by disabling the tensor-core prefill routing
-        from .binding import LORA_OPT_TC_THRESHOLD
+        # the TP path runs every token on the decode kernels; keep lora_plan's sizing consistent
         self.pool.set_option(LORA_OPT_TC_THRESHOLD, 1 << 30)
-        self._v = None
+        self.comm = comm
+        if comm is not None:
+            self.pool.tp_init(comm)
 
-    def load_adapter(self, aid: int, rank: int, A_full: np.ndarray, B_full: np.ndarray, scale: float) -> None:
-        """A_full [rank][H_in], B_full [rank][H_out] (host arrays of the whole adapter); this rank
-        keeps its slices (copied into pinned host memory for the side-stream load)."""
-        import torch
-        A = np.ascontiguousarray(A_full[:, self.in_lo:self.in_hi])
-        B = np.ascontiguousarray(B_full[:, self.out_lo:self.out_hi])
-        view = (lambda a: a.view(np.int16)) if A.dtype == np.uint16 else (lambda a: a)
-        self.pool.load_adapter(aid, rank, torch.from_numpy(view(A)).pin_memory(),
-                               torch.from_numpy(view(B)).pin_memory(), scale)
+    def load_adapter(self, aid: int, rank: int, A_full, B_full, scale: float) -> None:
+        """A_full [rank][H_in], B_full [rank][H_out]: the WHOLE adapter in pinned host memory (torch
+        tensors); the library copies this rank's columns with 2D copies on its side stream."""
+        self.pool.load_adapter_shard(aid, rank, A_full, self.in_lo, B_full, self.out_lo, scale)
 
-    def v_buffer(self, seg_indptr, adapter_ids):
-        import torch
-        self.pool.plan(seg_indptr, adapter_ids)
-        n = max(1, self.pool.metadata()["v_floats"])
-        if self._v is None or self._v.numel() < n:
-            self._v = torch.empty(n, dtype=torch.float32, device="cuda")
-        return self._v[:n]
-
-    def apply(self, x_shard, y_shard, seg_indptr, adapter_ids, stream=None, all_reduce=None) -> None:
-        """x_shard [T][in slice] and y_shard [T][out slice] are this rank's device tensors.
-        all_reduce: callable(tensor) summing it across the TP group (default: torch.distributed
-        all_reduce on self.group when tp_size > 1 and split_in)."""
-        v = self.v_buffer(seg_indptr, adapter_ids)
-        self.pool.apply_shrink(x_shard, seg_indptr, adapter_ids, v, stream=stream)
-        if self.split_in and self.tp_size > 1:
-            if all_reduce is None:
-                import torch.distributed as dist
-                dist.all_reduce(v, op=dist.ReduceOp.SUM, group=self.group)
-            else:
-                all_reduce(v)
-        self.pool.apply_expand(y_shard, v, stream=stream)
+    def apply(self, x, y, seg_indptr, adapter_ids, stream=None) -> None:
+        """x: [T][H_in] replicated activations (column-parallel, split_in) or this rank's [T][in slice]
+        shard; y: this rank's [T][out slice] output, or the full-width partial y of a row-parallel
+        layer.  Strided column views are passed through (no copies)."""
+        xs = x[:, self.in_lo:self.in_hi] if x.shape[1] == self.H_in and self.split_in else x
+        ys = y[:, self.out_lo:self.out_hi] if y.shape[1] == self.H_out and self.split_out else y
+        if self.comm is None and self.split_in and self.tp_size > 1:
+            raise ValueError("split_in with tp_size > 1 needs a TPComm (the v all-reduce)")
+        if self.comm is None or not self.split_in:
+            # the paper's scheme (A replicated) needs no collective: the plain apply on the B shard
+            if xs.is_contiguous() and ys.is_contiguous():
+                self.pool.apply(xs, ys, seg_indptr, adapter_ids, stream=stream)
+                return
+            raise ValueError("without a communicator x and y must be contiguous shards")
+        self.pool.apply_tp(xs, ys, seg_indptr, adapter_ids, stream=stream)
 
     def close(self) -> None:
         self.pool.close()

@@ -9,9 +9,9 @@ if [ -z "$SKIP_TESTS" ]; then
   timeout 1200 python -m pytest tests -m gpu -q "$@" > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; grep -E "FAILED|ERROR|passed|failed" $OUT/pytest_gpu_$TAG.log | tail -15
 fi
 Q="--prefill-layers 0 --c4-steps 0 --c5-reps 0 --fused-base-reps 0 --no-cpu-baseline --e2e-steps 3 --steps 50 --warmup 5"
-DK=${DK:-0 1}
-for la in $DK; do
-  timeout 300 python bench.py $Q --decode-kernel $la --json-out $OUT/bench_${TAG}_la$la.json > $OUT/bench_${TAG}_la$la.log 2>&1
+
+for la in 0; do
+  timeout 300 python bench.py $Q --json-out $OUT/bench_${TAG}_la$la.json > $OUT/bench_${TAG}_la$la.log 2>&1
   echo "bench decode_kernel=$la rc=$?"
   python - $OUT/bench_${TAG}_la$la.json <<'PY'
 import json,sys

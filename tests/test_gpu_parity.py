@@ -632,52 +632,3 @@ def test_prefill_few_tile_splits(L, H_in, H_out, n_tiles):
     ref = O.delta_for_batch(b, n_threads=16)
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
 
-
-@pytest.mark.parametrize("stages", [2, 3])
-def test_stream_kernel_bitwise_equals_pair(L, stages):
-    """The persistent streaming decode kernel (default, LORA_OPT_DECODE_KERNEL 0) and the PDL kernel
-    pair (1) run the same arithmetic in the same fixed orders: bitwise-equal y, over single-pool and
-    q/k/v-multi applies, uniform / Zipf / random batches (ranks 1..256, up to 8 tokens per chunk),
-    repeated applies (the per-gc counters must re-arm) and a CUDA graph replay."""
-    import torch
-    from paper_2401_11240_b200 import binding as B
-    batches = [gen.config_c2(y_zero=False), gen.config_c2(zipf=True, y_zero=False, tag=3),
-               gen.random_batch(4242, "bf16", 4096, 1024, max_seg=40, max_rank=256, max_len=5, n_adapters=24,
-                                y_zero=False),
-               gen.random_batch(4343, "bf16", 1000, 3000, max_seg=60, max_rank=200, max_len=12, n_adapters=16,
-                                y_zero=False)]
-    for b in batches:
-        pools = [make_pool(b, L, L_tc=1 << 30) for _ in range(3)]
-        x = to_torch(b.x, "cuda")
-        outs = {}
-        for kern in (1, 0):
-            for p in pools:
-                p.set_option(B.LORA_OPT_DECODE_KERNEL, kern)
-                p.set_option(B.LORA_OPT_DECODE_STAGES, stages)
-            ys = [to_torch(b.y_in, "cuda") for _ in range(4)]
-            for _ in range(3):
-                pools[0].apply(x, ys[0], b.seg_indptr, b.adapter_ids)
-                L.apply_multi(pools, [x] * 3, ys[1:], b.seg_indptr, b.adapter_ids)
-            torch.cuda.synchronize()
-            md = pools[0].metadata()
-            assert (md["decode_ctas"] > 0) == (kern == 0) and (kern == 1 or md["decode_stages"] == stages)
-            st = torch.cuda.Stream()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=st):
-                pools[0].apply(x, ys[0], b.seg_indptr, b.adapter_ids, stream=st)
-                L.apply_multi(pools, [x] * 3, ys[1:], b.seg_indptr, b.adapter_ids, stream=st)
-            with torch.cuda.stream(st):
-                for _ in range(2):
-                    g.replay()
-            torch.cuda.synchronize()
-            outs[kern] = [y.clone() for y in ys]
-        for a_, c_ in zip(outs[0], outs[1]):
-            assert torch.equal(a_, c_)
-        for p in pools:
-            p.close()
-    # and one fresh apply against the oracle
-    b = batches[2]
-    ref = O.delta_for_batch(b, n_threads=8)
-    y, md = run_gpu(b, L, L_tc=1 << 30)
-    assert md["decode_ctas"] > 0
-    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
