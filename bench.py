@@ -551,81 +551,111 @@ def bench_fused_base(L, dev, reps: int, tc_peak: float):
     return out
 
 
-def bench_c5(L, dev, reps: int, hbm_peak: float):
-    """c5: Llama-2-70B per-layer projection shapes (q/o 8192^2, k/v 8192->1024, gate/up 8192->28672,
-    down 28672->8192), decode 64 tokens over 32 adapters of ranks [16,32,64,128][a mod 4].  tp = 1:
-    lora_apply on the full shape.  tp = 2/4/8 (BJ scheme): ONE rank's work, i.e.
-    lora_apply_shrink on its H_in slice + lora_apply_expand on its H_out slice, with the v
-    all-reduce between them excluded (one GPU here; correctness of the split is tested on gloo and
-    NCCL world-1).  Device time per apply from a CUDA graph over enough distinct pools that the
-    adapter rows exceed L2."""
+def _graph_us(body, st, reps: int, n_per_replay: int) -> float:
+    """median device time (us) per call of `body` (n_per_replay calls per replay) from a CUDA graph."""
     import torch
+    with torch.cuda.stream(st):
+        body()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        body()
+    ts = []
+    for _ in range(max(1, reps)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        with torch.cuda.stream(st):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / n_per_replay)
+    del g
+    return float(np.median(ts))
+
+
+def bench_c5(L, dev, reps: int, hbm_peak: float, world: int = 1, rank: int = 0, use_dist: bool = False):
+    """c5: Llama-2-70B per-layer projection shapes (q/o 8192^2, k/v 8192->1024, gate/up 8192->28672,
+    down 28672->8192), decode 64 tokens over 32 adapters of ranks [16,32,64,128][a mod 4].
+    tp = 1: lora_apply on the full shape.  tp > 1 (BJ scheme): the rank's shard pool
+    (lora_load_adapter_shard from the full pinned adapters) and
+      shard_kernels: lora_apply_shrink (shrink + k-reduce into the compact v) + lora_apply_expand --
+                     one rank's kernels without the collective;
+      apply_tp:      lora_apply_tp = the same kernels + ncclAllReduce of the compact v (15,360 B) on the
+                     library's communicator.  With one GPU (this run) the communicator is world-1 (its
+                     all-reduce is a local no-op); under torchrun with N GPUs the tp = N row runs the
+                     real N-rank all-reduce over NVLink, timed as the max over ranks.
+    Device time per apply from a CUDA graph over enough distinct pools that the adapter rows exceed L2."""
+    import torch
+    from paper_2401_11240_b200.binding import TPComm
     shapes = {"q": (8192, 8192), "kv": (8192, 1024), "gate_up": (8192, 28672), "down": (28672, 8192)}
     ranks = [gen.C5_RANKS[a % 4] for a in range(32)]
     b = gen.config_c5("q")
     ip, ids = b.seg_indptr, b.adapter_ids
     T = 64
     st = torch.cuda.Stream(device=dev)
+    comm = TPComm.from_process_group() if use_dist else TPComm(L.binding.tp_unique_id(), 0, 1)
     out = {}
     for name, (H_in, H_out) in shapes.items():
         full = [gen.make_adapter(gen.BASE_SEED + 4, 50 + list(shapes).index(name), a, ranks[a], H_in, H_out, "bf16")
                 for a in range(32)]
+        pinned = [(torch.from_numpy(a.A.view(np.int16)).pin_memory(), torch.from_numpy(a.B.view(np.int16)).pin_memory())
+                  for a in full]
         row = {}
         for tp in (1, 2, 4, 8):
+            if use_dist and tp != world:
+                continue   # multi-GPU: the tp = N row with the real collective only
+            trank = rank if use_dist else 0
             hi, ho = H_in // tp, H_out // tp
             adapter_bytes = sum(ranks) * (hi + ho) * 2
             n_pools = max(2, -(-400_000_000 // adapter_bytes))
             pools = []
             for _ in range(n_pools):
                 pool = L.LoraPool(hi, ho, 32, "bf16", max_total_rank=sum(ranks))
-                for a in full:   # rank 0's shard: A[:, :hi] (stored [r][H_in]) and B[:, :ho]
-                    A = torch.from_numpy(np.ascontiguousarray(a.A[:, :hi]).view(np.int16)).pin_memory()
-                    B = torch.from_numpy(np.ascontiguousarray(a.B[:, :ho]).view(np.int16)).pin_memory()
-                    pool.load_adapter(a.id, a.rank, A, B, a.scale)
+                for a, (A, B) in zip(full, pinned):   # this rank's shard, straight from the full adapter
+                    pool.load_adapter_shard(a.id, a.rank, A, trank * hi, B, trank * ho, a.scale)
+                if tp > 1:
+                    pool.tp_init(comm)
                 pools.append(pool)
             torch.cuda.synchronize()
             x = torch.randn(T, hi).to(torch.bfloat16).to(dev)
             ys = [torch.zeros(T, ho, dtype=torch.bfloat16, device=dev) for _ in pools]
-            vs = None
-            if tp > 1:
+            byts = adapter_bytes + T * hi * 2 + 2 * T * ho * 2
+            r = {"adapter_MB_per_gpu": round(adapter_bytes / 1e6, 2)}
+            if tp == 1:
+                us = _graph_us(lambda: [p.apply(x, y, ip, ids, stream=st) for p, y in zip(pools, ys)], st, reps, n_pools)
+                r.update({"us_per_apply": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1),
+                          "roofline_frac": round(byts / (us * 1e-6) / 1e9 / hbm_peak, 4)})
+            else:
                 pools[0].plan(ip, ids)
                 nv = pools[0].metadata()["v_floats"]
                 vs = [torch.zeros(max(1, nv), dtype=torch.float32, device=dev) for _ in pools]
-
-            def body():
-                for i, (pool, y) in enumerate(zip(pools, ys)):
-                    if tp == 1:
-                        pool.apply(x, y, ip, ids, stream=st)
-                    else:
-                        pool.apply_shrink(x, ip, ids, vs[i], stream=st)
-                        pool.apply_expand(y, vs[i], stream=st)
-
-            with torch.cuda.stream(st):
-                body()
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=st):
-                body()
-            ts = []
-            for _ in range(max(1, reps)):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(st)
-                with torch.cuda.stream(st):
-                    g.replay()
-                e1.record(st)
-                torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1) * 1e3 / n_pools)
-            us = float(np.median(ts))
-            byts = adapter_bytes + T * hi * 2 + 2 * T * ho * 2
-            row["tp%d" % tp] = {"us_per_apply": round(us, 3), "adapter_MB_per_gpu": round(adapter_bytes / 1e6, 2),
-                                "GBps": round(byts / (us * 1e-6) / 1e9, 1),
-                                "roofline_frac": round(byts / (us * 1e-6) / 1e9 / hbm_peak, 4)}
+                us_k = _graph_us(lambda: [(p.apply_shrink(x, ip, ids, v, stream=st), p.apply_expand(y, v, stream=st))
+                                          for p, y, v in zip(pools, ys, vs)], st, reps, n_pools)
+                us_tp = _graph_us(lambda: [p.apply_tp(x, y, ip, ids, stream=st) for p, y in zip(pools, ys)], st, reps,
+                                  n_pools)
+                if use_dist:
+                    us_k = max_over_ranks(us_k, True)
+                    us_tp = max_over_ranks(us_tp, True)
+                r.update({"v_allreduce_bytes": int(nv * 4),
+                          "shard_kernels_us": round(us_k, 3),
+                          "shard_kernels_roofline_frac": round(byts / (us_k * 1e-6) / 1e9 / hbm_peak, 4),
+                          "apply_tp_us": round(us_tp, 3),
+                          "allreduce_us": round(us_tp - us_k, 3),
+                          "comm": "NCCL %d ranks (NVLink)" % world if use_dist else "NCCL world 1 (local: no transfer)"})
+                del vs
+            row["tp%d" % tp] = r
             for pool in pools:
                 pool.close()
-            del pools, ys, vs
-        for tp in (2, 4, 8):
-            row["tp%d" % tp]["speedup_vs_tp1"] = round(row["tp1"]["us_per_apply"] / row["tp%d" % tp]["us_per_apply"], 2)
+            del pools, ys
+        if "tp1" in row:
+            for tp in (2, 4, 8):
+                if "tp%d" % tp in row:
+                    row["tp%d" % tp]["shard_speedup_vs_tp1"] = round(row["tp1"]["us_per_apply"] /
+                                                                     row["tp%d" % tp]["shard_kernels_us"], 2)
         out[name] = row
+    comm.close()
+    if use_dist:
+        return {"workload": "c5 TP decode, tp = %d across the N GPUs of this run" % world, "per_shape": out}
     # prefill 8 x 512 tokens (32 token tiles: the planner splits each tile's columns over SMs/tiles CTAs)
     pf = {}
     for proj in ("q", "gate", "down"):
@@ -669,8 +699,8 @@ def bench_c5(L, dev, reps: int, hbm_peak: float):
             pool.close()
         del pools, ys
     return {"workload": "c5: Llama-2-70B projection shapes, decode 64 tokens over 32 adapters ranks 16..128, bf16; "
-                        "tp>1 = one rank's shard kernels (shrink + expand), v all-reduce excluded; prefill_tp1: 8 x 512 "
-                        "tokens over 8 adapters on the tcgen05 kernel",
+                        "tp>1 = one rank's shard pool: shard kernels alone and lora_apply_tp (+ the library's NCCL "
+                        "all-reduce of the compact v); prefill_tp1: 8 x 512 tokens over 8 adapters on the tcgen05 kernel",
             "prefill_tp1": pf,
             "shapes": {k: list(v) for k, v in shapes.items()}, "per_shape": out}
 
@@ -871,7 +901,7 @@ def main():
 
     c5 = None
     if args.c5_reps > 0:
-        c5 = bench_c5(L, dev, args.c5_reps, hbm_peak)
+        c5 = bench_c5(L, dev, args.c5_reps, hbm_peak, world, rank, use_dist and not SHARE_GPU)
 
     fused_base = None
     if args.fused_base_reps > 0 and rank == 0:

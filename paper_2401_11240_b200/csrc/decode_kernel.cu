@@ -52,8 +52,9 @@ struct DecodeArgs {
     int unit_words;              // 3 (full unit records) or 1 (gc | local only: large batches)
     // bf16 expand smem layout, sized per launch from the batch (max rank / tokens / columns)
     int e_vpitch, e_boff, e_yoff, e_dtoff, e_pgoff, e_smem;
-    float* vred;                 // compact k-reduced v (TP split): written by lora_vreduce_kernel, read by
-                                 // the expand when v_compact is set
+    float* vred;                 // compact k-reduced v (TP split): written by the shrink kernel's last CTA of
+                                 // each gc (tp_reduce_tail), read by the expand when v_compact is set
+    int* gc_cnt;                 // TP shrink: per-gc arrival counters (zero between applies)
     int v_compact;
     int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
     int job_expand_base[kMaxJobs];
@@ -212,6 +213,13 @@ struct Elem<float> {
 
 // ------------------------------------------------------------------ metadata access
 __device__ __forceinline__ int gc_field(const int32_t* M, int gc, int f) { return M[kHdrWords + gc * kGcFields + f]; }
+// TP split (a.vred set, expand not yet run): the shrink CTA that completes a gc's partials sums them
+// over the k-slices, in slice order, into the compact v [ntok][v_stride(r)] at GC_VRED -- the rank-r
+// payload the TP ranks all-reduce (c5 decode: 15,360 B).  The CTA's own partial stores precede the
+// counter increment (fence + barrier); the last arriver re-arms the counter for the next apply.
+template <int NT>
+__device__ __forceinline__ void tp_reduce_tail(const struct DecodeArgs& a, const int32_t* M, int gc, int* flag_smem);
+
 // page of rank row j of a page reference (kernel_config.h page_ref_add)
 __device__ __forceinline__ int page_at(const int32_t* M, int ref, int j) { return ref >= 0 ? M[ref + j] : (~ref) + j; }
 // unit u's work record.  3-word mode: one round of independent uniform loads; 1-word mode (batches
@@ -239,6 +247,32 @@ __device__ __forceinline__ UnitRec load_unit(const int32_t* M, int unit_tab, int
         if (shrink) d.pref = page_ref_add(d.pref, (d.local % shrink_jblocks(d.r, 2)) * kShrinkRowsMma);
     }
     return d;
+}
+
+template <int NT>
+__device__ __forceinline__ void tp_reduce_tail(const DecodeArgs& a, const int32_t* M, int gc, int* flag_smem) {
+    const int tid = threadIdx.x;
+    __threadfence();   // this thread's partial stores, gpu scope, before the counter
+    __syncthreads();
+    if (tid == 0) {
+        const bool last_gc = gc + 1 >= a.n_gc;
+        const int n_s = (last_gc ? a.n_shrink : gc_field(M, gc + 1, GC_SHRINK_BASE)) - gc_field(M, gc, GC_SHRINK_BASE);
+        const int prev = atomicAdd(a.gc_cnt + gc, 1);
+        *flag_smem = prev == n_s - 1;
+        if (prev == n_s - 1) a.gc_cnt[gc] = 0;   // every shrink unit of the gc has arrived: re-arm
+    }
+    __syncthreads();
+    if (!*flag_smem) return;
+    __threadfence();   // acquire side: the other CTAs' partials
+    const int r = gc_field(M, gc, GC_RANK), ntok = gc_field(M, gc, GC_NTOK), rs = v_stride(r);
+    const int ksplit = a.jobs[gc_field(M, gc, GC_JOB)].ksplit;
+    const float* src = a.vbuf + gc_field(M, gc, GC_VOFF);
+    float* dst = a.vred + gc_field(M, gc, GC_VRED);
+    for (int e = tid; e < ntok * rs; e += NT) {
+        float v = 0.f;
+        for (int k = 0; k < ksplit; ++k) v += ld_cg_f32(src + k * ntok * rs + e);
+        dst[e] = v;
+    }
 }
 
 // per-CTA unit description, decoded once by warp 0 and shared through smem
@@ -373,6 +407,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
             for (int p = 0; p < P; ++p) v += red[(row * P + p) * kTokChunk + t];
         a.vbuf[sh->voff + (ks * ntok + t) * v_stride(r) + j0 + row] = v;
     }
+    if (a.vred) tp_reduce_tail<kConsumerThreads>(a, M, sh->gc, &sh->ks);
     if (a.trace && tid == 0) {
         a.trace[(size_t)u * 8 + 0] = smid();
         a.trace[(size_t)u * 8 + 4] = sh->r;
@@ -732,6 +767,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         }
         a.vbuf[sh->voff + (ks * ntok + t) * v_stride(r) + j0 + row] = v;
     }
+    if (a.vred) tp_reduce_tail<kConsumerThreads>(a, M, sh->gc, &sh->ks);
     if (a.trace && tid == 0) {
         a.trace[(size_t)u * 8 + 0] = smid();
         a.trace[(size_t)u * 8 + 4] = sh->r;
@@ -976,27 +1012,6 @@ __global__ void __launch_bounds__(kConsumerThreads, MINB)
     expand_mma_body(a, M, blockIdx.x, smem);
 }
 
-// TP split: the k-slice partials of every gc summed in slice order into the compact v
-// [gc][ntok][v_stride(r)] (GC_VRED offsets) -- the rank-r payload the TP ranks all-reduce
-// (c5 decode 64 tokens x ranks 16..128 = 15,360 B).  One CTA per gc.
-template <int W>
-__global__ void __launch_bounds__(256)
-    lora_vreduce_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
-    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
-    pdl_wait_cta();   // the partials of the shrink kernel
-    const int gc = blockIdx.x;
-    const int r = gc_field(M, gc, GC_RANK), ntok = gc_field(M, gc, GC_NTOK), rs = v_stride(r);
-    const int ksplit = a.jobs[gc_field(M, gc, GC_JOB)].ksplit;
-    const float* src = a.vbuf + gc_field(M, gc, GC_VOFF);
-    float* dst = a.vred + gc_field(M, gc, GC_VRED);
-    for (int e = threadIdx.x; e < ntok * rs; e += blockDim.x) {
-        float v = 0.f;
-        for (int k = 0; k < ksplit; ++k) v += ld_cg_f32(src + k * ntok * rs + e);
-        dst[e] = v;
-    }
-    pdl_launch_dependents();
-}
-
 // copies a metadata blob too large for one kernel's parameters into device memory,
 // kUploadWords per launch (parameters are captured by value in CUDA graphs)
 constexpr int kUploadWords = 7936;
@@ -1081,11 +1096,6 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, ss, st, a, blob);
         if (e != cudaSuccess) return e;
         *launches += 1;
-        if (a.vred && !a.v_compact) {   // TP split: k-reduce the partials into the compact v
-            e = launch_pdl(lora_vreduce_kernel<W>, pl.n_gc, 256, 0, st, a, blob);
-            if (e != cudaSuccess) return e;
-            *launches += 1;
-        }
     }
     if (phases & 2) {
         const bool big = pl.n_expand > 3 * num_sms;
@@ -1111,8 +1121,9 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
                               static_cast<const char*>(B), hin, hout, ksplit_of(hin, (int)sizeof(T)), xld, yld};
     }
     a.vbuf = L.vbuf;
-    a.vred = L.vred;
     a.v_compact = (L.phases == 2 && L.vred) ? 1 : 0;
+    a.vred = (L.phases == 1 && !L.gc_cnt) ? nullptr : L.vred;   // the shrink's reduce tail needs the counters
+    a.gc_cnt = L.gc_cnt;
     a.meta_global = L.meta_dev;
     a.trace = L.trace;
     a.n_shrink = pl.n_shrink;

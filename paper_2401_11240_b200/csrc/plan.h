@@ -97,6 +97,7 @@ struct DecodeLaunch {
     float* vred = nullptr;       // phases 1: also reduce the partials over k-slices into this compact v;
                                  // phases 2: the expand reads this compact (k-reduced) v instead of vbuf
     int64_t x_ld = 0, y_ld = 0;  // row strides (elements) of x / y of job 0; 0 = H_in / H_out
+    int* gc_cnt = nullptr;       // phases 1 with vred: the pool's zeroed per-gc arrival counters
     struct More {                // jobs 1.. of a fused multi-pool apply (job 0 = the fields above)
         const void* x;
         void* y;

@@ -64,6 +64,8 @@ struct lora_pool {
     unsigned long long* trace = nullptr;   // lora_debug_set_trace
     bool capturing = false;               // the current apply's stream is being captured into a graph
     std::vector<void*> retired;           // outgrown scratch buffers: a captured graph may still use them
+    int32_t* gc_cnt = nullptr;            // TP shrink: per-gc arrival counters (zero between applies)
+    size_t gc_cnt_cap = 0;
     float* vred = nullptr;                // TP: the compact k-reduced v all-reduced by lora_apply_tp
     size_t vred_cap = 0;
     lora_tp_comm* tp = nullptr;           // lora_tp_init: the TP group's communicator (not owned)
@@ -271,6 +273,7 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->dB) cudaFree(p->dB);
         if (p->vbuf) cudaFree(p->vbuf);
         if (p->vred) cudaFree(p->vred);
+        if (p->gc_cnt) cudaFree(p->gc_cnt);
         if (p->pf_scratch) cudaFree(p->pf_scratch);
         if (p->meta_dev) cudaFree(p->meta_dev);
         for (void* b : p->retired) cudaFree(b);
@@ -514,6 +517,9 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
     }
+    if (pl.n_gc > 0 && mode == 1) {
+        if ((s = grow(p, p->gc_cnt, p->gc_cnt_cap, (size_t)pl.n_gc, true, "gc_cnt")) != LORA_OK) return s;
+    }
     if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p, p->meta_dev, p->meta_cap, pl.blob.size(), false, "meta")) != LORA_OK) return s;
     }
@@ -522,6 +528,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         DecodeLaunch L{x, y, p->dA, p->dB, p->vbuf, p->meta_dev, p->trace, p->H_in, p->H_out, p->esz, p->num_sms};
         L.phases = mode == 0 ? 3 : mode;
         L.vred = mode == 0 ? nullptr : v_ext;
+        L.gc_cnt = mode == 1 ? p->gc_cnt : nullptr;
         L.x_ld = x_ld;
         L.y_ld = y_ld;
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
@@ -855,6 +862,7 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             lora_status s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(1, value * ks * LORA_MAX_RANK), false, "vbuf");
             if (s == LORA_OK)
                 s = grow(p, p->meta_dev, p->meta_cap, (size_t)(kHdrWords + (kGcFields + 1) * value + 4096), false, "meta");
+            if (s == LORA_OK) s = grow(p, p->gc_cnt, p->gc_cnt_cap, (size_t)std::max<int64_t>(1, value), true, "gc_cnt");
             // prefill split-K partials: at most one 128 x 128 fp32 tile per CTA, and the planner keeps
             // split-K grids within the SM count
             const int64_t pf_ctas = std::min<int64_t>((value + 127) / 128 * 8, p->num_sms);

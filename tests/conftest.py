@@ -9,3 +9,13 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    # tests that open a (world-1) torch.distributed group leave it for later tests; close it once here
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
