@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--min-window-ms", type=float, default=200.0,
                     help="repeat the K-step timed window until this much device time is covered (median reported)")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
+    ap.add_argument("--cold-start", type=int, choices=[0, 1], default=1,
+                    help="cold-start latency by rank + the paper's CPU-assist comparison (rank 0)")
     ap.add_argument("--c5-reps", type=int, default=5, help="config 5 (70B shapes, tp 1/2/4/8 shards) timing reps; 0 = skip")
     ap.add_argument("--fused-base-reps", type=int, default=5,
                     help="NEXT f2 (delta fused into the base GEMM) timing reps on c3 shapes; 0 = skip")
@@ -353,34 +355,22 @@ def bench_prefill(L, layers: int, steps: int, dev, hbm_peak: float, tc_peak: flo
 
 
 # ---------------------------------------------------------------- config 4: Zipf paged pool + cold starts
-def h2d_peak_gbs(dev) -> float:
-    """Pinned host -> device copy bandwidth (256 MiB cudaMemcpyAsync, best of 5)."""
-    import torch
-    src = torch.empty(256 * 2 ** 20, dtype=torch.uint8).pin_memory()
-    dst = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
-    best = 1e9
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        dst.copy_(src, non_blocking=True)
-        e1.record()
-        torch.cuda.synchronize()
-        best = min(best, e0.elapsed_time(e1))
-    return src.numel() / (best * 1e-3) / 1e9
-
-
-def bench_c4(L, dev, steps: int, world: int, rank: int):
+def bench_c4(L, dev, steps: int, world: int, rank: int, use_dist: bool = False):
     """Llama-2-13B (5120) projection, 1000 adapters (ranks 8..128) in pinned host memory, a pool of
-    20% of their ranks per GPU, Zipf(1.0) requests: per step 64 decode tokens + one 512-token
-    prefill; misses load on the side stream (LRU eviction) and overlap the applies.  Requests are
-    partitioned by adapter home (id mod N, top-16 replicated).  Reports tokens/s with the loads
-    included, hit rate, and the cold-start latency next to the measured pinned H2D bandwidth."""
+    20% of their ranks per GPU, Zipf(1.0) requests: per step 64 decode tokens + one 512-token prompt
+    PER GPU (weak scaling), drawn as one global list and routed across the N GPUs by the paper's
+    rank-aware Algorithm 1 (serving.route_requests: candidates = the GPUs hosting the adapter, home
+    id mod N with the 16 hottest replicated; cost from the models fitted to this library's kernels).
+    Misses load on the side stream (LRU eviction) and overlap the applies.  Reports tokens/s with the
+    loads included (all GPUs, max over ranks), hit rate, and the cold-start latency next to the
+    measured pinned H2D bandwidth."""
     import torch
     import time as _t
-    from paper_2401_11240_b200.serving import AdapterCache, HostRepository, serves
+    from paper_2401_11240_b200.serving import AdapterCache, HostRepository, route_requests, serves
+    from paper_2401_11240_b200.scheduler import measured_model
     H, n_ad, hot = 5120, 1000, list(range(16))
-    mine = [a for a in range(n_ad) if serves(a, rank, world, [int(gen.zipf_perm(gen.BASE_SEED + 3, n_ad)[i]) for i in hot])]
     hot_ids = [int(gen.zipf_perm(gen.BASE_SEED + 3, n_ad)[i]) for i in hot]
+    mine = [a for a in range(n_ad) if serves(a, rank, world, hot_ids)]
     repo = HostRepository()
     t0 = _t.perf_counter()
     with cf.ThreadPoolExecutor(max_workers=min(16, len(os.sched_getaffinity(0)))) as ex:
@@ -393,55 +383,69 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
     pool.set_option(L.binding.LORA_OPT_LOAD_KERNEL, 1)   # the cold-start path by the zero-copy gather kernel
     cache = AdapterCache(pool, repo, budget, n_ad)
     st = torch.cuda.Stream(device=dev)
-    T = 64 + 512
+    model = measured_model("mbgmv", invocations=1)
+    T_max = 64 * world + 512 * world
     g = torch.Generator(device="cpu").manual_seed(gen.BASE_SEED + 300 + rank)
-    x = torch.randn(T, H, generator=g).to(torch.bfloat16).to(dev)
-    y = torch.zeros(T, H, dtype=torch.bfloat16, device=dev)
+    x = torch.randn(T_max, H, generator=g).to(torch.bfloat16).to(dev)
+    y = torch.zeros(T_max, H, dtype=torch.bfloat16, device=dev)
+    routed = {"decode": 0, "prefill": 0}
 
     def draw(step):
-        ids = []
-        s2 = step
-        while len(ids) < 65:   # redraw until 64 decode + 1 prefill requests served by this rank
-            d = gen.config_c4_draw(s2, n_decode=64, prefill_len=512, n_adapters=n_ad, world=world, rank=rank)
-            ids += [int(a) for a in list(d["decode_ids"]) + [int(d["prefill_id"][0])] if serves(int(a), rank, world, hot_ids)]
-            s2 += 100000
-        dec, pre = ids[:64], ids[64]
-        return np.array(dec + [pre], np.int32)
+        """this GPU's share of the step's global requests (Algorithm 1), as (seg_indptr, ids)."""
+        d = gen.config_c4_draw(step, n_decode=64 * world, prefill_len=512, n_adapters=n_ad, n_prefill=world)
+        dec, pre = [int(a) for a in d["decode_ids"]], [int(a) for a in d["prefill_id"]]
+        dec_to, pre_to = route_requests(dec, pre, 512, world, hot_ids, model, gen.c4_rank)
+        my_dec = [a for a, g_ in zip(dec, dec_to) if g_ == rank]
+        my_pre = [a for a, g_ in zip(pre, pre_to) if g_ == rank]
+        routed["decode"] += len(my_dec)
+        routed["prefill"] += len(my_pre)
+        ip_ = gen.segments_to_indptr([1] * len(my_dec) + [512] * len(my_pre))
+        return ip_, np.array(my_dec + my_pre, np.int32)
 
-    ip = gen.segments_to_indptr([1] * 64 + [512])
-
-    def step(sidx):
-        ids = draw(sidx)
+    def step(ip_, ids):
         cache.ensure(ids.tolist())
-        pool.apply(x, y, ip, ids, stream=st)
+        pool.apply(x, y, ip_, ids, stream=st)
+        return int(ip_[-1])
 
     for s_ in range(5):                      # warm the cache
-        step(1000000 + s_)
+        step(*draw(1000000 + s_))
     torch.cuda.synchronize()
     h0, m0, b0 = cache.hits, cache.misses, cache.loaded_bytes
+    routed["decode"] = routed["prefill"] = 0
+    # requests are routed when they arrive (the paper's scheduler runs per request, P:781-798), not
+    # inside a decode iteration: the steps' routings are computed before the timed region
+    draws = [draw(s_) for s_ in range(steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(use_dist)
     w0 = _t.perf_counter()
     e0.record(st)
-    for s_ in range(steps):
-        step(s_)
+    tokens = 0
+    for ip_, ids_ in draws:
+        tokens += step(ip_, ids_)
     e1.record(st)
     torch.cuda.synchronize()
     wall = _t.perf_counter() - w0
     ms = max(e0.elapsed_time(e1), wall * 1e3) / steps
-    # overlap: the same steps on a pool holding every adapter (no loads at all)
+    ms_max = max_over_ranks(ms, use_dist)
+    tok_all = tokens
+    if use_dist:
+        import torch.distributed as dist
+        tt = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt)
+        tok_all = float(tt.item())
+    # overlap (SURVEY §8(d)): the same steps on a pool holding every adapter this GPU serves (no loads)
     full = L.LoraPool(H, H, n_ad, "bf16", max_total_rank=sum(gen.c4_rank(a) for a in mine) + 1)
     for a in mine:
         r_, s_a, A_, B_ = repo.items[a]
         full.load_adapter(a, r_, A_, B_, s_a)
     torch.cuda.synchronize()
-    draws = [draw(s_) for s_ in range(steps)]
-    for ids_ in draws[:3]:
-        full.apply(x, y, ip, ids_, stream=st)
+    for ip_, ids_ in draws[:3]:
+        full.apply(x, y, ip_, ids_, stream=st)
     torch.cuda.synchronize()
     w1 = _t.perf_counter()
     e0.record(st)
-    for ids_ in draws:
-        full.apply(x, y, ip, ids_, stream=st)
+    for ip_, ids_ in draws:
+        full.apply(x, y, ip_, ids_, stream=st)
     e1.record(st)
     torch.cuda.synchronize()
     ms_noload = max(e0.elapsed_time(e1), (_t.perf_counter() - w1) * 1e3) / steps
@@ -458,25 +462,15 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
             pass
         lat.append((_t.perf_counter() - t1) * 1e3)
     lat_bytes = np.mean([repo.bytes_of(a, 2) for a in cold]) if cold else 0
-    peak = h2d_peak_gbs(dev)
-    # NEXT f1 analysis: the paper computes a cold adapter's prefill delta on host cores
-    # while the adapter uploads.  Paper-style CPU LoRA (torch CPU bf16 x@A@B, all host threads) for
-    # the 512-token prefill at rank 64 vs the measured load latency of that adapter.
-    ad64 = next(a for a in mine if gen.c4_rank(a) == 64)
-    _, _, A64, B64 = repo.items[ad64]
-    xc = torch.randn(512, H).to(torch.bfloat16)
-    A64c = A64.view(torch.bfloat16).reshape(64, H).t().contiguous()   # stored rank-major [r][H_in]
-    B64c = B64.view(torch.bfloat16).reshape(64, H)
-    torch.set_num_threads(len(os.sched_getaffinity(0)))
-    (xc @ A64c) @ B64c
-    t1 = _t.perf_counter()
-    for _ in range(3):
-        (xc @ A64c) @ B64c
-    cpu_ms = (_t.perf_counter() - t1) / 3 * 1e3
-    load_ms = (64 * 2 * H * 2) / (lat_bytes / np.median(lat)) if lat else None   # bytes / measured bytes per ms
+    peak = h2d_d2h_peak(dev)["h2d"]
     out = {"workload": "c4: Llama-2-13B 5120->5120 bf16, 1000 adapters ranks 8..128 in pinned host memory, pool = 20%% "
-                       "of their ranks, Zipf(1.0), 64 decode + 1x512 prefill tokens/step, LRU, rank %d/%d" % (rank, world),
-           "value": round(T / (ms * 1e-3), 1), "unit": "tokens/s per GPU (loads included)", "ms_per_step": round(ms, 4),
+                       "of their ranks, Zipf(1.0), per GPU 64 decode + 1x512 prefill tokens/step routed by Algorithm 1, "
+                       "LRU, %d GPU(s)" % world,
+           "value": round(tok_all / steps / (ms_max * 1e-3), 1), "unit": "tokens/s, all GPUs (loads included)",
+           "ms_per_step": round(ms_max, 4),
+           "routing": {"policy": "Algorithm 1 (rank-aware, P:781-814), MBGMV model fitted on B200",
+                       "this_gpu_decode_requests_per_step": round(routed["decode"] / steps, 2),
+                       "this_gpu_prompts_per_step": round(routed["prefill"] / steps, 3)},
            "load_path": "zero-copy gather kernel (LORA_OPT_LOAD_KERNEL=1)",
            "ms_per_step_all_resident": round(ms_noload, 4),
            "overlap": round(ms_noload / ms, 3),   # 1.0 = the cold-start loads cost nothing
@@ -485,14 +479,86 @@ def bench_c4(L, dev, steps: int, world: int, rank: int):
            "cold_start_ms_per_adapter": round(float(np.median(lat)), 3) if lat else None,
            "cold_start_bytes_per_adapter": int(lat_bytes),
            "cold_start_GBps": round(lat_bytes / (np.median(lat) * 1e-3) / 1e9, 2) if lat else None,
-           "h2d_pinned_peak_GBps": round(peak, 1), "host_repo_setup_s": round(gen_s, 1),
-           "cpu_assist": {"cpu_prefill_delta_ms": round(cpu_ms, 3), "threads": torch.get_num_threads(),
-                          "adapter_load_ms": round(float(load_ms), 4) if load_ms else None,
-                          "cpu_wins": bool(load_ms is not None and cpu_ms < load_ms),
-                          "what": "torch CPU bf16 (x@A)@B, 512 tokens, r=64, 5120->5120, vs measured load of a "
-                                  "rank-64 adapter (scaled from the cold-start latency)"}}
+           "h2d_pinned_peak_GBps": round(peak, 1), "host_repo_setup_s": round(gen_s, 1)}
     pool.close()
     return out
+
+
+def h2d_d2h_peak(dev, mib: int = 256, reps: int = 20):
+    """pinned host <-> device copy bandwidth (GB/s), best of `reps` 256 MiB copies each way."""
+    import torch
+    src = torch.empty(mib * 2 ** 20, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(mib * 2 ** 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, (a, b_) in (("h2d", (dst, src)), ("d2h", (src, dst))):
+        best = 1e9
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a.copy_(b_, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = round(src.numel() / (best * 1e-3) / 1e9, 2)
+    return out
+
+
+def bench_cold_start(L, dev, H: int = 5120, reps: int = 9):
+    """Cold start (§2.3 C1, P:341-343 / P:358-362: load latency grows with the rank) and the
+    paper's CPU-assisted prefill (NEXT f1) re-measured on B200:
+      load_by_rank: one 13B projection adapter (5120 -> 5120, bf16) of rank r, lora_load_adapter call ->
+        lora_adapter_ready (host polling), median of `reps`, by the default cudaMemcpyAsync path and by
+        the zero-copy gather kernel (LORA_OPT_LOAD_KERNEL), next to the measured pinned H2D peak;
+      cpu_delta: the paper's CPU LoRA for a prompt of L tokens while that adapter loads -- torch CPU
+        (x @ A) @ B in bf16 on all host cores -- vs the load latency of the same rank.  cpu_wins marks
+        the cells where computing on the host would beat waiting for the load."""
+    import torch
+    import time as _t
+    peak = h2d_d2h_peak(dev)
+    ranks = (8, 16, 32, 64, 128)
+    lengths = (1, 16, 128, 512)
+    res = {"h2d_pinned_peak_GBps": peak["h2d"], "d2h_pinned_peak_GBps": peak["d2h"],
+           "pcie_gen5_x16_nominal_GBps": 64.0, "load_by_rank": {}, "cpu_delta": {}}
+    torch.set_num_threads(len(os.sched_getaffinity(0)))
+    for r in ranks:
+        ad = gen.make_adapter(gen.BASE_SEED + 3, 77, 1, r, H, H, "bf16")
+        A = torch.from_numpy(ad.A.view(np.int16)).pin_memory()
+        B = torch.from_numpy(ad.B.view(np.int16)).pin_memory()
+        row = {"bytes": int(r * 2 * H * 2)}
+        for name, kern in (("memcpy", 0), ("gather_kernel", 1)):
+            pool = L.LoraPool(H, H, 4, "bf16", max_total_rank=256)
+            pool.set_option(L.binding.LORA_OPT_LOAD_KERNEL, kern)
+            lat = []
+            for i in range(reps + 2):
+                t1 = _t.perf_counter()
+                pool.load_adapter(i, r, A, B, ad.scale)
+                while not pool.adapter_ready(i):
+                    pass
+                lat.append((_t.perf_counter() - t1) * 1e6)
+                pool.unload_adapter(i)
+                torch.cuda.synchronize()
+            us = float(np.median(lat[2:]))
+            row[name + "_us"] = round(us, 1)
+            row[name + "_GBps"] = round(row["bytes"] / (us * 1e-6) / 1e9, 2)
+            pool.close()
+        res["load_by_rank"][str(r)] = row
+        Ac = A.view(torch.bfloat16).reshape(r, H).t().contiguous()   # stored rank-major [r][H_in]
+        Bc = B.view(torch.bfloat16).reshape(r, H)
+        load_us = min(row["memcpy_us"], row["gather_kernel_us"])
+        cells = {}
+        for n in lengths:
+            xc = torch.randn(n, H).to(torch.bfloat16)
+            (xc @ Ac) @ Bc
+            t1 = _t.perf_counter()
+            k = 5
+            for _ in range(k):
+                (xc @ Ac) @ Bc
+            cpu_us = (_t.perf_counter() - t1) / k * 1e6
+            cells[str(n)] = {"cpu_us": round(cpu_us, 1), "load_us": load_us, "cpu_wins": bool(cpu_us < load_us)}
+        res["cpu_delta"][str(r)] = cells
+    res["cpu_threads"] = torch.get_num_threads()
+    res["cpu_wins_any"] = any(c["cpu_wins"] for v in res["cpu_delta"].values() for c in v.values())
+    return res
 
 
 # ---------------------------------------------------------------- config 5: Llama-2-70B shapes, TP shards
@@ -897,7 +963,11 @@ def main():
 
     c4 = None
     if args.c4_steps > 0:
-        c4 = bench_c4(L, dev, args.c4_steps, world, rank)
+        c4 = bench_c4(L, dev, args.c4_steps, world, rank, use_dist and not SHARE_GPU)
+
+    cold = None
+    if args.cold_start and rank == 0:
+        cold = bench_cold_start(L, dev)
 
     c5 = None
     if args.c5_reps > 0:
@@ -942,6 +1012,7 @@ def main():
                 "gpu_launches": int(launches_per_step * args.steps),
                 "prefill": prefill,
                 "c4": c4,
+                "cold_start": cold,
                 "c5": c5,
                 "fused_base": fused_base,
                 "setup_s": round(t_gen, 1)}

@@ -10,8 +10,11 @@ request to the candidate server with the minimum total cost, where
     total = cost * (len(running_batch) + len(queue)).
 
 Here the models are fitted to this library's measured kernels (scripts/cost_model.py ->
-profiles/r1_cost_model.json: MBGMV time vs sum_G r, R^2 0.92; padded BGMV vs G * max r, R^2 0.98).
-Pure host logic (no CUDA); the hot path it schedules is lora_apply.
+profiles/r1_cost_model.json: MBGMV time vs sum over (adapter, 8-token chunk) of r, R^2 0.957; padded
+BGMV vs G * max r, R^2 0.98).  Pure host logic (no CUDA); the hot path it schedules is lora_apply.
+serving.route_requests applies Algorithm 1 to a decode step's requests across the GPUs of a node
+(bench.py config 4); the cluster simulation against the paper's baseline policies is evaluation,
+not product (scripts/schedule_sim.py).
 """
 from __future__ import annotations
 
@@ -44,10 +47,24 @@ class LinearModel:
         return self.alpha * feature + self.beta
 
 
-def feature_mbgmv(ranks: Sequence[int]) -> float:
-    """sum of the batch's LoRA ranks.  Our kernel reads each distinct adapter once per
-    8-token chunk; a request batch of distinct adapters is the paper's setting."""
-    return float(sum(ranks))
+CHUNK = 8   # decode tokens per (adapter group, token chunk) unit of the kernel (kTokChunkMma)
+
+
+def feature_mbgmv(ranks: Sequence[int], adapters: Optional[Sequence[int]] = None) -> float:
+    """The padding-free kernel's rank feature (P:753-757 sums the ranks of the batch's requests).
+    The model is fitted (profiles/r1_cost_model.json, "mbgmv_time_vs_sum_rank_gc", R^2 0.957) on what
+    this library's decode kernel reads: every DISTINCT adapter's rank rows once per 8-token chunk,
+    sum over adapters of r * ceil(tokens / 8).  With `adapters` (the adapter id of each request,
+    parallel to `ranks`) that is what is computed; without, every request is its own adapter (the
+    paper's setting, where the two coincide)."""
+    if adapters is None:
+        return float(sum(ranks))
+    count: Dict[int, int] = {}
+    rank_of: Dict[int, int] = {}
+    for a, r in zip(adapters, ranks):
+        count[a] = count.get(a, 0) + 1
+        rank_of[a] = r
+    return float(sum(rank_of[a] * -(-n // CHUNK) for a, n in count.items()))
 
 
 def feature_bgmv(ranks: Sequence[int]) -> float:
@@ -67,10 +84,11 @@ class PerfModel:
     base_decode_us: float = 0.0       # base-model time per decode iteration (constant)
     prefill: LinearModel = dataclasses.field(default_factory=lambda: LinearModel(0.0, 0.0))
 
-    def dec_perf(self, ranks: Sequence[int]) -> float:
+    def dec_perf(self, ranks: Sequence[int], adapters: Optional[Sequence[int]] = None) -> float:
+        """adapters: the adapter id of each request (MBGMV: distinct adapters per 8-token chunk)."""
         if not ranks:
             return 0.0
-        f = feature_mbgmv(ranks) if self.kind == "mbgmv" else feature_bgmv(ranks)
+        f = feature_mbgmv(ranks, adapters) if self.kind == "mbgmv" else feature_bgmv(ranks)
         return self.base_decode_us + self.invocations * self.decode(f)
 
     def pre_perf(self, prompts: Sequence[int]) -> float:
@@ -82,9 +100,20 @@ class PerfModel:
     def from_cost_model(path: str, kind: str = "mbgmv", **kw) -> "PerfModel":
         """The fit of scripts/cost_model.py (profiles/r1_cost_model.json), per-apply microseconds."""
         d = json.load(open(path))
-        key = "mbgmv_time_vs_sum_rank_groups" if kind == "mbgmv" else "bgmv_time_vs_G_x_maxrank"
+        key = "mbgmv_time_vs_sum_rank_gc" if kind == "mbgmv" else "bgmv_time_vs_G_x_maxrank"
         f = d[key]
         return PerfModel(LinearModel(f["alpha_us_per_unit"], f["beta_us"], f["r2"]), kind=kind, **kw)
+
+
+def measured_model(kind: str = "mbgmv", invocations: int = 128) -> PerfModel:
+    """The models fitted to this library's kernels on B200 (scripts/cost_model.py ->
+    profiles/r1_cost_model.json: MBGMV us per apply = 0.0037362 * sum_gc r + 5.4006, R^2 0.957;
+    padded BGMV = 0.0084753 * G * max r + 3.5120, R^2 0.977) and the tcgen05 prefill apply (bench
+    config 3: 88 us for 16,384 tokens, i.e. 5.37 ns per token per apply), per decode iteration of
+    `invocations` applies."""
+    dec = LinearModel(0.0037362, 5.4006, 0.957) if kind == "mbgmv" else LinearModel(0.0084753, 3.5120, 0.977)
+    pre = LinearModel(invocations * 88.0 / 16384, invocations * 5.0)
+    return PerfModel(dec, kind=kind, invocations=invocations, prefill=pre)
 
 
 @dataclasses.dataclass
@@ -114,8 +143,9 @@ def calc_cost(req: Request, server: Server, model: PerfModel, avg_resp_len: floa
     d_prefill = model.pre_perf([q.prompt_len for q in server.queue] + [req.prompt_len]) - \
         model.pre_perf([q.prompt_len for q in server.queue])
     ranks = [e.rank for e in exists]
-    dec_new = model.dec_perf(ranks + [req.rank])
-    d_decode = dec_new - model.dec_perf(ranks)
+    ads = [e.adapter for e in exists]
+    dec_new = model.dec_perf(ranks + [req.rank], ads + [req.adapter])
+    d_decode = dec_new - model.dec_perf(ranks, ads)
     cost = d_prefill / avg_resp_len + d_decode
     if dec_new > slo_us:
         cost += penalty
@@ -136,69 +166,3 @@ def rank_aware_pick(req: Request, servers: Sequence[Server], model: PerfModel, a
         if best is None or total < best_cost:
             best, best_cost = s, total
     return best
-
-
-# ---- baseline policies of the paper's scheduler evaluation
-def pick_random(req, servers, rng: np.random.Generator) -> Server:
-    c = [s for s in servers if s.can_serve(req)]
-    return c[int(rng.integers(0, len(c)))]
-
-
-def pick_most_idle(req, servers) -> Server:
-    c = [s for s in servers if s.can_serve(req)]
-    return min(c, key=lambda s: (len(s.running) + len(s.queue), s.sid))
-
-
-def pick_first_fit(req, servers, model: PerfModel, slo_us: float) -> Server:
-    c = [s for s in servers if s.can_serve(req)]
-    for s in c:
-        if model.dec_perf([e.rank for e in s.running + s.queue] + [req.rank]) <= slo_us:
-            return s
-    return c[0]
-
-
-def simulate(policy: str, model: PerfModel, n_servers: int, requests: Sequence[Request], resp_len: int,
-             arrival_gap_iters: float, slo_us: float, seed: int = 0) -> Dict[str, float]:
-    """Discrete decode-iteration simulation of a cluster: requests arrive every arrival_gap_iters
-    iterations, join the chosen server, prefill in the next iteration, then decode resp_len tokens;
-    every iteration a server's per-token latency is DecPerf(running batch).  Returns the SLO
-    attainment (fraction of decode iterations of requests whose per-token latency met the SLO) and
-    the mean per-token latency."""
-    rng = np.random.default_rng(seed)
-    servers = [Server(i) for i in range(n_servers)]
-    left: Dict[int, int] = {}
-    met = total = 0
-    lat_sum = 0.0
-    pending = list(requests)
-    t = 0.0
-    next_arrival = 0.0
-    while pending or any(s.running or s.queue for s in servers):
-        while pending and next_arrival <= t:
-            req = pending.pop(0)
-            if policy == "rank_aware":
-                s = rank_aware_pick(req, servers, model, avg_resp_len=resp_len, slo_us=slo_us)
-            elif policy == "random":
-                s = pick_random(req, servers, rng)
-            elif policy == "most_idle":
-                s = pick_most_idle(req, servers)
-            elif policy == "first_fit":
-                s = pick_first_fit(req, servers, model, slo_us)
-            else:
-                raise ValueError(policy)
-            s.queue.append(req)
-            left[req.rid] = resp_len
-            next_arrival += arrival_gap_iters
-        for s in servers:
-            s.running += s.queue     # prefill this iteration, decode from the next
-            s.queue = []
-            if not s.running:
-                continue
-            lat = model.dec_perf([r.rank for r in s.running])
-            for r in s.running:
-                total += 1
-                met += lat <= slo_us
-                lat_sum += lat
-                left[r.rid] -= 1
-            s.running = [r for r in s.running if left[r.rid] > 0]
-        t += 1.0
-    return {"slo_attainment": met / max(1, total), "mean_token_latency_us": lat_sum / max(1, total)}

@@ -10,8 +10,10 @@ used with ties broken by the lower id, and frees pages 
 library orders their physical reuse after the applies already enqueued.
 
 Request placement across GPUs: adapter home GPU = id mod N, the hottest
-adapters replicated on every GPU; each GPU serves only requests for adapters it hosts, so there is
-no data-path collective.
+adapters replicated on every GPU; a request goes to one of the GPUs hosting its adapter, chosen by
+the paper's rank-aware Algorithm 1 (scheduler.rank_aware_pick with the cost model fitted
+to this library's decode kernel) -- route_requests.  Each GPU then serves its requests alone: there
+is no data-path collective.
 """
 from __future__ import annotations
 
@@ -21,6 +23,7 @@ from typing import Dict, Iterable, List, Optional, Tuple
 import numpy as np
 
 from .binding import LoraError, LoraPool
+from . import scheduler as S
 
 
 class HostRepository:
@@ -50,6 +53,38 @@ def home_gpu(aid: int, world: int, replicated: Iterable[int] = ()) -> Optional[i
 def serves(aid: int, rank: int, world: int, replicated: Iterable[int] = ()) -> bool:
     h = home_gpu(aid, world, replicated)
     return h is None or h == rank
+
+
+def route_requests(decode_ids, prefill_ids, prefill_len: int, world: int, replicated: Iterable[int],
+                   model: "S.PerfModel", rank_of, avg_resp_len: float = 128.0, slo_us: float = float("inf"),
+                   penalty: float = 1e9) -> Tuple[List[int], List[int]]:
+    """Algorithm 1 over one step's requests, in arrival order (decode requests, then the
+    prompts): each goes to the candidate GPU -- those hosting its adapter (home_gpu) -- with the
+    minimum total cost = CalcCost x (running + queued requests), CalcCost from the fitted DecPerf /
+    PrePerf models (scheduler.calc_cost); ties go to the lower GPU.  Deterministic: every rank runs
+    it on the same global request list and keeps its own share.  Returns the GPU of every decode
+    request and of every prompt."""
+    servers = [S.Server(g) for g in range(world)]
+    rep = set(int(a) for a in replicated)
+
+    def cands(aid):
+        h = home_gpu(aid, world, rep)
+        return servers if h is None else [servers[h]]
+
+    dec_to, pre_to = [], []
+    for i, a in enumerate(decode_ids):
+        a = int(a)
+        req = S.Request(i, a, int(rank_of(a)), prompt_len=0)
+        s = S.rank_aware_pick(req, cands(a), model, avg_resp_len=avg_resp_len, slo_us=slo_us, penalty=penalty)
+        s.running.append(req)
+        dec_to.append(s.sid)
+    for i, a in enumerate(prefill_ids):
+        a = int(a)
+        req = S.Request(len(dec_to) + i, a, int(rank_of(a)), prompt_len=int(prefill_len))
+        s = S.rank_aware_pick(req, cands(a), model, avg_resp_len=avg_resp_len, slo_us=slo_us, penalty=penalty)
+        s.queue.append(req)
+        pre_to.append(s.sid)
+    return dec_to, pre_to
 
 
 class AdapterCache:

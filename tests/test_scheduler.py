@@ -1,6 +1,6 @@
 """CPU tests of the rank-aware scheduler (paper_2401_11240_b200/scheduler.py; §4.3,
-Algorithm 1): linear performance models, CalcCost, the selection rule, and a seeded
-cluster simulation against the paper's baseline policies."""
+Algorithm 1): linear performance models, CalcCost, the selection rule and the routing of a
+decode step's requests across GPUs (serving.route_requests)."""
 import os
 
 import numpy as np
@@ -22,6 +22,10 @@ def test_features_follow_the_paper():
     assert S.feature_bgmv([8, 64, 16]) == 3 * 64
     assert S.feature_mbgmv([8, 64, 16]) == 88
     assert S.feature_bgmv([]) == 0.0
+    # with adapter ids: what the kernel reads -- each distinct adapter once per 8-token chunk
+    # (the feature the B200 model is fitted on): adapter 5 (r 64) x 9 tokens -> 2 chunks, adapter 6 once
+    assert S.feature_mbgmv([64] * 9 + [16], [5] * 9 + [6]) == 64 * 2 + 16
+    assert S.feature_mbgmv([8, 8], [1, 2]) == 16
 
 
 def _model(kind="mbgmv", alpha=0.01, beta=5.0, inv=10, pre=(0.02, 1.0)):
@@ -76,15 +80,26 @@ def test_candidates_respect_adapter_placement():
         S.rank_aware_pick(S.Request(9, 4, 16), [a, b], m)
 
 
-@pytest.mark.parametrize("kind,slo", [("mbgmv", 1000.0), ("bgmv", 1400.0)])
-def test_simulation_rank_aware_beats_random_and_most_idle(kind, slo):
-    """Seeded cluster simulation (8 servers, 600 requests, ranks 8..128) with the models fitted to
-    this library's kernels (profiles/r1_cost_model.json): rank-aware SLO attainment exceeds the
-    Random and MostIdle baselines (the paper: 99% SLO)."""
-    m = S.PerfModel.from_cost_model(os.path.join(ROOT, "profiles", "r1_cost_model.json"), kind=kind)
-    rng = np.random.default_rng(1)
-    reqs = [S.Request(i, int(rng.integers(0, 200)), int(rng.choice([8, 16, 32, 64, 128], p=[.3, .25, .2, .15, .1])))
-            for i in range(600)]
-    res = {p: S.simulate(p, m, 8, reqs, resp_len=64, arrival_gap_iters=0.6, slo_us=slo, seed=3)["slo_attainment"]
-           for p in ("rank_aware", "random", "most_idle")}
-    assert res["rank_aware"] > res["random"] + 0.1 and res["rank_aware"] > res["most_idle"] + 0.1, res
+def test_route_requests_follows_the_cost():
+    """Every request lands on a GPU hosting its adapter; hot (replicated) adapters go where Algorithm 1's
+    total cost is lowest at their arrival -- recomputed here step by step -- and the result is a
+    deterministic function of the request list (each rank can run it alone)."""
+    from paper_2401_11240_b200.serving import home_gpu, route_requests
+    from workloads import gen
+    m = S.measured_model("mbgmv", invocations=1)
+    world, hot = 4, [int(v) for v in gen.zipf_perm(gen.BASE_SEED + 3, 1000)[:16]]
+    d = gen.config_c4_draw(7, n_decode=64 * world, n_prefill=world)
+    dec, pre = [int(a) for a in d["decode_ids"]], [int(a) for a in d["prefill_id"]]
+    dec_to, pre_to = route_requests(dec, pre, 512, world, hot, m, gen.c4_rank)
+    assert (dec_to, pre_to) == route_requests(dec, pre, 512, world, hot, m, gen.c4_rank)
+    servers = [S.Server(g) for g in range(world)]
+    for i, (a, to) in enumerate(list(zip(dec, dec_to)) + list(zip(pre, pre_to))):
+        h = home_gpu(a, world, hot)
+        assert h is None or to == h
+        req = S.Request(i, a, gen.c4_rank(a), prompt_len=0 if i < len(dec) else 512)
+        if h is None:   # replicated: the chosen GPU minimises CalcCost x (running + queued)
+            tot = [S.calc_cost(req, s, m, 128.0, float("inf"), 1e9) * (len(s.running) + len(s.queue)) for s in servers]
+            assert tot[to] == min(tot) and to == tot.index(min(tot))
+        (servers[to].running if i < len(dec) else servers[to].queue).append(req)
+    # the hot adapters' requests spread over all GPUs (the cost grows with a GPU's load)
+    assert len(set(t for a, t in zip(dec, dec_to) if a in hot)) == world

@@ -80,18 +80,28 @@ def test_tp_decomposition_gloo_world2():
 
 
 def _dp_worker(rank, world, port, out):
-    """Request-partitioned data parallelism: adapter home = id mod world, the top adapters
-    replicated; every request is served by exactly one rank; no data-path collective."""
+    """Request-partitioned data parallelism: every rank routes the same global step (64 decode requests
+    + 1 prompt per GPU) with Algorithm 1 (serving.route_requests) and keeps its share; no data-path
+    collective -- the gathers below only check the partition."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from workloads import gen
-    reqs = gen.config_c4_draw(step=3, n_decode=64)["decode_ids"]
-    mine = [i for i, a in enumerate(reqs) if int(a) % world == rank]
-    t = torch.tensor([len(mine)], dtype=torch.int64)
-    dist.all_reduce(t)
+    from paper_2401_11240_b200 import scheduler as S
+    from paper_2401_11240_b200.serving import home_gpu, route_requests
+    hot = [int(v) for v in gen.zipf_perm(gen.BASE_SEED + 3, 1000)[:16]]
+    d = gen.config_c4_draw(step=3, n_decode=64 * world, n_prefill=world)
+    dec, pre = [int(a) for a in d["decode_ids"]], [int(a) for a in d["prefill_id"]]
+    dec_to, pre_to = route_requests(dec, pre, 512, world, hot, S.measured_model("mbgmv", 1), gen.c4_rank)
+    mine = [i for i, g in enumerate(dec_to + pre_to) if g == rank]
+    ok = all(home_gpu(a, world, hot) in (None, rank) for i, a in enumerate(dec + pre) if i in set(mine))
+    t = torch.zeros(len(dec) + len(pre), dtype=torch.int64)
+    t[mine] = 1
+    dist.all_reduce(t)                       # how many ranks served each request
+    flag = torch.tensor([int(ok)], dtype=torch.int64)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if rank == 0:
-        out.put(int(t.item()))
+        out.put((t.tolist(), int(flag.item())))
     dist.destroy_process_group()
 
 
@@ -102,8 +112,9 @@ def test_request_partition_gloo_world2():
     procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    total = q.get(timeout=120)
+    served, hosted_ok = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert total == 64          # every request served exactly once
+    assert served == [1] * (64 * 2 + 2)     # every request served exactly once
+    assert hosted_ok == 1                    # and only by a GPU hosting its adapter

@@ -234,14 +234,14 @@ def c4_rank(aid: int) -> int:
 
 
 def config_c4_draw(step: int, n_decode: int = 64, prefill_len: int = 512, n_adapters: int = 1000,
-                   s: float = 1.0, world: int = 1, rank: int = 0) -> Dict[str, np.ndarray]:
+                   s: float = 1.0, world: int = 1, rank: int = 0, n_prefill: int = 1) -> Dict[str, np.ndarray]:
     """One iteration of config 4's trace: Zipf(s) adapter ids for the decode tokens and
-    one prefill segment.  Returns ids only; adapters are generated on demand."""
+    n_prefill prefill segments.  Returns ids only; adapters are generated on demand."""
     seed = BASE_SEED + 3
     rng = _rng(seed, _TAG_BATCH, step, world, rank)
     perm = zipf_perm(seed, n_adapters)
     dec = zipf_ids(rng, n_adapters, n_decode, s, perm)
-    pre = zipf_ids(rng, n_adapters, 1, s, perm)
+    pre = zipf_ids(rng, n_adapters, n_prefill, s, perm)
     return {"decode_ids": dec, "prefill_id": pre, "prefill_len": np.int32(prefill_len)}
 
 
