@@ -41,6 +41,7 @@ def test_bench_two_ranks_one_line():
     d = _run(["--steps", "10", "--warmup", "3", "--layers", "2", "--e2e-steps", "2", "--prefill-layers", "0",
               "--c4-steps", "2", "--c5-reps", "0", "--fused-base-reps", "0"])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["cpu_baseline"] is None
-    assert d["c4"]["value"] > 0 and "rank 0/2" in d["c4"]["workload"]
+    assert d["c4"]["value"] > 0 and "2 GPU(s)" in d["c4"]["workload"]
+    assert d["c4"]["routing"]["policy"].startswith("Algorithm 1")
     ref = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"])
     assert ref["impl"] == "reference" and ref["e2e"]["h2d_bytes_per_step"] == 0
