@@ -36,7 +36,7 @@ def _sources():
 
 def _digest():
     h = hashlib.sha256()
-    files = _sources() + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h")]
+    files = _sources() + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".h", ".cuh"))]
     files.append(os.path.join(ROOT, "include", "lora_delta.h"))
     files.append(os.path.abspath(__file__))
     h.update(" ".join(DEFS).encode())

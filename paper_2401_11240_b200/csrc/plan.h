@@ -106,6 +106,7 @@ struct DecodeLaunch {
         int H_in, H_out;
     } more[3];
     int n_jobs = 1;
+    int ring = 0;                // bf16 full applies: 0 = PDL pair, else the persistent ring pair (ring_kernel.cu)
 };
 struct PrefillLaunch {
     const void* x;
@@ -128,6 +129,9 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& merged, std::stri
 typedef struct CUstream_st* lora_cuda_stream;
 namespace lora {
 int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
+// the persistent ring pair (ring_kernel.cu); returns -1 when the batch does not fit its work-list
+// encoding or the kernel parameters (the caller then takes the PDL pair), else a cudaError_t
+int launch_decode_ring(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches, int ring_cfg);
 // zero-copy cold-start copy of one adapter (load_kernel.cu): sA/sB device-visible pinned host rows
 int launch_load(char* dA, char* dB, const void* sA, const void* sB, int64_t ra, int64_t rb, int rank,
                 const int32_t* pages, int num_sms, lora_cuda_stream st);
