@@ -73,8 +73,8 @@ def parse():
                          "o (input = attention output) is always its own lora_apply")
     ap.add_argument("--min-window-ms", type=float, default=200.0,
                     help="repeat the K-step timed window until this much device time is covered (median reported)")
-    ap.add_argument("--decode-ring", type=lambda v: int(v, 0), default=0,
-                    help="LORA_OPT_DECODE_RING for the c2 pools: 0 PDL pair, 1 persistent ring pair, 0x1se stages")
+    ap.add_argument("--decode-chunk-kb", type=int, default=None,
+                    help="LORA_OPT_DECODE_CHUNK_KB for the c2 pools (default: the library's)")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
     ap.add_argument("--cold-start", type=int, choices=[0, 1], default=1,
                     help="cold-start latency by rank + the paper's CPU-assist comparison (rank 0)")
@@ -799,7 +799,8 @@ def main():
             for p in range(len(PROJS)):
                 ads = futs[(l, p)].result()
                 pool = L.LoraPool(H, H, 32, "bf16", max_total_rank=sum(a.rank for a in ads))
-                pool.set_option(L.binding.LORA_OPT_DECODE_RING, args.decode_ring)
+                if args.decode_chunk_kb is not None:
+                    pool.set_option(L.binding.LORA_OPT_DECODE_CHUNK_KB, args.decode_chunk_kb)
                 for a in ads:
                     A = torch.from_numpy(a.A.view(np.int16)).pin_memory()
                     B = torch.from_numpy(a.B.view(np.int16)).pin_memory()
@@ -901,10 +902,8 @@ def main():
     achieved = bytes_apply / (kernel_us * 1e-6) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": load_ncu_traffic(),
-                "kernel": ("decode: lora_shrink_ring_kernel + lora_expand_ring_kernel (persistent ring pair per apply; "
-                           if args.decode_ring else
-                           "decode: lora_shrink_mma_kernel + lora_expand_mma_kernel (PDL-chained pair per apply; ")
-                          + "q/k/v mode %s)" % mode,
+                "kernel": "decode: lora_shrink_mma_kernel + lora_expand_mma_kernel (PDL-chained pair per apply; "
+                          "q/k/v mode %s)" % mode,
                 "algorithmic_bytes_per_launch": bytes_apply,
                 "avg_launch_us": round(kernel_us, 3), "peak_source": peak_src,
                 "note": "per projection apply: graph step time / 128 applies (gaps included); traffic = ncu dram "

@@ -95,15 +95,12 @@ typedef enum {
                                       loaded this way the steady-state decode apply was 7 % slower
                                       (unexplained). */
 
-#define LORA_OPT_DECODE_RING 7     /* bf16 decode work (full applies: lora_apply, lora_apply_multi) on
-                                      0: the PDL-chained kernel pair, one CTA per 32 KB work unit;
-                                      1: the persistent ring pair (one shrink + one expand CTA per SM
-                                      streaming their tile lists through SMEM rings; DESIGN.md §6 N1r).
-                                      0x100 | s << 4 | e (1 <= s, e <= 6): ring pair with s shrink and e
-                                      expand ring stages (experiments).  Bitwise-identical results.
-                                      The TP split calls and the padded comparison mode always take
-                                      the PDL pair; so do batches whose work lists exceed the kernel
-                                      parameters. */
+#define LORA_OPT_DECODE_CHUNK_KB 7 /* decode work of a full apply (lora_apply, lora_apply_multi; bf16) whose
+                                      adapter rows exceed this many KiB runs as a pipeline of grids over
+                                      chunks of its (adapter, token-chunk) groups: shrink(0) | expand(0) +
+                                      shrink(1) | ... | expand(n-1), so each grid's rows fit on chip next
+                                      to the previous grid's (DESIGN.md §6 N1).  0 = one shrink grid and
+                                      one expand grid.  Bitwise-identical results either way. */
 
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.

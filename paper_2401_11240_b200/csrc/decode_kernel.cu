@@ -25,8 +25,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <vector>
 
 #include "decode_common.cuh"
 #include "kernel_config.h"
@@ -48,6 +50,8 @@ struct DecodeArgs {
                                  // each gc (tp_reduce_tail), read by the expand when v_compact is set
     int* gc_cnt;                 // TP shrink: per-gc arrival counters (zero between applies)
     int v_compact;
+    int g_s_lo, g_e_lo, g_ne;    // this grid's units (pipelined schedule): shrink units from g_s_lo, expand
+                                 // units from g_e_lo; a mixed grid's first g_ne CTAs expand, the rest shrink
     int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
     int job_expand_base[kMaxJobs];
 };
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     char* xbuf = abuf + kShrinkRows * kSliceBytes;
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u = blockIdx.x;
+    const int u = a.g_s_lo + blockIdx.x;
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
 
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     char* ybuf = bbuf + kExpandBytes;                             // [kTokChunk][c]
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ue = blockIdx.x;
+    const int ue = a.g_e_lo + blockIdx.x;
     const int u = ue + a.n_shrink;
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by a preceding kernel
@@ -646,9 +650,10 @@ __global__ void __launch_bounds__(kConsumerThreads)
     lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
-    if (a.trace && threadIdx.x == 0) a.trace[(size_t)blockIdx.x * 8 + 1] = gtime();
+    const int u = a.g_s_lo + blockIdx.x;
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)u * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
-    shrink_mma_body(a, M, blockIdx.x, smem);
+    shrink_mma_body(a, M, u, smem);
 }
 
 // ---- expand (bf16): one CTA = (group-chunk gc, column slice [n0, n0+nc)).  Swap-AB:
@@ -873,9 +878,32 @@ __global__ void __launch_bounds__(kConsumerThreads, MINB)
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
-    if (a.trace && threadIdx.x == 0) a.trace[(size_t)(blockIdx.x + a.n_shrink) * 8 + 1] = gtime();
+    const int ue = a.g_e_lo + blockIdx.x;
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)(ue + a.n_shrink) * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();
-    expand_mma_body(a, M, blockIdx.x, smem);
+    expand_mma_body(a, M, ue, smem);
+}
+
+// ---- pipelined schedule (DESIGN.md §6 N1, "chunked applies"): a grid that expands the group-chunks
+// of chunk k-1 (their v complete: the previous grid shrank them) while it shrinks those of chunk k.
+// The first g_ne CTAs run expand units, the rest shrink units; both bodies are the ones above.
+template <int W, int MINB>
+__global__ void __launch_bounds__(kConsumerThreads, MINB)
+    lora_mixed_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
+    extern __shared__ __align__(128) char smem[];
+    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
+    const int b = blockIdx.x;
+    if (b < a.g_ne) {
+        const int ue = a.g_e_lo + b;
+        if (a.trace && threadIdx.x == 0) a.trace[(size_t)(ue + a.n_shrink) * 8 + 1] = gtime();
+        if (W == 1) pdl_wait_cta();
+        expand_mma_body(a, M, ue, smem);
+    } else {
+        const int u = a.g_s_lo + (b - a.g_ne);
+        if (a.trace && threadIdx.x == 0) a.trace[(size_t)u * 8 + 1] = gtime();
+        if (W == 1) pdl_wait_cta();
+        shrink_mma_body(a, M, u, smem);
+    }
 }
 
 // copies a metadata blob too large for one kernel's parameters into device memory,
@@ -935,9 +963,10 @@ static bool configure_once(std::atomic<uint64_t>& mask, cudaError_t (*fn)()) {
 }
 
 template <typename T, int W>
-static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t st, int* launches, int phases,
-                               int num_sms) {
+static cudaError_t launch_pair(const DecodeArgs& a0, const Plan& pl, cudaStream_t st, int* launches, int phases,
+                               int num_sms, const std::vector<int>& cuts) {
     using K = DecodeKernels<T, W>;
+    constexpr bool kBf16 = sizeof(T) == 2;
     static std::atomic<uint64_t> configured{0};
     if (!configure_once(configured, [] {
             // the opt-in maximum (the launch passes the real size; it decides occupancy)
@@ -946,6 +975,14 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
             if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(K::expand_big, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+            if constexpr (kBf16) {
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(lora_mixed_mma_kernel<W, LORA_EXPAND_MINB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(lora_mixed_mma_kernel<W, LORA_EXPAND_BIG_MINB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
+            }
             return e;
         }))
         return cudaErrorInvalidValue;
@@ -955,21 +992,79 @@ static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t
         for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
     }
     cudaError_t e = cudaSuccess;
-    if (phases & 1) {
-        // bf16: a grid of more than 4 shrink CTAs per SM (e.g. q/k/v in one multi launch) fits better
-        // at 5 per SM (DESIGN.md §6 N1 occupancy)
-        const int ss = pl.n_shrink > 4 * num_sms ? K::shrink_smem_big : K::shrink_smem;
-        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, ss, st, a, blob);
-        if (e != cudaSuccess) return e;
-        *launches += 1;
+    // shrink grid of ns units from s_lo / expand grid of ne units from e_lo / mixed grid of both
+    auto grid = [&](int s_lo, int ns, int e_lo, int ne) -> cudaError_t {
+        DecodeArgs a = a0;
+        a.g_s_lo = s_lo;
+        a.g_e_lo = e_lo;
+        a.g_ne = ne;
+        cudaError_t r = cudaSuccess;
+        if (ne == 0) {
+            // bf16: a grid of more than 4 shrink CTAs per SM (e.g. q/k/v in one multi launch) fits better
+            // at 5 per SM (DESIGN.md §6 N1 occupancy)
+            const int ss = ns > 4 * num_sms ? K::shrink_smem_big : K::shrink_smem;
+            r = launch_pdl(K::shrink, ns, kConsumerThreads, ss, st, a, blob);
+        } else if (ns == 0) {
+            const bool big = ne > 3 * num_sms;
+            r = launch_pdl(big ? K::expand_big : K::expand, ne, kConsumerThreads, K::expand_launch_smem(a), st, a, blob);
+        } else if constexpr (kBf16) {
+            const bool big = ns + ne > 3 * num_sms;
+            const int sm = std::max(K::expand_launch_smem(a), (int)K::shrink_smem_big);
+            r = launch_pdl(big ? lora_mixed_mma_kernel<W, LORA_EXPAND_BIG_MINB> : lora_mixed_mma_kernel<W, LORA_EXPAND_MINB>,
+                           ns + ne, kConsumerThreads, sm, st, a, blob);
+        } else {
+            r = cudaErrorInvalidValue;
+        }
+        if (r == cudaSuccess) *launches += 1;
+        return r;
+    };
+    const int nk = (int)cuts.size() - 1;
+    if (nk <= 1 || phases != 3) {
+        if (phases & 1) {
+            e = grid(0, pl.n_shrink, 0, 0);
+            if (e != cudaSuccess) return e;
+        }
+        if (phases & 2) e = grid(0, 0, 0, pl.n_expand);
+        return e;
     }
-    if (phases & 2) {
-        const bool big = pl.n_expand > 3 * num_sms;
-        e = launch_pdl(big ? K::expand_big : K::expand, pl.n_expand, kConsumerThreads, K::expand_launch_smem(a), st, a,
-                       blob);
-        *launches += 1;
+    // pipelined: S(0) | E(0) + S(1) | ... | E(nk-1), chunk k = group-chunks [cuts[k], cuts[k+1])
+    const int32_t* gcr = pl.blob.data() + kHdrWords;
+    auto sbase = [&](int gc) { return gc >= pl.n_gc ? pl.n_shrink : gcr[gc * kGcFields + GC_SHRINK_BASE]; };
+    auto ebase = [&](int gc) { return gc >= pl.n_gc ? pl.n_expand : gcr[gc * kGcFields + GC_EXPAND_BASE]; };
+    for (int k = 0; k <= nk; ++k) {
+        const int s_lo = k < nk ? sbase(cuts[k]) : 0, ns = k < nk ? sbase(cuts[k + 1]) - s_lo : 0;
+        const int e_lo = k > 0 ? ebase(cuts[k - 1]) : 0, ne = k > 0 ? ebase(cuts[k]) - e_lo : 0;
+        if (ns + ne == 0) continue;
+        e = grid(s_lo, ns, e_lo, ne);
+        if (e != cudaSuccess) return e;
     }
     return e;
+}
+
+// Chunk boundaries (group-chunk indices) of the pipelined schedule: chunks of about chunk_bytes of
+// adapter rows each (A + B), balanced; {0, n_gc} when the apply is one chunk.
+static void chunk_cuts(const Plan& pl, const DecodeArgs& a, int64_t chunk_bytes, int esz, std::vector<int>& cuts) {
+    cuts.assign(1, 0);
+    const int32_t* gcr = pl.blob.data() + kHdrWords;
+    int64_t total = 0;
+    for (int gc = 0; gc < pl.n_gc; ++gc) {
+        const DecodeJob& J = a.jobs[gcr[gc * kGcFields + GC_JOB]];
+        total += (int64_t)gcr[gc * kGcFields + GC_RANK] * (J.H_in + J.H_out) * esz;
+    }
+    const int64_t n = chunk_bytes > 0 ? (total + chunk_bytes - 1) / chunk_bytes : 1;
+    if (n > 1) {
+        int64_t acc = 0;
+        int k = 1;
+        for (int gc = 0; gc < pl.n_gc && k < n; ++gc) {
+            const DecodeJob& J = a.jobs[gcr[gc * kGcFields + GC_JOB]];
+            acc += (int64_t)gcr[gc * kGcFields + GC_RANK] * (J.H_in + J.H_out) * esz;
+            if (acc * n >= total * k && gc + 1 < pl.n_gc) {
+                cuts.push_back(gc + 1);
+                ++k;
+            }
+        }
+    }
+    cuts.push_back(pl.n_gc);
 }
 
 template <typename T>
@@ -1021,11 +1116,13 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         a.e_pgoff = a.e_dtoff + maxtok * (maxc + 4) * 4;
         a.e_smem = a.e_pgoff + maxr * 4;
     }
+    static thread_local std::vector<int> cuts;
+    chunk_cuts(pl, a, sizeof(T) == 2 && L.phases == 3 && !L.vred ? L.chunk_bytes : 0, (int)sizeof(T), cuts);
     const int n = (int)pl.blob.size();
-    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases, L.num_sms);
-    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases, L.num_sms);
-    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches, L.phases, L.num_sms);
-    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches, L.phases, L.num_sms);
+    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases, L.num_sms, cuts);
+    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases, L.num_sms, cuts);
+    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches, L.phases, L.num_sms, cuts);
+    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches, L.phases, L.num_sms, cuts);
     for (int off = 0; off < n && (L.phases & 1); off += kUploadWords) {   // expand-only reuses the shrink's upload
         const int m = n - off < kUploadWords ? n - off : kUploadWords;
         MetaBlob<kUploadWords> b;
@@ -1034,14 +1131,10 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         *launches += 1;
         if (e != cudaSuccess) return e;
     }
-    return launch_pair<T, 1>(a, pl, st, launches, L.phases, L.num_sms);
+    return launch_pair<T, 1>(a, pl, st, launches, L.phases, L.num_sms, cuts);
 }
 
 int launch_decode(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {
-    if (L.esz == 2 && L.ring && L.phases == 3 && !L.vred) {
-        const int rc = launch_decode_ring(pl, L, st, launches, L.ring);
-        if (rc != -1) return rc;
-    }
     if (L.esz == 2) return (int)launch_typed<__nv_bfloat16>(pl, L, st, launches);
     return (int)launch_typed<float>(pl, L, st, launches);
 }

@@ -106,7 +106,7 @@ struct DecodeLaunch {
         int H_in, H_out;
     } more[3];
     int n_jobs = 1;
-    int ring = 0;                // bf16 full applies: 0 = PDL pair, else the persistent ring pair (ring_kernel.cu)
+    int64_t chunk_bytes = 0;     // bf16 full applies: pipelined schedule in chunks of ~this many adapter bytes (0: off)
 };
 struct PrefillLaunch {
     const void* x;
@@ -129,9 +129,6 @@ lora_status merge_plans(const Plan* const* plans, int n, Plan& merged, std::stri
 typedef struct CUstream_st* lora_cuda_stream;
 namespace lora {
 int launch_decode(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches);
-// the persistent ring pair (ring_kernel.cu); returns -1 when the batch does not fit its work-list
-// encoding or the kernel parameters (the caller then takes the PDL pair), else a cudaError_t
-int launch_decode_ring(const Plan& pl, const DecodeLaunch& L, lora_cuda_stream st, int* launches, int ring_cfg);
 // zero-copy cold-start copy of one adapter (load_kernel.cu): sA/sB device-visible pinned host rows
 int launch_load(char* dA, char* dB, const void* sA, const void* sB, int64_t ra, int64_t rb, int rank,
                 const int32_t* pages, int num_sms, lora_cuda_stream st);
@@ -154,6 +151,7 @@ struct FusedBaseLaunch {
 int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_tiles, lora_cuda_stream st);
 bool prefill_supported(int H_in, int H_out, int esz);
 int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);
+constexpr int64_t kDefaultChunkBytes = 0;   // LORA_OPT_DECODE_CHUNK_KB default (DESIGN.md §6 N1)
 constexpr int kPfMaxRank = 128;        // tensor-core prefill path handles ranks up to this
 constexpr int kPfMaxBlobWords = 7680;
 

@@ -1,11 +1,12 @@
-"""GPU parity of the persistent ring decode pair (LORA_OPT_DECODE_RING, csrc/ring_kernel.cu).
+"""GPU parity of the pipelined decode schedule (LORA_OPT_DECODE_CHUNK_KB, decode_kernel.cu
+launch_pair): shrink(0) | expand(0) + shrink(1) | ... | expand(n-1) over chunks of group-chunks.
 
-The ring pair does the PDL pair's arithmetic in the same order, so every test checks it BITWISE
-against the PDL pair on the same pool and inputs, and within BASELINE.json's tolerance against the
-fp64 oracle (SURVEY.md §8(c) GPU parity matrix): c2, c2-Zipf, c5 70B shapes (incl. H_out = 1024 and
-H_in = 28672), ragged H (partial k-slices / column slices), ranks 1..256 with multi-token adapters
-(token chunks of 8), id < 0 rows, the fused q/k/v call, CUDA-graph replay, several ring depths, and a
-batch too large for the ring's kernel parameters (which takes the PDL pair)."""
+Same kernels bodies, same arithmetic order, so every test checks the chunked schedule BITWISE
+against the one-shrink-grid / one-expand-grid schedule (chunk 0) on the same pool and inputs, and
+within BASELINE.json's tolerance against the fp64 oracle (SURVEY.md §8(c) GPU parity matrix): c2,
+c2-Zipf, c5 70B shapes (incl. H_out = 1024 and H_in = 28672), ragged H, ranks 1..256 with
+multi-token adapters (token chunks of 8), id < 0 rows, the fused q/k/v call (chunks across pools),
+CUDA-graph replay of a dependent chain, and a batch whose metadata takes the device-upload path."""
 import numpy as np
 import pytest
 
@@ -26,10 +27,10 @@ def L():
     return lib
 
 
-def _apply(L, pool, b, ring, y_in=None, seg_indptr=None, adapter_ids=None):
+def _apply(L, pool, b, chunk, y_in=None, seg_indptr=None, adapter_ids=None):
     import torch
     from paper_2401_11240_b200 import binding as B
-    pool.set_option(B.LORA_OPT_DECODE_RING, ring)
+    pool.set_option(B.LORA_OPT_DECODE_CHUNK_KB, ck)
     x = to_torch(b.x, "cuda")
     y = to_torch(b.y_in if y_in is None else y_in, "cuda")
     pool.apply(x, y, b.seg_indptr if seg_indptr is None else seg_indptr,
@@ -38,44 +39,44 @@ def _apply(L, pool, b, ring, y_in=None, seg_indptr=None, adapter_ids=None):
     return y
 
 
-def _check(L, b, rings=(1,), oracle=True):
+def _check(L, b, chunks=(256,), oracle=True):
     pool = make_pool(b, L)
-    y_pair = _apply(L, pool, b, 0)
-    for ring in rings:
-        y_ring = _apply(L, pool, b, ring)
-        assert np.array_equal(from_torch(y_ring, "bf16"), from_torch(y_pair, "bf16")), hex(ring)
+    y_one = _apply(L, pool, b, 0)
+    for ck in chunks:
+        y_chunk = _apply(L, pool, b, ck)
+        assert np.array_equal(from_torch(y_chunk, "bf16"), from_torch(y_one, "bf16")), ck
     pool.close()
     if oracle:
         ref = O.delta_for_batch(b, n_threads=8)
-        assert rel_l2(from_torch(y_pair, "bf16"), ref, "bf16") <= TOL["bf16"]
+        assert rel_l2(from_torch(y_one, "bf16"), ref, "bf16") <= TOL["bf16"]
 
 
 @pytest.mark.parametrize("y_zero", [True, False], ids=["runA_delta", "runB_accumulate"])
-def test_ring_c2(L, y_zero):
-    _check(L, gen.config_c2(y_zero=y_zero), rings=(1, 0x111, 0x122, 0x163, 0x136))
+def test_chunked_c2(L, y_zero):
+    _check(L, gen.config_c2(y_zero=y_zero), chunks=(64, 1024, 4096, 8192, 1 << 20))
 
 
-def test_ring_c2_zipf(L):
+def test_chunked_c2_zipf(L):
     _check(L, gen.config_c2(zipf=True, y_zero=False))
 
 
 @pytest.mark.parametrize("proj", ["k", "q", "gate", "down"])
-def test_ring_c5_shapes(L, proj):
+def test_chunked_c5_shapes(L, proj):
     _check(L, gen.config_c5(proj, y_zero=False), oracle=proj in ("k", "down"))
 
 
 @pytest.mark.parametrize("H_in,H_out", [(1000, 1000), (2056, 3080), (64, 4104), (5120, 5120)])
-def test_ring_ragged_hidden(L, H_in, H_out):
+def test_chunked_ragged_hidden(L, H_in, H_out):
     rng = np.random.default_rng(H_in * 7 + H_out)
     lengths = [int(v) for v in rng.integers(1, 12, size=20)]
     ranks = {a: int(v) for a, v in enumerate(rng.choice([1, 3, 8, 17, 24, 40, 64, 100, 128], size=10))}
     ranks = {a: min(r, H_in, H_out) for a, r in ranks.items()}
     ids = [int(v) for v in rng.integers(-1, 10, size=20)]
     b = gen.build_batch("rr", 4242 + H_in, "bf16", H_in, H_out, lengths, ids, ranks, y_zero=False)
-    _check(L, b, rings=(1, 0x111))
+    _check(L, b, chunks=(16, 512))
 
 
-def test_ring_ranks_to_256_multi_token(L):
+def test_chunked_ranks_to_256_multi_token(L):
     # decode segments up to 63 tokens (L_tc = 64): adapters with several 8-token chunks, ranks to 256
     rng = np.random.default_rng(5)
     lengths = [int(v) for v in rng.integers(1, 40, size=12)]
@@ -85,7 +86,7 @@ def test_ring_ranks_to_256_multi_token(L):
     _check(L, b)
 
 
-def test_ring_random_sweep(L):
+def test_chunked_random_sweep(L):
     rng = np.random.default_rng(99)
     for trial in range(40):
         H_in = int(rng.integers(1, 40)) * 8 * int(rng.choice([1, 16]))
@@ -94,10 +95,10 @@ def test_ring_random_sweep(L):
                              max_len=int(rng.choice([1, 4, 40])), n_adapters=8, y_zero=bool(trial % 2))
         if b.T == 0:
             continue
-        _check(L, b, rings=(1,), oracle=trial % 4 == 0)
+        _check(L, b, chunks=(int(rng.choice([4, 64, 1024])),), oracle=trial % 4 == 0)
 
 
-def test_ring_multi_qkv_equals_pair(L):
+def test_chunked_multi_qkv_equals_pair(L):
     import torch
     from paper_2401_11240_b200 import binding as B
     shapes = [(4096, 4096), (4096, 1024), (4096, 1024)]
@@ -112,32 +113,32 @@ def test_ring_multi_qkv_equals_pair(L):
     pools = [make_pool(b, L) for b in batches]
     xs = [to_torch(b.x, "cuda") for b in batches]
     outs = {}
-    for ring in (0, 1):
+    for ck in (0, 8192, 3000):
         for p in pools:
-            p.set_option(B.LORA_OPT_DECODE_RING, ring)
+            p.set_option(B.LORA_OPT_DECODE_CHUNK_KB, ck)
         ys = [to_torch(b.y_in, "cuda") for b in batches]
         L.apply_multi(pools, xs, ys, batches[0].seg_indptr, batches[0].adapter_ids)
         torch.cuda.synchronize()
-        outs[ring] = ys
-    for b, y0, y1 in zip(batches, outs[0], outs[1]):
-        assert torch.equal(y0, y1)
+        outs[ck] = ys
+    for b, y0, y1, y2 in zip(batches, outs[0], outs[8192], outs[3000]):
+        assert torch.equal(y0, y1) and torch.equal(y0, y2)
         ref = O.delta_for_batch(b, n_threads=8)
         assert rel_l2(from_torch(y1, "bf16"), ref, "bf16") <= TOL["bf16"]
     for p in pools:
         p.close()
 
 
-def test_ring_graph_replay_and_chain(L):
-    """A CUDA graph of 6 dependent ring applies (each apply's x = the previous apply's y) replays
-    bitwise equal to the same chain issued eagerly on the PDL pair."""
+def test_chunked_graph_replay_and_chain(L):
+    """A CUDA graph of 6 dependent chunked applies (each apply's x = the previous apply's y) replays
+    bitwise equal to the same chain issued eagerly unchunked."""
     import torch
     from paper_2401_11240_b200 import binding as B
     b = gen.config_c2(y_zero=False)
     pool = make_pool(b, L)
     x0 = to_torch(b.x, "cuda")
 
-    def chain(ring, graph):
-        pool.set_option(B.LORA_OPT_DECODE_RING, ring)
+    def chain(ck, graph):
+        pool.set_option(B.LORA_OPT_DECODE_CHUNK_KB, ck)
         bufs = [x0.clone()] + [to_torch(b.y_in, "cuda") for _ in range(6)]
         st = torch.cuda.Stream()
         def run():
@@ -162,14 +163,14 @@ def test_ring_graph_replay_and_chain(L):
         return bufs[6].clone()
 
     ref = chain(0, False)
-    assert torch.equal(chain(1, True), ref)
-    assert torch.equal(chain(1, False), ref)
+    assert torch.equal(chain(2048, True), ref)
+    assert torch.equal(chain(2048, False), ref)
     pool.close()
 
 
-def test_ring_huge_batch_takes_pair(L):
-    # 512 tokens over 256 adapters: the ring's work lists exceed the kernel parameters -> PDL pair
+def test_chunked_huge_batch_metadata_upload(L):
+    # 512 tokens over 256 adapters: the metadata exceeds the kernel parameters (device upload path)
     ranks = {a: [8, 16, 32, 64][a % 4] for a in range(256)}
     ids = [a % 256 for a in range(512)]
     b = gen.build_batch("huge", 31337, "bf16", 1024, 1024, [1] * 512, ids, ranks, y_zero=False)
-    _check(L, b)
+    _check(L, b, chunks=(1024,))
