@@ -73,8 +73,6 @@ def parse():
                          "o (input = attention output) is always its own lora_apply")
     ap.add_argument("--min-window-ms", type=float, default=200.0,
                     help="repeat the K-step timed window until this much device time is covered (median reported)")
-    ap.add_argument("--decode-chunk-kb", type=int, default=None,
-                    help="LORA_OPT_DECODE_CHUNK_KB for the c2 pools (default: the library's)")
     ap.add_argument("--c4-steps", type=int, default=40, help="config 4 (Zipf paged pool, cold starts) steps; 0 = skip")
     ap.add_argument("--cold-start", type=int, choices=[0, 1], default=1,
                     help="cold-start latency by rank + the paper's CPU-assist comparison (rank 0)")
@@ -799,8 +797,6 @@ def main():
             for p in range(len(PROJS)):
                 ads = futs[(l, p)].result()
                 pool = L.LoraPool(H, H, 32, "bf16", max_total_rank=sum(a.rank for a in ads))
-                if args.decode_chunk_kb is not None:
-                    pool.set_option(L.binding.LORA_OPT_DECODE_CHUNK_KB, args.decode_chunk_kb)
                 for a in ads:
                     A = torch.from_numpy(a.A.view(np.int16)).pin_memory()
                     B = torch.from_numpy(a.B.view(np.int16)).pin_memory()

@@ -95,13 +95,6 @@ typedef enum {
                                       loaded this way the steady-state decode apply was 7 % slower
                                       (unexplained). */
 
-#define LORA_OPT_DECODE_CHUNK_KB 7 /* decode work of a full apply (lora_apply, lora_apply_multi; bf16) whose
-                                      adapter rows exceed this many KiB runs as a pipeline of grids over
-                                      chunks of its (adapter, token-chunk) groups: shrink(0) | expand(0) +
-                                      shrink(1) | ... | expand(n-1), so each grid's rows fit on chip next
-                                      to the previous grid's (DESIGN.md §6 N1).  0 = one shrink grid and
-                                      one expand grid.  Bitwise-identical results either way. */
-
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.
  *   hidden_in, hidden_out  H_in, H_out of the adapted projection (Eq. 1's H1, H2).

@@ -25,16 +25,22 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
-#include <algorithm>
 #include <atomic>
 #include <cstring>
-#include <vector>
 
-#include "decode_common.cuh"
 #include "kernel_config.h"
 #include "plan.h"
 
 namespace lora {
+
+struct DecodeJob {                // one pool's operands (lora_apply_multi fuses up to kMaxJobs)
+    const char* x;
+    char* y;
+    const char* A;                // pool page arrays
+    const char* B;
+    int H_in, H_out, ksplit;
+    int x_ld, y_ld;               // row strides of x and y in elements (H_in / H_out unless a TP shard view)
+};
 
 struct DecodeArgs {
     DecodeJob jobs[kMaxJobs];
@@ -50,8 +56,6 @@ struct DecodeArgs {
                                  // each gc (tp_reduce_tail), read by the expand when v_compact is set
     int* gc_cnt;                 // TP shrink: per-gc arrival counters (zero between applies)
     int v_compact;
-    int g_s_lo, g_e_lo, g_ne;    // this grid's units (pipelined schedule): shrink units from g_s_lo, expand
-                                 // units from g_e_lo; a mixed grid's first g_ne CTAs expand, the rest shrink
     int job_shrink_base[kMaxJobs];   // first unit of each fused job (units of a job are contiguous)
     int job_expand_base[kMaxJobs];
 };
@@ -63,6 +67,102 @@ __device__ __forceinline__ int job_of(int u, int n_jobs, const int (&base)[kMaxJ
     for (int i = 1; i < kMaxJobs; ++i)
         if (i < n_jobs && u >= base[i]) j = i;
     return j;
+}
+
+template <int W>
+struct MetaBlob {
+    int32_t w[W];
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LAB_WAIT;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+// per-thread 16-B async copy HBM -> SMEM (LDGSTS): no per-request copy-engine overhead, so it
+// keeps up with HBM for sub-2-KB row slices where cp.async.bulk does not (scripts/microbench_stream.cu)
+// (no L2::cache_hint operand: with it, ptxas 12.9 emitted for some expand instantiations an LDGSTS
+// whose 64-bit descriptor sits in an odd uniform register -- "illegal instruction" at run time)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t /*policy*/) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// L2 prefetch (no data returned to the SM).  Safe before griddepcontrol.wait even for lines a
+// preceding kernel still writes: L2 is the point of coherence, the later real read sees them.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long gtime_raw() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// one thread waits on the preceding grid, the rest park at the barrier (a waiting
+// griddepcontrol.wait polls and would steal issue slots from co-resident CTAs)
+__device__ __forceinline__ void pdl_wait_cta() {
+    if (threadIdx.x == 0) pdl_wait();
+    __syncthreads();
+}
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ void stg128_na(void* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
 }
 
 // ------------------------------------------------------------------ element traits
@@ -202,7 +302,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     char* xbuf = abuf + kShrinkRows * kSliceBytes;
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u = a.g_s_lo + blockIdx.x;
+    const int u = blockIdx.x;
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
 
@@ -334,7 +434,7 @@ __global__ void __launch_bounds__(kConsumerThreads)
     char* ybuf = bbuf + kExpandBytes;                             // [kTokChunk][c]
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int ue = a.g_e_lo + blockIdx.x;
+    const int ue = blockIdx.x;
     const int u = ue + a.n_shrink;
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by a preceding kernel
@@ -499,6 +599,36 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // HBM bytes are exactly the algorithmic ones.
 constexpr int kPitchPad = 16;   // bytes added to each smem row: conflict-free ldmatrix
 
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t& r0, uint32_t& r1, uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+// D[16x8] += A[16x16] (row) * B[16x8] (col), bf16 inputs, fp32 accumulate
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ldg_cg128(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
 // ---- shrink (bf16): one CTA = (group-chunk gc, k-slice of kKSlice, 16 rank rows).  The rank
 // rows go HBM -> SMEM with cp.async.bulk before griddepcontrol.wait (the copy engine, not the
 // LSU: a co-resident CTA's critical-path loads/ldmatrix never queue behind this prefetch).
@@ -650,10 +780,9 @@ __global__ void __launch_bounds__(kConsumerThreads)
     lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
-    const int u = a.g_s_lo + blockIdx.x;
-    if (a.trace && threadIdx.x == 0) a.trace[(size_t)u * 8 + 1] = gtime();
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)blockIdx.x * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();   // metadata uploaded by the preceding kernel
-    shrink_mma_body(a, M, u, smem);
+    shrink_mma_body(a, M, blockIdx.x, smem);
 }
 
 // ---- expand (bf16): one CTA = (group-chunk gc, column slice [n0, n0+nc)).  Swap-AB:
@@ -878,32 +1007,9 @@ __global__ void __launch_bounds__(kConsumerThreads, MINB)
     lora_expand_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
-    const int ue = a.g_e_lo + blockIdx.x;
-    if (a.trace && threadIdx.x == 0) a.trace[(size_t)(ue + a.n_shrink) * 8 + 1] = gtime();
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)(blockIdx.x + a.n_shrink) * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();
-    expand_mma_body(a, M, ue, smem);
-}
-
-// ---- pipelined schedule (DESIGN.md §6 N1, "chunked applies"): a grid that expands the group-chunks
-// of chunk k-1 (their v complete: the previous grid shrank them) while it shrinks those of chunk k.
-// The first g_ne CTAs run expand units, the rest shrink units; both bodies are the ones above.
-template <int W, int MINB>
-__global__ void __launch_bounds__(kConsumerThreads, MINB)
-    lora_mixed_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
-    extern __shared__ __align__(128) char smem[];
-    const int32_t* M = (W > 1) ? blob.w : a.meta_global;
-    const int b = blockIdx.x;
-    if (b < a.g_ne) {
-        const int ue = a.g_e_lo + b;
-        if (a.trace && threadIdx.x == 0) a.trace[(size_t)(ue + a.n_shrink) * 8 + 1] = gtime();
-        if (W == 1) pdl_wait_cta();
-        expand_mma_body(a, M, ue, smem);
-    } else {
-        const int u = a.g_s_lo + (b - a.g_ne);
-        if (a.trace && threadIdx.x == 0) a.trace[(size_t)u * 8 + 1] = gtime();
-        if (W == 1) pdl_wait_cta();
-        shrink_mma_body(a, M, u, smem);
-    }
+    expand_mma_body(a, M, blockIdx.x, smem);
 }
 
 // copies a metadata blob too large for one kernel's parameters into device memory,
@@ -963,10 +1069,9 @@ static bool configure_once(std::atomic<uint64_t>& mask, cudaError_t (*fn)()) {
 }
 
 template <typename T, int W>
-static cudaError_t launch_pair(const DecodeArgs& a0, const Plan& pl, cudaStream_t st, int* launches, int phases,
-                               int num_sms, const std::vector<int>& cuts) {
+static cudaError_t launch_pair(const DecodeArgs& a, const Plan& pl, cudaStream_t st, int* launches, int phases,
+                               int num_sms) {
     using K = DecodeKernels<T, W>;
-    constexpr bool kBf16 = sizeof(T) == 2;
     static std::atomic<uint64_t> configured{0};
     if (!configure_once(configured, [] {
             // the opt-in maximum (the launch passes the real size; it decides occupancy)
@@ -975,14 +1080,6 @@ static cudaError_t launch_pair(const DecodeArgs& a0, const Plan& pl, cudaStream_
             if (e == cudaSuccess) e = cudaFuncSetAttribute(K::expand, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(K::expand_big, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
-            if constexpr (kBf16) {
-                if (e == cudaSuccess)
-                    e = cudaFuncSetAttribute(lora_mixed_mma_kernel<W, LORA_EXPAND_MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
-                if (e == cudaSuccess)
-                    e = cudaFuncSetAttribute(lora_mixed_mma_kernel<W, LORA_EXPAND_BIG_MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxOptin);
-            }
             return e;
         }))
         return cudaErrorInvalidValue;
@@ -992,79 +1089,21 @@ static cudaError_t launch_pair(const DecodeArgs& a0, const Plan& pl, cudaStream_
         for (int i = 0; i < n; ++i) blob.w[i] = pl.blob[i];
     }
     cudaError_t e = cudaSuccess;
-    // shrink grid of ns units from s_lo / expand grid of ne units from e_lo / mixed grid of both
-    auto grid = [&](int s_lo, int ns, int e_lo, int ne) -> cudaError_t {
-        DecodeArgs a = a0;
-        a.g_s_lo = s_lo;
-        a.g_e_lo = e_lo;
-        a.g_ne = ne;
-        cudaError_t r = cudaSuccess;
-        if (ne == 0) {
-            // bf16: a grid of more than 4 shrink CTAs per SM (e.g. q/k/v in one multi launch) fits better
-            // at 5 per SM (DESIGN.md §6 N1 occupancy)
-            const int ss = ns > 4 * num_sms ? K::shrink_smem_big : K::shrink_smem;
-            r = launch_pdl(K::shrink, ns, kConsumerThreads, ss, st, a, blob);
-        } else if (ns == 0) {
-            const bool big = ne > 3 * num_sms;
-            r = launch_pdl(big ? K::expand_big : K::expand, ne, kConsumerThreads, K::expand_launch_smem(a), st, a, blob);
-        } else if constexpr (kBf16) {
-            const bool big = ns + ne > 3 * num_sms;
-            const int sm = std::max(K::expand_launch_smem(a), (int)K::shrink_smem_big);
-            r = launch_pdl(big ? lora_mixed_mma_kernel<W, LORA_EXPAND_BIG_MINB> : lora_mixed_mma_kernel<W, LORA_EXPAND_MINB>,
-                           ns + ne, kConsumerThreads, sm, st, a, blob);
-        } else {
-            r = cudaErrorInvalidValue;
-        }
-        if (r == cudaSuccess) *launches += 1;
-        return r;
-    };
-    const int nk = (int)cuts.size() - 1;
-    if (nk <= 1 || phases != 3) {
-        if (phases & 1) {
-            e = grid(0, pl.n_shrink, 0, 0);
-            if (e != cudaSuccess) return e;
-        }
-        if (phases & 2) e = grid(0, 0, 0, pl.n_expand);
-        return e;
-    }
-    // pipelined: S(0) | E(0) + S(1) | ... | E(nk-1), chunk k = group-chunks [cuts[k], cuts[k+1])
-    const int32_t* gcr = pl.blob.data() + kHdrWords;
-    auto sbase = [&](int gc) { return gc >= pl.n_gc ? pl.n_shrink : gcr[gc * kGcFields + GC_SHRINK_BASE]; };
-    auto ebase = [&](int gc) { return gc >= pl.n_gc ? pl.n_expand : gcr[gc * kGcFields + GC_EXPAND_BASE]; };
-    for (int k = 0; k <= nk; ++k) {
-        const int s_lo = k < nk ? sbase(cuts[k]) : 0, ns = k < nk ? sbase(cuts[k + 1]) - s_lo : 0;
-        const int e_lo = k > 0 ? ebase(cuts[k - 1]) : 0, ne = k > 0 ? ebase(cuts[k]) - e_lo : 0;
-        if (ns + ne == 0) continue;
-        e = grid(s_lo, ns, e_lo, ne);
+    if (phases & 1) {
+        // bf16: a grid of more than 4 shrink CTAs per SM (e.g. q/k/v in one multi launch) fits better
+        // at 5 per SM (DESIGN.md §6 N1 occupancy)
+        const int ss = pl.n_shrink > 4 * num_sms ? K::shrink_smem_big : K::shrink_smem;
+        e = launch_pdl(K::shrink, pl.n_shrink, kConsumerThreads, ss, st, a, blob);
         if (e != cudaSuccess) return e;
+        *launches += 1;
+    }
+    if (phases & 2) {
+        const bool big = pl.n_expand > 3 * num_sms;
+        e = launch_pdl(big ? K::expand_big : K::expand, pl.n_expand, kConsumerThreads, K::expand_launch_smem(a), st, a,
+                       blob);
+        *launches += 1;
     }
     return e;
-}
-
-// Chunk boundaries (group-chunk indices) of the pipelined schedule: chunks of about chunk_bytes of
-// adapter rows each (A + B), balanced; {0, n_gc} when the apply is one chunk.
-static void chunk_cuts(const Plan& pl, const DecodeArgs& a, int64_t chunk_bytes, int esz, std::vector<int>& cuts) {
-    cuts.assign(1, 0);
-    const int32_t* gcr = pl.blob.data() + kHdrWords;
-    int64_t total = 0;
-    for (int gc = 0; gc < pl.n_gc; ++gc) {
-        const DecodeJob& J = a.jobs[gcr[gc * kGcFields + GC_JOB]];
-        total += (int64_t)gcr[gc * kGcFields + GC_RANK] * (J.H_in + J.H_out) * esz;
-    }
-    const int64_t n = chunk_bytes > 0 ? (total + chunk_bytes - 1) / chunk_bytes : 1;
-    if (n > 1) {
-        int64_t acc = 0;
-        int k = 1;
-        for (int gc = 0; gc < pl.n_gc && k < n; ++gc) {
-            const DecodeJob& J = a.jobs[gcr[gc * kGcFields + GC_JOB]];
-            acc += (int64_t)gcr[gc * kGcFields + GC_RANK] * (J.H_in + J.H_out) * esz;
-            if (acc * n >= total * k && gc + 1 < pl.n_gc) {
-                cuts.push_back(gc + 1);
-                ++k;
-            }
-        }
-    }
-    cuts.push_back(pl.n_gc);
 }
 
 template <typename T>
@@ -1116,13 +1155,11 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         a.e_pgoff = a.e_dtoff + maxtok * (maxc + 4) * 4;
         a.e_smem = a.e_pgoff + maxr * 4;
     }
-    static thread_local std::vector<int> cuts;
-    chunk_cuts(pl, a, sizeof(T) == 2 && L.phases == 3 && !L.vred ? L.chunk_bytes : 0, (int)sizeof(T), cuts);
     const int n = (int)pl.blob.size();
-    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases, L.num_sms, cuts);
-    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases, L.num_sms, cuts);
-    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches, L.phases, L.num_sms, cuts);
-    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches, L.phases, L.num_sms, cuts);
+    if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases, L.num_sms);
+    if (n <= 2048) return launch_pair<T, 2048>(a, pl, st, launches, L.phases, L.num_sms);
+    if (n <= 4096) return launch_pair<T, 4096>(a, pl, st, launches, L.phases, L.num_sms);
+    if (n <= kUploadWords) return launch_pair<T, kUploadWords>(a, pl, st, launches, L.phases, L.num_sms);
     for (int off = 0; off < n && (L.phases & 1); off += kUploadWords) {   // expand-only reuses the shrink's upload
         const int m = n - off < kUploadWords ? n - off : kUploadWords;
         MetaBlob<kUploadWords> b;
@@ -1131,7 +1168,7 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         *launches += 1;
         if (e != cudaSuccess) return e;
     }
-    return launch_pair<T, 1>(a, pl, st, launches, L.phases, L.num_sms, cuts);
+    return launch_pair<T, 1>(a, pl, st, launches, L.phases, L.num_sms);
 }
 
 int launch_decode(const Plan& pl, const DecodeLaunch& L, cudaStream_t st, int* launches) {

@@ -106,7 +106,6 @@ struct DecodeLaunch {
         int H_in, H_out;
     } more[3];
     int n_jobs = 1;
-    int64_t chunk_bytes = 0;     // bf16 full applies: pipelined schedule in chunks of ~this many adapter bytes (0: off)
 };
 struct PrefillLaunch {
     const void* x;
@@ -151,7 +150,6 @@ struct FusedBaseLaunch {
 int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_tiles, lora_cuda_stream st);
 bool prefill_supported(int H_in, int H_out, int esz);
 int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);
-constexpr int64_t kDefaultChunkBytes = 0;   // LORA_OPT_DECODE_CHUNK_KB default (DESIGN.md §6 N1)
 constexpr int kPfMaxRank = 128;        // tensor-core prefill path handles ranks up to this
 constexpr int kPfMaxBlobWords = 7680;
 

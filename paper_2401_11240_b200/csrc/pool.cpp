@@ -56,7 +56,6 @@ struct lora_pool {
     size_t meta_cap = 0;                 // words
     bool load_kernel = false;            // LORA_OPT_LOAD_KERNEL: cold-start copies by a zero-copy gather kernel
     bool pad_max_rank = false;           // LORA_OPT_PAD_MAX_RANK: BGMV-style padded decode work (comparison)
-    int64_t chunk_bytes = kDefaultChunkBytes;   // LORA_OPT_DECODE_CHUNK_KB: pipelined decode schedule
     Plan plan;
     Plan fused;                          // merged kernel work of the last lora_apply_multi led by this pool
     int L_tc = 64;
@@ -532,7 +531,6 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         L.gc_cnt = mode == 1 ? p->gc_cnt : nullptr;
         L.x_ld = x_ld;
         L.y_ld = y_ld;
-        L.chunk_bytes = p->chunk_bytes;
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
@@ -615,7 +613,6 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         DecodeLaunch L{xs[0], ys[0], p0->dA, p0->dB, p0->vbuf, p0->meta_dev, p0->trace, p0->H_in, p0->H_out, p0->esz,
                        p0->num_sms};
         L.n_jobs = n_pools;
-        L.chunk_bytes = p0->chunk_bytes;
         for (int i = 1; i < n_pools; ++i)
             L.more[i - 1] = DecodeLaunch::More{xs[i], ys[i], pools[i]->dA, pools[i]->dB, pools[i]->H_in, pools[i]->H_out};
         cudaError_t e = (cudaError_t)launch_decode(fz, L, st, &launches);
@@ -880,10 +877,6 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
         case LORA_OPT_PAD_MAX_RANK:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_PAD_MAX_RANK takes 0 or 1");
             p->pad_max_rank = value == 1;
-            return LORA_OK;
-        case LORA_OPT_DECODE_CHUNK_KB:
-            if (value < 0 || value > (int64_t)1 << 30) return fail(LORA_ERR_ARG, "LORA_OPT_DECODE_CHUNK_KB must be in [0, 2^30]");
-            p->chunk_bytes = value * 1024;
             return LORA_OK;
         default:
             return fail(LORA_ERR_ARG, "unknown option " + std::to_string(option));
