@@ -68,11 +68,12 @@ def _check(L, b, W, fragmented=False):
 
 
 @pytest.mark.parametrize("fragmented", [False, True], ids=["box_loads", "gather4_loads"])
-@pytest.mark.parametrize("H_out", [384, 512], ids=["nt128", "nt256"])
+@pytest.mark.parametrize("H_out", [256, 768], ids=["one_ctile", "three_ctiles"])
 def test_fused_base_ragged_small(L, fragmented, H_out):
-    """Ragged segments (1..300 tokens, tails inside a tile), ranks 1 / 8 / 128, an id < 0 segment,
-    an adapter used by two segments; 128- and 256-column tiles; adapters in one page run (2D box
-    loads) or fragmented (gather4 loads)."""
+    """Ragged segments (1..300 tokens, tails inside a tile; odd tile counts, so some 128-token tiles
+    run without a pair partner), ranks 1 / 8 / 128, an id < 0 segment, an adapter used by two
+    segments; one or three 256-column tiles; adapters in one page run (2D box loads in the shrink
+    pass) or fragmented (gather4 loads)."""
     b = gen.build_batch("fb_small", 811, "bf16", 256, H_out, [300, 1, 128, 50, 129], [0, -1, 1, 2, 0],
                         {0: 8, 1: 128, 2: 1}, y_zero=True)
     W = _weight(5, 256, H_out)
@@ -85,6 +86,23 @@ def test_fused_base_prefill_mix(L):
     b = gen.build_batch("fb_mix", 812, "bf16", 1024, 2048, [512] * 8, list(range(8)), ranks, y_zero=True)
     W = _weight(6, 1024, 2048)
     _check(L, b, W)
+
+
+def test_fused_base_base_only_batch(L):
+    """Every segment id < 0: no shrink pass, y = x·W (K loop without extension)."""
+    b = gen.build_batch("fb_base", 816, "bf16", 512, 512, [130, 300], [-1, -1], {0: 8}, y_zero=True)
+    import torch
+    pool = make_pool(b, L)
+    x = to_torch(b.x, "cuda")
+    W = _weight(9, 512, 512)
+    y = torch.full((b.T, b.H_out), 0x7fc0, dtype=torch.int16, device="cuda")
+    pool.apply_fused_base(x, to_torch(W, "cuda"), y, b.seg_indptr, b.adapter_ids)
+    torch.cuda.synchronize()
+    got = gen.storage_to_f64(from_torch(y, "bf16"), "bf16").reshape(b.T, b.H_out)
+    base = gen.storage_to_f64(b.x, "bf16").reshape(b.T, b.H_in) @ gen.storage_to_f64(W, "bf16").reshape(b.H_in, b.H_out)
+    assert np.isfinite(got).all()
+    assert np.linalg.norm(got - base) / np.linalg.norm(base) <= TOL["bf16"]
+    pool.close()
 
 
 def test_fused_base_rejects_unsupported(L):
@@ -100,6 +118,13 @@ def test_fused_base_rejects_unsupported(L):
     with pytest.raises(L.LoraError) as ei:
         pool.apply_fused_base(x, W, x, b.seg_indptr, b.adapter_ids)   # y overlaps x
     assert ei.value.name == "LORA_ERR_ARG"
+    pool.close()
+    b2 = gen.build_batch("fb_n384", 814, "bf16", 256, 384, [64], [0], {0: 8}, y_zero=True)   # hidden_out % 256
+    pool = make_pool(b2, L)
+    with pytest.raises(L.LoraError) as ei:
+        pool.apply_fused_base(to_torch(b2.x, "cuda"), to_torch(_weight(7, 256, 384), "cuda"),
+                              torch.zeros((b2.T, 384), dtype=torch.int16, device="cuda"), b2.seg_indptr, b2.adapter_ids)
+    assert ei.value.name == "LORA_ERR_UNSUPPORTED"
     pool.close()
 
 
