@@ -36,6 +36,9 @@ constexpr int kFgStageBytes = 32768;   // per CTA: A chunk (x or V) 16 KB + B ch
 constexpr int kFgEpiBytes = 4 * 2 * 2048;   // per epilogue warp: two 32-row x 64-B staging slots
 constexpr int kFgSmem = 1024 + kFgStages * kFgStageBytes + kFgEpiBytes + 256;
 constexpr int kFgPairWords = 8;
+#ifndef FG_B_KMAJOR
+#define FG_B_KMAJOR 0   // experiment builds: 1 = W given as W^T [H_out][H_in] (nn.Linear layout), K-major B
+#endif
 
 struct FgArgs {
     CUtensorMap tm_x;   // x [T][H_in], box {64, 128}, SW128
@@ -105,21 +108,27 @@ __device__ __forceinline__ uint64_t fg_desc(uint32_t addr, uint32_t lbo, uint32_
     return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
-// instruction descriptor: D fp32, A/B bf16, A K-major, B MN-major, M = 256 (CTA pair), N = 256
-constexpr uint32_t kFgIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
-__device__ __forceinline__ void fg_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+// instruction descriptor: D fp32, A/B bf16, A K-major, B MN-major (1) or K-major (0), M = 256 (CTA pair), N = 256
+constexpr uint32_t fg_idesc(uint32_t b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (b_mn << 16) | ((256u >> 3) << 17) | ((256u >> 4) << 24);
+}
+// executed by the whole (converged) warp; one elected lane issues (warp-uniform operands stay in
+// uniform registers: no per-lane waterfall around the instruction)
+__device__ __forceinline__ void fg_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(kFgIdesc), "r"(acc)
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
         : "memory");
 }
 // commit the leader's MMAs so far: arrive on the barrier at this offset in BOTH CTAs of the pair
-__device__ __forceinline__ void fg_commit2(uint32_t bar) {
+__device__ __forceinline__ void fg_commit2(uint32_t bar) {   // whole warp; one elected lane commits
     asm volatile(
-        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(bar)
+        "{\n\t.reg .b16 m;\n\t.reg .pred e;\n\tmov.b16 m, 3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(bar)
         : "memory");
 }
 __device__ __forceinline__ void fg_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -210,8 +219,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
                     if (lane == 0) {
                         if (leader) fg_arrive_tx(full(stage), 2u * kFgStageBytes);
                         fg_tma_2d(sb, &a.tm_x, kc * 64, tok0, cbar);
+#if FG_B_KMAJOR
+                        fg_tma_2d(sb + 16384, &a.tm_w, kc * 64, nb0, cbar);   // W^T [H_out][H_in]: box {64 K, 128 N}
+#else
                         fg_tma_2d(sb + 16384, &a.tm_w, nb0, kc * 64, cbar);
                         fg_tma_2d(sb + 16384 + 8192, &a.tm_w, nb0 + 64, kc * 64, cbar);
+#endif
                     }
                 } else {
                     const int e = kc - nkc;
@@ -236,7 +249,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA, one lane) =====================
+        // Descriptors are built once and advanced by adding to their start-address field (addr >> 4,
+        // low 14 bits): +2 per 32-B K step of the K-major A / K-major B atoms, +128 per 2 KB K step of
+        // the MN-major B atoms, +2048 per 32 KB ring stage.  The x·W chunks issue their 4 K steps
+        // unrolled; only the adapter-rank chunks have a variable step count.
         if (leader) {
+            const uint64_t a0 = fg_desc(ring, 16, 1024);
+            const uint64_t b0 = FG_B_KMAJOR ? fg_desc(ring + 16384, 16, 1024) : fg_desc(ring + 16384, 8192, 1024);
+            const uint64_t be0 = fg_desc(ring + 16384, 8192, 1024);   // adapter B rows: MN-major
+            constexpr uint64_t kBStep = FG_B_KMAJOR ? 2 : 128;
+            constexpr uint32_t kIdW = fg_idesc(FG_B_KMAJOR ? 0u : 1u), kIdB = fg_idesc(1u);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -252,12 +274,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
                 for (int kc = 0; kc < nch; ++kc) {
                     fg_wait(full(stage), phase);
                     fg_fence_after();
-                    if (lane == 0) {
-                        const uint32_t sb = ring + (uint32_t)stage * kFgStageBytes;
-                        const int ks = kc < nkc ? 4 : min(4, (rp - (kc - nkc) * 64) / 16);
-                        for (int kk = 0; kk < ks; ++kk)
-                            fg_mma2(dacc, fg_desc(sb + kk * 32, 16, 1024), fg_desc(sb + 16384 + kk * 2048, 8192, 1024),
-                                    (kc | kk) != 0);
+                    {
+                        const uint64_t so = (uint64_t)stage * (kFgStageBytes >> 4);
+                        const uint64_t ad = a0 + so;
+                        if (kc < nkc) {
+                            const uint64_t bd = b0 + so;
+                            fg_mma2(dacc, ad, bd, kIdW, kc != 0);
+                            fg_mma2(dacc, ad + 2, bd + kBStep, kIdW, 1u);
+                            fg_mma2(dacc, ad + 4, bd + 2 * kBStep, kIdW, 1u);
+                            fg_mma2(dacc, ad + 6, bd + 3 * kBStep, kIdW, 1u);
+                        } else {
+                            const uint64_t bd = be0 + so;
+                            const int ks = min(4, (rp - (kc - nkc) * 64) / 16);
+                            for (int kk = 0; kk < ks; ++kk) fg_mma2(dacc, ad + 2 * kk, bd + 128 * kk, kIdB, 1u);
+                        }
                         fg_commit2(empty(stage));
                         if (kc == nch - 1) fg_commit2(tfull(b));
                     }
@@ -331,7 +361,11 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
     FgArgs a;
     std::memset(&a, 0, sizeof(a));
     int e = make_tmap_bf16(&a.tm_x, L.x, L.T, L.H_in, 128);
+#if FG_B_KMAJOR
+    if (!e) e = make_tmap_bf16(&a.tm_w, L.w, L.H_out, L.H_in, 128);   // experiment: W^T [H_out][H_in]
+#else
     if (!e) e = make_tmap_bf16(&a.tm_w, L.w, L.H_in, L.H_out, 64);
+#endif
     if (!e && L.vtiles) e = make_tmap_bf16(&a.tm_v, L.vtiles, (int64_t)L.n_vtiles * 128, L.v_cols, 128);
     else if (!e) e = make_tmap_bf16(&a.tm_v, L.x, L.T, L.H_in, 128);   // (no adapter tiles: never loaded)
     if (e) return e;

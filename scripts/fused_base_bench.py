@@ -26,6 +26,8 @@ for a in b.adapters:
                       torch.from_numpy(a.B.view(np.int16)).pin_memory(), a.scale)
 x = torch.from_numpy(b.x.view(np.int16)).cuda().view(torch.bfloat16)
 W = (torch.randn(b.H_in, b.H_out, device="cuda") / b.H_in ** 0.5).to(torch.bfloat16)
+WT = W.t().contiguous()   # nn.Linear layout [H_out][H_in]
+W_fused = WT if "-DFG_B_KMAJOR=1" in os.environ.get("LORA_BUILD_DEFS", "") else W
 y = torch.empty(b.T, b.H_out, dtype=torch.bfloat16, device="cuda")
 st = torch.cuda.Stream()
 flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
@@ -33,7 +35,7 @@ NP = 4
 
 
 def fused():
-    pool.apply_fused_base(x, W, y, b.seg_indptr, b.adapter_ids, stream=st)
+    pool.apply_fused_base(x, W_fused, y, b.seg_indptr, b.adapter_ids, stream=st)
 
 
 def unfused():
@@ -43,6 +45,17 @@ def unfused():
 
 def base():
     torch.matmul(x, W, out=y)
+
+
+no_ids = np.full_like(b.adapter_ids, -1)
+
+
+def fused_gemm_only():   # every segment id < 0: no shrink pass, the GEMM without K extension
+    pool.apply_fused_base(x, W_fused, y, b.seg_indptr, no_ids, stream=st)
+
+
+def shrink_pass_only():   # the prefill kernel alone (expand included): an upper bound for the V pass
+    pool.apply(x, y, b.seg_indptr, b.adapter_ids, stream=st)
 
 
 def timed(fn):
@@ -71,7 +84,8 @@ sum_tr = sum(int(b.seg_indptr[i + 1] - b.seg_indptr[i]) * b.adapters[[a.id for a
              for i in range(len(b.adapter_ids)))
 flops = 2.0 * b.T * b.H_in * b.H_out + 2.0 * sum_tr * (b.H_in + b.H_out)
 out = {"T": b.T, "H": b.H_in, "tflop": round(flops / 1e12, 4)}
-for name, fn in (("fused", fused), ("unfused", unfused), ("base", base)):
+for name, fn in (("fused", fused), ("unfused", unfused), ("base", base), ("fused_gemm_only", fused_gemm_only),
+                 ("prefill_delta", shrink_pass_only)):
     us = timed(fn)
     out[name] = {"us": round(us, 1), "tflops": round(flops / (us * 1e-6) / 1e12, 1),
                  "frac_bf16_peak": round(flops / (us * 1e-6) / 1e12 / peaks["bf16_tflops"], 3)}
