@@ -187,7 +187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     fg_fence_before();
-    fg_cluster_sync();
+    fg_cluster_sync();   // the peer's barriers are initialised before any remote arrive / TMA complete_tx
+    __syncthreads();     // (also orders the TMEM address write before every reader, as racecheck models it)
     fg_fence_after();
     const uint32_t tmem = *tmem_slot;
     // x, W, V and y may belong to preceding kernels in the stream
