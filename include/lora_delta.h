@@ -204,9 +204,9 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
  *   UNSUPPORTED (host-only pool).
  * lora_apply_tp -- y[:, this rank's out slice] += s·(Σ_ranks x_k·A_k)·B_shard for one batch, all on
  *   `stream` without host synchronisation: the shrink kernel (partials over this rank's
- *   H_in slice, per 1,024-wide k-slice), the k-reduce kernel (slices summed in fixed order into the
- *   compact v [Σ_gc ntok x round_up(r, 4)] fp32), ncclAllReduce(SUM) of that compact v in place
- *   over the group, the expand kernel.  Every token takes the decode kernels.  Capturable in a CUDA
+ *   H_in slice, per 1,024-wide k-slice; the last CTA of each group-chunk to finish sums the slices in
+ *   fixed order into the compact v [Σ_gc ntok x round_up(r, 4)] fp32), ncclAllReduce(SUM) of that
+ *   compact v in place over the group, the expand kernel.  Every token takes the decode kernels.  Capturable in a CUDA
  *   graph (NCCL calls are).
  *     x   device, T rows of hidden_in elements, row stride x_ld elements (0 = hidden_in), 16-B aligned.
  *     y   device, T rows of hidden_out elements, row stride y_ld elements (0 = hidden_out), 16-B aligned.
