@@ -117,8 +117,6 @@ struct PrefillLaunch {
     unsigned long long* trace;
     int T, H_in, H_out, zero_page, num_sms;
     float* pscratch = nullptr;   // split-K partials: [CTA][128 rows][128] fp32 (L2-resident exchange)
-    void* vtiles = nullptr;      // V-out mode (fused base GEMM's shrink pass): [n_pf_tiles * 128][v_cols] bf16
-    int v_cols = 0;              // 64 or 128
 };
 
 // Concatenates the SIMT work lists of plans[0..n) (one per fused pool = job index) into merged
@@ -148,11 +146,13 @@ struct FusedBaseLaunch {
     const void* tm_b;
     int T, H_in, H_out, zero_page;
     const void* box_maps = nullptr;   // device: the pool's 2D box maps (contiguous adapters)
-    const void* vtiles = nullptr;     // the shrink pass's V tiles [n_vtiles * 128][v_cols] bf16 (null: no adapter)
-    int n_vtiles = 0, v_cols = 0;
+    const void* vtiles = nullptr;     // V tiles [n_vtiles * 128][v_cols] bf16 (written by the V items)
+    int* vsync = nullptr;             // [2 + n_vtiles] ints, zero-initialised once, persistent (launch epochs)
+    int n_vtiles = 0, v_cols = 0, n_vp = 0;   // n_vp: pairs with an adapter (ordered first)
+    unsigned long long* trace = nullptr;      // lora_debug_set_trace buffer, or null
 };
-// words: [n_pairs][8] pair records {vtile, tok0_a, nvalid_a, tok0_b, nvalid_b (0: no partner), rank,
-// page_off, first_page}, then page lists (fused_base_kernel.cu)
+// words: [n_pairs][10] pair records {vtile, tok0_a, nvalid_a, tok0_b, nvalid_b (0: no partner), rank,
+// page_off, scale_bits, first_page (-1: fragmented), 0}, then page lists (fused_base_kernel.cu)
 int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_pairs, int num_sms,
                       lora_cuda_stream st);
 bool prefill_supported(int H_in, int H_out, int esz);

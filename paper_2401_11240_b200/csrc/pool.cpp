@@ -51,8 +51,10 @@ struct lora_pool {
     float* vbuf = nullptr;
     float* pf_scratch = nullptr;         // prefill split-K partials (grown on demand)
     size_t pf_scratch_cap = 0;
-    uint16_t* fb_vtiles = nullptr;       // lora_apply_fused_base (bf16): the shrink pass's V tiles (grown on demand)
+    uint16_t* fb_vtiles = nullptr;       // lora_apply_fused_base: V tiles (bf16, grown on demand)
     size_t fb_vtiles_cap = 0;
+    int* fb_vsync = nullptr;             // lora_apply_fused_base: launch epochs + per-V-tile flags (zeroed once)
+    size_t fb_vsync_cap = 0;
     size_t vbuf_cap = 0;                 // floats
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
@@ -278,6 +280,7 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->gc_cnt) cudaFree(p->gc_cnt);
         if (p->pf_scratch) cudaFree(p->pf_scratch);
         if (p->fb_vtiles) cudaFree(p->fb_vtiles);
+        if (p->fb_vsync) cudaFree(p->fb_vsync);
         if (p->meta_dev) cudaFree(p->meta_dev);
         for (void* b : p->retired) cudaFree(b);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
@@ -776,18 +779,17 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
         const size_t xb = (size_t)T * p->H_in * 2, wb = (size_t)p->H_in * p->H_out * 2, yb = (size_t)T * p->H_out * 2;
         if ((xs < ys + yb && ys < xs + xb) || (ws < ys + yb && ys < ws + wb)) return fail(LORA_ERR_ARG, "y overlaps x or W");
     }
-    // Two launches (fused_base_kernel.cu): (1) the shrink pass -- the prefill kernel in V-out mode,
-    // one CTA per 128-token tile of an adapter segment, V = bf16(s·x·A) into tile-private rows of the
-    // pool's V scratch; (2) the fused GEMM y = [x | V]·[W ; B] over pairs of 128-token tiles of one
-    // segment (an odd last tile runs alone), K extended by the adapter's rank.
+    // One launch (fused_base_kernel.cu): the GEMM y = [x | V]·[W ; B] over pairs of 128-token tiles of
+    // one segment (an odd last tile runs alone), K extended by the adapter's rank; V = bf16(s·x·A) is
+    // computed inside it by each adapter pair's first column tile (the "V items") into tile-private
+    // rows of the pool's V scratch.  Pairs with an adapter come first (the kernel schedules their V
+    // items first).
     if (p->H_out % 256)
         return fail(LORA_ERR_UNSUPPORTED, "the fused base GEMM needs hidden_out % 256 == 0");
-    static thread_local std::vector<int32_t> words;              // GEMM: pair records, then page lists
+    static thread_local std::vector<int32_t> words;              // pair records, then page lists
+    static thread_local std::vector<int32_t> plain;              // pairs without an adapter (appended last)
     static thread_local std::vector<std::pair<int32_t, int32_t>> offs;   // (id, page offset in words)
-    static thread_local Plan vplan;                              // the shrink pass's prefill tile records
-    static thread_local std::vector<int32_t> vpages;
-    static thread_local std::vector<std::pair<int32_t, int32_t>> voffs;
-    int n_pairs = 0, n_vtiles = 0, max_rp = 0;
+    int n_pairs = 0, n_vtiles = 0, max_rp = 0, n_vp = 0;
     for (int i = 0; i < num_segments; ++i) {
         const int len = seg_indptr[i + 1] - seg_indptr[i];
         if (len <= 0) continue;
@@ -796,21 +798,19 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
             const AdapterRec& a = p->table.at(adapter_ids[i]);
             if (a.rank > kPfMaxRank) return fail(LORA_ERR_UNSUPPORTED, "the fused base GEMM supports rank <= 128");
             n_vtiles += (len + 127) / 128;
+            n_vp += (len + 255) / 256;
             max_rp = std::max(max_rp, (a.rank + 15) & ~15);
         }
     }
-    words.assign((size_t)n_pairs * 8, 0);
+    words.assign((size_t)n_pairs * 10, 0);
+    plain.clear();
     offs.clear();
-    vplan.reset();
-    vplan.pf_blob.assign((size_t)n_vtiles * 8, 0);
-    vpages.clear();
-    voffs.clear();
     int pix = 0, vix = 0;
     for (int i = 0; i < num_segments; ++i) {
         const int len = seg_indptr[i + 1] - seg_indptr[i];
         if (len <= 0) continue;
         const int32_t id = adapter_ids[i];
-        int rank = 0, off = 0, voff = 0, first_page = -1;
+        int rank = 0, off = 0;
         int32_t sb = 0;
         if (id >= 0) {
             const AdapterRec& a = p->table.at(id);
@@ -823,47 +823,37 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
                 off = (int)words.size();
                 offs.emplace_back(id, off);
                 words.insert(words.end(), a.pages.begin(), a.pages.end());
-                voffs.emplace_back(id, (int)vpages.size());
-                vpages.insert(vpages.end(), a.pages.begin(), a.pages.end());
             }
-            for (const auto& o : voffs)
-                if (o.first == id) voff = o.second;
+        }
+        int first_page = -1;   // the adapter's pages as one run: 2D box loads of its rank rows
+        if (rank > 0) {
+            const AdapterRec& a = p->table.at(id);
             bool run = true;
             for (int j = 1; j < rank && run; ++j) run = a.pages[j] == a.pages[0] + j;
             first_page = run ? a.pages[0] : -1;
         }
-        const int vtile0 = vix;
-        if (rank > 0)
-            for (int t0 = 0; t0 < len; t0 += 128, ++vix) {
-                int32_t* rec = vplan.pf_blob.data() + (size_t)vix * 8;
-                rec[0] = seg_indptr[i] + t0;
-                rec[1] = std::min(128, len - t0);
-                rec[2] = rank;
-                rec[3] = voff;   // relocated below, once the record block's size is final
-                rec[4] = sb;
-                rec[5] = first_page;
-                rec[6] = 1;      // no expand column tiles: V-out only
-                rec[7] = 1;
-            }
-        for (int t0 = 0; t0 < len; t0 += 256, ++pix) {
-            int32_t* rec = words.data() + (size_t)pix * 8;
-            rec[0] = rank > 0 ? vtile0 + t0 / 128 : 0;
+        for (int t0 = 0; t0 < len; t0 += 256) {
+            int32_t rec[10];
+            rec[0] = rank > 0 ? vix + t0 / 128 : 0;
             rec[1] = seg_indptr[i] + t0;
             rec[2] = std::min(128, len - t0);
             rec[3] = len - t0 > 128 ? seg_indptr[i] + t0 + 128 : 0;
             rec[4] = len - t0 > 128 ? std::min(128, len - t0 - 128) : 0;
             rec[5] = rank;
             rec[6] = off;
-            rec[7] = first_page;
+            rec[7] = sb;
+            rec[8] = first_page;
+            rec[9] = 0;
+            if (rank > 0) {
+                std::copy(rec, rec + 10, words.begin() + (size_t)pix * 10);
+                ++pix;
+            } else {
+                plain.insert(plain.end(), rec, rec + 10);
+            }
         }
+        if (rank > 0) vix += (len + 127) / 128;
     }
-    for (int v = 0; v < n_vtiles; ++v) vplan.pf_blob[(size_t)v * 8 + 3] += n_vtiles * 8;
-    vplan.pf_blob.insert(vplan.pf_blob.end(), vpages.begin(), vpages.end());
-    vplan.n_pf_tiles = n_vtiles;
-    vplan.pf_cs = 1;
-    if (n_vtiles > 0 && (int)vplan.pf_blob.size() > kPfMaxBlobWords)
-        return fail(LORA_ERR_UNSUPPORTED, "batch too large for one fused launch (shrink-pass tiles and page lists exceed " +
-                                              std::to_string(kPfMaxBlobWords) + " words)");
+    std::copy(plain.begin(), plain.end(), words.begin() + (size_t)pix * 10);
     if ((int)words.size() > kFusedBaseMaxWords)
         return fail(LORA_ERR_UNSUPPORTED, "batch too large for one fused launch (tiles and page lists exceed " +
                                               std::to_string(kFusedBaseMaxWords) + " words)");
@@ -884,17 +874,16 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
     if (n_vtiles > 0) {
         if ((s = grow(p, p->fb_vtiles, p->fb_vtiles_cap, (size_t)n_vtiles * 128 * v_cols, false, "fused V tiles")) != LORA_OK)
             return s;
-        PrefillLaunch PL{x, y, p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
-        PL.vtiles = p->fb_vtiles;
-        PL.v_cols = v_cols;
-        cudaError_t e = (cudaError_t)launch_prefill(vplan, PL, st, &launches);
-        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_fused_base: shrink pass launch");
+        if ((s = grow(p, p->fb_vsync, p->fb_vsync_cap, (size_t)n_vtiles + 2, true, "fused V sync")) != LORA_OK) return s;
     }
     FusedBaseLaunch L{x, W, y, p->tm_a, p->tm_b, T, p->H_in, p->H_out, p->n_pages};
     L.box_maps = p->box_maps;
     L.vtiles = n_vtiles > 0 ? p->fb_vtiles : nullptr;
+    L.vsync = n_vtiles > 0 ? p->fb_vsync : nullptr;
     L.n_vtiles = n_vtiles;
     L.v_cols = v_cols;
+    L.n_vp = n_vp;
+    L.trace = p->trace;
     cudaError_t e = (cudaError_t)launch_fused_base(L, words.data(), (int)words.size(), n_pairs, p->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "lora_apply_fused_base: kernel launch");
     launches += 1;

@@ -160,3 +160,42 @@ def test_fused_base_rejects_fp32_pool(L):
         pool.apply_fused_base(x, x, torch.zeros_like(x), [0, 4], [-1])
     assert ei.value.name == "LORA_ERR_UNSUPPORTED"
     pool.close()
+
+
+def test_fused_base_graph_replays_and_epochs(L):
+    """The V items publish V behind per-tile flags holding the launch's epoch (advanced by every
+    launch, never reset).  A graph of two fused calls (two batches, the second reusing the first's
+    V tiles) replayed three times with new x each time, interleaved with eager calls, must match the
+    eager results every time -- a stale flag from an earlier launch would let a column tile read an
+    old V."""
+    import torch
+    b1 = gen.build_batch("fb_ep1", 817, "bf16", 512, 768, [300, 260], [0, 1], {0: 16, 1: 128}, y_zero=True)
+    b2 = gen.build_batch("fb_ep2", 818, "bf16", 512, 768, [200, 356], [1, 0], {0: 16, 1: 128}, y_zero=True)
+    b2.adapters = b1.adapters
+    pool = make_pool(b1, L)
+    W = to_torch(_weight(10, 512, 768), "cuda")
+    x1 = to_torch(b1.x, "cuda")
+    x2 = to_torch(b2.x, "cuda")
+    yg1 = torch.zeros((b1.T, 768), dtype=torch.int16, device="cuda")
+    yg2 = torch.zeros((b2.T, 768), dtype=torch.int16, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):   # warm-up outside the capture (scratch sizing)
+        pool.apply_fused_base(x1, W, yg1, b1.seg_indptr, b1.adapter_ids, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        pool.apply_fused_base(x1, W, yg1, b1.seg_indptr, b1.adapter_ids, stream=s)
+        pool.apply_fused_base(x2, W, yg2, b2.seg_indptr, b2.adapter_ids, stream=s)
+    for rep in range(3):
+        x1.copy_(torch.roll(x1, 1, 0))
+        x2.copy_(torch.roll(x2, 3, 0))
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize()
+        ye1 = torch.zeros_like(yg1)
+        ye2 = torch.zeros_like(yg2)
+        pool.apply_fused_base(x2, W, ye2, b2.seg_indptr, b2.adapter_ids)
+        pool.apply_fused_base(x1, W, ye1, b1.seg_indptr, b1.adapter_ids)
+        torch.cuda.synchronize()
+        assert torch.equal(yg1, ye1) and torch.equal(yg2, ye2), rep
+    pool.close()
