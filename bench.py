@@ -220,27 +220,37 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------- CPU oracle baseline
-def cpu_oracle_tokens_per_s(n_layers_sample: int, world_rank: int = 0, n_threads: int = 0, reps: int = 1):
-    """The fp64 oracle on n_layers_sample layers x 4 projections of the same workload,
-    extrapolated to the metric's unit (tokens through all 32 layers x 4 projections)."""
-    from oracle import oracle as O
-    n_threads = n_threads or len(os.sched_getaffinity(0))
+def _oracle_work(n_layers_sample: int, world_rank: int = 0):
+    """Inputs of the fp64 oracle for n_layers_sample layers x 4 projections of the bench workload."""
     ip, ids = layer_batch_meta(world_rank)
     rng = np.random.default_rng(0)
     x = rng.standard_normal((T_DECODE, H))
-    y0 = np.zeros((T_DECODE, H))
+    x = gen.storage_to_f64(gen.f32_to_bf16_bits(x.astype(np.float32)), "bf16")
     work = []
     for l in range(n_layers_sample):
         for p in range(len(PROJS)):
             ads = make_pool_adapters(l, p, world_rank)
             work.append([(a.id, a.rank, a.scale, gen.storage_to_f64(a.A, "bf16"), gen.storage_to_f64(a.B, "bf16"))
                          for a in ads])
-    x = gen.storage_to_f64(gen.f32_to_bf16_bits(x.astype(np.float32)), "bf16")
+    return ip, ids, x, np.zeros((T_DECODE, H)), work
+
+
+def _oracle_run(w, n_threads: int) -> float:
+    """seconds for one pass of the oracle over the work of _oracle_work"""
+    from oracle import oracle as O
+    ip, ids, x, y0, work = w
     t0 = time.perf_counter()
-    for _ in range(reps):
-        for ads in work:
-            O.delta(H, H, ip, ids, ads, x, y0, n_threads=n_threads)
-    dt = time.perf_counter() - t0
+    for ads in work:
+        O.delta(H, H, ip, ids, ads, x, y0, n_threads=n_threads)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_tokens_per_s(n_layers_sample: int, world_rank: int = 0, n_threads: int = 0, reps: int = 1):
+    """The fp64 oracle on n_layers_sample layers x 4 projections of the same workload,
+    extrapolated to the metric's unit (tokens through all 32 layers x 4 projections)."""
+    n_threads = n_threads or len(os.sched_getaffinity(0))
+    w = _oracle_work(n_layers_sample, world_rank)
+    dt = sum(_oracle_run(w, n_threads) for _ in range(reps))
     frac = (n_layers_sample * reps) / LAYERS
     return T_DECODE * frac / dt, n_threads, dt
 
@@ -256,26 +266,29 @@ def _cpu_model() -> str:
 
 
 def run_reference(args):
-    """--impl reference: the oracle (fp64 C, OpenMP) as the reference arm, same metric."""
+    """--impl reference: the oracle (fp64 C, OpenMP on every host core) as the reference arm, same
+    metric, workload and unit.  Each of the --steps K timed steps (after --warmup W untimed ones) is a
+    bounded sample of one bench step: the oracle over 1 of the 32 layers (q/k/v/o, 64 tokens), the
+    step time extrapolated x32 (layers are identical work)."""
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    for _ in range(max(0, args.warmup and 1)):
-        cpu_oracle_tokens_per_s(1, 0)
-    vals, secs = [], 0.0
-    for _ in range(args.steps if args.steps <= 3 else 3):
-        v, cores, dt = cpu_oracle_tokens_per_s(1, 0)
-        vals.append(v)
-        secs += dt
-    v = float(np.median(vals))
+    n_threads = len(os.sched_getaffinity(0))
+    w = _oracle_work(1, 0)
+    for _ in range(args.warmup):
+        _oracle_run(w, n_threads)
+    dts = [_oracle_run(w, n_threads) for _ in range(args.steps)]
+    step_s = float(np.median(dts)) * LAYERS
+    v = T_DECODE / step_s
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": len(vals), "warmup": args.warmup, "ms_per_step": 1000.0 * T_DECODE / v,
+            "steps": len(dts), "warmup": args.warmup, "ms_per_step": 1000.0 * step_s,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (workloads.gen, seeded)",
             "config": {"workload": WORKLOAD, "layers": LAYERS, "tokens_per_step": T_DECODE, "adapters": 32,
                        "parallelism": "dp%d" % world},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
-                             "sample": "1 of 32 layers (4 applies x 64 tokens) per step, extrapolated x32; %.1f s" % secs},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": n_threads, "kind": "oracle", "cpu_model": _cpu_model(),
+                             "sample": "per step: 1 of 32 layers (4 applies x 64 tokens), median of %d steps, "
+                                       "extrapolated x32; %.1f s of CPU work" % (len(dts), sum(dts))},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
