@@ -95,12 +95,6 @@ typedef enum {
                                       loaded this way the steady-state decode apply was 7 % slower
                                       (unexplained). */
 
-#define LORA_OPT_PREFILL_TWO_PHASE 7   /* tensor-core (prefill) segments of a bf16 pool with hidden_out % 256
-                                      == 0: 0 = one kernel per 128-token tile (shrink, V, expand);
-                                      1 = two phases: V = bf16(s·x·A) per tile (split-K clusters when the
-                                      batch has few tiles), then the persistent 2-CTA GEMM adds V·B to y
-                                      over (tile pair, 256-column) items on every SM (DESIGN.md §6 N2). */
-
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.
  *   hidden_in, hidden_out  H_in, H_out of the adapted projection (Eq. 1's H1, H2).

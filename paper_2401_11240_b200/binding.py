@@ -23,7 +23,6 @@ LORA_POOL_HOST_ONLY = 1
 LORA_KIND_NONE, LORA_KIND_DECODE, LORA_KIND_PREFILL = -1, 0, 1
 LORA_OPT_TC_THRESHOLD, LORA_OPT_RESERVE_TOKENS = 1, 2
 LORA_OPT_PAD_MAX_RANK, LORA_OPT_LOAD_KERNEL = 5, 6
-LORA_OPT_PREFILL_TWO_PHASE = 7
 LORA_MAX_RANK = 256
 
 STATUS = {0: "LORA_OK", 1: "LORA_ERR_ARG", 2: "LORA_ERR_SHAPE", 3: "LORA_ERR_ALIGN",

@@ -46,15 +46,8 @@ constexpr int kFgAStages = FG_ASTAGES;   // V items: A-row ring depth
 constexpr int kFgStageBytes = 32768;   // per CTA: A chunk (x or V) 16 KB + B chunk (W or B_g) 16 KB
 constexpr int kFgAStageBytes = 8192;   // V items: this CTA's half of the adapter's A rows (<= 64 x 128 B)
 constexpr int kFgEpiBytes = 4 * 2 * 2048;   // per epilogue warp: two 32-row x 64-B staging slots
-constexpr int kFgBarBytes = 512;
-constexpr int kFgSmem = 1024 + kFgStages * kFgStageBytes + kFgAStages * kFgAStageBytes + kFgEpiBytes + kFgBarBytes;
+constexpr int kFgSmem = 1024 + kFgStages * kFgStageBytes + kFgAStages * kFgAStageBytes + kFgEpiBytes + 256;
 static_assert(kFgSmem <= 232448, "opt-in shared memory");
-// delta mode (two-phase prefill: y += V·B, K = the rank only): a 2-stage ring; each epilogue warp
-// double-buffers its 32 rows x 256 columns of y (16 KB per buffer: 8 SW64 chunks of 32 x 32)
-constexpr int kFgStagesD = 2;
-constexpr int kFgYWarpBytes = 16384;
-constexpr int kFgSmemD = 1024 + kFgStagesD * kFgStageBytes + 2 * 4 * kFgYWarpBytes + kFgBarBytes;
-static_assert(kFgSmemD <= 232448, "opt-in shared memory (delta)");
 constexpr int kFgPairWords = 10;
 #ifndef FG_B_KMAJOR
 #define FG_B_KMAJOR 0   // experiment builds: 1 = W given as W^T [H_out][H_in] (nn.Linear layout), K-major B
@@ -66,7 +59,6 @@ struct FgArgs {
     CUtensorMap tm_v;   // V tiles [n_vtiles * 128][Rv], box {64, 128}, SW128
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1} (gather4)
     CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1} (gather4): the V items' shrink
-    CUtensorMap tm_y;   // delta mode: y [T][H_out], box {32, 32}, SWIZZLE_64B (loads and stores)
     char* y;
     const char* box_maps;   // the pool's page arrays as 2D boxes {64, 8 << k}: A maps k, then B maps kBoxKinds + k
     char* vtiles;       // V tiles [n_vtiles * 128][v_cols] bf16, written by the V items
@@ -181,17 +173,6 @@ __device__ __forceinline__ void fg_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-// tcgen05.ld without the wait (the caller waits once for several loads)
-__device__ __forceinline__ void fg_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
-        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-}
 }  // namespace
 
 // work item w -> (token pair p, column tile ct, computes V?).  Pairs with an adapter come first
@@ -252,32 +233,28 @@ __device__ __forceinline__ void fg_load_rows(uint32_t dst, const char* box_maps,
     }
 }
 
-template <bool DELTA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
     lora_fused_gemm_kernel(const __grid_constant__ FgArgs a, const __grid_constant__ FgBlob blob) {
-    constexpr int NS = DELTA ? kFgStagesD : kFgStages;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = fg_smem(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;   // SW128 atoms need 1 KB alignment
     uint8_t* gbase = smem_raw + (base - raw);
     const uint32_t ring = base;
-    const uint32_t aring = base + NS * kFgStageBytes;              // V items: adapter A rows, kFgAStages x 8 KB
+    const uint32_t aring = base + kFgStages * kFgStageBytes;       // V items: adapter A rows, kFgAStages x 8 KB
     const uint32_t epi = aring + kFgAStages * kFgAStageBytes;
-    const uint32_t ybuf = base + NS * kFgStageBytes;               // delta mode: [2 buffers][4 warps][16 KB]
-    const uint32_t bars = DELTA ? ybuf + 8 * kFgYWarpBytes : epi + kFgEpiBytes;
+    const uint32_t bars = epi + kFgEpiBytes;
     auto full = [&](int s) { return bars + 8u * s; };                       // leader's is the live one
-    auto empty = [&](int s) { return bars + 8u * (NS + s); };                // both CTAs (MMA commit multicast)
-    auto tfull = [&](int b) { return bars + 8u * (2 * NS + b); };            // both CTAs
-    auto tempty = [&](int b) { return bars + 8u * (2 * NS + 2 + b); };       // leader: both epilogues arrive
-    auto afull = [&](int s) { return bars + 8u * (2 * NS + 4 + s); };       // leader
-    auto aempty = [&](int s) { return bars + 8u * (2 * NS + 4 + kFgAStages + s); };   // both CTAs
-    constexpr int kB0 = 2 * NS + 4 + 2 * kFgAStages;
+    auto empty = [&](int s) { return bars + 8u * (kFgStages + s); };         // both CTAs (MMA commit multicast)
+    auto tfull = [&](int b) { return bars + 8u * (2 * kFgStages + b); };     // both CTAs
+    auto tempty = [&](int b) { return bars + 8u * (2 * kFgStages + 2 + b); };   // leader: both epilogues arrive
+    auto afull = [&](int s) { return bars + 8u * (2 * kFgStages + 4 + s); };    // leader
+    auto aempty = [&](int s) { return bars + 8u * (2 * kFgStages + 4 + kFgAStages + s); };   // both CTAs
+    constexpr int kB0 = 2 * kFgStages + 4 + 2 * kFgAStages;
     const uint32_t d1full = bars + 8u * kB0;                  // both CTAs
     const uint32_t vsm_full = bars + 8u * (kB0 + 1);          // leader: both CTAs' V in SMEM
     const uint32_t vsm_free = bars + 8u * (kB0 + 2);          // both CTAs: V-item rank MMAs done
-    auto ybar = [&](int bf, int w) { return bars + 8u * (kB0 + 3 + bf * 4 + w); };   // delta: y rows landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (kB0 + 11) - base));
-    static_assert(8 * (kB0 + 11) + 4 <= kFgBarBytes, "barrier block");
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (kB0 + 3) - base));
+    static_assert(8 * (kB0 + 3) + 4 <= 256, "barrier block");
     // a V item's V (128 rows x rank, bf16 K-major SW128, two 64-column atoms) lives in the A-row ring
     // and the epilogue staging (contiguous 32 KB; both idle then) for its own rank K steps
     const uint32_t vsm = aring;
@@ -287,10 +264,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
     const uint32_t crank = fg_cta_rank();
     const bool leader = crank == 0;
     const int cluster = blockIdx.x >> 1;
-    const int nkc = DELTA ? 0 : a.H_in / 64;   // x·W chunks (none in delta mode)
+    const int nkc = a.H_in / 64;
 
     if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
+        for (int s = 0; s < kFgStages; ++s) {
             fg_bar_init(full(s), 1);
             fg_bar_init(empty(s), 1);
         }
@@ -305,7 +282,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
         fg_bar_init(d1full, 1);
         fg_bar_init(vsm_full, 2);
         fg_bar_init(vsm_free, 1);
-        for (int i = 0; i < 8; ++i) fg_bar_init(ybar(i >> 2, i & 3), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {   // both CTAs: two 256-column fp32 accumulators
@@ -346,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
             // lane 1 owns the V-tile flag, its fences and the V-tile TMA loads: lane 0 has TMA loads in
             // flight, which a proxy fence on lane 0 would wait for
             int vf = 0;
-            if (!DELTA && !itm.vit && r > 0 && lane == 1) vf = fg_ld_relaxed(vflag + vtile);
+            if (!itm.vit && r > 0 && lane == 1) vf = fg_ld_relaxed(vflag + vtile);
             // the rank chunks' operands are read ~20 us from now: into L2 at the item's start (V tile rows
             // -- stale lines are harmless, the V stores update L2 -- and a contiguous adapter's B rows)
             if (r > 0 && lane == 0) {
@@ -360,7 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
             }
             if (itm.vit && nvi++ > 0) fg_wait(vsm_free, (uint32_t)((nvi - 2) & 1));   // previous V item's V read
             for (int kc = 0; kc < nch; ++kc) {
-                if (!DELTA && kc == nkc && !itm.vit && lane == 1) {
+                if (kc == nkc && !itm.vit && lane == 1) {
                     while (vf != epoch) {
                         __nanosleep(64);
                         vf = fg_ld_relaxed(vflag + vtile);
@@ -409,7 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
                                      blob.w + poff, e * 64, rows, r, a.zero_page, cbar, lane);
                 }
                 __syncwarp();
-                if (++stage == NS) { stage = 0; phase ^= 1u; }
+                if (++stage == kFgStages) { stage = 0; phase ^= 1u; }
             }
         }
     } else if (warp == 1) {
@@ -485,14 +461,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
                             av = v0 + (uint64_t)e * (16384 >> 4);
                         }
                         const int ks = min(4, (rp - e * 64) / 16);
-                        for (int kk = 0; kk < ks; ++kk) fg_mma2(dacc, av + 2 * kk, bd + 128 * kk, kIdB, (kc | kk) != 0);
+                        for (int kk = 0; kk < ks; ++kk) fg_mma2(dacc, av + 2 * kk, bd + 128 * kk, kIdB, 1u);
                         if (itm.vit && kc == nch - 1) fg_commit2(vsm_free);
                     }
                     fg_commit2(empty(stage));
                     if (kc == nch - 1) fg_commit2(tfull(b));
                     if (trc && lane == 0 && kc == nkc - 1) trc[1] = fg_gtime();
                     __syncwarp();
-                    if (++stage == NS) { stage = 0; phase ^= 1u; }
+                    if (++stage == kFgStages) { stage = 0; phase ^= 1u; }
                 }
             }
         }
@@ -505,120 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
         const uint32_t lvsmfull = fg_mapa(vsm_full, 0);
         uint8_t* stg0 = gbase + (epi - base) + sub * 4096;
         int it = 0, nd = 0;
-        if constexpr (DELTA) {
-            // y[rows][n0, n0 + 256) += D: this warp's 32 rows x 256 columns of y arrive by TMA (8 SW64
-            // chunks of 32 x 32) one item ahead in a double buffer, take D with one rounding in place
-            // (thread = row), and leave by TMA store -- or by plain stores for the valid rows of a warp
-            // whose 32 rows run past the segment (the next segment's rows are another item's).
-            auto wrows = [&](int w2) {   // valid rows of this warp in item w2
-                const FgItem i2 = fg_item(w2, a.n_vp, a.n_ctiles);
-                const int32_t* r2 = blob.w + i2.p * kFgPairWords;
-                const int nv = crank == 0 ? r2[2] : (r2[4] == 0 ? 0 : r2[4]);
-                return min(max(nv - sub * 32, 0), 32);
-            };
-            auto issue_y = [&](int w2, int bf) {   // lane 0
-                if (w2 >= a.n_items || wrows(w2) == 0) return;
-                const FgItem i2 = fg_item(w2, a.n_vp, a.n_ctiles);
-                const int32_t* r2 = blob.w + i2.p * kFgPairWords;
-                const int t0 = crank == 0 ? r2[1] : r2[3];
-                const uint32_t yb = ybuf + (uint32_t)(bf * 4 + sub) * kFgYWarpBytes;
-                fg_arrive_tx(ybar(bf, sub), (uint32_t)kFgYWarpBytes);
-                for (int c = 0; c < 8; ++c)
-                    asm volatile(
-                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                            yb + (uint32_t)c * 2048u),
-                        "l"(&a.tm_y), "r"(i2.ct * 256 + c * 32), "r"(t0 + sub * 32), "r"(ybar(bf, sub))
-                        : "memory");
-            };
-            if (lane == 0) {
-                issue_y(cluster, 0);
-                issue_y(cluster + a.n_clusters, 1);
-            }
-            uint32_t ycnt[2] = {0u, 0u};
-            for (int w = cluster; w < a.n_items; w += a.n_clusters, ++it) {
-                const FgItem itm = fg_item(w, a.n_vp, a.n_ctiles);
-                const int32_t* rec = blob.w + itm.p * kFgPairWords;
-                const int tok0 = crank == 0 ? rec[1] : rec[3];
-                const int b = it & 1, bf = it & 1;
-                const int v = wrows(w);
-                fg_wait(tfull(b), (uint32_t)((it >> 1) & 1));
-                fg_fence_after();
-                unsigned long long* trc = a.trace && leader && it < 64 ? a.trace + ((size_t)cluster * 64 + it) * 4 : nullptr;
-                if (trc && tid == 64) trc[2] = fg_gtime();
-                uint8_t* yb = gbase + (ybuf - base) + (bf * 4 + sub) * kFgYWarpBytes;
-                if (v > 0) {
-                    fg_wait(ybar(bf, sub), ycnt[bf] & 1u);
-                    ++ycnt[bf];
-                }
-                const int n0 = itm.ct * 256;
-#pragma unroll 1
-                for (int c2 = 0; c2 < 8; c2 += 2) {
-                    // two 32-column TMEM loads in flight per wait
-                    uint32_t dr[2][32];
-                    fg_ld32_nowait(tmem + lane_addr + (uint32_t)b * 256u + (uint32_t)(c2 * 32), dr[0]);
-                    fg_ld32_nowait(tmem + lane_addr + (uint32_t)b * 256u + (uint32_t)(c2 * 32 + 32), dr[1]);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                    const int c = c2 + h;
-                    float d[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) d[i] = __uint_as_float(dr[h][i]);
-                    if (lane < v) {
-                        // SW64: 16-B chunk q of row `lane` at lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)
-                        uint8_t* rowp = yb + c * 2048 + lane * 64;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint4* pp = reinterpret_cast<uint4*>(rowp + ((q ^ ((lane >> 1) & 3)) << 4));
-                            const uint4 yv = *pp;
-                            const uint32_t wv[4] = {yv.x, yv.y, yv.z, yv.w};
-                            uint32_t o[4];
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float lo = __uint_as_float(wv[e] << 16) + d[q * 8 + 2 * e];
-                                const float hi = __uint_as_float(wv[e] & 0xffff0000u) + d[q * 8 + 2 * e + 1];
-                                __nv_bfloat162 hb = __floats2bfloat162_rn(lo, hi);
-                                o[e] = *reinterpret_cast<uint32_t*>(&hb);
-                            }
-                            *pp = make_uint4(o[0], o[1], o[2], o[3]);
-                        }
-                    }
-                    }
-                }
-                // the accumulator is drained: release it to the MMA warp
-                fg_fence_before();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (tid == 64) fg_arrive_cluster(ltempty0 + 8u * (uint32_t)b);
-                if (v == 32) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
-                    __syncwarp();
-                    if (lane == 0) {
-                        for (int c = 0; c < 8; ++c)
-                            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                                             &a.tm_y),
-                                         "r"(n0 + c * 32), "r"(tok0 + sub * 32),
-                                         "r"(ybuf + (uint32_t)(bf * 4 + sub) * kFgYWarpBytes + (uint32_t)c * 2048u)
-                                         : "memory");
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    }
-                } else if (v > 0 && lane < v) {
-                    for (int c = 0; c < 8; ++c)
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            *reinterpret_cast<uint4*>(a.y + ((size_t)(tok0 + sub * 32 + lane) * a.H_out + n0 + c * 32 + q * 8) * 2) =
-                                *reinterpret_cast<const uint4*>(yb + c * 2048 + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4));
-                }
-                __syncwarp();
-                // the buffer is refilled with item it + 2 once its stores have read it
-                if (lane == 0) {
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    issue_y(w + 2 * a.n_clusters, bf);
-                }
-                if (trc && tid == 64) trc[3] = fg_gtime();
-            }
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        }
-        for (int w = cluster; !DELTA && w < a.n_items; w += a.n_clusters, ++it) {
+        for (int w = cluster; w < a.n_items; w += a.n_clusters, ++it) {
             const FgItem itm = fg_item(w, a.n_vp, a.n_ctiles);
             const int32_t* rec = blob.w + itm.p * kFgPairWords;
             const bool solo = rec[4] == 0;
@@ -736,43 +599,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
 
 int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);   // prefill_kernel.cu
 
-// 2D bf16 tensor map [rows][cols] with a {32, 32} SWIZZLE_64B box (delta mode's y tiles)
-static int make_tmap_y64(void* tm_out, const void* base, int64_t rows, int64_t cols) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        void* fp = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
-    }
-    if (!enc) return (int)cudaErrorNotSupported;
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {32, 32};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(reinterpret_cast<CUtensorMap*>(tm_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-                     dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
-}
-
 int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_words, int n_pairs, int num_sms,
                       lora_cuda_stream st) {
     if (n_words > kFusedBaseMaxWords || n_pairs <= 0 || L.H_out % 256 || L.H_in % 64) return (int)cudaErrorInvalidValue;
     if (L.n_vp > 0 && (!L.vtiles || !L.vsync)) return (int)cudaErrorInvalidValue;
-    if (L.delta && (!L.vtiles || L.n_vp > 0)) return (int)cudaErrorInvalidValue;
     FgArgs a;
     std::memset(&a, 0, sizeof(a));
     int e = make_tmap_bf16(&a.tm_x, L.x, L.T, L.H_in, 128);
 #if FG_B_KMAJOR
     if (!e) e = make_tmap_bf16(&a.tm_w, L.w, L.H_out, L.H_in, 128);   // experiment: W^T [H_out][H_in]
 #else
-    if (!e) e = make_tmap_bf16(&a.tm_w, L.delta ? L.y : L.w, L.delta ? L.T : L.H_in, L.H_out, 64);   // (delta: unused)
+    if (!e) e = make_tmap_bf16(&a.tm_w, L.w, L.H_in, L.H_out, 64);
 #endif
-    if (!e && (L.n_vp > 0 || L.delta)) e = make_tmap_bf16(&a.tm_v, L.vtiles, (int64_t)L.n_vtiles * 128, L.v_cols, 128);
+    if (!e && L.n_vp > 0) e = make_tmap_bf16(&a.tm_v, L.vtiles, (int64_t)L.n_vtiles * 128, L.v_cols, 128);
     else if (!e) e = make_tmap_bf16(&a.tm_v, L.x, L.T, L.H_in, 128);   // (no adapter: never loaded)
-    if (!e && L.delta) e = make_tmap_y64(&a.tm_y, L.y, L.T, L.H_out);
     if (e) return e;
     std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
     std::memcpy(&a.tm_a, L.tm_a, sizeof(CUtensorMap));
@@ -798,24 +638,21 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
     if (cudaGetDevice(&dev) != cudaSuccess) return (int)cudaErrorInvalidDevice;
     const uint64_t bit = dev < 64 ? 1ull << dev : 0ull;
     if (!bit || !(configured.load(std::memory_order_acquire) & bit)) {
-        cudaError_t ce = cudaFuncSetAttribute(lora_fused_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFgSmem);
-        if (ce == cudaSuccess)
-            ce = cudaFuncSetAttribute(lora_fused_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFgSmemD);
+        cudaError_t ce = cudaFuncSetAttribute(lora_fused_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFgSmem);
         if (ce != cudaSuccess) return (int)ce;
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.n_ctas);
     cfg.blockDim = dim3(kFgThreads);
-    cfg.dynamicSmemBytes = L.delta ? kFgSmemD : kFgSmem;
+    cfg.dynamicSmemBytes = kFgSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)(L.delta ? cudaLaunchKernelEx(&cfg, lora_fused_gemm_kernel<true>, a, blob)
-                         : cudaLaunchKernelEx(&cfg, lora_fused_gemm_kernel<false>, a, blob));
+    return (int)cudaLaunchKernelEx(&cfg, lora_fused_gemm_kernel, a, blob);
 }
 
 }  // namespace lora

@@ -117,8 +117,6 @@ struct PrefillLaunch {
     unsigned long long* trace;
     int T, H_in, H_out, zero_page, num_sms;
     float* pscratch = nullptr;   // split-K partials: [CTA][128 rows][128] fp32 (L2-resident exchange)
-    void* vtiles = nullptr;      // V-out mode (two-phase prefill's V pass): [token tiles * 128][v_cols] bf16
-    int v_cols = 0;              // 64 or 128
 };
 
 // Concatenates the SIMT work lists of plans[0..n) (one per fused pool = job index) into merged
@@ -152,7 +150,6 @@ struct FusedBaseLaunch {
     int* vsync = nullptr;             // [2 + n_vtiles] ints, zero-initialised once, persistent (launch epochs)
     int n_vtiles = 0, v_cols = 0, n_vp = 0;   // n_vp: pairs with an adapter (ordered first)
     unsigned long long* trace = nullptr;      // lora_debug_set_trace buffer, or null
-    int delta = 0;                            // 1: y += V·B only (the two-phase prefill's second pass; W unused)
 };
 // words: [n_pairs][10] pair records {vtile, tok0_a, nvalid_a, tok0_b, nvalid_b (0: no partner), rank,
 // page_off, scale_bits, first_page (-1: fragmented), 0}, then page lists (fused_base_kernel.cu)

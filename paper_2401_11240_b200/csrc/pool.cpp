@@ -55,9 +55,6 @@ struct lora_pool {
     size_t fb_vtiles_cap = 0;
     int* fb_vsync = nullptr;             // lora_apply_fused_base: launch epochs + per-V-tile flags (zeroed once)
     size_t fb_vsync_cap = 0;
-    int prefill_two_phase = 0;           // LORA_OPT_PREFILL_TWO_PHASE: V pass + persistent delta GEMM
-    uint16_t* pf_vtiles = nullptr;       // two-phase prefill: V tiles (bf16, grown on demand)
-    size_t pf_vtiles_cap = 0;
     size_t vbuf_cap = 0;                 // floats
     int32_t* meta_dev = nullptr;
     size_t meta_cap = 0;                 // words
@@ -284,7 +281,6 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->pf_scratch) cudaFree(p->pf_scratch);
         if (p->fb_vtiles) cudaFree(p->fb_vtiles);
         if (p->fb_vsync) cudaFree(p->fb_vsync);
-        if (p->pf_vtiles) cudaFree(p->pf_vtiles);
         if (p->meta_dev) cudaFree(p->meta_dev);
         for (void* b : p->retired) cudaFree(b);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
@@ -447,119 +443,6 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     return LORA_OK;
 }
 
-// The tensor-core (prefill) part of a planned apply.  One phase: the N2 kernel (per 128-token tile:
-// shrink, V, expand).  Two phases (LORA_OPT_PREFILL_TWO_PHASE, hidden_out % 256 == 0): the N2 kernel
-// in V-out mode writes V = bf16(s·x·A) per tile (split-K clusters when there are few tiles), then the
-// persistent 2-CTA GEMM in delta mode adds V·B to y over (tile pair, 256-column) items balanced on
-// every SM (DESIGN.md §6 N2).
-static lora_status launch_prefill_path(lora_pool* p, const Plan& pl, const void* x, void* y, int T, cudaStream_t st,
-                                       int* launches) {
-    lora_status s = LORA_OK;
-    if (!(p->prefill_two_phase && p->H_out % 256 == 0)) {
-        if (pl.pf_cs > 1 &&
-            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
-            return s;
-        PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
-        L.pscratch = p->pf_scratch;
-        cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, launches);
-        return e == cudaSuccess ? LORA_OK : cuda_fail(e, "lora_apply: prefill kernel launch");
-    }
-    static thread_local Plan vplan;   // the V pass: per token tile, cs CTAs (split-K when few tiles)
-    static thread_local std::vector<int32_t> words, pages;
-    static thread_local std::vector<std::pair<int32_t, int32_t>> goff;   // (group, page offset)
-    int n_tiles = 0, max_rp = 0;
-    for (const PrefillSeg& sg : pl.prefill) {
-        n_tiles += (sg.len + 127) / 128;
-        max_rp = std::max(max_rp, (pl.group_rank[sg.group] + 15) & ~15);
-    }
-    // the planner's split-K factor (the one-phase kernel's): both paths sum the same partials in the
-    // same order, so the path choice never changes a result bit
-    int cs = std::max(1, pl.pf_cs);
-    while (cs > 1 && (n_tiles * cs * 8 + (int)pl.pages.size() > kPfMaxBlobWords)) --cs;
-    const int v_cols = max_rp > 64 ? 128 : 64;
-    vplan.reset();
-    vplan.pf_blob.assign((size_t)n_tiles * cs * 8, 0);
-    pages.clear();
-    goff.clear();
-    int n_pairs = 0;
-    for (const PrefillSeg& sg : pl.prefill) n_pairs += (sg.len + 255) / 256;
-    words.assign((size_t)n_pairs * 10, 0);
-    int vt = 0, pix = 0;
-    for (const PrefillSeg& sg : pl.prefill) {
-        const int g = sg.group, r = pl.group_rank[g];
-        int off = -1;
-        for (const auto& o : goff)
-            if (o.first == g) off = o.second;
-        if (off < 0) {
-            off = (int)pages.size();
-            goff.emplace_back(g, off);
-            pages.insert(pages.end(), pl.pages.begin() + pl.group_page_off[g], pl.pages.begin() + pl.group_page_off[g] + r);
-        }
-        const int32_t* gp = pl.pages.data() + pl.group_page_off[g];
-        bool run = true;
-        for (int j = 1; j < r && run; ++j) run = gp[j] == gp[0] + j;
-        int32_t sb;
-        std::memcpy(&sb, &pl.group_scale[g], 4);
-        const int vt0 = vt;
-        for (int t0 = 0; t0 < sg.len; t0 += 128, ++vt)
-            for (int c = 0; c < cs; ++c) {
-                int32_t* rec = vplan.pf_blob.data() + ((size_t)vt * cs + c) * 8;
-                rec[0] = sg.tok0 + t0;
-                rec[1] = std::min(128, sg.len - t0);
-                rec[2] = r;
-                rec[3] = off;   // relocated below
-                rec[4] = sb;
-                rec[5] = run ? gp[0] : -1;
-                rec[6] = 1;     // no expand column tiles: V-out only
-                rec[7] = 1;
-            }
-        for (int t0 = 0; t0 < sg.len; t0 += 256, ++pix) {
-            int32_t* rec = words.data() + (size_t)pix * 10;
-            rec[0] = vt0 + t0 / 128;
-            rec[1] = sg.tok0 + t0;
-            rec[2] = std::min(128, sg.len - t0);
-            rec[3] = sg.len - t0 > 128 ? sg.tok0 + t0 + 128 : 0;
-            rec[4] = sg.len - t0 > 128 ? std::min(128, sg.len - t0 - 128) : 0;
-            rec[5] = r;
-            rec[6] = off;   // relocated below
-            rec[7] = sb;
-            rec[8] = run ? gp[0] : -1;
-            rec[9] = 0;
-        }
-    }
-    const int vrec = n_tiles * cs * 8;
-    for (int i = 0; i < n_tiles * cs; ++i) vplan.pf_blob[(size_t)i * 8 + 3] += vrec;
-    vplan.pf_blob.insert(vplan.pf_blob.end(), pages.begin(), pages.end());
-    for (int i = 0; i < n_pairs; ++i) words[(size_t)i * 10 + 6] += n_pairs * 10;
-    words.insert(words.end(), pages.begin(), pages.end());
-    if ((int)vplan.pf_blob.size() > kPfMaxBlobWords || (int)words.size() > kFusedBaseMaxWords)
-        return fail(LORA_ERR_UNSUPPORTED, "prefill batch too large for the two-phase path's parameter blobs");
-    vplan.n_pf_tiles = n_tiles * cs;
-    vplan.pf_cs = cs;
-    if ((s = grow(p, p->pf_vtiles, p->pf_vtiles_cap, (size_t)n_tiles * 128 * v_cols, false, "prefill V tiles")) != LORA_OK)
-        return s;
-    if (cs > 1 &&
-        (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)n_tiles * cs * 128 * 128, false, "pf_scratch")) != LORA_OK)
-        return s;
-    PrefillLaunch PL{x, y, p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
-    PL.pscratch = p->pf_scratch;
-    PL.vtiles = p->pf_vtiles;
-    PL.v_cols = v_cols;
-    cudaError_t e = (cudaError_t)launch_prefill(vplan, PL, st, launches);
-    if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill V pass launch");
-    FusedBaseLaunch L{x, nullptr, y, p->tm_a, p->tm_b, T, p->H_in, p->H_out, p->n_pages};
-    L.box_maps = p->box_maps;
-    L.vtiles = p->pf_vtiles;
-    L.n_vtiles = n_tiles;
-    L.v_cols = v_cols;
-    L.delta = 1;
-    L.trace = p->trace;
-    e = (cudaError_t)launch_fused_base(L, words.data(), (int)words.size(), n_pairs, p->num_sms, st);
-    if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill delta GEMM launch");
-    *launches += 1;
-    return LORA_OK;
-}
-
 // mode 0: full apply; 1: shrink only (partial v -> v_ext); 2: expand only (v_ext -> y, plan of the
 // last shrink).  Modes 1/2 serve tensor parallelism: the caller all-reduces v in between.
 static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_t* seg_indptr,
@@ -657,8 +540,15 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         cudaError_t e = (cudaError_t)launch_decode(pl, L, st, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "lora_apply: decode kernel launch");
     }
-    if (pl.n_pf_tiles > 0 && mode == 0)
-        if ((s = launch_prefill_path(p, pl, x, y, T, st, &launches)) != LORA_OK) return s;
+    if (pl.n_pf_tiles > 0 && mode == 0) {
+        if (pl.pf_cs > 1 &&
+            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
+            return s;
+        PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
+        L.pscratch = p->pf_scratch;
+        cudaError_t e = (cudaError_t)launch_prefill(pl, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply: prefill kernel launch");
+    }
     p->launches += launches;
     if (std::find(p->apply_streams.begin(), p->apply_streams.end(), st) == p->apply_streams.end())
         p->apply_streams.push_back(st);
@@ -737,7 +627,15 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
         if (p->plan.n_pf_tiles == 0) continue;
-        if ((s = launch_prefill_path(p, p->plan, xs[i], ys[i], T, st, &launches)) != LORA_OK) return s;
+        if (p->plan.pf_cs > 1 &&
+            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * 128, false, "pf_scratch")) !=
+                LORA_OK)
+            return s;
+        PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
+                        p->num_sms};
+        L.pscratch = p->pf_scratch;
+        cudaError_t e = (cudaError_t)launch_prefill(p->plan, L, st, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "lora_apply_multi: prefill kernel launch");
     }
     p0->launches += launches;
     for (int i = 0; i < n_pools; ++i)
@@ -1022,10 +920,6 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
         case LORA_OPT_LOAD_KERNEL:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_LOAD_KERNEL takes 0 or 1");
             p->load_kernel = value == 1;
-            return LORA_OK;
-        case LORA_OPT_PREFILL_TWO_PHASE:
-            if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_PREFILL_TWO_PHASE takes 0 or 1");
-            p->prefill_two_phase = (int)value;
             return LORA_OK;
         case LORA_OPT_PAD_MAX_RANK:
             if (value != 0 && value != 1) return fail(LORA_ERR_ARG, "LORA_OPT_PAD_MAX_RANK takes 0 or 1");

@@ -47,7 +47,6 @@ struct PrefillArgs {
     CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads; writes go per row)
-    CUtensorMap tm_v;   // V-out mode: V tiles [n_tiles * 128][Rv], box {64, 128}, SW128 (the fused GEMM's A rows)
     const char* box_maps;   // pool page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), SW128
     int cs;                 // cluster size: the cs CTAs of a token tile split its shrink K and its columns
     float* pscratch;        // split-K partials [CTA][128][128] fp32 (L2-resident exchange)
@@ -55,7 +54,6 @@ struct PrefillArgs {
     const int32_t* meta_global;
     unsigned long long* trace;
     int H_in, H_out, n_tiles, zero_page;
-    int vout;           // 1: shrink only -- V = s·x·A of tile i (bf16, K-major SW128) is stored to V tile i
 };
 
 template <int W>
@@ -451,20 +449,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         tc_fence_before();
         pf_arrive(v_ready);
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 3] = pf_gtime();
-        if (a.vout) {
-            // V-out mode (the two-phase prefill's V pass): the V atoms leave by TMA store to the token
-            // tile's own 128-row block of the V tiles (tile-private rows: no overlap between segments);
-            // in a split-K cluster every CTA holds the summed V, rank 0 stores it
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (tid == 64 && ck == 0) {
-                for (int kk = 0; kk * 64 < rp; ++kk)
-                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&a.tm_v),
-                                 "r"(kk * 64), "r"((tile / cs) * 128), "r"(vhi + (uint32_t)kk * 16384u)
-                                 : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-            }
-        }
         // ---- per expand tile: y[row][n0 .. n0+128) += D2 (one rounding).  y tiles are staged
         //      by TMA one tile ahead (2 slots, SW128: row at (row/8)*1024 + (row%8)*128 per 64-col
         //      half, 16-B chunk c at c ^ (row%8)); results go straight to global, valid rows only
@@ -647,10 +631,6 @@ int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int*
     a.pscratch = L.pscratch;
     if (a.cs > 1 && !a.pscratch) return (int)cudaErrorInvalidValue;
     a.zero_page = L.zero_page;
-    if (L.vtiles) {
-        a.vout = 1;
-        if ((e = make_tmap_bf16(&a.tm_v, L.vtiles, (int64_t)(pl.n_pf_tiles / a.cs) * 128, L.v_cols, 128))) return e;
-    }
     const size_t n = pl.pf_blob.size();
     cudaError_t r;
     if (n <= 2048) r = launch_pf<2048>(a, pl, st);
