@@ -663,6 +663,11 @@ def bench_c5(L, dev, reps: int, hbm_peak: float, world: int = 1, rank: int = 0, 
                      library's communicator.  With one GPU (this run) the communicator is world-1 (its
                      all-reduce is a local no-op); under torchrun with N GPUs the tp = N row runs the
                      real N-rank all-reduce over NVLink, timed as the max over ranks.
+      nocomm:        the scheme without a collective: column-parallel shapes (q, kv, gate_up)
+                     keep A whole and split B by output columns (the paper's scheme); the row-parallel
+                     shape (down) splits A with its x shard and keeps B whole, adding the full-width delta of
+                     its partial v into the partial y that the base layer's own all-reduce completes
+                     (linearity) -- more adapter bytes per GPU, no exchange.  `pick` names the faster.
     Device time per apply from a CUDA graph over enough distinct pools that the adapter rows exceed L2."""
     import torch
     from paper_2401_11240_b200.binding import TPComm
@@ -715,6 +720,31 @@ def bench_c5(L, dev, reps: int, hbm_peak: float, world: int = 1, rank: int = 0, 
                 if use_dist:
                     us_k = max_over_ranks(us_k, True)
                     us_tp = max_over_ranks(us_tp, True)
+                # the scheme without a collective: plain lora_apply on the wider shard
+                row_par = name == "down"
+                nhi, nho = (hi, H_out) if row_par else (H_in, ho)
+                nb = sum(ranks) * (nhi + nho) * 2
+                npools = max(2, -(-400_000_000 // nb))
+                npl = []
+                for _ in range(npools):
+                    pool = L.LoraPool(nhi, nho, 32, "bf16", max_total_rank=sum(ranks))
+                    for a, (A, B) in zip(full, pinned):
+                        pool.load_adapter_shard(a.id, a.rank, A, trank * hi if row_par else 0, B, 0 if row_par else trank * ho,
+                                                a.scale)
+                    npl.append(pool)
+                torch.cuda.synchronize()
+                xn = torch.randn(T, nhi).to(torch.bfloat16).to(dev)
+                yn = [torch.zeros(T, nho, dtype=torch.bfloat16, device=dev) for _ in npl]
+                us_n = _graph_us(lambda: [p.apply(xn, y, ip, ids, stream=st) for p, y in zip(npl, yn)], st, reps, npools)
+                if use_dist:
+                    us_n = max_over_ranks(us_n, True)
+                for pool in npl:
+                    pool.close()
+                del npl, yn
+                r.update({"nocomm": {"scheme": "A split, B whole, delta into the partial y" if row_par
+                                     else "A whole, B split (the paper's)",
+                                     "adapter_MB_per_gpu": round(nb / 1e6, 2), "us": round(us_n, 3)},
+                          "pick": "nocomm" if us_n < us_tp else "allreduce_v"})
                 r.update({"v_allreduce_bytes": int(nv * 4),
                           "shard_kernels_us": round(us_k, 3),
                           "shard_kernels_roofline_frac": round(byts / (us_k * 1e-6) / 1e9 / hbm_peak, 4),

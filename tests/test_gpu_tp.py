@@ -190,3 +190,39 @@ def test_split_apply_equals_fused_apply(torch_cuda):
     with pytest.raises(L.LoraError):
         pool.apply_expand(y2, v)             # no pending shrink
     pool.close()
+
+
+@pytest.mark.parametrize("proj,tp,kind", [("q", 4, "column"), ("down", 2, "row")])
+def test_tp_nocomm_schemes(torch_cuda, proj, tp, kind):
+    """The TP schemes without a collective (bench c5 `nocomm`).  Column-parallel: every
+    rank keeps A whole and B's output-column slice (the paper's scheme) -- its y slice is the
+    oracle's, exactly as an unsharded apply.  Row-parallel: rank k keeps A's rows of its x shard and B
+    whole and adds s·(x_k·A_k)·B into its partial y; the sum over ranks (the base layer's own
+    all-reduce, emulated) is the unsharded oracle's delta (linearity; each partial y is rounded once)."""
+    torch = torch_cuda
+    import paper_2401_11240_b200 as L
+    b = gen.config_c5(proj, y_zero=True)
+    ref = O.delta_for_batch(b, n_threads=16).reshape(b.T, b.H_out)
+    full = _pinned_full(b, torch)
+    x = to_torch(b.x, "cuda")
+    total = np.zeros((b.T, b.H_out))
+    got_cols = []
+    for k in range(tp):
+        hi, ho = (b.H_in // tp, b.H_out) if kind == "row" else (b.H_in, b.H_out // tp)
+        pool = L.LoraPool(hi, ho, 40, "bf16", max_total_rank=sum(a.rank for a in b.adapters) + 8)
+        for a in b.adapters:
+            A, B = full[a.id]
+            pool.load_adapter_shard(a.id, a.rank, A, k * hi if kind == "row" else 0, B, 0 if kind == "row" else k * ho,
+                                    a.scale)
+        xk = x[:, k * hi:(k + 1) * hi].contiguous() if kind == "row" else x
+        y = torch.zeros((b.T, ho), dtype=torch.int16, device="cuda")
+        pool.apply(xk, y, b.seg_indptr, b.adapter_ids)
+        torch.cuda.synchronize()
+        yk = gen.storage_to_f64(from_torch(y, "bf16"), "bf16").reshape(b.T, ho)
+        if kind == "row":
+            total += yk
+        else:
+            got_cols.append(yk)
+        pool.close()
+    got = total if kind == "row" else np.concatenate(got_cols, axis=1)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= TOL["bf16"]
