@@ -18,3 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lor
    python bench.py --layers 1 --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline --prefill-layers 1 --prefill-steps 2 --c4-steps 0 --c5-reps 0 \
    > gpurun_out/prof_prefill_$TAG.log 2>&1
 echo "prefill full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lora_fused_gemm" -s 2 -c 1 -f \
+   -o gpurun_out/prof_fused_$TAG \
+   python scripts/fused_base_bench.py > gpurun_out/prof_fused_$TAG.log 2>&1
+echo "fused full rc=$?"

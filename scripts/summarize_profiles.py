@@ -72,6 +72,8 @@ if __name__ == "__main__":
     agg = launches()
     dec = full("decode")
     pf = full("prefill")
+    if os.path.exists(os.path.join(ROOT, "gpurun_out", "prof_fused_%s.ncu-rep" % TAG)):
+        full("fused")
     # decode capture = one c2 layer step (scripts/ncu_decode_step.py): the q/k/v lora_apply_multi pair and
     # the o pair, i.e. 4 projection applies -> DRAM bytes per projection apply for bench.py's roofline
     rd = lambda v: v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)  # noqa  (bytes)
