@@ -31,14 +31,19 @@
 
 namespace lora {
 
-constexpr int kPfThreads = 192;        // warp 0: TMA producer, warp 1: MMA issuer, warps 2-5: epilogue
+// warp 0: TMA producer, warp 1: MMA issuer, warps 2-5 and 6-9: two epilogue groups (each the 128
+// TMEM lanes) taking the expand tiles alternately, one per TMEM accumulator buffer
+constexpr int kPfThreads = 320;
+constexpr int kPfEpiThreads = 256;
 constexpr int kPfStages = 3;           // expand-phase ring (B tiles)
 constexpr int kPfShrinkStages = 7;     // shrink-phase ring: the 3 ring stages + the V and y buffers, idle until D1 is done
 constexpr int kPfStageBytes = 32768;   // X chunk 16 KB + A chunk <= 16 KB, or one B tile (<= 32 KB)
 constexpr int kPfVBytes = 128 * 128 * 2;   // one V part (hi or lo): 128 tokens x r16 <= 128, bf16
 constexpr int kPfYBytes = 128 * 128 * 2;   // one staged y tile (128 tokens x 128 columns, bf16)
 constexpr int kPfYSlots = 3;               // staged y tiles in flight (the third lives in the unused V-lo space)
-constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 2 * kPfYBytes + 256;
+constexpr int kPfBarBytes = 512;
+constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 2 * kPfYBytes + kPfBarBytes;
+static_assert(kPfSmem <= 232448, "prefill smem");
 constexpr int kPfNTile = 128;          // expand columns per tile
 constexpr int kPfTileWords = 8;        // per-tile record in the metadata blob
 
@@ -46,7 +51,8 @@ struct PrefillArgs {
     CUtensorMap tm_x;   // x [T][H_in], box {64, 128}, SW128
     CUtensorMap tm_a;   // A pages [n_pages+1][H_in], box {64, 1}, SW128 (gather4)
     CUtensorMap tm_b;   // B pages [n_pages+1][H_out], box {64, 1}, SW128 (gather4)
-    CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads; writes go per row)
+    CUtensorMap tm_y;   // y [T][H_out], box {64, 128}, SW128 (staged reads)
+    CUtensorMap tm_y32; // y [T][H_out], box {64, 32}, SW128 (one epilogue warp's rows, TMA store)
     const char* box_maps;   // pool page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), SW128
     int cs;                 // cluster size: the cs CTAs of a token tile split its shrink K and its columns
     float* pscratch;        // split-K partials [CTA][128][128] fp32 (L2-resident exchange)
@@ -95,6 +101,12 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm,
         "%5, %6}], [%7];" ::"r"(dst),
         "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
         : "memory");
+}
+// smem -> global tensor store (bulk group of the issuing thread)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tm), "r"(src),
+                 "r"(c0), "r"(c1)
+                 : "memory");
 }
 // ---- cluster split-K helpers
 __device__ __forceinline__ uint32_t pf_cluster_rank() {
@@ -193,11 +205,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     auto tm_full = [&](int b) { return v_ready + 8u + 8u * b; };
     auto tm_empty = [&](int b) { return v_ready + 24u + 8u * b; };
     auto y_full = [&](int b) { return v_ready + 40u + 8u * b; };
+    auto y_empty = [&](int b) { return v_ready + 64u + 8u * b; };   // the 4 warps of the tile's group
     // split-K exchange (cs > 1): every peer's partial of the tile is in the L2 scratch
-    const uint32_t pready = bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 9);
+    const uint32_t pready = bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 12);
     uint32_t* tmem_slot =
-        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 11) - base));
-    static_assert(8 * (2 * kPfShrinkStages + 2 * kPfStages + 11) + 4 <= 256, "barrier region");
+        reinterpret_cast<uint32_t*>(gbase + (bars + 8u * (2 * kPfShrinkStages + 2 * kPfStages + 13) - base));
+    static_assert(8 * (2 * kPfShrinkStages + 2 * kPfStages + 13) + 4 <= kPfBarBytes, "barrier region");
 
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -228,13 +241,16 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             pf_bar_init(empty2(s), 1);
         }
         pf_bar_init(d1_full, 1);
-        pf_bar_init(v_ready, 128);
+        pf_bar_init(v_ready, kPfEpiThreads);
         pf_bar_init(pready, (uint32_t)cs);
         for (int b = 0; b < 2; ++b) {
             pf_bar_init(tm_full(b), 1);
             pf_bar_init(tm_empty(b), 128);
         }
-        for (int b = 0; b < kPfYSlots; ++b) pf_bar_init(y_full(b), 1);
+        for (int b = 0; b < kPfYSlots; ++b) {
+            pf_bar_init(y_full(b), 1);
+            pf_bar_init(y_empty(b), 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {   // TMEM: D1 at columns [0,128), D2 buffers at [128,256) and [256,384)
@@ -305,6 +321,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         // atom (kg, ng) at (ng * rp/8 + kg) * 1 KB; a gather4 fills 4 rows of one atom
         for (int q = 0; q < nnt; ++q) {
             const int nt = nt_lo + q;
+            // the y tile into slot q % 3 once the group that had tile q - 3 stored it
+            if (lane == 0) {
+                const int yb = q % kPfYSlots;
+                pf_wait(y_empty(yb), ((q / kPfYSlots) & 1) ^ 1u);
+                const uint32_t dst = yring + (uint32_t)yb * kPfYBytes;
+                pf_arrive_tx(y_full(yb), (uint32_t)kPfYBytes);
+                tma_2d(dst, &a.tm_y, nt * kPfNTile, tok0, y_full(yb));
+                tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(yb));
+            }
             pf_wait(empty2(stage), phase ^ 1u);
             const uint32_t sb = ring + stage * kPfStageBytes;
             if (lane == 0) {
@@ -370,12 +395,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
         }
     } else {
-        // ===================== epilogue: warps 2..5 -> TMEM lanes 32*(warp%4) .. +32 =====================
+        // ===================== epilogue: group eg = warps 2+4eg .. 5+4eg; warp w -> TMEM lanes 32*(w%4) .. +32
+        const int eg = (warp - 2) >> 2;
+        const int etid = tid - 64;   // 0 .. 255
         const int sub = warp & 3;
         const int row = sub * 32 + lane;   // token row within the tile
         const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
         // ---- v = s * D1 -> bf16, K-major SW128: atom kk = cols [64kk, 64kk+64), row at
-        //      (row/8)*1024 + (row%8)*128 inside the 16 KB atom, 16-B chunk c stored at c ^ (row%8)
+        //      (row/8)*1024 + (row%8)*128 inside the 16 KB atom, 16-B chunk c stored at c ^ (row%8).
+        //      The two groups take alternate 32-column chunks.
         pf_wait(d1_full, 0);
         tc_fence_after();
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 2] = pf_gtime();
@@ -384,7 +412,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         // mbarrier arrive, cluster scope), each CTA sums all cs of them in rank order (deterministic).
         float* pmine = a.pscratch + ((size_t)blockIdx.x * 128 + row) * 128;
         if (cs > 1) {
-            for (int c0 = 0; c0 < rp; c0 += 32) {
+            for (int c0 = 32 * eg; c0 < rp; c0 += 64) {
                 float v[32];
                 tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
                 const int nv = rp - c0 < 32 ? (rp - c0) / 4 : 8;   // only the row's rp columns (rp % 16 == 0)
@@ -395,12 +423,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                             make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
             asm volatile("fence.acq_rel.cluster;" ::: "memory");
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (tid == 64)
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (etid == 0)
                 for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(pready, (uint32_t)c));
             pf_wait_cluster(pready, 0);
         }
-        for (int c0 = 0; c0 < rp; c0 += 32) {
+        for (int c0 = 32 * eg; c0 < rp; c0 += 64) {
             float v[32];
             if (cs > 1) {
 #pragma unroll
@@ -449,27 +477,16 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         tc_fence_before();
         pf_arrive(v_ready);
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 3] = pf_gtime();
-        // ---- per expand tile: y[row][n0 .. n0+128) += D2 (one rounding).  y tiles are staged
-        //      by TMA one tile ahead (2 slots, SW128: row at (row/8)*1024 + (row%8)*128 per 64-col
-        //      half, 16-B chunk c at c ^ (row%8)); results go straight to global, valid rows only
-        //      (rows past the segment belong to other segments' tiles).
+        // ---- expand tiles q = eg, eg + 2, ...: y[row][n0 .. n0+128) += D2 (one rounding) in the staged
+        //      y tile (the producer loads it by TMA into slot q % 3; SW128: row at (row/8)*1024 +
+        //      (row%8)*128 per 64-column half, 16-B chunk c at c ^ (row%8)).  A warp whose 32 rows are all
+        //      in the segment stores them by TMA; a warp holding rows past the segment (they belong to
+        //      other segments' tiles) stores its valid rows with STG.
         const bool valid = row < nvalid;
-        const bool leader = (tid == 64);
-        auto issue_y = [&](int q) {   // q: this CTA's column-tile index
-            const int b = q % kPfYSlots;
+        const bool warp_full = sub * 32 + 32 <= nvalid;
+        for (int q = eg; q < nnt; q += 2) {
             const int nt = nt_lo + q;
-            const uint32_t dst = yring + (uint32_t)b * kPfYBytes;
-            pf_arrive_tx(y_full(b), (uint32_t)kPfYBytes);
-            tma_2d(dst, &a.tm_y, nt * kPfNTile, tok0, y_full(b));
-            tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(b));
-        };
-        if (leader) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            for (int q = 0; q < kPfYSlots && q < nnt; ++q) issue_y(q);
-        }
-        for (int q = 0; q < nnt; ++q) {
-            const int nt = nt_lo + q;
-            const int b = q & 1;
+            const int b = eg;   // TMEM buffer q & 1
             pf_wait(tm_full(b), (q >> 1) & 1);
             const int yb = q % kPfYSlots;
             pf_wait(y_full(yb), (q / kPfYSlots) & 1);
@@ -482,36 +499,47 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 if (valid) {
                     uint4 o4[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int col = c0 + q * 8;
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const int col = c0 + q4 * 8;
                         const int h = col >> 6, chunk = (col & 63) >> 3;
                         const uint4 yv = *reinterpret_cast<const uint4*>(ys + h * (kPfYBytes / 2) + ((chunk ^ (row & 7)) << 4));
                         const uint32_t w[4] = {yv.x, yv.y, yv.z, yv.w};
                         uint32_t o[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const float lo = __uint_as_float(w[e] << 16) + d[q * 8 + 2 * e];
-                            const float hi = __uint_as_float(w[e] & 0xffff0000u) + d[q * 8 + 2 * e + 1];
+                            const float lo = __uint_as_float(w[e] << 16) + d[q4 * 8 + 2 * e];
+                            const float hi = __uint_as_float(w[e] & 0xffff0000u) + d[q4 * 8 + 2 * e + 1];
                             __nv_bfloat162 hb = __floats2bfloat162_rn(lo, hi);
                             o[e] = *reinterpret_cast<uint32_t*>(&hb);
                         }
-                        o4[q] = make_uint4(o[0], o[1], o[2], o[3]);
+                        o4[q4] = make_uint4(o[0], o[1], o[2], o[3]);
                     }
                     // back into the row's own (swizzled) slots of the staged tile
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int col = c0 + q * 8;
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const int col = c0 + q4 * 8;
                         const int h = col >> 6, chunk = (col & 63) >> 3;
-                        *reinterpret_cast<uint4*>(ys + h * (kPfYBytes / 2) + ((chunk ^ (row & 7)) << 4)) = o4[q];
+                        *reinterpret_cast<uint4*>(ys + h * (kPfYBytes / 2) + ((chunk ^ (row & 7)) << 4)) = o4[q4];
                     }
                 }
             }
             tc_fence_before();
             pf_arrive(tm_empty(b));
-            // coalesced write-back: the warp's 32 rows leave as 256-B row segments, two rows per
-            // STG.128 instruction (a thread-per-row store touches 32 rows per instruction)
-            __syncwarp();
-            {
+            const uint32_t yslot_s = yring + (uint32_t)yb * kPfYBytes;
+            if (warp_full) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // STS -> TMA store reads
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&a.tm_y32, yslot_s + (uint32_t)sub * 4096u, nt * kPfNTile, tok0 + sub * 32);
+                    tma_store_2d(&a.tm_y32, yslot_s + kPfYBytes / 2 + (uint32_t)sub * 4096u, nt * kPfNTile + 64,
+                                 tok0 + sub * 32);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // slot may be refilled
+                    pf_arrive(y_empty(yb));
+                }
+            } else {
+                // the warp's valid rows as 256-B row segments, two rows per STG.128 instruction
+                __syncwarp();
                 const uint8_t* yslot = gy + yb * kPfYBytes;
 #pragma unroll 4
                 for (int i = 0; i < 16; ++i) {
@@ -523,11 +551,12 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                         *reinterpret_cast<uint4*>(a.y + ((size_t)(tok0 + rr) * a.H_out + nt * kPfNTile + c16 * 8) * 2) = v;
                     }
                 }
+                __syncwarp();
+                if (lane == 0) pf_arrive(y_empty(yb));
             }
-            // every epilogue thread is done with y slot b -> refill it with tile nt + 2
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (leader && q + kPfYSlots < nnt) issue_y(q + kPfYSlots);
         }
+        // the TMA stores are complete (not just read) before the CTA retires
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -620,6 +649,8 @@ int launch_prefill(const Plan& pl, const PrefillLaunch& L, cudaStream_t st, int*
     std::memcpy(&a.tm_b, L.tm_b, sizeof(CUtensorMap));
     a.box_maps = static_cast<const char*>(L.box_maps);
     e = make_tmap_bf16(&a.tm_y, L.y, L.T, L.H_out, 128);
+    if (e) return e;
+    e = make_tmap_bf16(&a.tm_y32, L.y, L.T, L.H_out, 32);
     if (e) return e;
     a.y = static_cast<char*>(L.y);
     a.meta_global = L.meta_dev;
