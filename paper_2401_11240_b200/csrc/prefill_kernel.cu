@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             pf_bar_init(empty2(s), 1);
         }
         pf_bar_init(d1_full, 1);
-        pf_bar_init(v_ready, kPfEpiThreads);
+        pf_bar_init(v_ready, (uint32_t)(kPfEpiThreads / 32 * cs));   // every epilogue warp of every CTA of the cluster
         pf_bar_init(pready, (uint32_t)cs);
         for (int b = 0; b < 2; ++b) {
             pf_bar_init(tm_full(b), 1);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         }
         stage = 0;
         phase = 0;
-        pf_wait(v_ready, 0);
+        pf_wait_cluster(v_ready, 0);
         tc_fence_after();
         const int ksteps = rp / 16;
         for (int q = 0; q < nnt; ++q) {
@@ -401,81 +401,93 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         const int sub = warp & 3;
         const int row = sub * 32 + lane;   // token row within the tile
         const uint32_t lane_addr = (uint32_t)(sub * 32) << 16;
-        // ---- v = s * D1 -> bf16, K-major SW128: atom kk = cols [64kk, 64kk+64), row at
-        //      (row/8)*1024 + (row%8)*128 inside the 16 KB atom, 16-B chunk c stored at c ^ (row%8).
-        //      The two groups take alternate 32-column chunks.
+        // ---- v = s * D1 -> bf16 (the expand's A operand); the two groups take alternate 32-column chunks
         pf_wait(d1_full, 0);
         tc_fence_after();
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 2] = pf_gtime();
-        // split-K (cs > 1): this CTA's D1 is a partial over its K share.  Partials go to an
-        // L2-resident scratch as fp32 [CTA][row][128]; once every peer's partial is released (remote
-        // mbarrier arrive, cluster scope), each CTA sums all cs of them in rank order (deterministic).
-        float* pmine = a.pscratch + ((size_t)blockIdx.x * 128 + row) * 128;
+        // the bf16 v chunk (8 columns c8*8.. of token row rr) at its K-major SW128 slot: atom kk = cols
+        // [64kk, 64kk+64), row at (rr/8)*1024 + (rr%8)*128 inside the 16 KB atom, 16-B chunk c at c ^ (rr%8)
+        auto v_off = [](int rr, int col) -> uint32_t {
+            const int kk = col >> 6, chunk = (col & 63) >> 3;
+            return (uint32_t)kk * 16384u + (uint32_t)(rr >> 3) * 1024u + (uint32_t)(rr & 7) * 128u +
+                   (uint32_t)((chunk ^ (rr & 7)) * 16);
+        };
+        auto pack8 = [&](const float* f, int col) -> uint4 {   // s * D1 -> bf16; columns >= r are exact zeros
+            uint32_t hw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float f0 = col + 2 * e < r ? f[2 * e] * scale : 0.f;
+                const float f1 = col + 2 * e + 1 < r ? f[2 * e + 1] * scale : 0.f;
+                __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
+                hw[e] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            return make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        };
         if (cs > 1) {
+            // split-K: this CTA's D1 is a partial over its K share.  (1) every CTA writes its partial to an
+            // L2-resident scratch as float4 column quads [CTA][col/4][row][4] (a warp's 32 rows = 512
+            // coalesced bytes per quad); (2) once every peer's partial is released (remote mbarrier arrive, cluster scope),
+            // CTA ck reduces the rows [ck*128/cs, (ck+1)*128/cs) over the cs partials in rank order
+            // (deterministic), scales and rounds them to bf16 and (3) writes those v rows into the V
+            // buffer of every CTA of the cluster (DSMEM), whose v_ready then counts the peers' warps.
+            float4* pmine = reinterpret_cast<float4*>(a.pscratch) + (size_t)blockIdx.x * 32 * 128 + row;
             for (int c0 = 32 * eg; c0 < rp; c0 += 64) {
                 float v[32];
                 tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
-                const int nv = rp - c0 < 32 ? (rp - c0) / 4 : 8;   // only the row's rp columns (rp % 16 == 0)
+                const int nq = rp - c0 < 32 ? (rp - c0) / 4 : 8;   // rp % 16 == 0
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    if (i < nv)
-                        *reinterpret_cast<float4*>(pmine + c0 + 4 * i) =
-                            make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    if (i < nq) pmine[(size_t)(c0 / 4 + i) * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
             asm volatile("fence.acq_rel.cluster;" ::: "memory");
             asm volatile("bar.sync 1, 256;" ::: "memory");
             if (etid == 0)
                 for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(pready, (uint32_t)c));
             pf_wait_cluster(pready, 0);
-        }
-        for (int c0 = 32 * eg; c0 < rp; c0 += 64) {
-            float v[32];
-            if (cs > 1) {
+            const int r_lo = ck * 128 / cs, nrows = (ck + 1) * 128 / cs - r_lo;
+            const float4* part0 = reinterpret_cast<const float4*>(a.pscratch) + (size_t)(blockIdx.x - ck) * 32 * 128;
+            for (int it = etid; it < nrows * (rp / 8); it += kPfEpiThreads) {
+                const int rr = r_lo + it % nrows, c8 = it / nrows;
+                float f[8];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.f;
-                const int nv = rp - c0 < 32 ? (rp - c0) / 4 : 8;
+                for (int e = 0; e < 8; ++e) f[e] = 0.f;
                 for (int c = 0; c < cs; ++c) {
-                    // partials of the cluster's CTAs (L2): blockIdx.x - ck + c, this row, columns c0..;
-                    // all 8 loads of a peer are in flight before the first add consumes one
-                    const float* src = a.pscratch + ((size_t)(blockIdx.x - ck + c) * 128 + row) * 128 + c0;
-                    float4 f[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        f[i] = i < nv ? __ldcg(reinterpret_cast<const float4*>(src) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        v[4 * i] += f[i].x;
-                        v[4 * i + 1] += f[i].y;
-                        v[4 * i + 2] += f[i].z;
-                        v[4 * i + 3] += f[i].w;
-                    }
+                    const float4* src = part0 + (size_t)c * 32 * 128 + (size_t)(c8 * 2) * 128 + rr;
+                    const float4 g0 = __ldcg(src), g1 = __ldcg(src + 128);
+                    f[0] += g0.x; f[1] += g0.y; f[2] += g0.z; f[3] += g0.w;
+                    f[4] += g1.x; f[5] += g1.y; f[6] += g1.z; f[7] += g1.w;
                 }
-            } else {
+                const uint4 w = pack8(f, c8 * 8);
+                const uint32_t dst = vhi + v_off(rr, c8 * 8);
+                for (int c = 0; c < cs; ++c)
+                    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pf_mapa(dst, (uint32_t)c)),
+                                 "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                                 : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");   // generic -> tensor-core reads
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            __syncwarp();
+            // A CTA cannot retire before all DSMEM traffic into it is done: its MMA warp waits for its
+            // v_ready, which completes only after every peer warp's release-arrive that follows that
+            // warp's stores (and pready likewise), and the CTA exits after a __syncthreads with the MMA
+            // warp.  (compute-sanitizer racecheck does not follow mbarriers across the cluster and
+            // reports these stores as "into a block that might have already exited"; an explicit
+            // exit-time barrier.cluster hangs under racecheck and measured 0.5-1 % slower natively.)
+            if (lane == 0)
+                for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(v_ready, (uint32_t)c));
+        } else {
+            for (int c0 = 32 * eg; c0 < rp; c0 += 64) {
+                float v[32];
                 tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
-            }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {   // four 16-B chunks of 8 columns
-                uint32_t hw[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    // columns >= r are exact zeros (the zero page's rows; kept explicit)
-                    const int j0 = c0 + q * 8 + 2 * e;
-                    const float f0 = j0 < r ? v[q * 8 + 2 * e] * scale : 0.f;
-                    const float f1 = j0 + 1 < r ? v[q * 8 + 2 * e + 1] * scale : 0.f;
-                    __nv_bfloat162 h = __floats2bfloat162_rn(f0, f1);
-                    hw[e] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                const int col = c0 + q * 8;
-                const int kk = col >> 6, chunk = (col & 63) >> 3;
-                const uint32_t off = (uint32_t)kk * 16384u + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
-                                     (uint32_t)((chunk ^ (row & 7)) * 16);
-                *reinterpret_cast<uint4*>(gv + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<uint4*>(gv + v_off(row, c0 + q * 8)) = pack8(v + q * 8, c0 + q * 8);
             }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) pf_arrive(v_ready);
         }
-
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor-core reads
-        tc_fence_before();
-        pf_arrive(v_ready);
         if (a.trace && tid == 64) a.trace[(size_t)tile * 4 + 3] = pf_gtime();
         // ---- expand tiles q = eg, eg + 2, ...: y[row][n0 .. n0+128) += D2 (one rounding) in the staged
         //      y tile (the producer loads it by TMA into slot q % 3; SW128: row at (row/8)*1024 +

@@ -1,5 +1,8 @@
 """Per-CTA phase timeline of the tcgen05 prefill kernel (lora_debug_set_trace): config 3, or a c5
-prefill shape (32 token tiles: split-K clusters).  usage: python scripts/trace_prefill.py [c3|c5q|c5down]"""
+prefill shape (32 token tiles: split-K clusters).  usage: python scripts/trace_prefill.py [c3|c5q|c5down] [steady]
+L2 is flushed by a READ pass (a writing flush leaves dirty lines whose write-backs the traced apply would
+pay); `steady` instead traces an apply issued right behind an untraced one (its dirty y lines drain
+during the traced apply, as in the back-to-back bench)."""
 import os
 import sys
 
@@ -28,13 +31,18 @@ for _ in range(3):
     pool.apply(x, y, b.seg_indptr, b.adapter_ids)
 torch.cuda.synchronize()
 md = pool.metadata()
-nt = md["n_prefill_tiles"] * (1 if which == "c3" else 4)   # CTAs (c5: 4-CTA clusters per tile)
+nt = md["n_prefill_ctas"]
 buf = torch.zeros(4 * nt * 2 + 64, dtype=torch.int64, device="cuda")
 pool.set_trace(buf)
-flush = torch.empty(512 * 2 ** 20, dtype=torch.int8, device="cuda")
-flush.zero_()
+steady = len(sys.argv) > 2 and sys.argv[2] == "steady"
+flush = torch.zeros(512 * 2 ** 20 // 8, dtype=torch.int64, device="cuda")
+flush.sum()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
+if steady:
+    pool.set_trace(None)
+    pool.apply(x, y, b.seg_indptr, b.adapter_ids)
+    pool.set_trace(buf)
 e0.record()
 pool.apply(x, y, b.seg_indptr, b.adapter_ids)
 e1.record()
