@@ -157,7 +157,8 @@ int launch_fused_base(const FusedBaseLaunch& L, const int32_t* words, int n_word
                       lora_cuda_stream st);
 bool prefill_supported(int H_in, int H_out, int esz);
 int make_tmap_bf16(void* tm_out, const void* base, int64_t rows, int64_t cols, int box_rows);
-constexpr int kPfMaxRank = 128;        // tensor-core prefill path handles ranks up to this
+constexpr int kPfMaxRank = 256;        // tensor-core prefill path handles ranks up to this (= LORA_MAX_RANK)
+constexpr int kFusedMaxRank = 128;     // the fused base GEMM (f2): rank rows ride in one 128-row K chunk
 constexpr int kPfMaxBlobWords = 7680;
 
 }  // namespace lora

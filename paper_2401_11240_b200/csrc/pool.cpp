@@ -542,7 +542,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     }
     if (pl.n_pf_tiles > 0 && mode == 0) {
         if (pl.pf_cs > 1 &&
-            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * 128, false, "pf_scratch")) != LORA_OK)
+            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pl.n_pf_tiles * 128 * kPfMaxRank, false, "pf_scratch")) != LORA_OK)
             return s;
         PrefillLaunch L{x, y, p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages, p->num_sms};
         L.pscratch = p->pf_scratch;
@@ -628,7 +628,7 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
         lora_pool* p = pools[i];
         if (p->plan.n_pf_tiles == 0) continue;
         if (p->plan.pf_cs > 1 &&
-            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * 128, false, "pf_scratch")) !=
+            (s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)p->plan.n_pf_tiles * 128 * kPfMaxRank, false, "pf_scratch")) !=
                 LORA_OK)
             return s;
         PrefillLaunch L{xs[i], ys[i], p->tm_a, p->tm_b, p->box_maps, nullptr, p->trace, T, p->H_in, p->H_out, p->n_pages,
@@ -796,7 +796,7 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
         n_pairs += (len + 255) / 256;
         if (adapter_ids[i] >= 0) {
             const AdapterRec& a = p->table.at(adapter_ids[i]);
-            if (a.rank > kPfMaxRank) return fail(LORA_ERR_UNSUPPORTED, "the fused base GEMM supports rank <= 128");
+            if (a.rank > kFusedMaxRank) return fail(LORA_ERR_UNSUPPORTED, "the fused base GEMM supports rank <= 128");
             n_vtiles += (len + 127) / 128;
             n_vp += (len + 255) / 256;
             max_rp = std::max(max_rp, (a.rank + 15) & ~15);
@@ -914,7 +914,7 @@ lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
             // split-K grids within the SM count
             const int64_t pf_ctas = std::min<int64_t>((value + 127) / 128 * 8, p->num_sms);
             if (s == LORA_OK && p->tc_prefill && value > 0)
-                s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pf_ctas * 128 * 128, false, "pf_scratch");
+                s = grow(p, p->pf_scratch, p->pf_scratch_cap, (size_t)pf_ctas * 128 * kPfMaxRank, false, "pf_scratch");
             return s;
         }
         case LORA_OPT_LOAD_KERNEL:

@@ -1,7 +1,7 @@
 // prefill_kernel.cu -- N2: the LoRA delta of long prefill segments on the 5th-gen tensor
 // cores (tcgen05 + TMEM + TMA), sm_100a.
 //
-// For a segment of tokens [t0, t0+len) on adapter g (rank r <= 128), per 128-token tile:
+// For a segment of tokens [t0, t0+len) on adapter g (rank r <= 256), per 128-token tile:
 //     V[t][j]  = s_g · Σ_k X[t][k] · A_g[k][j]      shrink  D1[128 x r16] in TMEM  (Eq. 1)
 //     Y[t][n] += Σ_j V[t][j] · B_g[j][n]            expand  D2[128 x 128] in TMEM, per 128-column tile
 //
@@ -35,12 +35,16 @@ namespace lora {
 // TMEM lanes) taking the expand tiles alternately, one per TMEM accumulator buffer
 constexpr int kPfThreads = 320;
 constexpr int kPfEpiThreads = 256;
-constexpr int kPfStages = 3;           // expand-phase ring (B tiles)
-constexpr int kPfShrinkStages = 7;     // shrink-phase ring: the 3 ring stages + the V and y buffers, idle until D1 is done
-constexpr int kPfStageBytes = 32768;   // X chunk 16 KB + A chunk <= 16 KB, or one B tile (<= 32 KB)
-constexpr int kPfVBytes = 128 * 128 * 2;   // one V part (hi or lo): 128 tokens x r16 <= 128, bf16
+// SMEM (after 1 KB alignment): [0, 96K) expand ring, 3 x 32 KB (B rows of a column tile; a rank > 128
+// tile takes two stages, rank rows [0,128) and [128,r)); [96K, 224K) V (32 KB, 64 KB for rank > 128)
+// then the staged y tiles (3, or 2 for rank > 128); the shrink ring spans all of [0, 224K) until D1 is
+// done: 7 stages of 32 KB (x chunk 16 KB + A chunk <= 16 KB) or, for rank > 128, 4 of 48 KB.
+constexpr int kPfStages = 3;           // expand-phase ring (B rows)
+constexpr int kPfShrinkStages = 7;     // shrink-phase ring (at most)
+constexpr int kPfStageBytes = 32768;
+constexpr int kPfVBytes = 128 * 128 * 2;   // 32 KB: one V part of 128 tokens x 128 rank columns, bf16
 constexpr int kPfYBytes = 128 * 128 * 2;   // one staged y tile (128 tokens x 128 columns, bf16)
-constexpr int kPfYSlots = 3;               // staged y tiles in flight (the third lives in the unused V-lo space)
+constexpr int kPfYSlots = 3;               // staged y tiles in flight (at most)
 constexpr int kPfBarBytes = 512;
 constexpr int kPfSmem = 1024 /*align*/ + kPfStages * kPfStageBytes + 2 * kPfVBytes + 2 * kPfYBytes + kPfBarBytes;
 static_assert(kPfSmem <= 232448, "prefill smem");
@@ -55,7 +59,7 @@ struct PrefillArgs {
     CUtensorMap tm_y32; // y [T][H_out], box {64, 32}, SW128 (one epilogue warp's rows, TMA store)
     const char* box_maps;   // pool page arrays as 2D boxes {64, 8 << k} (A maps, then B maps), SW128
     int cs;                 // cluster size: the cs CTAs of a token tile split its shrink K and its columns
-    float* pscratch;        // split-K partials [CTA][128][128] fp32 (L2-resident exchange)
+    float* pscratch;        // split-K partials [CTA][r/4 <= 64][128 rows][4] fp32 (L2-resident exchange)
     char* y;
     const int32_t* meta_global;
     unsigned long long* trace;
@@ -188,13 +192,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     uint8_t* gbase = smem_raw + (base - raw);
     const uint32_t ring = base;                         // kPfStages x 32 KB
     const uint32_t vhi = base + kPfStages * kPfStageBytes;
-    const uint32_t vlo = vhi + kPfVBytes;
-    uint8_t* gv = gbase + kPfStages * kPfStageBytes;   // generic pointer to vhi
-    // v goes to the expand as bf16 (SURVEY §8(c) reading 4 allows it on the tcgen05 expand; rel-L2
-    // budget in DESIGN.md), so the lo-part buffer serves as a third staged y tile: 3 x 32 KB at vlo
-    const uint32_t yring = vlo;
-    uint8_t* gy = gbase + (yring - base);
-    const uint32_t bars = vlo + kPfVBytes + 2 * kPfYBytes;   // mbarriers + tmem slot
+    uint8_t* gv = gbase + kPfStages * kPfStageBytes;   // generic pointer to V
+    const uint32_t bars = vhi + 2 * kPfVBytes + 2 * kPfYBytes;   // mbarriers + tmem slot
     // barriers: shrink ring full/empty [7] x 2, expand ring full/empty [3] x 2, then the rest
     auto full = [&](int s) { return bars + 8u * s; };
     auto empty = [&](int s) { return bars + 8u * (kPfShrinkStages + s); };
@@ -220,6 +219,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const float scale = __int_as_float(rec[4]);
     const int first_page = rec[5];   // >= 0: rank rows are pages [first_page, first_page + r)
     const int rp = (r + 15) & ~15;                      // rank padded to the MMA N/K granularity
+    // v goes to the expand as bf16 (SURVEY §8(c) reading 4 allows it on the tcgen05 expand; rel-L2
+    // budget in DESIGN.md); the y tiles are staged after it
+    const bool wide = rp > 128;
+    const int nys = wide ? 2 : 3;                                  // staged y slots
+    const uint32_t yring = vhi + (wide ? 2u : 1u) * kPfVBytes;
+    uint8_t* gy = gbase + (yring - base);
+    const int nss = wide ? 4 : kPfShrinkStages;                    // shrink stages
+    const uint32_t ssz = wide ? 49152u : 32768u;                   // shrink stage bytes
+    const int nhalf = wide ? 2 : 1;                                // expand ring stages per column tile
     const int nkc_all = a.H_in / 64;                    // shrink K chunks of the tile
     const int cs = a.cs;
     const int ck = cs > 1 ? (int)pf_cluster_rank() : 0;  // this CTA's share of K: [kc_lo, kc_lo + nkc)
@@ -247,13 +255,13 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             pf_bar_init(tm_full(b), 1);
             pf_bar_init(tm_empty(b), 128);
         }
-        for (int b = 0; b < kPfYSlots; ++b) {
+        for (int b = 0; b < kPfYSlots; ++b) {   // slots [nys, 3) stay unused
             pf_bar_init(y_full(b), 1);
             pf_bar_init(y_empty(b), 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {   // TMEM: D1 at columns [0,128), D2 buffers at [128,256) and [256,384)
+    if (warp == 1) {   // TMEM: D1 at columns [0,256), D2 buffers at [256,384) and [384,512)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(pf_smem(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -272,13 +280,15 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         const int ngr = rp / 4;   // gather4 groups (rank rows, padded with the zero page)
-        // each lane owns <= 1 gather4 group per chunk (rp <= 128 -> ngr <= 32)
-        int pg[4];
+        // lane owns gather4 groups lane (rank rows [4 lane, 4 lane + 4)) and lane + 32 (rows 128 + ...)
+        int pg[2][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = lane * 4 + q;
-            pg[q] = j < r ? M[poff + j] : a.zero_page;
-        }
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = (lane + 32 * u) * 4 + q;
+                pg[u][q] = j < r ? M[poff + j] : a.zero_page;
+            }
         // contiguous adapters: the first rb = r & ~7 rank rows as 2D boxes of 128/64/32/16/8 rows
         // (one TMA request instead of rb/4 gather4s; the request rate bounded the rank-128 tiles).
         // Rows [rb, rp) come by gather4 with the pool's zero page past r, never from the pages
@@ -286,67 +296,79 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         // 0 * B into NaN in this tenant's y)
         const bool use_box = first_page >= 0 && a.box_maps != nullptr;
         const int rb = use_box ? (r & ~7) : 0;
-        auto boxes = [&](uint32_t dst, int map_base, int col, uint32_t bar) {
-            int row = 0;
+        // rank rows [row0, row1) of the run as boxes; row `row` lands at dst + (row - row0) * 128
+        auto boxes = [&](uint32_t dst, int map_base, int col, uint32_t bar, int row0, int row1) {
+            int row = row0;
             for (int k = 4; k >= 0; --k) {
                 const int R = 8 << k;
-                while (rb - row >= R) {
-                    tma_2d(dst + (uint32_t)row * 128u,
+                while (row1 - row >= R) {
+                    tma_2d(dst + (uint32_t)(row - row0) * 128u,
                            reinterpret_cast<const CUtensorMap*>(a.box_maps + (map_base + k) * 128), col,
                            first_page + row, bar);
                     row += R;
                 }
             }
         };
-        const bool gat = lane >= rb / 4 && lane < ngr;   // this lane's gather4 group (rows 4 lane .. 4 lane + 3)
+        // this lane's gather4 groups gi = lane + 32 u (rows 4 gi .. 4 gi + 3) not covered by the boxes
+        const bool gat0 = lane >= rb / 4 && lane < ngr;
+        const bool gat1 = lane + 32 >= rb / 4 && lane + 32 < ngr;
         for (int kq = 0; kq < nkc; ++kq) {
             const int kc = kc_lo + kq;
             pf_wait(empty(stage), phase ^ 1u);
-            const uint32_t sb = ring + stage * kPfStageBytes;
+            const uint32_t sb = ring + stage * ssz;
             if (lane == 0) {
                 pf_arrive_tx(full(stage), (uint32_t)(128 * 128 + rp * 128));
                 tma_2d(sb, &a.tm_x, kc * 64, tok0, full(stage));
-                if (rb > 0) boxes(sb + 16384, 0, kc * 64, full(stage));
+                if (rb > 0) boxes(sb + 16384, 0, kc * 64, full(stage), 0, rb);
             }
             __syncwarp();
-            if (gat)
-                tma_gather4(sb + 16384 + lane * 512, &a.tm_a, kc * 64, pg[0], pg[1], pg[2], pg[3], full(stage));
-            if (++stage == kPfShrinkStages) { stage = 0; phase ^= 1u; }
+            if (gat0)
+                tma_gather4(sb + 16384 + lane * 512, &a.tm_a, kc * 64, pg[0][0], pg[0][1], pg[0][2], pg[0][3], full(stage));
+            if (gat1)
+                tma_gather4(sb + 16384 + (lane + 32) * 512, &a.tm_a, kc * 64, pg[1][0], pg[1][1], pg[1][2], pg[1][3],
+                            full(stage));
+            if (++stage == nss) { stage = 0; phase ^= 1u; }
         }
         // the expand ring reuses shrink stages 0-2: wait until every shrink MMA has read them
         pf_wait(d1_full, 0);
         stage = 0;
         phase = 0;
-        // expand: B rows of each 128-column tile, MN-major SW128 atoms (8 rank rows x 64 cols);
-        // atom (kg, ng) at (ng * rp/8 + kg) * 1 KB; a gather4 fills 4 rows of one atom
+        // expand: B rows of each 128-column tile, per ring stage the rank rows [128 hf, 128 hf + rh) of
+        // half hf as MN-major SW128 atoms (8 rank rows x 64 cols): atom (kg, ng) at (ng * rh/8 + kg) * 1 KB;
+        // a gather4 fills 4 rows of one atom
         for (int q = 0; q < nnt; ++q) {
             const int nt = nt_lo + q;
-            // the y tile into slot q % 3 once the group that had tile q - 3 stored it
+            // the y tile into slot q % nys once the group that had tile q - nys stored it
             if (lane == 0) {
-                const int yb = q % kPfYSlots;
-                pf_wait(y_empty(yb), ((q / kPfYSlots) & 1) ^ 1u);
+                const int yb = q % nys;
+                pf_wait(y_empty(yb), ((q / nys) & 1) ^ 1u);
                 const uint32_t dst = yring + (uint32_t)yb * kPfYBytes;
                 pf_arrive_tx(y_full(yb), (uint32_t)kPfYBytes);
                 tma_2d(dst, &a.tm_y, nt * kPfNTile, tok0, y_full(yb));
                 tma_2d(dst + kPfYBytes / 2, &a.tm_y, nt * kPfNTile + 64, tok0, y_full(yb));
             }
-            pf_wait(empty2(stage), phase ^ 1u);
-            const uint32_t sb = ring + stage * kPfStageBytes;
-            if (lane == 0) {
-                pf_arrive_tx(full2(stage), (uint32_t)(rp * kPfNTile * 2));
-                if (rb > 0)
-                    for (int h = 0; h < 2; ++h)
-                        boxes(sb + (uint32_t)(h * (rp / 8)) * 1024u, kBoxKinds, nt * kPfNTile + h * 64, full2(stage));
-            }
-            __syncwarp();
-            if (gat) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t dst = sb + (uint32_t)((h * (rp / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
-                    tma_gather4(dst, &a.tm_b, nt * kPfNTile + h * 64, pg[0], pg[1], pg[2], pg[3], full2(stage));
+            for (int hf = 0; hf < nhalf; ++hf) {
+                const int rh = min(128, rp - 128 * hf);
+                pf_wait(empty2(stage), phase ^ 1u);
+                const uint32_t sb = ring + stage * kPfStageBytes;
+                if (lane == 0) {
+                    pf_arrive_tx(full2(stage), (uint32_t)(rh * kPfNTile * 2));
+                    const int b0 = 128 * hf, b1 = min(rb, 128 * hf + 128);
+                    if (b1 > b0)
+                        for (int h = 0; h < 2; ++h)
+                            boxes(sb + (uint32_t)(h * (rh / 8)) * 1024u, kBoxKinds, nt * kPfNTile + h * 64, full2(stage), b0, b1);
                 }
+                __syncwarp();
+                if (hf == 0 ? gat0 : gat1) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t dst = sb + (uint32_t)((h * (rh / 8) + (lane >> 1)) * 1024 + (lane & 1) * 512);
+                        tma_gather4(dst, &a.tm_b, nt * kPfNTile + h * 64, pg[hf][0], pg[hf][1], pg[hf][2], pg[hf][3],
+                                    full2(stage));
+                    }
+                }
+                if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
             }
-            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (one elected lane) =====================
@@ -358,7 +380,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             pf_wait(full(stage), phase);
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t sb = ring + stage * kPfStageBytes;
+                const uint32_t sb = ring + stage * ssz;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
                     umma_f16(tmem, umma_desc(sb + kk * 32, 16, 1024), umma_desc(sb + 16384 + kk * 32, 16, 1024), id1,
@@ -367,32 +389,35 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 if (kc == nkc - 1) umma_commit(d1_full);
             }
             __syncwarp();
-            if (++stage == kPfShrinkStages) { stage = 0; phase ^= 1u; }
+            if (++stage == nss) { stage = 0; phase ^= 1u; }
         }
         stage = 0;
         phase = 0;
         pf_wait_cluster(v_ready, 0);
         tc_fence_after();
-        const int ksteps = rp / 16;
         for (int q = 0; q < nnt; ++q) {
             const int b = q & 1;
             pf_wait(tm_empty(b), ((q >> 1) & 1) ^ 1u);
-            pf_wait(full2(stage), phase);
-            tc_fence_after();
-            if (lane == 0) {
-                const uint32_t sb = ring + stage * kPfStageBytes;
-                const uint32_t dcol = tmem + 128u + 128u * b;
-                const uint32_t lbo = (uint32_t)(rp / 8) * 1024u;   // MN-direction atom stride
-                for (int ks = 0; ks < ksteps; ++ks) {
-                    const uint32_t voff = (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u;
-                    const uint64_t bd = umma_desc(sb + (uint32_t)ks * 2048u, lbo, 1024);
-                    umma_f16(dcol, umma_desc(vhi + voff, 16, 1024), bd, id2, ks != 0);
+            for (int hf = 0; hf < nhalf; ++hf) {
+                const int rh = min(128, rp - 128 * hf);
+                pf_wait(full2(stage), phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t sb = ring + stage * kPfStageBytes;
+                    const uint32_t dcol = tmem + 256u + 128u * b;
+                    const uint32_t lbo = (uint32_t)(rh / 8) * 1024u;   // MN-direction atom stride
+                    for (int ks = 0; ks < rh / 16; ++ks) {
+                        const int kg = 8 * hf + ks;   // k-step over the whole rank
+                        const uint32_t voff = (uint32_t)(kg >> 2) * 16384u + (uint32_t)(kg & 3) * 32u;
+                        const uint64_t bd = umma_desc(sb + (uint32_t)ks * 2048u, lbo, 1024);
+                        umma_f16(dcol, umma_desc(vhi + voff, 16, 1024), bd, id2, kg != 0);
+                    }
+                    umma_commit(empty2(stage));
+                    if (hf == nhalf - 1) umma_commit(tm_full(b));
                 }
-                umma_commit(empty2(stage));
-                umma_commit(tm_full(b));
+                __syncwarp();
+                if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
             }
-            __syncwarp();
-            if (++stage == kPfStages) { stage = 0; phase ^= 1u; }
         }
     } else {
         // ===================== epilogue: group eg = warps 2+4eg .. 5+4eg; warp w -> TMEM lanes 32*(w%4) .. +32
@@ -430,7 +455,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             // CTA ck reduces the rows [ck*128/cs, (ck+1)*128/cs) over the cs partials in rank order
             // (deterministic), scales and rounds them to bf16 and (3) writes those v rows into the V
             // buffer of every CTA of the cluster (DSMEM), whose v_ready then counts the peers' warps.
-            float4* pmine = reinterpret_cast<float4*>(a.pscratch) + (size_t)blockIdx.x * 32 * 128 + row;
+            float4* pmine = reinterpret_cast<float4*>(a.pscratch) + (size_t)blockIdx.x * (kPfMaxRank / 4) * 128 + row;
             for (int c0 = 32 * eg; c0 < rp; c0 += 64) {
                 float v[32];
                 tmem_ld32(tmem + lane_addr + (uint32_t)c0, v);
@@ -445,14 +470,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
                 for (int c = 0; c < cs; ++c) pf_arrive_remote(pf_mapa(pready, (uint32_t)c));
             pf_wait_cluster(pready, 0);
             const int r_lo = ck * 128 / cs, nrows = (ck + 1) * 128 / cs - r_lo;
-            const float4* part0 = reinterpret_cast<const float4*>(a.pscratch) + (size_t)(blockIdx.x - ck) * 32 * 128;
+            const float4* part0 = reinterpret_cast<const float4*>(a.pscratch) + (size_t)(blockIdx.x - ck) * (kPfMaxRank / 4) * 128;
             for (int it = etid; it < nrows * (rp / 8); it += kPfEpiThreads) {
                 const int rr = r_lo + it % nrows, c8 = it / nrows;
                 float f[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) f[e] = 0.f;
                 for (int c = 0; c < cs; ++c) {
-                    const float4* src = part0 + (size_t)c * 32 * 128 + (size_t)(c8 * 2) * 128 + rr;
+                    const float4* src = part0 + (size_t)c * (kPfMaxRank / 4) * 128 + (size_t)(c8 * 2) * 128 + rr;
                     const float4 g0 = __ldcg(src), g1 = __ldcg(src + 128);
                     f[0] += g0.x; f[1] += g0.y; f[2] += g0.z; f[3] += g0.w;
                     f[4] += g1.x; f[5] += g1.y; f[6] += g1.z; f[7] += g1.w;
@@ -500,14 +525,14 @@ __global__ void __launch_bounds__(kPfThreads, 1)
             const int nt = nt_lo + q;
             const int b = eg;   // TMEM buffer q & 1
             pf_wait(tm_full(b), (q >> 1) & 1);
-            const int yb = q % kPfYSlots;
-            pf_wait(y_full(yb), (q / kPfYSlots) & 1);
+            const int yb = q % nys;
+            pf_wait(y_full(yb), (q / nys) & 1);
             tc_fence_after();
             uint8_t* ys = gy + yb * kPfYBytes + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll 1
             for (int c0 = 0; c0 < kPfNTile; c0 += 32) {
                 float d[32];
-                tmem_ld32(tmem + lane_addr + 128u + 128u * b + (uint32_t)c0, d);
+                tmem_ld32(tmem + lane_addr + 256u + 128u * b + (uint32_t)c0, d);
                 if (valid) {
                     uint4 o4[4];
 #pragma unroll

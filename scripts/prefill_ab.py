@@ -2,7 +2,8 @@
 Each measurement: a CUDA graph of NP applies on distinct pools, replayed back to back (steady state:
 the previous apply's dirty y lines drain during the next, as in bench.py's prefill object); device
 time per apply and the HBM roofline fraction of the algorithmic bytes.
-usage: python scripts/prefill_ab.py A.so B.so [reps]      (the in-tree library is restored afterwards)"""
+usage: python scripts/prefill_ab.py A.so B.so [reps] [cases]   (the in-tree library is restored afterwards)
+cases: comma list of c3,c5q,c5gate,c5down (default) and c3w (c3 shapes with ranks 144/192/256)"""
 import json
 import os
 import shutil
@@ -20,9 +21,14 @@ import paper_2401_11240_b200 as L
 from workloads import gen
 peak = json.load(open(os.path.join(%r, "MEASURED_PEAKS.json")))["hbm_gbs"]
 out = {}
-cases = (("c3", gen.config_c3(), 8), ("c5q", gen.config_c5("q", prefill=True), 6),
-         ("c5gate", gen.config_c5("gate", prefill=True), 3), ("c5down", gen.config_c5("down", prefill=True), 3))
-for name, b, NP in cases:
+want = "@CASES@".split(",")
+mk = {"c3": lambda: gen.config_c3(), "c5q": lambda: gen.config_c5("q", prefill=True),
+      "c5gate": lambda: gen.config_c5("gate", prefill=True), "c5down": lambda: gen.config_c5("down", prefill=True),
+      "c3w": lambda: gen.build_batch("c3w", 31, "bf16", 4096, 4096, [512] * 32, list(range(32)),
+                                     {i: (144, 192, 256)[i %% 3] for i in range(32)})}
+NPS = {"c3": 8, "c5q": 6, "c5gate": 3, "c5down": 3, "c3w": 6}
+for name in want:
+    b, NP = mk[name](), NPS[name]
     pools = []
     for _ in range(NP):
         pool = L.LoraPool(b.H_in, b.H_out, 64, "bf16", max_total_rank=sum(a.rank for a in b.adapters))
@@ -68,13 +74,14 @@ print(json.dumps(out))
 def main():
     libs = sys.argv[1:3]
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    cases = sys.argv[4] if len(sys.argv) > 4 else "c3,c5q,c5gate,c5down"
     keep = LIB + ".ab_keep"
     shutil.copy(LIB, keep)
     try:
         for rep in range(reps):
             for tag, so in zip("AB", libs):
                 shutil.copy(so, LIB)
-                r = subprocess.run([sys.executable, "-c", CHILD], capture_output=True, text=True, cwd=ROOT, timeout=600)
+                r = subprocess.run([sys.executable, "-c", CHILD.replace("@CASES@", cases)], capture_output=True, text=True, cwd=ROOT, timeout=600)
                 line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-800:]
                 print("%s rep%d %s   (us/apply, HBM frac, tiles)" % (tag, rep, line), flush=True)
     finally:

@@ -577,15 +577,70 @@ def test_c5_prefill_column_split(L, proj):
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
 
 
-def test_prefill_rank_above_tcgen05_limit_falls_back(L):
-    """Prefill-length segments of rank > 128 (the tcgen05 path's limit) run on the decode kernel pair
-    in 8-token chunks, next to rank <= 128 segments on the tensor-core path, in one apply."""
+def test_prefill_rank_129_to_256_on_tcgen05(L):
+    """Prefill-length segments of rank 129..256 run on the tcgen05 kernel too (D1 up to 256 TMEM
+    columns, the V operand in 64 KB, each column tile's B rows in two ring stages), next to rank
+    <= 128 segments, in one apply; ragged lengths, odd ranks (zero-page padding), the oracle."""
     b = gen.build_batch("r200", 4711, "bf16", 512, 512, [300, 150, 1, 1], [0, 1, 0, 1], {0: 200, 1: 96},
                         y_zero=False)
     y, md = run_gpu(b, L)
-    assert md["n_prefill_tiles"] == 2          # only the rank-96 segment (150 tokens) is on tcgen05
+    assert md["n_prefill_tiles"] == 3 + 2
     ref = O.delta_for_batch(b, n_threads=8)
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_prefill_wide_ranks_vs_simt_and_oracle(L, seed):
+    """Ranks 129..256 (incl. 129, 136, 255, 256) mixed with small ranks: the tcgen05 path (L_tc = 16)
+    and the decode kernels alone both match the oracle; contiguous page runs (TMA boxes across the
+    rank-128 boundary) and, for odd seeds, a fragmented free list (gather4 rows in both halves)."""
+    rng = np.random.default_rng(100 + seed)
+    lens = [int(v) for v in rng.integers(40, 420, size=5)]
+    pick = [129, 136, 160, 200, 255, 256, 8, 64, 128]
+    ranks = {i: int(r) for i, r in enumerate(rng.choice(pick, size=5, replace=False))}
+    ranks[0] = [256, 129, 255, 200][seed]
+    H_in, H_out = [(512, 512), (1024, 384), (256, 1024), (768, 256)][seed]
+    b = gen.build_batch("wide%d" % seed, 5150 + seed, "bf16", H_in, H_out, lens, list(range(5)), ranks,
+                        y_zero=bool(seed % 2))
+    ref = O.delta_for_batch(b, n_threads=8)
+    import torch
+    pool = L.LoraPool(b.H_in, b.H_out, 16, "bf16", max_total_rank=sum(ranks.values()) + 64)
+    pool.set_option(L.binding.LORA_OPT_TC_THRESHOLD, 16)
+    if seed % 2:   # a 24-page hole at the front of the pool: adapter 0 (wide) straddles it and a spacer
+        filler = gen.make_adapter(1, 2, 999, 24, b.H_in, b.H_out, "bf16")
+        spacer = gen.make_adapter(1, 3, 997, 8, b.H_in, b.H_out, "bf16")
+        pool.load_adapter(999, 24, to_torch(filler.A, pin=True), to_torch(filler.B, pin=True), 1.0)
+        pool.load_adapter(997, 8, to_torch(spacer.A, pin=True), to_torch(spacer.B, pin=True), 1.0)
+        pool.unload_adapter(999)
+    for a in b.adapters:
+        pool.load_adapter(a.id, a.rank, to_torch(a.A, pin=True), to_torch(a.B, pin=True), a.scale)
+    if seed % 2:
+        pg = pool.adapter_pages(0)
+        assert pg[:24] == list(range(24)) and pg[24] == 32, pg[:30]
+    torch.cuda.synchronize()
+    y_tc, md = run_gpu(b, L, pool=pool)
+    assert md["n_prefill_tiles"] == sum((n + 127) // 128 for n in lens)
+    assert rel_l2(y_tc, ref, "bf16") <= TOL["bf16"]
+    pool.close()
+    y_simt, md_s = run_gpu(b, L, L_tc=1 << 30)
+    assert md_s["n_prefill_tiles"] == 0
+    assert rel_l2(y_simt, ref, "bf16") <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("H_in,H_out,n_tiles", [(4096, 1024, 2), (1024, 1024, 24), (1024, 4096, 3)])
+def test_prefill_wide_rank_few_tiles(L, H_in, H_out, n_tiles):
+    """Rank 256 / 200 / 144 on the few-tile paths: split-K clusters (partials of up to 256 columns
+    in the L2 scratch, v rows over DSMEM) and the column split with shrink recompute."""
+    rng = np.random.default_rng(n_tiles)
+    lens = [128 * n_tiles - 37, 1, 1]
+    ranks = {0: 256, 1: 200, 2: 144}
+    b = gen.build_batch("wft%d" % n_tiles, 6000 + n_tiles, "bf16", H_in, H_out, lens, [0, 1, 2], ranks,
+                        y_zero=False)
+    y, md = run_gpu(b, L)
+    assert md["n_prefill_tiles"] == n_tiles
+    ref = O.delta_for_batch(b, n_threads=16)
+    assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
+    del rng
 
 
 def _few_tile_batch(name, seed, H_in, H_out, n_tiles):
