@@ -131,7 +131,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,clocks.mem")
 
     def __init__(self, device_index: int):
         self.dev = device_index
@@ -162,7 +162,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, smax, reasons = [], 0.0, set()
+        sm, smax, reasons, mem, pw = [], 0.0, set(), [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -173,11 +173,17 @@ class ClockSampler:
                 smax = max(smax, float(parts[1]))
             except ValueError:
                 continue
+            for lst, v in ((pw, parts[2]), (mem, parts[7] if len(parts) > 7 else "")):
+                try:
+                    lst.append(float(v))
+                except ValueError:
+                    pass
             for n, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "mem_mhz": float(np.median(mem)) if mem else None, "power_w": float(np.median(pw)) if pw else None}
 
 
 # ---------------------------------------------------------------- workload

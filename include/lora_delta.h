@@ -91,9 +91,10 @@ typedef enum {
                                       one 1 MB adapter in 18 us (56 GB/s).  0 (default): cudaMemcpyAsync
                                       per run of pages (also the fallback when the host rows have no
                                       device mapping).  Same bytes (tested bitwise), same ready-event
-                                      semantics.  Not the default: in 2 of 4 c2 bench runs of pools
-                                      loaded this way the steady-state decode apply was 7 % slower
-                                      (unexplained). */
+                                      semantics.  Not the default: after many kernel loads, some
+                                      processes run every later decode apply ~5 % slower (a
+                                      process-wide state: pools loaded by memcpy in the same process
+                                      slow down too; profiles/r2_load_kernel_bimodal.txt). */
 
 /*
  * lora_pool_create -- make an empty paged adapter pool for one projection shape.

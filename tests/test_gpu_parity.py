@@ -484,7 +484,7 @@ def test_pad_max_rank_bgmv_mode(L, name):
 
 @pytest.mark.parametrize("kernel", [1, 0], ids=["gather_kernel", "memcpy"])
 def test_load_paths_land_exact_bytes(L, kernel):
-    """LORA_OPT_LOAD_KERNEL 1 (zero-copy gather kernel, default) and 0 (cudaMemcpyAsync) land the
+    """LORA_OPT_LOAD_KERNEL 1 (zero-copy gather kernel) and 0 (cudaMemcpyAsync, default) land the
     adapter bytes in its pages bitwise (read back, pin P12), including fragmented page runs, and the
     apply matches the oracle."""
     import torch
