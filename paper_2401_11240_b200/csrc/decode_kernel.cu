@@ -50,8 +50,7 @@ struct DecodeArgs {
     int n_shrink, n_expand, n_gc, n_jobs;
     int unit_tab;                // blob word offset of the per-unit table (plan.cpp append_unit_table)
     int unit_words;              // 3 (full unit records) or 1 (gc | local only: large batches)
-    // bf16 expand smem layout, sized per launch from the batch (max rank / tokens / columns)
-    int e_vpitch, e_boff, e_yoff, e_dtoff, e_pgoff, e_smem;
+    int e_smem;                  // bf16 expand: dynamic smem of the launch (the largest unit's layout)
     float* vred;                 // compact k-reduced v (TP split): written by the shrink kernel's last CTA of
                                  // each gc (tp_reduce_tail), read by the expand when v_compact is set
     int* gc_cnt;                 // TP shrink: per-gc arrival counters (zero between applies)
@@ -786,12 +785,15 @@ __global__ void __launch_bounds__(kConsumerThreads)
 }
 
 // ---- expand (bf16): one CTA = (group-chunk gc, column slice [n0, n0+nc)).  Swap-AB:
-// D[col][token] = B^T[col][rank] · v^T[rank][token], M = 16 columns, N = 8 tokens, K = 16
-// ranks; v is split into bf16 hi + lo parts (two MMAs) so v keeps fp32-level accuracy.
-// D is added into the y tile staged in smem (one rounding) and written back with 16-B stores.
-// smem: [0,256) barriers + UnitSh | 64 zero bytes | v hi, v lo [8 tokens][e_vpitch] bf16 |
-// B rows [r][c + pad] | y rows [ntok][c + pad] | D^T fp32 [ntok][c + 4] | pages [r]; the region
-// sizes follow the launch's largest rank / token chunk / column slice (expand_smem_layout).
+// D[col][n] = B^T[col][rank] · V[rank][n], M = 16 columns, N = 8, K = 16 ranks, where the 8 N
+// columns are (token, part) pairs: v is split into bf16 hi + lo parts (so v keeps fp32-level
+// accuracy) and each part is its own N column, D(col, t) = D[col][2t] + D[col][2t+1] -- one MMA per
+// (tile, k-step) covers 4 tokens' hi and lo parts (a chunk of <= 4 tokens needs half the MMAs of a
+// hi-MMA + lo-MMA scheme with tokens as N).  D is added into the y tile staged in smem (one rounding)
+// and written back with 16-B stores.
+// smem (per unit, kernel_config.h expand_mma_smem): [0,256) barriers + UnitSh | 64 zero bytes |
+// V [token groups of 4][8 (token, part)][rp + 8] bf16 | B rows [r][c + 8] | y rows [ntok][c + 8] |
+// D^T fp32 [ntok][c + 4] | pages [r]; c = the gc's unit width (GC_NCOLS).
 constexpr int kBulkMinBytes = 2048;   // B row slices at least this long go through cp.async.bulk
 #ifndef LORA_EXPAND_MINB
 #define LORA_EXPAND_MINB 3                // expand CTAs per SM the register budget allows (experiments)
@@ -805,13 +807,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);          // [0] B rows, [1] y rows
     UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
     char* zero = smem + 256;                                      // 64 zero bytes
-    const int vpitch = a.e_vpitch;
-    char* vhi = smem + 320;                                       // [8 tokens][vpitch] bf16
-    char* vlo = vhi + kTokChunkMma * vpitch;
-    char* bbuf = smem + a.e_boff;                                 // [r][c + pad]
-    char* ybuf = smem + a.e_yoff;                                 // [ntok][c + pad]
-    float* dt = reinterpret_cast<float*>(smem + a.e_dtoff);      // [ntok][nc + 4]
-    int* spages = reinterpret_cast<int*>(smem + a.e_pgoff);       // [r]
+    char* vt_s = smem + 320;                                      // V [ngrp][8][vpitch] bf16
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int u = ue + a.n_shrink;
 
@@ -829,10 +825,12 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         const int gc = ur.gc, local = ur.local;
         const int r = ur.r, ntok = ur.ntok;
         const DecodeJob J = a.jobs[job];
-        const int c = expand_ncols(r, ES);
+        const int c = gc_field(M, gc, GC_NCOLS);
         const int n0 = local * c;
         const int nc = min(c, J.H_out - n0);
         const int bpitch = c * ES + kPitchPad;
+        char* bbuf = smem + expand_mma_boff(r, ntok);
+        int* spages = reinterpret_cast<int*>(smem + expand_mma_smem(r, c, ntok) - r * 4);
         int pages[LORA_MAX_RANK / 32];
 #pragma unroll
         for (int q = 0; q < LORA_MAX_RANK / 32; ++q) pages[q] = (q * 32 + lane < r) ? page_at(M, poff, q * 32 + lane) : 0;
@@ -841,7 +839,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         const bool bulk = row_bytes >= kBulkMinBytes;
         if (lane == 0) {
             if (bulk) mbar_arrive_expect_tx(&bars[0], (uint32_t)r * row_bytes);
-            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc;
+            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc; sh->j0 = c;
             sh->voff = gc_field(M, gc, GC_VOFF);
             sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
         }
@@ -869,9 +867,15 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     __syncthreads();
     const DecodeJob J = a.jobs[sh->job];
     const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
-    const int c = expand_ncols(r, ES);
+    const int c = sh->j0;                   // the gc's unit width
     const int bpitch = c * ES + kPitchPad;
     const int ypitch = c * ES + kPitchPad;
+    const int rp = (r + 15) & ~15;
+    const int vpitch = (rp + 8) * 2;
+    char* bbuf = smem + expand_mma_boff(r, ntok);
+    char* ybuf = bbuf + r * bpitch;
+    float* dt = reinterpret_cast<float*>(ybuf + ntok * ypitch);   // [ntok][nc + 4]
+    const int* spages = reinterpret_cast<const int*>(smem + expand_mma_smem(r, c, ntok) - r * 4);
     const bool bulk = nc * ES >= kBulkMinBytes;
     if (!bulk) {
         // sub-2-KB row slices: every thread streams 16-B pieces (a warp covers 512 contiguous bytes)
@@ -893,15 +897,16 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
             bulk_g2s(ybuf + lane * ypitch, J.y + ((size_t)tok * J.y_ld + n0) * ES, (uint32_t)nc * ES, &bars[1],
                      policy_evict_normal());
     }
-    // v (fp32, summed over k-slices, scaled) -> bf16 hi/lo tiles [8 tokens][r padded to 16]
-    const int rp = (r + 15) & ~15;
+    const int ngrp = (ntok + 3) >> 2;       // token groups of 4: one MMA each per (tile, k-step)
+    // v (fp32, summed over k-slices, scaled) -> bf16 (hi, lo) rows: token t = 4 grp + tl at rows
+    // [grp][2 tl] (hi) and [grp][2 tl + 1] (lo)
     {
         // v: the k-slice partials summed in slice order, or the compact k-reduced v (TP split)
         const int voff = a.v_compact ? gc_field(M, sh->gc, GC_VRED) : sh->voff;
         const int ksplit = a.v_compact ? 1 : J.ksplit;
         const float* vsrc = a.v_compact ? a.vred : a.vbuf;
         const float scale = sh->scale;
-        for (int i = tid; i < kTokChunkMma * rp; i += kConsumerThreads) {
+        for (int i = tid; i < 4 * ngrp * rp; i += kConsumerThreads) {
             const int t = i / rp, j = i - t * rp;
             float v = 0.f;
             if (t < ntok && j < r) {
@@ -919,8 +924,9 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
             }
             const __nv_bfloat16 h = __float2bfloat16_rn(v);
             const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
-            *reinterpret_cast<__nv_bfloat16*>(vhi + t * vpitch + j * 2) = h;
-            *reinterpret_cast<__nv_bfloat16*>(vlo + t * vpitch + j * 2) = l;
+            char* row = vt_s + ((t >> 2) * 8 + 2 * (t & 3)) * vpitch + j * 2;
+            *reinterpret_cast<__nv_bfloat16*>(row) = h;
+            *reinterpret_cast<__nv_bfloat16*>(row + vpitch) = l;
         }
     }
     if (!bulk) cp_async_wait_all();
@@ -932,49 +938,46 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     // A operand (B^T) via ldmatrix.x4.trans: matrix m = lane/8, row i = lane%8 -> rank j, column n
     const int am = lane >> 3, ai = lane & 7;
     const int aj = ai + ((am & 2) ? 8 : 0), an = (am & 1) * 8;
-    // B operand (v): lanes 0-7 token rows at j, lanes 8-15 at j+8
-    const int vt = lane & 7, vh = (lane >> 3) & 1;
+    // B operand (V): lanes 0-7 rows (token, part) at rank j, lanes 8-15 at j+8
+    const int vn = lane & 7, vh = (lane >> 3) & 1;
     const uint32_t zaddr = smem_u32(zero);
-    const uint32_t vhi_base = smem_u32(vhi) + vt * vpitch + vh * 16;
-    const uint32_t vlo_base = smem_u32(vlo) + vt * vpitch + vh * 16;
+    const uint32_t v_base = smem_u32(vt_s) + vn * vpitch + vh * 16;
     const uint32_t b_base = smem_u32(bbuf);
-    const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), tokens 2cc, 2cc+1
+    const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), N columns 2cc (hi), 2cc+1 (lo) = token cc
     constexpr int kTW = 4;                    // 16-column tiles per warp per pass (2 measured no better on c2)
-    constexpr int kPasses = kMaxNcols / 16 / (kConsumerWarps * kTW);   // 2
     const int dpitch = nc + 4;
 #pragma unroll 1
-    for (int ps = 0; ps < kPasses; ++ps) {
-        const int tile0 = (ps * kConsumerWarps + warp) * kTW;
-        if (tile0 >= ntiles) break;
-        // v = v_hi + v_lo: both MMAs accumulate into one fp32 tile (fixed order)
-        float d[kTW][4];
+    for (int tile0 = warp * kTW; tile0 < ntiles; tile0 += kConsumerWarps * kTW) {
+#pragma unroll 1
+        for (int grp = 0; grp < ngrp; ++grp) {
+            float d[kTW][4];
 #pragma unroll
-        for (int i = 0; i < kTW; ++i)
+            for (int i = 0; i < kTW; ++i)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) d[i][q] = 0.f;
-        for (int s = 0; s < ksteps; ++s) {
-            const int j = s * 16 + aj;
-            uint32_t h0, h1, l0, l1, af[kTW][4];
-            ldsm_x2(h0, h1, vhi_base + s * 32);
-            ldsm_x2(l0, l1, vlo_base + s * 32);
+                for (int q = 0; q < 4; ++q) d[i][q] = 0.f;
+            const uint32_t vg = v_base + grp * 8 * vpitch;
+            for (int s = 0; s < ksteps; ++s) {
+                const int j = s * 16 + aj;
+                uint32_t v0, v1, af[kTW][4];
+                ldsm_x2(v0, v1, vg + s * 32);
 #pragma unroll
-            for (int i = 0; i < kTW; ++i) {
-                const int col = (tile0 + i) * 16 + an;
-                ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
-                              (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
+                for (int i = 0; i < kTW; ++i) {
+                    const int col = (tile0 + i) * 16 + an;
+                    ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
+                                  (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
+                }
+#pragma unroll
+                for (int i = 0; i < kTW; ++i) mma_bf16(d[i], af[i][0], af[i][1], af[i][2], af[i][3], v0, v1);
             }
+            // D^T (hi + lo) -> fp32 [token][col] staging (its own region: no barrier against B readers)
+            const int t = grp * 4 + cc;
+            if (t < ntok) {
 #pragma unroll
-            for (int i = 0; i < kTW; ++i) mma_bf16(d[i], af[i][0], af[i][1], af[i][2], af[i][3], h0, h1);
-#pragma unroll
-            for (int i = 0; i < kTW; ++i) mma_bf16(d[i], af[i][0], af[i][1], af[i][2], af[i][3], l0, l1);
-        }
-        // D^T -> fp32 [token][col] staging (its own region: no barrier against B readers)
-#pragma unroll
-        for (int i = 0; i < kTW; ++i) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int n = (tile0 + i) * 16 + g + ((q & 2) ? 8 : 0), t = 2 * cc + (q & 1);
-                if (t < ntok && n < nc) dt[t * dpitch + n] = d[i][q];
+                for (int i = 0; i < kTW; ++i) {
+                    const int n = (tile0 + i) * 16 + g;
+                    if (n < nc) dt[t * dpitch + n] = d[i][0] + d[i][1];
+                    if (n + 8 < nc) dt[t * dpitch + n + 8] = d[i][2] + d[i][3];
+                }
             }
         }
     }
@@ -1137,23 +1140,14 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         a.job_expand_base[j] = pl.job_expand_base[j];
     }
     if (sizeof(T) == 2) {
-        // bf16 expand smem regions sized for this launch's largest unit
-        int maxr = 1, maxtok = 1, maxc = 8, bsize = 0;
+        // bf16 expand: every CTA lays out its own unit (expand_mma_smem); the launch reserves the largest
+        int e_smem = 0;
         for (int gc = 0; gc < pl.n_gc; ++gc) {
             const int32_t* e = pl.blob.data() + kHdrWords + kGcFields * gc;
-            const int r = e[GC_RANK], c = expand_ncols(r, 2);
-            maxr = r > maxr ? r : maxr;
-            maxtok = e[GC_NTOK] > maxtok ? e[GC_NTOK] : maxtok;
-            maxc = c > maxc ? c : maxc;
-            bsize = r * (c * 2 + kPitchPad) > bsize ? r * (c * 2 + kPitchPad) : bsize;
+            const int need = expand_mma_smem(e[GC_RANK], e[GC_NCOLS], e[GC_NTOK]);
+            e_smem = need > e_smem ? need : e_smem;
         }
-        const int rp = (maxr + 15) & ~15;
-        a.e_vpitch = (rp + 8) * 2;
-        a.e_boff = (320 + 2 * kTokChunkMma * a.e_vpitch + 127) & ~127;
-        a.e_yoff = a.e_boff + bsize;
-        a.e_dtoff = a.e_yoff + maxtok * (maxc * 2 + kPitchPad);
-        a.e_pgoff = a.e_dtoff + maxtok * (maxc + 4) * 4;
-        a.e_smem = a.e_pgoff + maxr * 4;
+        a.e_smem = e_smem;
     }
     const int n = (int)pl.blob.size();
     if (n <= 1024) return launch_pair<T, 1024>(a, pl, st, launches, L.phases, L.num_sms);

@@ -264,8 +264,9 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         e[GC_SCALE] = f32_bits(pl.group_scale[g]);
         e[GC_JOB] = 0;
         e[GC_VRED] = (int32_t)vred;
+        const int nc = expand_cols_gc(r, gcs[c].ntok, H_out, esz);
+        e[GC_NCOLS] = nc;
         shrink += ksplit * shrink_jblocks(r, esz);
-        const int nc = expand_ncols(r, esz);
         expand += (H_out + nc - 1) / nc;
         voff += (int64_t)ksplit * gcs[c].ntok * v_stride(r);
         vred += (int64_t)gcs[c].ntok * v_stride(r);
