@@ -639,16 +639,20 @@ __device__ __forceinline__ uint4 ldg_cg128(const void* p) {
 constexpr int kKPerWarp = kKSlice / kConsumerWarps;   // 128
 constexpr int kKBlocks = kKPerWarp / 32;              // 4
 constexpr int kAPitch = kKSlice * 2 + 64;             // bf16 row pitch: rows g, g+1 land 16 banks apart
-constexpr int kShrinkMmaSmem = 1024 + kShrinkRowsMma * kAPitch + kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4;
-// Launch size of the bf16 shrink CTA (>= the ~39 KB it touches) sets how many shrink CTAs share an
+// smem: [0,128) barrier + unit record | A rows [16][kAPitch] (reused for the warps' partial D tiles
+// [8 warps][16 rows][8 tokens] fp32 once every warp has its A fragments in registers)
+constexpr int kShrinkMmaSmem = 128 + kShrinkRowsMma * kAPitch;
+static_assert(kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4 <= kShrinkRowsMma * kAPitch, "partials fit the A rows");
+// Launch size of the bf16 shrink CTA (>= the ~33 KB it touches) sets how many shrink CTAs share an
 // SM.  One pool per launch prefers 52 KB (4/SM: the grid spreads over more SMs; serial sweep
 // 40 KB 89.9K, 52 KB 94.3K tok/s); grids of more than 4 CTAs per SM (q/k/v in one
-// lora_apply_multi launch, 3x the units) prefer 40 KB (5/SM: more of the grid in one wave).
+// lora_apply_multi launch, 3x the units) take 34 KB (6/SM at <= 40 registers: more of the grid
+// resident while the previous apply's expand CTAs still hold SMEM).
 #ifndef LORA_SHRINK_LAUNCH_KB
 #define LORA_SHRINK_LAUNCH_KB 52                 // grids of <= 4 shrink CTAs per SM (one pool)
 #endif
 #ifndef LORA_SHRINK_LAUNCH_KB_BIG
-#define LORA_SHRINK_LAUNCH_KB_BIG 40             // larger grids (q/k/v multi: 40 KB 99.3K vs 52 KB 98.1K tok/s)
+#define LORA_SHRINK_LAUNCH_KB_BIG 34             // larger grids (q/k/v multi)
 #endif
 constexpr int kShrinkMmaLaunchSmem =
     kShrinkMmaSmem > LORA_SHRINK_LAUNCH_KB * 1024 ? kShrinkMmaSmem : LORA_SHRINK_LAUNCH_KB * 1024;
@@ -659,8 +663,8 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
     constexpr int ES = 2;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                    // [0] A rows
     UnitSh* sh = reinterpret_cast<UnitSh*>(smem + 16);
-    char* abuf = smem + 1024;                                              // [16 rows][kAPitch]
-    float* part = reinterpret_cast<float*>(abuf + kShrinkRowsMma * kAPitch);   // [warp][16 rows][8 tokens]
+    char* abuf = smem + 128;                                               // [16 rows][kAPitch]
+    float* part = reinterpret_cast<float*>(abuf);                          // [warp][16 rows][8 tokens] (after the A reads)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (warp == 0) {
@@ -721,37 +725,26 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
     }
     mbar_wait(&bars[0], 0);
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
-    uint4 ra[kKBlocks], rb[kKBlocks];
+    // one accumulator chain over the warp's k-blocks (fixed order); A fragments loaded per k-block
+    // (<= 40 registers: 6 CTAs per SM)
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int b = 0; b < kKBlocks; ++b) {
         const int k = warp * kKPerWarp + b * 32 + c * 8;
         const bool kin = k < nk;
-        ra[b] = (g < nj && kin) ? lds128(abuf + g * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
-        rb[b] = (g + 8 < nj && kin) ? lds128(abuf + (g + 8) * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 ra = (g < nj && kin) ? lds128(abuf + g * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 rb = (g + 8 < nj && kin) ? lds128(abuf + (g + 8) * kAPitch + k * ES) : make_uint4(0u, 0u, 0u, 0u);
+        mma_bf16(acc, ra.x, rb.x, ra.y, rb.y, xr[b].x, xr[b].y);
+        mma_bf16(acc, ra.z, rb.z, ra.w, rb.w, xr[b].z, xr[b].w);
     }
-    float acc[kKBlocks][4];
-#pragma unroll
-    for (int b = 0; b < kKBlocks; ++b) {
-        acc[b][0] = acc[b][1] = acc[b][2] = acc[b][3] = 0.f;
-        mma_bf16(acc[b], ra[b].x, rb[b].x, ra[b].y, rb[b].y, xr[b].x, xr[b].y);
-        mma_bf16(acc[b], ra[b].z, rb[b].z, ra[b].w, rb[b].w, xr[b].z, xr[b].w);
-    }
+    __syncthreads();   // every warp's A reads done: the partial tiles reuse the A rows
     // D: (row g, tokens 2c, 2c+1) and (row g+8, tokens 2c, 2c+1)
     {
         float* pw = part + warp * kShrinkRowsMma * kTokChunkMma;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            // fixed-order pairwise sum of the warp's k-blocks (kKBlocks = 4 for a 1024-wide k-slice)
-            float kb[kKBlocks];
-#pragma unroll
-            for (int b = 0; b < kKBlocks; ++b) kb[b] = acc[b][q];
-#pragma unroll
-            for (int w = 1; w < kKBlocks; w *= 2)
-#pragma unroll
-                for (int b = 0; b + w < kKBlocks; b += 2 * w) kb[b] += kb[b + w];
-            const float v = kb[0];
             const int row = g + ((q & 2) ? 8 : 0), t = 2 * c + (q & 1);
-            pw[row * kTokChunkMma + t] = v;
+            pw[row * kTokChunkMma + t] = acc[q];
         }
     }
     __syncthreads();
@@ -775,7 +768,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
 }
 
 template <int W>
-__global__ void __launch_bounds__(kConsumerThreads)
+__global__ void __launch_bounds__(kConsumerThreads, 6)
     lora_shrink_mma_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ MetaBlob<W> blob) {
     extern __shared__ __align__(128) char smem[];
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
@@ -794,7 +787,10 @@ __global__ void __launch_bounds__(kConsumerThreads)
 // smem (per unit, kernel_config.h expand_mma_smem): [0,256) barriers + UnitSh | 64 zero bytes |
 // V [token groups of 4][8 (token, part)][rp + 8] bf16 | B rows [r][c + 8] | y rows [ntok][c + 8] |
 // D^T fp32 [ntok][c + 4] | pages [r]; c = the gc's unit width (GC_NCOLS).
-constexpr int kBulkMinBytes = 2048;   // B row slices at least this long go through cp.async.bulk
+#ifndef LORA_EXPAND_BULK_MIN
+#define LORA_EXPAND_BULK_MIN 2048
+#endif
+constexpr int kBulkMinBytes = LORA_EXPAND_BULK_MIN;   // B row slices at least this long go through cp.async.bulk
 #ifndef LORA_EXPAND_MINB
 #define LORA_EXPAND_MINB 3                // expand CTAs per SM the register budget allows (experiments)
 #endif
