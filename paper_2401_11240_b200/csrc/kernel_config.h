@@ -26,11 +26,17 @@ constexpr int kKSlice = LORA_KSLICE;              // k elements per shrink unit 
 constexpr int kSliceBytes = kKSlice * 4;          // fp32 smem row slice
 constexpr int kExpandBytes = 32768;               // fp32 SIMT expand: B bytes per unit (r * ncols * esz)
 constexpr int kMaxNcols = 1024;                   // fp32 SIMT expand: columns per unit
-constexpr int kMaxNcolsMma = 2048;                // bf16 expand: columns per unit
+#ifndef LORA_EXPAND_MAXC
+#define LORA_EXPAND_MAXC 2048
+#endif
+constexpr int kMaxNcolsMma = LORA_EXPAND_MAXC;    // bf16 expand: columns per unit
 // bf16 expand CTA budget: its whole SMEM (v tiles, B rows, staged y rows, fp32 D^T, pages) fits
 // 4 CTAs per SM (228 KB per SM, 1 KB reserved per CTA), so an expand grid of <= 4 x 148 units --
 // q/k/v of a c2 decode batch in one lora_apply_multi -- is resident in ONE wave
-constexpr int kExpandSmemBudget = 56 * 1024;
+#ifndef LORA_EXPAND_BUDGET
+#define LORA_EXPAND_BUDGET (56 * 1024)
+#endif
+constexpr int kExpandSmemBudget = LORA_EXPAND_BUDGET;
 
 // metadata blob layout (int32 words)
 constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, unit_tab, pad
