@@ -798,6 +798,55 @@ constexpr int kBulkMinBytes = LORA_EXPAND_BULK_MIN;   // B row slices at least t
 #define LORA_EXPAND_BIG_MINB 4            // ... for grids of more than 3 expand CTAs per SM
 #endif
 
+// The expand MMAs of one unit: warp w owns 16-column tiles [TW w + 8 TW p, +TW) for passes p; per
+// (tile, k-step) one ldmatrix.x4.trans of B^T feeds NG MMAs (token groups of 4: hi and lo parts as
+// the N columns); D(col, t) = D[col][2t] + D[col][2t+1] goes to the fp32 staging tile dt.
+template <int NG, int TW>
+__device__ __forceinline__ void expand_mma_tiles(int ntiles, int ksteps, int r, int nc, int ntok, int warp, int aj, int an,
+                                                 int g, int cc, uint32_t zaddr, uint32_t v_base, int vpitch,
+                                                 uint32_t b_base, int bpitch, float* dt, int dpitch) {
+    constexpr int ES = 2;
+#pragma unroll 1
+    for (int tile0 = warp * TW; tile0 < ntiles; tile0 += kConsumerWarps * TW) {
+        float d[NG][TW][4];
+#pragma unroll
+        for (int q = 0; q < NG; ++q)
+#pragma unroll
+            for (int i = 0; i < TW; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) d[q][i][e] = 0.f;
+        for (int s = 0; s < ksteps; ++s) {
+            const int j = s * 16 + aj;
+            uint32_t v[NG][2], af[TW][4];
+#pragma unroll
+            for (int q = 0; q < NG; ++q) ldsm_x2(v[q][0], v[q][1], v_base + q * 8 * vpitch + s * 32);
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const int col = (tile0 + i) * 16 + an;
+                ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
+                              (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
+            }
+#pragma unroll
+            for (int q = 0; q < NG; ++q)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) mma_bf16(d[q][i], af[i][0], af[i][1], af[i][2], af[i][3], v[q][0], v[q][1]);
+        }
+        // D^T (hi + lo) -> fp32 [token][col] staging (its own region: no barrier against B readers)
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+            const int t = q * 4 + cc;
+            if (t < ntok) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) {
+                    const int n = (tile0 + i) * 16 + g;
+                    if (n < nc) dt[t * dpitch + n] = d[q][i][0] + d[q][i][1];
+                    if (n + 8 < nc) dt[t * dpitch + n + 8] = d[q][i][2] + d[q][i][3];
+                }
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32_t* M, const int ue, char* smem) {
     constexpr int ES = 2;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);          // [0] B rows, [1] y rows
@@ -940,43 +989,15 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     const uint32_t v_base = smem_u32(vt_s) + vn * vpitch + vh * 16;
     const uint32_t b_base = smem_u32(bbuf);
     const int g = lane >> 2, cc = lane & 3;   // D: column g (+8), N columns 2cc (hi), 2cc+1 (lo) = token cc
-    constexpr int kTW = 4;                    // 16-column tiles per warp per pass (2 measured no better on c2)
     const int dpitch = nc + 4;
-#pragma unroll 1
-    for (int tile0 = warp * kTW; tile0 < ntiles; tile0 += kConsumerWarps * kTW) {
-#pragma unroll 1
-        for (int grp = 0; grp < ngrp; ++grp) {
-            float d[kTW][4];
-#pragma unroll
-            for (int i = 0; i < kTW; ++i)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[i][q] = 0.f;
-            const uint32_t vg = v_base + grp * 8 * vpitch;
-            for (int s = 0; s < ksteps; ++s) {
-                const int j = s * 16 + aj;
-                uint32_t v0, v1, af[kTW][4];
-                ldsm_x2(v0, v1, vg + s * 32);
-#pragma unroll
-                for (int i = 0; i < kTW; ++i) {
-                    const int col = (tile0 + i) * 16 + an;
-                    ldsm_x4_trans(af[i][0], af[i][1], af[i][2], af[i][3],
-                                  (j < r && tile0 + i < ntiles) ? b_base + j * bpitch + col * ES : zaddr);
-                }
-#pragma unroll
-                for (int i = 0; i < kTW; ++i) mma_bf16(d[i], af[i][0], af[i][1], af[i][2], af[i][3], v0, v1);
-            }
-            // D^T (hi + lo) -> fp32 [token][col] staging (its own region: no barrier against B readers)
-            const int t = grp * 4 + cc;
-            if (t < ntok) {
-#pragma unroll
-                for (int i = 0; i < kTW; ++i) {
-                    const int n = (tile0 + i) * 16 + g;
-                    if (n < nc) dt[t * dpitch + n] = d[i][0] + d[i][1];
-                    if (n + 8 < nc) dt[t * dpitch + n + 8] = d[i][2] + d[i][3];
-                }
-            }
-        }
-    }
+    // chunks of <= 4 tokens: one token group, 4 column tiles per warp pass; 5..8 tokens: both groups
+    // share every B fragment (2 MMAs per ldmatrix), 2 tiles per pass (same accumulator registers)
+    if (ngrp == 1)
+        expand_mma_tiles<1, 4>(ntiles, ksteps, r, nc, ntok, warp, aj, an, g, cc, zaddr, v_base, vpitch, b_base, bpitch,
+                               dt, dpitch);
+    else
+        expand_mma_tiles<2, 2>(ntiles, ksteps, r, nc, ntok, warp, aj, an, g, cc, zaddr, v_base, vpitch, b_base, bpitch,
+                               dt, dpitch);
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 7] = gtime();
     mbar_wait(&bars[1], 0);
     if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 6] = gtime();

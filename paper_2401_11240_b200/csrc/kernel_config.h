@@ -37,6 +37,7 @@ constexpr int kMaxNcolsMma = LORA_EXPAND_MAXC;    // bf16 expand: columns per un
 #define LORA_EXPAND_BUDGET (56 * 1024)
 #endif
 constexpr int kExpandSmemBudget = LORA_EXPAND_BUDGET;
+constexpr int kExpandSmemBudget3 = 75 * 1024;   // the largest bf16 expand CTA of which 3 share an SM
 
 // metadata blob layout (int32 words)
 constexpr int kHdrWords = 8;     // n_gc, n_shrink, n_expand, n_pages, n_toks, ksplit, unit_tab, pad
@@ -85,12 +86,12 @@ LORA_HD int expand_mma_smem(int r, int nc, int ntok) {
 // expand unit width of a gc (columns, the last unit of a gc may be narrower).  fp32: the power-of-two
 // rule above.  bf16: as few units as fit kExpandSmemBudget each -- widths are multiples of 16 (MMA
 // tiles; an odd number of 16-B vectors in the SMEM row pitch keeps ldmatrix conflict-free), not
-// powers of two, so a gc's B bytes split into near-equal units of up to ~48 KB
-LORA_HD int expand_cols_gc(int r, int ntok, int H_out, int esz) {
-    if (esz != 2) return expand_ncols(r, esz);
+// powers of two, so a gc's B bytes split into near-equal units (budget 0: the power-of-two rule)
+LORA_HD int expand_cols_gc(int r, int ntok, int H_out, int esz, int budget) {
+    if (esz != 2 || budget <= 0) return expand_ncols(r, esz);   // budget 0: round 1's power-of-two units
     for (int nu = (H_out + kMaxNcolsMma - 1) / kMaxNcolsMma;; ++nu) {
         const int nc = ((H_out + nu - 1) / nu + 15) & ~15;
-        if (nc <= 16 || expand_mma_smem(r, nc, ntok) <= kExpandSmemBudget) return nc;
+        if (nc <= 16 || expand_mma_smem(r, nc, ntok) <= budget) return nc;
     }
 }
 // row stride of a gc's rank-r intermediate in the v scratch: r rounded up to 4 floats, so every

@@ -29,7 +29,7 @@ static lora_status append_unit_table(Plan& pl, std::string& err);
 
 lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, int H_in, int H_out,
                        int esz, int L_tc, bool tc_enabled, const AdapterTable& table, std::string& err,
-                       int pad_zero_page, int pf_sms) {
+                       int pad_zero_page, int pf_sms, int expand_budget) {
     if (S < 0) { err = "num_segments < 0"; return LORA_ERR_ARG; }
     if (S > 0 && (ip == nullptr || ids == nullptr)) { err = "seg_indptr/adapter_ids is NULL"; return LORA_ERR_ARG; }
     if (S > 0 && ip[0] != 0) { err = "seg_indptr[0] != 0"; return LORA_ERR_ARG; }
@@ -251,6 +251,31 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
     const int toks_base = pages_base + (int)blob_pages.size();
     int shrink = 0, expand = 0;
     int64_t voff = 0, vred = 0;
+    // expand unit widths (DESIGN.md §6 N1).  expand_budget > 0: the widest units within that SMEM
+    // budget (lora_apply_multi: kExpandSmemBudget, so a q/k/v grid is resident in one wave).  Single-
+    // pool applies (expand_budget <= 0): round 1's power-of-two 32 KB units -- more, shorter CTAs --
+    // while that grid is resident in one wave at >= 3 CTAs per SM, else the kExpandSmemBudget units.
+    static thread_local std::vector<int32_t> gc_nc;
+    gc_nc.resize(n_gc);
+    auto size_units = [&](int budget) {
+        int units = 0, smem = 0;
+        for (int c = 0; c < n_gc; ++c) {
+            const int r = pad_zero_page >= 0 ? (int)pl.max_rank : pl.group_rank[gcs[c].g];
+            gc_nc[c] = expand_cols_gc(r, gcs[c].ntok, H_out, esz, budget);
+            units += (H_out + gc_nc[c] - 1) / gc_nc[c];
+            if (esz == 2) smem = std::max(smem, expand_mma_smem(r, gc_nc[c], gcs[c].ntok));
+        }
+        return std::make_pair(units, smem);
+    };
+    if (expand_budget > 0) {
+        size_units(expand_budget);
+    } else if (esz == 2) {
+        const auto pw2 = size_units(0);
+        const int sms = pf_sms > 0 ? pf_sms : 148;
+        if (pw2.first > 3 * sms || pw2.second > kExpandSmemBudget3) size_units(kExpandSmemBudget);
+    } else {
+        size_units(0);
+    }
     for (int c = 0; c < n_gc; ++c) {
         const int g = gcs[c].g, r = pad_zero_page >= 0 ? (int)pl.max_rank : pl.group_rank[g];
         int32_t* e = gct + kGcFields * c;
@@ -264,7 +289,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
         e[GC_SCALE] = f32_bits(pl.group_scale[g]);
         e[GC_JOB] = 0;
         e[GC_VRED] = (int32_t)vred;
-        const int nc = expand_cols_gc(r, gcs[c].ntok, H_out, esz);
+        const int nc = gc_nc[c];
         e[GC_NCOLS] = nc;
         shrink += ksplit * shrink_jblocks(r, esz);
         expand += (H_out + nc - 1) / nc;

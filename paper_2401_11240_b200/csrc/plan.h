@@ -81,7 +81,8 @@ struct Plan {
 // Returns LORA_OK or an error status with `err` naming the offending operand.
 lora_status build_plan(Plan& plan, const int32_t* seg_indptr, const int32_t* adapter_ids, int S,
                        int H_in, int H_out, int esz, int L_tc, bool tc_enabled,
-                       const AdapterTable& table, std::string& err, int pad_zero_page = -1, int pf_sms = 0);
+                       const AdapterTable& table, std::string& err, int pad_zero_page = -1, int pf_sms = 0,
+                       int expand_budget = 0);   // bytes per expand CTA, 0: single-pool rule (plan.cpp)
 
 // ---- kernel launch descriptors (pool.cpp -> *_kernel.cu) ----
 struct DecodeLaunch {

@@ -592,7 +592,8 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
         lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
-                                   p->tc_prefill, p->table, err, -1, p->num_sms);
+                                   p->tc_prefill, p->table, err, -1, p->num_sms,
+                                   n_pools > 1 ? kExpandSmemBudget : 0);
         if (s != LORA_OK) return fail(s, "pool " + std::to_string(i) + ": " + err);
         p->split_ready = false;
     }
