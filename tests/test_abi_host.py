@@ -170,3 +170,61 @@ def test_pad_max_rank_keeps_metadata_and_pads_work():
     assert padded["n_shrink_units"] % (n_gc * (64 // 16)) == 0
     assert padded["n_shrink_units"] > plain["n_shrink_units"]
     assert padded["n_expand_units"] > plain["n_expand_units"]
+
+
+def _mma_unit_smem(r, nc, ntok):
+    # bf16 expand CTA layout (kernel_config.h expand_mma_smem): header + v tiles | B rows | y rows |
+    # fp32 D^T | pages
+    rp = (r + 15) & ~15
+    boff = (320 + ((ntok + 3) >> 2) * 8 * (rp + 8) * 2 + 127) & ~127
+    pitch = nc * 2 + 16
+    return boff + r * pitch + ntok * pitch + ntok * (nc + 4) * 4 + r * 4
+
+
+def _pow2_units(r, H):
+    c = 1
+    while c * 2 <= 32768 // (r * 2):
+        c *= 2
+    c = min(c, 1024)
+    return -(-H // c), c
+
+
+def test_expand_unit_sizing_rule():
+    """Decode expand units (DESIGN.md §6 N1): a single-pool batch whose power-of-two 32 KB units fit
+    one wave keeps them; a bigger one switches to the widest multiple-of-16 units of <= 56 KB each,
+    so the expand grid stays within 4 CTAs per SM."""
+    b = gen.config_c2()
+    pool = L.LoraPool(b.H_in, b.H_out, 40, "bf16", max_total_rank=sum(a.rank for a in b.adapters), host_only=True)
+    for a in b.adapters:
+        pool.load_adapter(a.id, a.rank, None, None, a.scale)
+    pool.plan(b.seg_indptr, b.adapter_ids)
+    md = pool.metadata()
+    pool.close()
+    ranks = {a.id: a.rank for a in b.adapters}
+    want = sum(_pow2_units(ranks[i], b.H_out)[0] for i in sorted(set(b.adapter_ids.tolist())))
+    assert md["n_expand_units"] == want == 256
+
+    # 256 adapters x 2 tokens: power-of-two units would need 2048 CTAs (> 3 x 148)
+    n_ad, H = 256, 4096
+    rk = [8, 16, 32, 64]
+    pool = L.LoraPool(H, H, n_ad, "bf16", max_total_rank=sum(rk[i % 4] for i in range(n_ad)), host_only=True)
+    for i in range(n_ad):
+        pool.load_adapter(i, rk[i % 4], None, None, 1.0)
+    ids = np.repeat(np.arange(n_ad, dtype=np.int32), 2)
+    ip = np.arange(len(ids) + 1, dtype=np.int32)
+    pool.plan(ip, ids)
+    md = pool.metadata()
+    pool.close()
+    units = 0
+    for i in range(n_ad):
+        r = rk[i % 4]
+        nu = (H + 2047) // 2048
+        while True:
+            nc = ((H + nu - 1) // nu + 15) & ~15
+            if nc <= 16 or _mma_unit_smem(r, nc, 2) <= 56 * 1024:
+                break
+            nu += 1
+        assert _mma_unit_smem(r, nc, 2) <= 56 * 1024 and nc % 16 == 0
+        units += -(-H // nc)
+    assert md["n_expand_units"] == units
+    assert units < sum(_pow2_units(rk[i % 4], H)[0] for i in range(n_ad))
