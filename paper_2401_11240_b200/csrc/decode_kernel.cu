@@ -648,6 +648,12 @@ static_assert(kConsumerWarps * kShrinkRowsMma * kTokChunkMma * 4 <= kShrinkRowsM
 // 40 KB 89.9K, 52 KB 94.3K tok/s); grids of more than 4 CTAs per SM (q/k/v in one
 // lora_apply_multi launch, 3x the units) take 34 KB (6/SM at <= 40 registers: more of the grid
 // resident while the previous apply's expand CTAs still hold SMEM).
+#ifndef LORA_X_PREFETCH
+#define LORA_X_PREFETCH 1                         // shrink: L2 prefetch of the x rows before the PDL wait
+#endif
+#ifndef LORA_Y_PREFETCH
+#define LORA_Y_PREFETCH 1                         // expand: L2 prefetch of the y rows before the PDL wait
+#endif
 #ifndef LORA_SHRINK_LAUNCH_KB
 #define LORA_SHRINK_LAUNCH_KB 52                 // grids of <= 4 shrink CTAs per SM (one pool)
 #endif
@@ -691,7 +697,7 @@ __device__ __forceinline__ void shrink_mma_body(const DecodeArgs& a, const int32
         const int voff = gc_field(M, gc, GC_VOFF);
         if (a.trace) { asm volatile("" ::"r"(page), "r"(tokv)); if (lane == 0) a.trace[(size_t)u * 8 + 7] = gtime(); }
         if (lane < kTokChunkMma) sh->tok[lane] = tokv;
-        if (tokv >= 0) prefetch_l2(J.x + ((size_t)tokv * J.x_ld + k0) * ES, (uint32_t)(nk * ES));
+        if (LORA_X_PREFETCH && tokv >= 0) prefetch_l2(J.x + ((size_t)tokv * J.x_ld + k0) * ES, (uint32_t)(nk * ES));
         if (lane == 0) {
             mbar_arrive_expect_tx(&bars[0], (uint32_t)(nj * nk * ES));
             sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->ks = ks; sh->j0 = j0; sh->nj = nj;
@@ -890,7 +896,7 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
         }
         if (lane < ntok) {
             sh->tok[lane] = tok;
-            prefetch_l2(J.y + ((size_t)tok * J.y_ld + n0) * ES, row_bytes);
+            if (LORA_Y_PREFETCH) prefetch_l2(J.y + ((size_t)tok * J.y_ld + n0) * ES, row_bytes);
         }
         if (lane < 16) reinterpret_cast<uint32_t*>(zero)[lane] = 0u;
         __syncwarp();
