@@ -687,3 +687,44 @@ def test_prefill_few_tile_splits(L, H_in, H_out, n_tiles):
     ref = O.delta_for_batch(b, n_threads=16)
     assert rel_l2(y, ref, "bf16") <= TOL["bf16"]
 
+
+
+@pytest.mark.gpu
+def test_expand_unit_widths_multi_and_large_single(L):
+    """Decode expand units of both sizing rules (DESIGN.md §6 N1): a q/k/v-style lora_apply_multi
+    (widest <= 56 KB units, non-power-of-two widths, H_out = 1000 so the last unit of each gc is
+    ragged) with chunks of 1..8 tokens (one and two token groups per MMA) == separate lora_apply
+    calls bit for bit and within tolerance of the oracle; and a single-pool batch large enough to
+    leave the power-of-two rule (256 adapters x 2 tokens) against the oracle."""
+    import torch
+    rng = np.random.default_rng(5150)
+    lens = [int(v) for v in rng.integers(1, 9, size=40)]
+    ids = [int(v) for v in rng.integers(0, 24, size=40)]
+    ranks = {a: int(v) for a, v in enumerate(rng.choice([1, 8, 13, 16, 24, 32, 64, 100, 128], size=24))}
+    shapes = [(1024, 1000), (1024, 256), (1024, 256)]
+    batches = [gen.build_batch("wm%d" % i, 5150 + i, "bf16", hin, hout, lens, ids, ranks, y_zero=False)
+               for i, (hin, hout) in enumerate(shapes)]
+    batches[1].x = batches[0].x.copy()
+    batches[2].x = batches[0].x.copy()
+    pools = [make_pool(b, L) for b in batches]
+    xs = [to_torch(b.x, "cuda") for b in batches]
+    y_sep = [to_torch(b.y_in, "cuda") for b in batches]
+    y_fus = [to_torch(b.y_in, "cuda") for b in batches]
+    for p, x, y, b in zip(pools, xs, y_sep, batches):
+        p.apply(x, y, b.seg_indptr, b.adapter_ids)
+    L.apply_multi(pools, xs, y_fus, batches[0].seg_indptr, batches[0].adapter_ids)
+    torch.cuda.synchronize()
+    for b, ys_, yf in zip(batches, y_sep, y_fus):
+        assert torch.equal(ys_, yf)
+        ref = O.delta_for_batch(b, n_threads=8)
+        assert rel_l2(from_torch(yf, "bf16"), ref, "bf16") <= TOL["bf16"]
+    for p in pools:
+        p.close()
+
+    n_ad = 256
+    big = gen.build_batch("wide", 5160, "bf16", 1024, 1000, [2] * n_ad, list(range(n_ad)),
+                          {a: [8, 16, 32, 64][a % 4] for a in range(n_ad)}, y_zero=False)
+    y, md = run_gpu(big, L)
+    assert md["n_expand_units"] < sum(-(-1000 // c) for c in
+                                      [1024 if r <= 16 else 32768 // (2 * r) for r in [8, 16, 32, 64] * 64])
+    assert rel_l2(y, O.delta_for_batch(big, n_threads=8), "bf16") <= TOL["bf16"]
