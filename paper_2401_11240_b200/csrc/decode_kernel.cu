@@ -587,15 +587,16 @@ __global__ void __launch_bounds__(kConsumerThreads)
 
 // ------------------------------------------------------------------ bf16 tensor-core (mma.sync) kernels
 // The decode delta is HBM-bound; what limits a kernel that computes only after its data
-// arrived is the burst of issue slots and shared-memory bandwidth spent once the
-// preceding grid completes.  The bf16 kernels therefore (a) keep the shrink operand out of
-// shared memory entirely -- A rows go HBM -> registers with coalesced 128-bit loads issued
-// BEFORE griddepcontrol.wait, in the m16n8k16 fragment layout up to a permutation of k
-// that the x fragments repeat (the dot product is order-free in k) -- and (b) read the
-// expand operand from shared memory exactly once (swap-AB: B^T tiles via ldmatrix.trans,
-// v fragments hoisted per warp).  The MMA (fp32 accumulate) is a dot-product engine here:
-// tiles are padded with zero rows (tokens to 8, ranks to 16) in registers / smem only;
-// HBM bytes are exactly the algorithmic ones.
+// arrived is the chain after griddepcontrol.wait and how many adapter rows can be in flight
+// before it (SMEM capacity).  The bf16 kernels therefore (a) stream every adapter row HBM -> SMEM
+// before the wait (cp.async.bulk / LDGSTS) and read it once into mma.sync fragments (the shrink's
+// A rows in the m16n8k16 layout up to a permutation of k that the x fragments repeat -- the dot
+// product is order-free in k), (b) size their units so a q/k/v-sized grid is resident in one
+// wave (6 shrink / 4 expand CTAs per SM), and (c) read the expand operand from shared memory
+// exactly once (swap-AB: B^T tiles via ldmatrix.trans, each fragment feeding every token group).
+// The MMA (fp32 accumulate) is a dot-product engine here: tiles are padded with zero rows (tokens
+// to 8 N columns of (token, hi|lo) pairs, ranks to 16) in registers / smem only; HBM bytes are
+// exactly the algorithmic ones.
 constexpr int kPitchPad = 16;   // bytes added to each smem row: conflict-free ldmatrix
 
 __device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
