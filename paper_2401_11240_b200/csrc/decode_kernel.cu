@@ -1027,221 +1027,6 @@ __device__ __forceinline__ void expand_mma_body(const DecodeArgs& a, const int32
     }
 }
 
-#if LORA_EXPAND_TC
-// ---- expand (bf16) on the 5th-generation tensor cores: one CTA = (group-chunk gc, column slice).
-// D[col][n] = B^T[col][rank] · V[rank][n] as tcgen05.mma kind::f16, M = 128 columns (A = B^T, MN-major:
-// the B rows as SWIZZLE_128B atoms of 64 columns x 8 ranks, loaded by LDGSTS straight into that
-// layout; ranks r..rp-1 zero-filled), N = 8 per group of 4 tokens (hi and lo part of v as their own
-// columns), K = 16 ranks, fp32 accumulators in TMEM.  One thread issues every MMA of the unit; the
-// epilogue reads D with tcgen05.ld (thread = column), adds hi + lo into the staged y rows (one
-// rounding) and writes them back with 16-B stores.
-__device__ __forceinline__ uint64_t tc_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {   // SW128, sm_100 v1
-    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
-}
-__device__ __forceinline__ void expand_tc_body(const DecodeArgs& a, const int32_t* M, const int ue, char* smem) {
-    constexpr int ES = 2;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u = ue + a.n_shrink;
-    const uint32_t raw = smem_u32(smem);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    char* gb = smem + (base - raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gb);            // [1] y rows, [2] MMAs done
-    UnitSh* sh = reinterpret_cast<UnitSh*>(gb + 32);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(gb + 256);
-    const uint32_t vbase = base + 1024;
-
-    int tok = 0;
-    if (warp == 0) {
-        if (lane == 0) {
-            mbar_init(&bars[1], 1);
-            mbar_init(&bars[2], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        const int job = job_of(ue, a.n_jobs, a.job_expand_base);
-        const UnitRec ur = load_unit(M, a.unit_tab, a.unit_words, a.n_shrink + ue, false);
-        const int gc = ur.gc, r = ur.r, ntok = ur.ntok;
-        const DecodeJob J = a.jobs[job];
-        const int c = gc_field(M, gc, GC_NCOLS);
-        const int n0 = ur.local * c;
-        const int nc = min(c, J.H_out - n0);
-        int* spages = reinterpret_cast<int*>(gb + 1024 + expand_tc_vbytes(r, ntok) + expand_tc_bbytes(r, c) +
-                                             ntok * (c * ES + kPitchPad));
-#pragma unroll
-        for (int q = 0; q < LORA_MAX_RANK / 32; ++q)
-            if (q * 32 + lane < r) spages[q * 32 + lane] = page_at(M, ur.pref, q * 32 + lane);
-        tok = lane < ntok ? M[ur.toff + lane] : 0;
-        if (lane == 0) {
-            sh->gc = gc; sh->job = job; sh->r = r; sh->ntok = ntok; sh->n0 = n0; sh->nc = nc; sh->j0 = c;
-            sh->voff = gc_field(M, gc, GC_VOFF);
-            sh->scale = __int_as_float(gc_field(M, gc, GC_SCALE));
-        }
-        if (lane < ntok) {
-            sh->tok[lane] = tok;
-            if (LORA_Y_PREFETCH) prefetch_l2(J.y + ((size_t)tok * J.y_ld + n0) * ES, (uint32_t)nc * ES);
-        }
-        // TMEM: 8 ngrp fp32 columns per 128-column MMA tile (power of two >= 32)
-        const int need = ((nc + 127) >> 7) * 8 * ((ntok + 3) >> 2);
-        uint32_t ncols = 32;
-        while ((int)ncols < need) ncols <<= 1;
-        __syncwarp();
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(ncols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        if (lane == 0) tslot[1] = ncols;
-    }
-    __syncthreads();
-    const DecodeJob J = a.jobs[sh->job];
-    const int r = sh->r, ntok = sh->ntok, n0 = sh->n0, nc = sh->nc;
-    const int c = sh->j0;
-    const int rp = (r + 15) & ~15;
-    const int ngrp = (ntok + 3) >> 2;
-    const uint32_t bt = vbase + (uint32_t)expand_tc_vbytes(r, ntok);      // B^T atoms [2 ceil(c/128)][rp][128 B]
-    char* gbt = gb + (bt - base);
-    const int ypitch = c * ES + kPitchPad;
-    char* ybuf = gbt + expand_tc_bbytes(r, c);
-    const int* spages = reinterpret_cast<const int*>(ybuf + ntok * ypitch);
-    float* dt = reinterpret_cast<float*>(ybuf + ntok * ypitch + ((r * 4 + 15) & ~15));   // [ntok][nc + 4]
-    const int dpitch = nc + 4;
-    {
-        // B rows [0, r) of this unit's columns: 16-B LDGSTS pieces into the swizzled atoms; ranks
-        // [r, rp) of every atom zero (the MMA reads them: never a neighbouring page)
-        const uint64_t pol = policy_evict_first();
-        const int vpr = nc / 8;
-        for (int i = tid; i < r * vpr; i += kConsumerThreads) {
-            const int j = i / vpr, q = i - j * vpr;
-            cp_async16(gbt + (q >> 3) * rp * 128 + j * 128 + (((q & 7) ^ (j & 7)) << 4),
-                       J.B + ((size_t)spages[j] * J.H_out + n0 + q * 8) * ES, pol);
-        }
-        cp_async_commit();
-        const int natoms = ((c + 127) >> 7) * 2;
-        for (int i = tid; i < natoms * (rp - r) * 8; i += kConsumerThreads) {
-            const int at = i / ((rp - r) * 8), rem = i - at * (rp - r) * 8;
-            *reinterpret_cast<uint4*>(gbt + at * rp * 128 + (r + (rem >> 3)) * 128 + ((rem & 7) << 4)) =
-                make_uint4(0u, 0u, 0u, 0u);
-        }
-    }
-    pdl_launch_dependents();
-    pdl_wait_cta();   // v from the shrink kernel, y from whoever wrote it
-    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 2] = gtime();
-    if (warp == 0) {
-        if (lane == 0) mbar_arrive_expect_tx(&bars[1], (uint32_t)(ntok * nc * ES));
-        __syncwarp();
-        if (lane < ntok)
-            bulk_g2s(ybuf + lane * ypitch, J.y + ((size_t)tok * J.y_ld + n0) * ES, (uint32_t)nc * ES, &bars[1],
-                     policy_evict_normal());
-    }
-    {
-        // v (fp32, k-slice partials summed in slice order, scaled) -> bf16 hi / lo as the K-major B
-        // operand: row n = 2 (t % 4) + part of token group t / 4, SWIZZLE_128B
-        const int voff = a.v_compact ? gc_field(M, sh->gc, GC_VRED) : sh->voff;
-        const int ksplit = a.v_compact ? 1 : J.ksplit;
-        const float* vsrc = a.v_compact ? a.vred : a.vbuf;
-        const float scale = sh->scale;
-        char* gv = gb + 1024;
-        for (int i = tid; i < 4 * ngrp * rp; i += kConsumerThreads) {
-            const int t = i / rp, j = i - t * rp;
-            float v = 0.f;
-            if (t < ntok && j < r) {
-                const float* src = vsrc + voff + t * v_stride(r) + j;
-                const int stride = ntok * v_stride(r);
-                for (int k0 = 0; k0 < ksplit; k0 += 8) {
-                    float p[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) p[q] = k0 + q < ksplit ? ld_cg_f32(src + (k0 + q) * stride) : 0.f;
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) v += p[q];
-                }
-                v *= scale;
-            }
-            const __nv_bfloat16 h = __float2bfloat16_rn(v);
-            const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
-            const int n = 2 * t;                      // rows n (hi), n + 1 (lo) over all groups
-            const int kb = (j & 63) * 2;
-            char* at = gv + (j >> 6) * ngrp * 1024;
-            *reinterpret_cast<__nv_bfloat16*>(at + n * 128 + ((((kb >> 4) ^ (n & 7))) << 4) + (kb & 15)) = h;
-            *reinterpret_cast<__nv_bfloat16*>(at + (n + 1) * 128 + ((((kb >> 4) ^ ((n + 1) & 7))) << 4) + (kb & 15)) = l;
-        }
-    }
-    cp_async_wait_all();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> tensor-core reads
-    __syncthreads();
-    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 3] = gtime();
-    const uint32_t tmem = *tslot;
-    const int nmt = (nc + 127) >> 7;
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0) {
-            // D fp32, A / B bf16, A MN-major, B K-major, N = 8 ngrp, M = 128
-            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)ngrp << 17) | (8u << 24);
-            // k-step outer, tile inner: consecutive MMAs write different accumulators (no dependency)
-            for (int ks = 0; ks < rp / 16; ++ks)
-                for (int m = 0; m < nmt; ++m) {
-                    const uint64_t ad = tc_desc(bt + (uint32_t)(2 * m * rp * 128 + ks * 2048), (uint32_t)rp * 128u, 1024);
-                    const uint64_t bd = tc_desc(vbase + (uint32_t)((ks >> 2) * ngrp * 1024 + (ks & 3) * 32), 16, 1024);
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(m * 8 * ngrp)),
-                        "l"(ad), "l"(bd), "r"(idesc), "r"(ks)
-                        : "memory");
-                }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bars[2]))
-                         : "memory");
-        }
-        __syncwarp();
-    }
-    mbar_wait(&bars[1], 0);   // y rows staged
-    mbar_wait(&bars[2], 0);   // every MMA done
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (a.trace && tid == 0) a.trace[(size_t)u * 8 + 7] = gtime();
-    {
-        // warp w reads TMEM lanes 32 (w % 4) .. of the tiles m = w / 4, w / 4 + 2, ...: thread = column
-        const int lq = warp & 3;
-        for (int m = warp >> 2; m < nmt; m += kConsumerWarps / 4) {
-            const uint32_t taddr = tmem + ((uint32_t)(32 * lq) << 16) + (uint32_t)(m * 8 * ngrp);
-            uint32_t d[16];
-            if (ngrp == 1) {
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
-                             : "r"(taddr));
-            } else {
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                             : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
-                               "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
-                             : "r"(taddr));
-            }
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int col = m * 128 + 32 * lq + lane;
-            if (col < nc) {
-#pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    if (t < ntok) dt[t * dpitch + col] = __uint_as_float(d[2 * t]) + __uint_as_float(d[2 * t + 1]);
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tslot[1]));
-    {
-        const int vpr = nc / 8;   // 16-B vectors per token row
-        for (int i = tid; i < ntok * vpr; i += kConsumerThreads) {
-            const int t = i / vpr, q = i - t * vpr;
-            const float4 d0 = *reinterpret_cast<const float4*>(dt + t * dpitch + q * 8);
-            const float4 d1 = *reinterpret_cast<const float4*>(dt + t * dpitch + q * 8 + 4);
-            const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-            const uint4 yo = lds128(ybuf + t * ypitch + q * 16);
-            stg128_na(J.y + ((size_t)sh->tok[t] * J.y_ld + n0 + q * 8) * ES, Elem<__nv_bfloat16>::add_round(yo, d));
-        }
-    }
-    if (a.trace && tid == 0) {
-        a.trace[(size_t)u * 8 + 0] = smid();
-        a.trace[(size_t)u * 8 + 4] = sh->r;
-        a.trace[(size_t)u * 8 + 6] = gtime();
-        a.trace[(size_t)u * 8 + 5] = gtime();
-    }
-}
-#endif
-
 // MINB: CTAs per SM the register budget allows (3: <= 85 registers; 4: <= 64, no spills) -- the
 // launcher takes 4 only for grids of more than 3 expand CTAs per SM (q/k/v multi launches)
 template <int W, int MINB = LORA_EXPAND_MINB>
@@ -1251,11 +1036,7 @@ __global__ void __launch_bounds__(kConsumerThreads, MINB)
     const int32_t* M = (W > 1) ? blob.w : a.meta_global;
     if (a.trace && threadIdx.x == 0) a.trace[(size_t)(blockIdx.x + a.n_shrink) * 8 + 1] = gtime();
     if (W == 1) pdl_wait_cta();
-#if LORA_EXPAND_TC
-    expand_tc_body(a, M, blockIdx.x, smem);
-#else
     expand_mma_body(a, M, blockIdx.x, smem);
-#endif
 }
 
 // copies a metadata blob too large for one kernel's parameters into device memory,
@@ -1387,7 +1168,7 @@ static cudaError_t launch_typed(const Plan& pl, const DecodeLaunch& L, cudaStrea
         int e_smem = 0;
         for (int gc = 0; gc < pl.n_gc; ++gc) {
             const int32_t* e = pl.blob.data() + kHdrWords + kGcFields * gc;
-            const int need = expand_unit_smem(e[GC_RANK], e[GC_NCOLS], e[GC_NTOK]);
+            const int need = expand_mma_smem(e[GC_RANK], e[GC_NCOLS], e[GC_NTOK]);
             e_smem = need > e_smem ? need : e_smem;
         }
         a.e_smem = e_smem;

@@ -83,22 +83,6 @@ LORA_HD int expand_mma_smem(int r, int nc, int ntok) {
     const int pitch = nc * 2 + 16;
     return expand_mma_boff(r, ntok) + r * pitch + ntok * pitch + ntok * (nc + 4) * 4 + r * 4;
 }
-// tcgen05 expand (LORA_EXPAND_TC): [align slack 1 KB] | [0,1024) barriers, unit record, TMEM slot |
-// V as the K-major B operand, SWIZZLE_128B [rp / 64][8 ngrp rows][128 B] | B^T as the MN-major A operand,
-// SWIZZLE_128B [2 ceil(nc / 128) column atoms][rp][128 B] | y rows [ntok][nc + 8] | pages [r] |
-// fp32 D^T [ntok][nc + 4]
-#ifndef LORA_EXPAND_TC
-#define LORA_EXPAND_TC 0
-#endif
-LORA_HD int expand_tc_vbytes(int r, int ntok) { return ((((r + 15) & ~15) + 63) >> 6) * ((ntok + 3) >> 2) * 1024; }
-LORA_HD int expand_tc_bbytes(int r, int nc) { return ((nc + 127) >> 7) * 2 * ((r + 15) & ~15) * 128; }
-LORA_HD int expand_tc_smem(int r, int nc, int ntok) {
-    return 1024 + 1024 + expand_tc_vbytes(r, ntok) + expand_tc_bbytes(r, nc) + ntok * (nc * 2 + 16) +
-           ((r * 4 + 15) & ~15) + ntok * (nc + 4) * 4;
-}
-LORA_HD int expand_unit_smem(int r, int nc, int ntok) {
-    return LORA_EXPAND_TC ? expand_tc_smem(r, nc, ntok) : expand_mma_smem(r, nc, ntok);
-}
 // expand unit width of a gc (columns, the last unit of a gc may be narrower).  fp32: the power-of-two
 // rule above.  bf16: as few units as fit kExpandSmemBudget each -- widths are multiples of 16 (MMA
 // tiles; an odd number of 16-B vectors in the SMEM row pitch keeps ldmatrix conflict-free), not
@@ -107,7 +91,7 @@ LORA_HD int expand_cols_gc(int r, int ntok, int H_out, int esz, int budget) {
     if (esz != 2 || budget <= 0) return expand_ncols(r, esz);   // budget 0: round 1's power-of-two units
     for (int nu = (H_out + kMaxNcolsMma - 1) / kMaxNcolsMma;; ++nu) {
         const int nc = ((H_out + nu - 1) / nu + 15) & ~15;
-        if (nc <= 16 || expand_unit_smem(r, nc, ntok) <= budget) return nc;
+        if (nc <= 16 || expand_mma_smem(r, nc, ntok) <= budget) return nc;
     }
 }
 // row stride of a gc's rank-r intermediate in the v scratch: r rounded up to 4 floats, so every

@@ -263,7 +263,7 @@ lora_status build_plan(Plan& pl, const int32_t* ip, const int32_t* ids, int S, i
             const int r = pad_zero_page >= 0 ? (int)pl.max_rank : pl.group_rank[gcs[c].g];
             gc_nc[c] = expand_cols_gc(r, gcs[c].ntok, H_out, esz, budget);
             units += (H_out + gc_nc[c] - 1) / gc_nc[c];
-            if (esz == 2) smem = std::max(smem, expand_unit_smem(r, gc_nc[c], gcs[c].ntok));
+            if (esz == 2) smem = std::max(smem, expand_mma_smem(r, gc_nc[c], gcs[c].ntok));
         }
         return std::make_pair(units, smem);
     };
