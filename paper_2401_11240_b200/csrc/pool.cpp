@@ -73,7 +73,49 @@ struct lora_pool {
     float* vred = nullptr;                // TP: the compact k-reduced v all-reduced by lora_apply_tp
     size_t vred_cap = 0;
     lora_tp_comm* tp = nullptr;           // lora_tp_init: the TP group's communicator (not owned)
+    // plan cache (plan_cached): `plan` is rebuilt only when the batch, the adapter table or a planner
+    // setting changed -- a decode batch repeats from step to step, and the library is invoked for
+    // every projection of every layer (per-invocation overhead matters)
+    uint64_t table_version = 1;           // bumped by every change the planner reads (adapters, options)
+    struct PlanKey {
+        uint64_t version = 0;             // 0: invalid
+        int tc = -1, pad = -1, budget = -1, L_tc = -1;
+        std::vector<int32_t> ip, ids;
+    } pkey;
+    uint64_t plan_gen = 1;                // bumped whenever `plan` is rebuilt
+    uint64_t ready_gen = 0;               // == plan_gen: every adapter of `plan` is known loaded
+    struct FusedKey {                     // the pools and plan generations `fused` was merged from
+        int n = 0;
+        const lora_pool* pools[kMaxJobs] = {};
+        uint64_t gens[kMaxJobs] = {};
+    } fkey;
 };
+
+namespace {
+// p->plan for (seg_indptr, adapter_ids) under the given planner settings; rebuilt only on a change
+lora_status plan_cached(lora_pool* p, const int32_t* ip, const int32_t* ids, int S, bool tc, int pad, int budget,
+                        std::string& err) {
+    lora_pool::PlanKey& k = p->pkey;
+    if (k.version == p->table_version && k.tc == (int)tc && k.pad == pad && k.budget == budget && k.L_tc == p->L_tc &&
+        (int)k.ids.size() == S && std::equal(ids, ids + S, k.ids.begin()) && std::equal(ip, ip + S + 1, k.ip.begin()))
+        return LORA_OK;
+    k.version = 0;
+    ++p->plan_gen;
+    lora_status s = build_plan(p->plan, ip, ids, S, p->H_in, p->H_out, p->esz, p->L_tc, tc, p->table, err, pad,
+                               p->num_sms, budget);
+    if (s != LORA_OK) return s;
+    k.version = p->table_version;
+    k.tc = (int)tc; k.pad = pad; k.budget = budget; k.L_tc = p->L_tc;
+    k.ip.assign(ip, ip + S + 1);
+    k.ids.assign(ids, ids + S);
+    return LORA_OK;
+}
+// p->plan was (re)built outside plan_cached
+void plan_uncached(lora_pool* p) {
+    p->pkey.version = 0;
+    ++p->plan_gen;
+}
+}  // namespace
 
 // ---- NCCL, resolved at run time (dlopen): the library loads without NCCL; only the TP calls need it.
 // The few types and constants used are NCCL's stable ABI (nccl.h 2.x: ncclUniqueId is 128 bytes,
@@ -374,6 +416,7 @@ static lora_status load_impl(lora_pool* p, int32_t id, int rank, const void* A_h
     for (int pg : rec.pages) p->page_used[pg] = 1;
     p->free_pages -= rank;
     p->table.emplace(id, std::move(rec));
+    ++p->table_version;
     return LORA_OK;
 }
 
@@ -414,6 +457,7 @@ lora_status lora_unload_adapter(lora_pool* p, int32_t id) {
     for (int pg : it->second.pages) p->page_used[pg] = 0;
     p->free_pages += it->second.rank;
     p->table.erase(it);
+    ++p->table_version;
     return LORA_OK;
 }
 
@@ -439,6 +483,7 @@ lora_status lora_plan(lora_pool* p, const int32_t* seg_indptr, const int32_t* ad
     const bool tc = !p->host_only ? p->tc_prefill : prefill_supported(p->H_in, p->H_out, p->esz);
     lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz,
                                p->L_tc, tc, p->table, err, p->pad_max_rank ? p->n_pages : -1, p->num_sms);
+    plan_uncached(p);
     if (s != LORA_OK) return fail(s, err);
     return LORA_OK;
 }
@@ -457,6 +502,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
         if (num_segments == 0) {
             p->split_ready = mode == 1;
             p->plan = Plan();
+            plan_uncached(p);
             return LORA_OK;
         }
         if (!seg_indptr || !adapter_ids) return fail(LORA_ERR_ARG, "seg_indptr/adapter_ids is NULL");
@@ -465,6 +511,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
             std::string err;
             s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, false,
                            p->table, err);
+            plan_uncached(p);
             p->split_ready = (s == LORA_OK && mode == 1);
             return s == LORA_OK ? LORA_OK : fail(s, err);
         }
@@ -499,8 +546,7 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     if (mode != 2) {
         std::string err;
         const bool tc = p->tc_prefill && mode == 0;   // the split path keeps every token on the decode kernels
-        s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, tc, p->table,
-                       err, p->pad_max_rank ? p->n_pages : -1, p->num_sms);
+        s = plan_cached(p, seg_indptr, adapter_ids, num_segments, tc, p->pad_max_rank ? p->n_pages : -1, 0, err);
         if (s != LORA_OK) return fail(s, err);
         if (mode == 1 && p->plan.vred_floats > v_cap)
             return fail(LORA_ERR_ARG, "v buffer too small: need " + std::to_string(p->plan.vred_floats) + " floats");
@@ -516,9 +562,15 @@ static lora_status apply_impl(lora_pool* p, const void* x, void* y, const int32_
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply: capture query");
     p->capturing = cap != cudaStreamCaptureStatusNone;
-    for (int gi = 0; gi < pl.G; ++gi)
-        if ((s = wait_loaded(p->table.at(pl.group_id[gi]), st, p->capturing, "lora_apply: wait load")) != LORA_OK)
-            return s;
+    if (p->ready_gen != p->plan_gen) {   // (every adapter of an unchanged plan stays loaded)
+        bool all = true;
+        for (int gi = 0; gi < pl.G; ++gi) {
+            AdapterRec& a = p->table.at(pl.group_id[gi]);
+            if ((s = wait_loaded(a, st, p->capturing, "lora_apply: wait load")) != LORA_OK) return s;
+            all = all && a.ready_known;
+        }
+        if (all) p->ready_gen = p->plan_gen;
+    }
     // scratch (the k-slice partials live in the pool; the TP split's compact v is the caller's)
     if (pl.n_gc > 0 && mode != 2) {
         if ((s = grow(p, p->vbuf, p->vbuf_cap, (size_t)std::max<int64_t>(pl.vbuf_floats, 1), false, "vbuf")) != LORA_OK) return s;
@@ -591,26 +643,39 @@ lora_status lora_apply_multi(lora_pool* const* pools, const void* const* xs, voi
     std::string err;
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
-        lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc,
-                                   p->tc_prefill, p->table, err, -1, p->num_sms,
-                                   n_pools > 1 ? kExpandSmemBudget : 0);
+        lora_status s = plan_cached(p, seg_indptr, adapter_ids, num_segments, p->tc_prefill, -1,
+                                    n_pools > 1 ? kExpandSmemBudget : 0, err);
         if (s != LORA_OK) return fail(s, "pool " + std::to_string(i) + ": " + err);
         p->split_ready = false;
     }
     if (T == 0) return LORA_OK;
-    const Plan* parts[kMaxJobs];
-    for (int i = 0; i < n_pools; ++i) parts[i] = &pools[i]->plan;
-    lora_status s = merge_plans(parts, n_pools, p0->fused, err);
-    if (s != LORA_OK) return fail(s, err);
+    lora_pool::FusedKey& fk = p0->fkey;
+    bool same = fk.n == n_pools;
+    for (int i = 0; same && i < n_pools; ++i) same = fk.pools[i] == pools[i] && fk.gens[i] == pools[i]->plan_gen;
+    if (!same) {
+        const Plan* parts[kMaxJobs];
+        for (int i = 0; i < n_pools; ++i) parts[i] = &pools[i]->plan;
+        fk.n = 0;
+        lora_status s = merge_plans(parts, n_pools, p0->fused, err);
+        if (s != LORA_OK) return fail(s, err);
+        fk.n = n_pools;
+        for (int i = 0; i < n_pools; ++i) { fk.pools[i] = pools[i]; fk.gens[i] = pools[i]->plan_gen; }
+    }
+    lora_status s = LORA_OK;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CUDA_TRY(cudaStreamIsCapturing(st, &cap), "lora_apply_multi: capture query");
     for (int i = 0; i < n_pools; ++i) pools[i]->capturing = cap != cudaStreamCaptureStatusNone;
     for (int i = 0; i < n_pools; ++i) {
         lora_pool* p = pools[i];
-        for (int gi = 0; gi < p->plan.G; ++gi)
-            if ((s = wait_loaded(p->table.at(p->plan.group_id[gi]), st, cap != cudaStreamCaptureStatusNone,
-                                 "lora_apply_multi: wait load")) != LORA_OK)
+        if (p->ready_gen == p->plan_gen) continue;   // every adapter of an unchanged plan stays loaded
+        bool all = true;
+        for (int gi = 0; gi < p->plan.G; ++gi) {
+            AdapterRec& a = p->table.at(p->plan.group_id[gi]);
+            if ((s = wait_loaded(a, st, cap != cudaStreamCaptureStatusNone, "lora_apply_multi: wait load")) != LORA_OK)
                 return s;
+            all = all && a.ready_known;
+        }
+        if (all) p->ready_gen = p->plan_gen;
     }
     Plan& fz = p0->fused;
     int launches = 0;
@@ -726,6 +791,7 @@ lora_status lora_apply_tp(lora_pool* p, const void* x, int64_t x_ld, void* y, in
     // buffer can be sized before anything is enqueued
     lora_status s = build_plan(p->plan, seg_indptr, adapter_ids, num_segments, p->H_in, p->H_out, p->esz, p->L_tc, false,
                                p->table, err);
+    plan_uncached(p);
     if (s != LORA_OK) return fail(s, err);
     const size_t nv = (size_t)std::max<int64_t>(p->plan.vred_floats, 1);
     {
@@ -896,6 +962,7 @@ lora_status lora_apply_fused_base(lora_pool* p, const void* x, const void* W, vo
 
 lora_status lora_set_option(lora_pool* p, int option, int64_t value) {
     if (!p) return fail(LORA_ERR_ARG, "pool is NULL");
+    ++p->table_version;   // planner settings may change: the cached plan is stale
     switch (option) {
         case LORA_OPT_TC_THRESHOLD:
             if (value < 1 || value > INT32_MAX) return fail(LORA_ERR_ARG, "L_tc must be >= 1");

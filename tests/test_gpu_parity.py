@@ -728,3 +728,46 @@ def test_expand_unit_widths_multi_and_large_single(L):
     assert md["n_expand_units"] < sum(-(-1000 // c) for c in
                                       [1024 if r <= 16 else 32768 // (2 * r) for r in [8, 16, 32, 64] * 64])
     assert rel_l2(y, O.delta_for_batch(big, n_threads=8), "bf16") <= TOL["bf16"]
+
+
+@pytest.mark.gpu
+def test_plan_cache_follows_batch_and_table_changes(L):
+    """The pool reuses its plan while (batch, adapter table, planner settings) are unchanged
+    (pool.cpp plan_cached).  Alternating batches, a reload of an adapter id with another rank and
+    pages, an option change and a multi-pool apply between single applies must all give the oracle's
+    result (a stale plan would read wrong pages / ranks)."""
+    import torch
+    ba = gen.build_batch("pcA", 7100, "bf16", 512, 512, [1] * 12, list(range(12)),
+                         {a: [8, 16, 24, 64][a % 4] for a in range(12)}, y_zero=False)
+    bb = gen.build_batch("pcB", 7101, "bf16", 512, 512, [2, 1, 3], [3, 0, 7],
+                         {a: [8, 16, 24, 64][a % 4] for a in range(12)}, y_zero=False)
+    bb.adapters = ba.adapters   # one adapter set (the pool's), two batches over it
+    pool = make_pool(ba, L, extra_pages=256)
+    x_a, x_b = to_torch(ba.x, "cuda"), to_torch(bb.x, "cuda")
+
+    def check(b, x):
+        y = to_torch(b.y_in, "cuda")
+        pool.apply(x, y, b.seg_indptr, b.adapter_ids)
+        torch.cuda.synchronize()
+        assert rel_l2(from_torch(y, "bf16"), O.delta_for_batch(b, n_threads=8), "bf16") <= TOL["bf16"]
+
+    for b, x in ((ba, x_a), (ba, x_a), (bb, x_b), (ba, x_a), (bb, x_b)):
+        check(b, x)
+    # reload id 3 with another rank: same batch arrays, new table
+    new3 = gen.make_adapter(gen.BASE_SEED + 9, 7103, 3, 40, 512, 512, "bf16")
+    pool.unload_adapter(3)
+    pool.load_adapter(3, new3.rank, to_torch(new3.A, pin=True), to_torch(new3.B, pin=True), new3.scale)
+    ba.adapters = bb.adapters = [new3 if a.id == 3 else a for a in ba.adapters]
+    check(ba, x_a)
+    check(bb, x_b)
+    # planner option change, then a multi-pool apply led by this pool, then a single apply again
+    pool.set_option(L.binding.LORA_OPT_TC_THRESHOLD, 2)
+    check(bb, x_b)
+    other = make_pool(ba, L)
+    ys = [to_torch(ba.y_in, "cuda"), to_torch(ba.y_in, "cuda")]
+    L.apply_multi([pool, other], [x_a, x_a], ys, ba.seg_indptr, ba.adapter_ids)
+    torch.cuda.synchronize()
+    assert rel_l2(from_torch(ys[0], "bf16"), O.delta_for_batch(ba, n_threads=8), "bf16") <= TOL["bf16"]
+    check(ba, x_a)
+    pool.close()
+    other.close()
