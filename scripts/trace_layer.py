@@ -50,9 +50,10 @@ def step():
 with torch.cuda.stream(st):
     step()
 torch.cuda.synchronize()
-md = pools[0][3].metadata()
-ns1, ne1 = md["n_shrink_units"], md["n_expand_units"]
-counts = {"qkv": (3 * ns1, 3 * ne1), "o": (ns1, ne1)}
+# unit counts per launch: the q/k/v pools' plans come from lora_apply_multi (its unit sizing), the o
+# pool's from its single lora_apply
+mq, mo = pools[0][0].metadata(), pools[0][3].metadata()
+counts = {"qkv": (3 * mq["n_shrink_units"], 3 * mq["n_expand_units"]), "o": (mo["n_shrink_units"], mo["n_expand_units"])}
 bufs = {}
 for l in range(NL):
     for k, p in (("qkv", pools[l][0]), ("o", pools[l][3])):
