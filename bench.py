@@ -964,42 +964,52 @@ def main():
     d2h = y_host.numel() * 2
 
     # pipelined in NCH layer chunks on two copy streams (PCIe is full duplex): chunk k's x H2D, its
-    # applies, its y D2H; the next step's x may land while this step's y is still leaving
+    # applies, its y D2H.  Only true buffer reuse orders consecutive steps: step i+1's x H2D of chunk
+    # k waits for step i's applies of chunk k (they read x), and its applies of chunk k wait for step
+    # i's y D2H of chunk k (it reads y) -- so the next step's H2D and applies overlap this step's D2H
     NCH = 4 if layers % 4 == 0 else 1
     LPC = layers // NCH
     h2d_st = torch.cuda.Stream(device=dev)
     d2h_st = torch.cuda.Stream(device=dev)
-    ev_x = [torch.cuda.Event() for _ in range(NCH)]
-    ev_y = [torch.cuda.Event() for _ in range(NCH)]
+    ev_x = [torch.cuda.Event() for _ in range(NCH)]      # x chunk k landed
+    ev_used = [torch.cuda.Event() for _ in range(NCH)]   # applies of chunk k done (x free, y ready)
+    ev_out = [torch.cuda.Event() for _ in range(NCH)]    # y chunk k left for the host
+    for k in range(NCH):
+        ev_used[k].record(stream)
+        ev_out[k].record(d2h_st)
 
     def e2e_step():
-        h2d_st.wait_stream(stream)      # previous step's applies have read x
-        stream.wait_stream(d2h_st)      # previous step's y has left before y is updated again
         for k in range(NCH):
             sl = slice(k * LPC, (k + 1) * LPC)
+            h2d_st.wait_event(ev_used[k])
             with torch.cuda.stream(h2d_st):
                 xs_all[sl].copy_(x_host[sl], non_blocking=True)
                 ev_x[k].record(h2d_st)
         for k in range(NCH):
             sl = slice(k * LPC, (k + 1) * LPC)
             stream.wait_event(ev_x[k])
+            stream.wait_event(ev_out[k])
             with torch.cuda.stream(stream):
                 for l in range(k * LPC, (k + 1) * LPC):
                     step(stream, only=l)
-                ev_y[k].record(stream)
-            d2h_st.wait_event(ev_y[k])
+                ev_used[k].record(stream)
+            d2h_st.wait_event(ev_used[k])
             with torch.cuda.stream(d2h_st):
                 y_host[sl].copy_(ys_all[sl], non_blocking=True)
-        stream.wait_stream(d2h_st)      # the step ends when its last y has landed
+                ev_out[k].record(d2h_st)
 
     for _ in range(3):
         e2e_step()
+    torch.cuda.synchronize()
     barrier(use_dist)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record(stream)
+    h2d_st.wait_event(e0)           # the first timed copy starts after e0
+    d2h_st.wait_event(e0)
     for _ in range(args.e2e_steps):
         e2e_step()
+    stream.wait_stream(d2h_st)      # the timed region ends when the last step's y has landed
     e1.record(stream)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1000.0
