@@ -319,7 +319,13 @@ static lora_status append_unit_table(Plan& pl, std::string& err) {
     // full 3-word records while the blob fits the kernel parameters, else 1 word per unit (the
     // kernels then read rank / tokens / pages from the gc record: one more dependent load)
     const size_t units = (size_t)n_shrink + n_expand;
-    const int uw = base + (size_t)kUnitWords * units <= (size_t)kMaxParamBlobWords ? kUnitWords : 1;
+// 3-word records only while the blob stays <= 16 KB of kernel parameters: a q/k/v lora_apply_multi of a
+// c2 batch at 3 words (5,216 words, launched as 31.7 KB of parameters per grid) measured 117.7K vs
+// 118.4K tok/s with 1-word records (2,552 words, 16 KB) -- the larger parameter block costs launch time
+#ifndef LORA_UNIT_WORDS_MAX_BLOB
+#define LORA_UNIT_WORDS_MAX_BLOB 4096
+#endif
+    const int uw = base + (size_t)kUnitWords * units <= (size_t)LORA_UNIT_WORDS_MAX_BLOB ? kUnitWords : 1;
     pl.unit_words = uw;
     pl.blob.resize(base + (size_t)uw * units);
     h = pl.blob.data();
