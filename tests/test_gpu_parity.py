@@ -771,3 +771,46 @@ def test_plan_cache_follows_batch_and_table_changes(L):
     check(ba, x_a)
     pool.close()
     other.close()
+
+
+@pytest.mark.gpu
+def test_randomized_multi_sweep(L):
+    """lora_apply_multi over 2..4 pools of random shapes sharing one random batch (decode and prefill
+    segments, ranks 1..128, ids < 0): bitwise equal to separate lora_apply calls and within tolerance of
+    the oracle.  Covers the multi-launch unit sizing (<= 56 KB expand units), 1-word and 3-word unit
+    records and chunks of 1..8 tokens."""
+    import torch
+    rng = np.random.default_rng(4242)
+    for trial in range(24):
+        n_pools = int(rng.integers(2, 5))
+        H_in = int(rng.integers(8, 97)) * 16
+        lengths = [int(v) for v in rng.choice([1, 1, 2, 3, 5, 8, 9, 70], size=int(rng.integers(4, 60)))]
+        n_ad = int(rng.integers(2, 40))
+        ids = [int(rng.integers(0, n_ad)) if rng.random() > 0.1 else -1 for _ in lengths]
+        H_outs = [int(rng.integers(1, 97)) * 16 for _ in range(n_pools)]
+        rmax = min(128, H_in, min(H_outs))
+        ranks = {a: int(rng.integers(1, rmax + 1)) for a in range(n_ad)}
+        batches = []
+        for p in range(n_pools):
+            H_out = H_outs[p]
+            b = gen.build_batch("ms%d_%d" % (trial, p), 9000 + 10 * trial + p, "bf16", H_in, H_out, lengths, ids, ranks,
+                                y_zero=bool(p % 2))
+            if p:
+                b.x = batches[0].x.copy()
+            batches.append(b)
+        if batches[0].T == 0:
+            continue
+        pools = [make_pool(b, L) for b in batches]
+        xs = [to_torch(b.x, "cuda") for b in batches]
+        y_sep = [to_torch(b.y_in, "cuda") for b in batches]
+        y_fus = [to_torch(b.y_in, "cuda") for b in batches]
+        for p, x, y, b in zip(pools, xs, y_sep, batches):
+            p.apply(x, y, b.seg_indptr, b.adapter_ids)
+        L.apply_multi(pools, xs, y_fus, batches[0].seg_indptr, batches[0].adapter_ids)
+        torch.cuda.synchronize()
+        for b, ys_, yf in zip(batches, y_sep, y_fus):
+            assert torch.equal(ys_, yf), (trial, b.H_in, b.H_out)
+            ref = O.delta_for_batch(b, n_threads=8)
+            assert rel_l2(from_torch(yf, "bf16"), ref, "bf16") <= TOL["bf16"], (trial, b.H_in, b.H_out)
+        for p in pools:
+            p.close()
