@@ -44,7 +44,12 @@ struct lora_pool {
     std::vector<uint8_t> page_used;
     int free_pages = 0;
     AdapterTable table;
-    cudaStream_t side = nullptr;
+    // cold-start loads round-robin over kSideStreams side streams, so consecutive small loads (PCIe
+    // latency-bound one at a time) overlap; ordering against page reuse is by events (unload)
+    static constexpr int kSideStreams = 4;
+    cudaStream_t sides[kSideStreams] = {};
+    int next_side = 0;
+    cudaStream_t side = nullptr;          // == sides[0]
     cudaEvent_t unload_fence = nullptr;
     bool fence_pending = false;
     std::vector<cudaStream_t> apply_streams;   // streams applied on since the last unload
@@ -289,7 +294,9 @@ lora_status lora_pool_create_ex(int hidden_in, int hidden_out, int max_adapters,
                 if (e == cudaSuccess) e = cudaMemcpy(p->box_maps, maps, sizeof(maps), cudaMemcpyHostToDevice);
             }
         }
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+        for (int i = 0; i < lora_pool::kSideStreams && e == cudaSuccess; ++i)
+            e = cudaStreamCreateWithFlags(&p->sides[i], cudaStreamNonBlocking);
+        p->side = p->sides[0];
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->unload_fence, cudaEventDisableTiming);
         if (e != cudaSuccess) {
             lora_pool_destroy(p);
@@ -309,7 +316,8 @@ lora_status lora_pool_destroy(lora_pool* p) {
     if (!p) return LORA_OK;
     if (!p->host_only) {
         DeviceGuard g(p->device);
-        if (p->side) cudaStreamSynchronize(p->side);
+        for (cudaStream_t s : p->sides)
+            if (s) cudaStreamSynchronize(s);
         for (cudaStream_t s : p->apply_streams) cudaStreamSynchronize(s);
         cudaDeviceSynchronize();
         for (auto& kv : p->table)
@@ -326,7 +334,8 @@ lora_status lora_pool_destroy(lora_pool* p) {
         if (p->meta_dev) cudaFree(p->meta_dev);
         for (void* b : p->retired) cudaFree(b);
         if (p->unload_fence) cudaEventDestroy(p->unload_fence);
-        if (p->side) cudaStreamDestroy(p->side);
+        for (cudaStream_t s : p->sides)
+            if (s) cudaStreamDestroy(s);
     }
     delete p;
     return LORA_OK;
@@ -365,8 +374,10 @@ static lora_status load_impl(lora_pool* p, int32_t id, int rank, const void* A_h
         DeviceGuard g(p->device);
         cudaEvent_t ev = nullptr;
         CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "lora_load_adapter: event");
+        cudaStream_t ss = p->sides[p->next_side];
+        p->next_side = (p->next_side + 1) % lora_pool::kSideStreams;
         if (p->fence_pending) {
-            cudaError_t e = cudaStreamWaitEvent(p->side, p->unload_fence, 0);
+            cudaError_t e = cudaStreamWaitEvent(ss, p->unload_fence, 0);
             if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: fence"); }
             p->fence_pending = false;
         }
@@ -381,17 +392,17 @@ static lora_status load_impl(lora_pool* p, int32_t id, int rank, const void* A_h
                 int k = j + 1;
                 while (k < rank && rec.pages[k] == rec.pages[k - 1] + 1) ++k;
                 cudaError_t e = cudaMemcpy2DAsync(p->dA + (size_t)rec.pages[j] * ra, ra, (const char*)A_host + j * a_pitch,
-                                                  a_pitch, ra, (size_t)(k - j), cudaMemcpyHostToDevice, p->side);
+                                                  a_pitch, ra, (size_t)(k - j), cudaMemcpyHostToDevice, ss);
                 if (e == cudaSuccess)
                     e = cudaMemcpy2DAsync(p->dB + (size_t)rec.pages[j] * rb, rb, (const char*)B_host + j * b_pitch, b_pitch,
-                                          rb, (size_t)(k - j), cudaMemcpyHostToDevice, p->side);
+                                          rb, (size_t)(k - j), cudaMemcpyHostToDevice, ss);
                 if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter_shard: copy"); }
                 j = k;
             }
         } else if (p->load_kernel && devA && devB && ((uintptr_t)devA % 16) == 0 && ((uintptr_t)devB % 16) == 0) {
             // zero-copy gather kernel (LORA_OPT_LOAD_KERNEL)
             cudaError_t e = (cudaError_t)launch_load(p->dA, p->dB, devA, devB, (int64_t)ra, (int64_t)rb, rank,
-                                                     rec.pages.data(), p->num_sms, p->side);
+                                                     rec.pages.data(), p->num_sms, ss);
             if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: load kernel"); }
         } else
         // one copy per run of consecutive pages
@@ -400,14 +411,14 @@ static lora_status load_impl(lora_pool* p, int32_t id, int rank, const void* A_h
             while (k < rank && rec.pages[k] == rec.pages[k - 1] + 1) ++k;
             const size_t n = (size_t)(k - j);
             cudaError_t e = cudaMemcpyAsync(p->dA + (size_t)rec.pages[j] * ra, (const char*)A_host + j * ra, n * ra,
-                                            cudaMemcpyHostToDevice, p->side);
+                                            cudaMemcpyHostToDevice, ss);
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(p->dB + (size_t)rec.pages[j] * rb, (const char*)B_host + j * rb, n * rb,
-                                    cudaMemcpyHostToDevice, p->side);
+                                    cudaMemcpyHostToDevice, ss);
             if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: copy"); }
             j = k;
         }
-        cudaError_t e = cudaEventRecord(ev, p->side);
+        cudaError_t e = cudaEventRecord(ev, ss);
         if (e != cudaSuccess) { cudaEventDestroy(ev); return cuda_fail(e, "lora_load_adapter: record"); }
         rec.ready = ev;
     } else {
@@ -446,11 +457,16 @@ lora_status lora_unload_adapter(lora_pool* p, int32_t id) {
         // physical reuse of these pages must follow every apply already enqueued (events)
         for (cudaStream_t s : p->apply_streams) {
             CUDA_TRY(cudaEventRecord(p->unload_fence, s), "lora_unload_adapter: fence");
-            CUDA_TRY(cudaStreamWaitEvent(p->side, p->unload_fence, 0), "lora_unload_adapter: fence wait");
+            for (cudaStream_t ss : p->sides)
+                CUDA_TRY(cudaStreamWaitEvent(ss, p->unload_fence, 0), "lora_unload_adapter: fence wait");
         }
         p->apply_streams.clear();
         if (it->second.ready) {
-            // the load itself must also be finished before its pages are rewritten: side-stream order
+            // the load itself must also be finished before its pages are rewritten by a later load on
+            // any side stream
+            if (!it->second.ready_known)
+                for (cudaStream_t ss : p->sides)
+                    CUDA_TRY(cudaStreamWaitEvent(ss, (cudaEvent_t)it->second.ready, 0), "lora_unload_adapter: load wait");
             cudaEventDestroy((cudaEvent_t)it->second.ready);
         }
     }
@@ -1068,7 +1084,7 @@ lora_status lora_debug_read_pages(lora_pool* p, int32_t id, void* A_out, void* B
     auto it = p->table.find(id);
     if (it == p->table.end()) return fail(LORA_ERR_UNKNOWN_ADAPTER, "adapter " + std::to_string(id) + " is not loaded");
     DeviceGuard g(p->device);
-    CUDA_TRY(cudaStreamSynchronize(p->side), "lora_debug_read_pages: sync");
+    for (cudaStream_t ss : p->sides) CUDA_TRY(cudaStreamSynchronize(ss), "lora_debug_read_pages: sync");
     const size_t ra = (size_t)p->H_in * p->esz, rb = (size_t)p->H_out * p->esz;
     for (int j = 0; j < it->second.rank; ++j) {
         CUDA_TRY(cudaMemcpy((char*)A_out + j * ra, p->dA + (size_t)it->second.pages[j] * ra, ra, cudaMemcpyDeviceToHost), "read A");
