@@ -114,7 +114,7 @@ lora_status lora_pool_create(int hidden_in, int hidden_out, int max_adapters, lo
 lora_status lora_pool_create_ex(int hidden_in, int hidden_out, int max_adapters, lora_dtype dtype,
                                 int max_total_rank, unsigned flags, lora_pool** out);
 
-/* lora_pool_destroy -- synchronises the pool's side stream and every stream the pool was
+/* lora_pool_destroy -- synchronises the pool's side streams and every stream the pool was
  * applied on, then frees pages, scratch, events and staging.  NULL is a no-op. */
 lora_status lora_pool_destroy(lora_pool* p);
 
@@ -126,8 +126,8 @@ lora_status lora_pool_destroy(lora_pool* p);
  *   B_host  pinned host buffer [rank][hidden_out].
  *   scale   s_a (fp32).
  * Allocates the rank lowest-indexed free pages (ascending; reading R9), then
- * enqueues the host->HBM copies on the pool's side stream and records a ready event; it
- * returns without waiting.  The buffers must stay valid and unmodified until
+ * enqueues the host->HBM copies on one of the pool's side streams (8, round-robin, so
+ * consecutive loads overlap) and records a ready event; it returns without waiting.  The buffers must stay valid and unmodified until
  * lora_adapter_ready reports 1; the library never frees them.  Physical reuse of pages
  * freed by lora_unload_adapter is ordered after the applies that read them (events).
  * Errors: ARG (id < 0, null buffer), SHAPE (rank), EXISTS, POOL_FULL, NOT_PINNED, CUDA.
@@ -137,7 +137,8 @@ lora_status lora_load_adapter(lora_pool* p, int32_t id, int rank,
                               const void* A_host, const void* B_host, float scale);
 
 /* lora_unload_adapter -- frees the adapter's slot and pages at call time (logical); the
- * pages are physically rewritten only after the applies already enqueued have finished. */
+ * pages are physically rewritten only after the applies already enqueued and the adapter's
+ * own load have finished (every side stream waits on both). */
 lora_status lora_unload_adapter(lora_pool* p, int32_t id);
 
 /* lora_adapter_ready -- *ready = 1 once the adapter's load has completed (cudaEventQuery). */
@@ -314,7 +315,7 @@ lora_status lora_debug_metadata(lora_pool* p, lora_metadata_view* out);
 lora_status lora_debug_adapter_pages(lora_pool* p, int32_t id, int32_t* pages, int cap, int* rank);
 
 /* lora_debug_read_pages -- synchronous D2H read-back of an adapter's pages into host
- * buffers laid out like lora_load_adapter's (pin P12).  Synchronises the side stream. */
+ * buffers laid out like lora_load_adapter's (pin P12).  Synchronises the side streams. */
 lora_status lora_debug_read_pages(lora_pool* p, int32_t id, void* A_out, void* B_out);
 
 /* lora_debug_set_trace -- profiling aid: when dev_buf (device memory, uint64 words) is non-NULL,
