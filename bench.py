@@ -399,7 +399,8 @@ def bench_c4(L, dev, steps: int, world: int, rank: int, use_dist: bool = False):
     gen_s = _t.perf_counter() - t0
     budget = sum(gen.c4_rank(a) for a in range(n_ad)) // 5
     pool = L.LoraPool(H, H, n_ad, "bf16", max_total_rank=budget)
-    pool.set_option(L.binding.LORA_OPT_LOAD_KERNEL, 1)   # the cold-start path by the zero-copy gather kernel
+    load_kernel = int(os.environ.get("LORA_BENCH_C4_LOAD_KERNEL", "1"))   # A/B of the two load paths
+    pool.set_option(L.binding.LORA_OPT_LOAD_KERNEL, load_kernel)
     cache = AdapterCache(pool, repo, budget, n_ad)
     st = torch.cuda.Stream(device=dev)
     model = measured_model("mbgmv", invocations=1)
@@ -490,7 +491,8 @@ def bench_c4(L, dev, steps: int, world: int, rank: int, use_dist: bool = False):
            "routing": {"policy": "Algorithm 1 (rank-aware, P:781-814), MBGMV model fitted on B200",
                        "this_gpu_decode_requests_per_step": round(routed["decode"] / steps, 2),
                        "this_gpu_prompts_per_step": round(routed["prefill"] / steps, 3)},
-           "load_path": "zero-copy gather kernel (LORA_OPT_LOAD_KERNEL=1)",
+           "load_path": "zero-copy gather kernel (LORA_OPT_LOAD_KERNEL=1)" if load_kernel else
+                        "cudaMemcpyAsync per page run (default)",
            "ms_per_step_all_resident": round(ms_noload, 4),
            "overlap": round(ms_noload / ms, 3),   # 1.0 = the cold-start loads cost nothing
            "steps": steps, "hit_rate": round(hits / max(1, hits + misses), 4), "loads_per_step": round(misses / steps, 2),
